@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""Benchmark of the PRNGD hot path on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg3|cfg5|cfg4|...]
+                    [--impl ours|reference]
+
+A step is one pass of the hot path over one batch: S1-S6 (generate n_streams x n_per_stream
+doubles into HBM) for the write workloads, plus S7 (fused histogram + moments) and the NCCL
+all-reduce of the histogram/moments for cfg5.  Default workload = cfg3 (BASELINE configs[2],
+"Single-GPU bulk": 2^20 streams x 1024 = 2^30 doubles = 8 GiB per GPU per step).  With N > 1
+every rank generates its own 2^20-stream range (stream_begin = rank * 2^20): weak scaling, no
+communication on the generation path.
+
+--impl reference times the CPU oracle (oracle/, plain C, one thread) on a bounded sample of the
+same workload; it is the only other place this file executes oracle/.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1401_8230_b200 import workloads as W  # noqa: E402
+
+METRIC = "Gdoubles/s generated (1/2/4/8 B200) and % of HBM-write roofline"
+FALLBACK_HBM = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="cfg3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--flags", type=int, default=0, help="prngd flags (A/B of store paths)")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def workload_params(name: str, rank: int, world: int) -> dict:
+    p = W.config(name)
+    # per-GPU shard of the global stream space: rank r owns [r*n, (r+1)*n)
+    p["stream_begin"] = rank * p["n_streams"]
+    return p
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def traffic_per_launch():
+    """dram read+write bytes per launch of the generate kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["nvml unavailable"]}
+        rs = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max,
+                "reasons": rs, "samples": len(self.samples)}
+
+
+def cpu_baseline(p: dict, target_s: float = 12.0) -> dict:
+    """The oracle as it stands, one host thread, on the first streams of the workload."""
+    import oracle
+    oracle.build()
+    ns = 1024
+    t0 = time.perf_counter()
+    oracle.generate(p, stream_begin=p["stream_begin"], n_streams=ns, want_out=False,
+                    want_stats=p.get("_consume", False))
+    dt = time.perf_counter() - t0
+    ns = max(1024, min(p["n_streams"], int(ns * target_s / max(dt, 1e-3)) // 1024 * 1024))
+    t0 = time.perf_counter()
+    oracle.generate(p, stream_begin=p["stream_begin"], n_streams=ns, want_out=True,
+                    want_stats=p.get("_consume", False))
+    dt = time.perf_counter() - t0
+    n = ns * p["n_per_stream"]
+    return {"value": n / dt / 1e9, "unit": "Gdoubles/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {ns} of {p['n_streams']} streams x {p['n_per_stream']} "
+                      f"({n} doubles, {dt:.1f} s, outputs written to host RAM)"}
+
+
+def run_reference(args, rank, world):
+    """Reference arm = the CPU oracle (this tier has no upstream code)."""
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    p = workload_params(args.workload, 0, 1)
+    cons = args.workload == "cfg5"
+    ns = 4096  # bounded sample per step: 4096 streams x n_per_stream
+    nout = ns * p["n_per_stream"]
+    for _ in range(args.warmup):
+        oracle.generate(p, stream_begin=0, n_streams=ns, want_out=True, want_stats=cons)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        oracle.generate(p, stream_begin=k * ns, n_streams=ns, want_out=True, want_stats=cons)
+    dt = time.perf_counter() - t0
+    v = nout * args.steps / dt / 1e9
+    sample = f"{ns} streams x {p['n_per_stream']} per step ({args.workload} shape)"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Gdoubles/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "Gdoubles/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "Gdoubles/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1401_8230_b200 import prngd as P
+
+    if not torch.cuda.is_available():
+        print(json.dumps({"error": "no CUDA device"}))
+        return 1
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    p = workload_params(args.workload, rank, world)
+    p["flags"] = args.flags
+    consume = args.workload == "cfg5"
+    g = P.Generator(**p)
+    nout = p["n_streams"] * p["n_per_stream"]
+    out = torch.empty((p["n_streams"], p["n_per_stream"]), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    if consume:
+        hist = torch.zeros(65536, dtype=torch.int64, device="cuda")
+        pw = torch.zeros(4, dtype=torch.float64, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def step():
+        if consume:
+            hist.zero_(), pw.zero_(), cnt.zero_()
+            P.prngd_generate_consume(g.handle, out, hist, pw, cnt, stream)
+            if world > 1:
+                dist.all_reduce(hist)
+                dist.all_reduce(pw)
+                dist.all_reduce(cnt)
+        else:
+            P.prngd_generate(g.handle, out, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = g.last_launches
+
+    # -------------------------------------------------- timed region (device events)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for k in range(args.steps):
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = t0.elapsed_time(t1)
+    per = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = t.item()
+    ms = total_ms / args.steps
+    value = world * nout / (ms * 1e-3) / 1e9
+
+    # -------------------------------------------------- roofline of the dominant kernel
+    # For write workloads the step is exactly one generate launch; its average duration is
+    # the mean of the per-step event pairs on the launching stream.
+    peak, peak_src = peaks()
+    kern_ms = statistics.mean(per) if not consume else None
+    bytes_launch = 8 * nout
+    tr = traffic_per_launch()
+    traffic = None
+    if tr and tr.get("workload") == args.workload:
+        traffic = tr.get("dram_bytes_per_launch")
+    if consume:
+        # dominant kernel = fused generate+consume; its own duration needs the launch list.
+        kern_ms = statistics.mean(per)
+    achieved = bytes_launch / (kern_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+            "kernel": "gen_kernel<FULL32,SPEC,TMA>" if not consume else "consume_kernel+finalize",
+            "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kern_ms,
+            "frac_of_8TBs_nominal": achieved / 8000.0}
+
+    # -------------------------------------------------- end to end through the C ABI, host buffer
+    e2e = None
+    if args.e2e_steps > 0 and not consume:
+        host = torch.empty((p["n_streams"], p["n_per_stream"]), dtype=torch.float64,
+                           pin_memory=True)
+        P.prngd_generate_host(g.handle, host, stream)  # warm-up (allocates staging)
+        if world > 1:
+            dist.barrier()
+        te = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            P.prngd_generate_host(g.handle, host, stream)
+        torch.cuda.synchronize()
+        de = torch.tensor([time.perf_counter() - te], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(de, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * nout * args.e2e_steps / de.item() / 1e9, "unit": "Gdoubles/s",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * nout,
+               "note": "prngd_generate_host: chunked generate + pinned D2H, overlapped; inputs "
+                       "are the parameter struct only"}
+        del host
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        q = dict(p)
+        q["_consume"] = consume
+        cpu = cpu_baseline(q)
+
+    if rank == 0:
+        desc = W.DESCRIPTIONS.get(args.workload, args.workload)
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gdoubles/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {desc}",
+                       "streams_per_gpu": p["n_streams"], "n_per_stream": p["n_per_stream"],
+                       "seed": p["seed"], "bytes_written_per_step_per_gpu": 8 * nout,
+                       "l2": "inputs none; 8 B/output written, >126 MB L2 per step (no flush)",
+                       "parallelism": f"stream-range shards x{world}",
+                       "flags": args.flags},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": launches_per_step * args.steps,
+            "pct_hbm_write_roofline": 100.0 * achieved / peak,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

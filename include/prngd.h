@@ -1,0 +1,151 @@
+/*
+ * prngd.h -- C ABI of the B200-native PRNGD library (libprngd_b200.so).
+ *
+ * Method: Demchik & Gulov, "Increasing precision of uniform pseudorandom number generators"
+ * (arXiv 1401.8230).  Citations are PAPER.md lines ("P:57") and equation numbers; the readings
+ * R1..R17 of the paper are listed in DESIGN.md section 2.
+ *
+ * One output z' is built from one ACCEPTED pair (x1, x2) of w-bit pseudorandom integers:
+ *   Eq.(1)  z  = x1 + k*x2,  k = 2^-w
+ *   rule    drop the pair if x1 = a0 or x1 = a (more generally unless a0 < x1 < a) (R3)
+ *   Eq.(4)  z' = (z - (a0 + k*b)) / (a - a0 - k*(b - b0))  in [0,1)
+ * PRNGD(k, min, max) of Alg. 1 is w = -log2(k), a0 = b0 = min, a = b = max.
+ *
+ * The base generator is Marsaglia's xorshift128 (one per "stream"), seeded per stream from
+ * SplitMix64(seed) (R6).  x1 and x2 are the top bitlen(a) / bitlen(b) bits of consecutive
+ * draws (R4).  Output j of stream s is produced by the j-th accepted pair of that stream (R2),
+ * so every stream yields exactly n_per_stream outputs and the layout is deterministic.
+ *
+ * Conventions for every entry point:
+ *   - Device pointers ("d_") are CUDA device memory on the current device, owned by the caller.
+ *     Host pointers ("h_") are host memory owned by the caller (pinned memory is fastest).
+ *   - Work is enqueued on `cuda_stream` (a cudaStream_t; NULL = the legacy default stream) and
+ *     the call returns without synchronising, except prngd_generate_host which returns after
+ *     the host buffer is complete.  Kernel faults surface at the caller's next synchronisation.
+ *   - No call throws or aborts; errors are returned as prngd_status, with a detail string in
+ *     prngd_last_error() (thread-local).  A handle is immutable after prngd_create, so several
+ *     threads may use one handle concurrently on different streams / buffers.
+ */
+#ifndef PRNGD_H
+#define PRNGD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRNGD_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PRNGD_API __attribute__((visibility("default")))
+#else
+#define PRNGD_API
+#endif
+
+typedef enum {
+    PRNGD_OK = 0,
+    PRNGD_EINVAL = 1,       /* invalid parameters, NULL or misaligned pointer, size overflow */
+    PRNGD_ECUDA = 2,        /* a CUDA runtime / driver call or a kernel launch failed */
+    PRNGD_ENOMEM = 3,       /* device or host allocation failed */
+    PRNGD_EUNSUPPORTED = 4  /* no sm_100a device, or a flag combination not implemented */
+} prngd_status;
+
+/* flags */
+#define PRNGD_FLAG_IEEE_DIV   0x1u  /* use the IEEE division instruction sequence instead of the
+                                       reciprocal + 2 FMA correction (R10); same bits, slower */
+#define PRNGD_FLAG_NO_TMA     0x2u  /* store through the warp-coalesced st.global path even when
+                                       the TMA tensor-store path is eligible */
+#define PRNGD_FLAG_ALG1       0x4u  /* NEXT-2 reading of Alg. 1: a rejected x1 is
+                                       redrawn alone (x2 is drawn only after acceptance) */
+
+typedef struct {
+    uint32_t w;             /* k = 2^-w, 1 <= w <= 32                                        */
+    uint32_t flags;         /* PRNGD_FLAG_*; 0 = canonical (pair-drop, Eq.(4), clamp)         */
+    uint64_t a0, a;         /* x1 range [a0; a]: a < 2^32, a - a0 >= 2                        */
+    uint64_t b0, b;         /* x2 range [b0; b]: b0 == 0, b + 1 a power of two, b < 2^w (R5) */
+    uint64_t seed;          /* SplitMix64 seed (R6)                                           */
+    uint64_t stream_begin;  /* first GLOBAL stream id of this call (multi-GPU shard)          */
+    uint64_t n_streams;     /* >= 1                                                           */
+    uint64_t n_per_stream;  /* >= 1; n_streams * n_per_stream < 2^62; n_per_stream < 2^32     */
+} prngd_params;
+
+typedef struct prngd_handle prngd_handle;
+
+typedef struct {
+    /* Eq.(3)/(4) constants as the library computed them (R7) and their scaled GPU forms (R10) */
+    double C, D;            /* C = a0 + k*b, D = (a - a0) - k*(b - b0)                       */
+    double C_s, D_s, y;     /* C*2^w, D*2^w, RN(1/D_s)                                        */
+    uint32_t sh1, sh2;      /* x1 = u1 >> sh1, x2 = u2 >> sh2 (R4)                           */
+    uint32_t clamp;         /* 1 if some accepted pair maps to 1.0 before the clamp (R11)    */
+    uint32_t speculative;   /* 1 if the kernel checks acceptance once per batch (rare rejection) */
+    uint64_t n_outputs;     /* n_streams * n_per_stream                                      */
+    uint64_t out_bytes;     /* 8 * n_outputs                                                 */
+} prngd_info;
+
+/* Validate *p and build an immutable handle (host only: no CUDA call, no device memory).
+ * Returns PRNGD_EINVAL for parameters outside the domain documented on prngd_params. */
+PRNGD_API prngd_status prngd_create(const prngd_params *p, prngd_handle **out);
+
+/* Release a handle and any device scratch it owns.  NULL-safe.  Not synchronising: the caller
+ * must not destroy a handle while its work is still running on a stream. */
+PRNGD_API prngd_status prngd_destroy(prngd_handle *h);
+
+/* Constants and dispatch choices of the handle (host only). */
+PRNGD_API prngd_status prngd_get_info(const prngd_handle *h, prngd_info *info);
+
+/* S1-S6: d_out[i * n_per_stream + j] = output j of global stream stream_begin + i.
+ * d_out: device, >= n_streams * n_per_stream doubles, 8-byte aligned (16-byte aligned and an
+ * even n_per_stream enable the TMA tensor-store path).  One kernel launch. */
+PRNGD_API prngd_status prngd_generate(const prngd_handle *h, double *d_out, void *cuda_stream);
+
+/* S1-S7: as prngd_generate (outputs written only if d_out != NULL), plus the fused consumer:
+ *   d_hist[bin] += #{outputs with (uint32)(z' * 65536.0) == bin}    (65536 int64, R16)
+ *   d_pow[p-1] += sum z'^p, p = 1..4                                  (4 doubles)
+ *   d_count[0] += number of outputs                                  (1 int64)
+ * All three accumulate, so shards may add into one buffer.  d_hist, d_pow, d_count: device,
+ * 8-byte aligned, required.  Two kernel launches (generate+bin, then slab reduction). */
+PRNGD_API prngd_status prngd_generate_consume(const prngd_handle *h, double *d_out, int64_t *d_hist,
+                                    double *d_pow, int64_t *d_count, void *cuda_stream);
+
+/* End-to-end form for host memory: h_out (host, >= n_outputs doubles) receives the same
+ * values as prngd_generate would write.  Generates in chunks of streams into device scratch
+ * owned by the handle and overlaps the device->host copies with generation.  Synchronous:
+ * returns after h_out is complete.  PRNGD_ENOMEM if the scratch cannot be allocated. */
+PRNGD_API prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stream);
+
+/* Number of kernel launches the last successful call on this handle enqueued. */
+PRNGD_API uint32_t prngd_last_launches(const prngd_handle *h);
+
+PRNGD_API const char *prngd_status_string(prngd_status s);
+PRNGD_API const char *prngd_last_error(void);
+PRNGD_API int prngd_abi_version(void);
+
+/* ---- validation hooks (not timed; same __device__ code as the production kernels) ---- */
+
+/* d_raw[i * draws_per_stream + d] = d-th xorshift128 output of global stream stream_begin+i. */
+PRNGD_API prngd_status prngd_debug_raw(const prngd_handle *h, uint32_t *d_raw, uint64_t draws_per_stream,
+                             void *cuda_stream);
+
+/* d_pair_index[i * n_per_stream + j] = 0-based index of the pair that produced output j of
+ * stream i (pair p = draws 2p, 2p+1); d_pairs_consumed[i] = pairs consumed by stream i.
+ * Either pointer may be NULL. */
+PRNGD_API prngd_status prngd_debug_pairs(const prngd_handle *h, uint32_t *d_pair_index,
+                               uint64_t *d_pairs_consumed, void *cuda_stream);
+
+/* d_z[i] = Eq.(4) + clamp of the pair (d_x1[i], d_x2[i]) in integer units, through the same
+ * device mapping as the generator (no acceptance test).  n may be 0. */
+PRNGD_API prngd_status prngd_debug_map(const prngd_handle *h, const uint32_t *d_x1, const uint32_t *d_x2,
+                             double *d_z, uint64_t n, void *cuda_stream);
+
+/* d_mismatch[0] += number of n_s in the sample for which the reciprocal + 2 FMA quotient
+ * differs from the IEEE division (R10).  Samples: n = RN(v) - C_s for v = x1*2^w + x2 with
+ * (x1, x2) from a counter-based hash of (seed, i), i < n.  Validation of R10 on the GPU. */
+PRNGD_API prngd_status prngd_debug_div_check(const prngd_handle *h, uint64_t n, uint64_t seed,
+                                   unsigned long long *d_mismatch, void *cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRNGD_H */

@@ -1,0 +1,83 @@
+// prngd_device.cuh -- __device__ building blocks of the PRNGD path (sm_100a).
+// Product code; written independently of oracle/ (shares nothing with it).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace prngd {
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;      // SplitMix64 increment
+constexpr double kBelowOne = 0x1.fffffffffffffp-1;       // 1 - 2^-53, R11 clamp value
+
+// ---- S1: stream init (R6) --------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix_finalize(uint64_t v) {
+    v ^= v >> 30;
+    v *= 0xBF58476D1CE4E5B9ull;
+    v ^= v >> 27;
+    v *= 0x94D049BB133111EBull;
+    return v ^ (v >> 31);
+}
+
+struct Xs128 {
+    uint32_t x, y, z, w;
+};
+
+// Global stream s starts from SplitMix64(seed) outputs #2s and #2s+1 (counter addressed).
+__device__ __forceinline__ Xs128 stream_start(uint64_t seed, uint64_t s) {
+    const uint64_t lo = splitmix_finalize(seed + (2 * s + 1) * kGamma);
+    const uint64_t hi = splitmix_finalize(seed + (2 * s + 2) * kGamma);
+    Xs128 r;
+    r.x = (uint32_t)lo;
+    r.y = (uint32_t)(lo >> 32);
+    r.z = (uint32_t)hi;
+    r.w = (uint32_t)(hi >> 32);
+    return r;
+}
+
+// ---- S2: base draw, Marsaglia xor128 (Alg. 1 "r <- PRNG()") ---------------------
+__device__ __forceinline__ uint32_t draw(Xs128 &s) {
+    const uint32_t t = s.x ^ (s.x << 11);
+    s.x = s.y;
+    s.y = s.z;
+    s.z = s.w;
+    s.w = s.w ^ (s.w >> 19) ^ t ^ (t >> 8);
+    return s.w;
+}
+
+// ---- S3: accept-reject (R3): a0 < x1 < a  <=>  (x1 - (a0+1)) < (a - a0 - 1) unsigned --
+__device__ __forceinline__ bool accepted(uint32_t x1, uint32_t lo, uint32_t span) {
+    return (uint32_t)(x1 - lo) < span;
+}
+
+// ---- S4 + S5: Eq.(1) and Eq.(4) in scaled integer units (R10) --------------------------------
+// v = x1*2^w + x2 is exact in 64 bits; RN(v) = 2^w * RN(x1 + k*x2); subtracting C_s = 2^w*C and
+// dividing by D_s = 2^w*D gives bit-for-bit the quotient RN(RN(z - C) / D) of Eq.(4).
+template <bool IEEE_DIV, bool CLAMP>
+__device__ __forceinline__ double eq4_scaled(uint64_t v, double Cs, double Ds, double y) {
+    const double n = __dsub_rn(__ull2double_rn(v), Cs);
+    double q;
+    if (IEEE_DIV) {
+        q = __ddiv_rn(n, Ds);
+    } else {
+        // Markstein: q0 = RN(n*y) is faithful; r = n - q0*D_s is exact in one FMA; the second
+        // FMA rounds q0 + r*y to the correctly rounded quotient (y = RN(1/D_s)).
+        const double q0 = __dmul_rn(n, y);
+        const double r = __fma_rn(-q0, Ds, n);
+        q = __fma_rn(r, y, q0);
+    }
+    if (CLAMP) q = fmin(q, kBelowOne);  // R11: literal Eq.(4) can round to 1.0 for w >= 27
+    return q;
+}
+
+template <bool IEEE_DIV, bool CLAMP>
+__device__ __forceinline__ double eq4_pair(uint32_t x1, uint32_t x2, uint32_t w, double Cs,
+                                           double Ds, double y) {
+    return eq4_scaled<IEEE_DIV, CLAMP>(((uint64_t)x1 << w) | (uint64_t)x2, Cs, Ds, y);
+}
+
+// ---- S7: bin of the 2^16-bin histogram (R16): exact scaling by 2^16, truncation -------------
+__device__ __forceinline__ uint32_t bin16(double q) {
+    return (uint32_t)__double2uint_rz(__dmul_rn(q, 65536.0));
+}
+
+}  // namespace prngd

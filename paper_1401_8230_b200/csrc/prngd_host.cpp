@@ -1,0 +1,399 @@
+// prngd_host.cpp -- C ABI (include/prngd.h): validation, Eq.(3)/(4) constants, dispatch,
+// host-buffer pipeline.  Product code; written independently of oracle/.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+
+#include "prngd_internal.h"
+
+using prngd::GenArgs;
+using prngd::Plan;
+using prngd::Store;
+
+struct prngd_handle {
+    prngd_params p;
+    prngd_info info;
+    GenArgs args;
+    Plan plan;
+    mutable std::atomic<uint32_t> last_launches{0};
+    // device scratch, created lazily (consume slabs, host-pipeline staging)
+    std::mutex mu;
+    int scratch_dev = -1;
+    void *cons_scratch = nullptr;
+    size_t cons_bytes = 0;
+    double *stage[2] = {nullptr, nullptr};
+    size_t stage_rows = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_gen[2] = {nullptr, nullptr};
+    cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+};
+
+static thread_local char g_err[512] = "";
+
+static prngd_status fail(prngd_status s, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+static prngd_status cuda_fail(cudaError_t e, const char *what) {
+    return fail(PRNGD_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+static int bit_length(uint64_t v) {
+    int n = 0;
+    for (; v; v >>= 1) ++n;
+    return n;
+}
+
+// Device checks done once per (thread, device): sm_100 and SM count.
+static prngd_status device_ready(int *num_sms) {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    int major = 0, minor = 0, sms = 0;
+    if ((e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev)) != cudaSuccess)
+        return cuda_fail(e, "cudaDeviceGetAttribute");
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (major != 10 || minor != 0)
+        return fail(PRNGD_EUNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a",
+                    dev, major, minor);
+    *num_sms = sms;
+    return PRNGD_OK;
+}
+
+extern "C" {
+
+const char *prngd_status_string(prngd_status s) {
+    switch (s) {
+        case PRNGD_OK: return "PRNGD_OK";
+        case PRNGD_EINVAL: return "PRNGD_EINVAL: invalid argument";
+        case PRNGD_ECUDA: return "PRNGD_ECUDA: CUDA error";
+        case PRNGD_ENOMEM: return "PRNGD_ENOMEM: out of memory";
+        case PRNGD_EUNSUPPORTED: return "PRNGD_EUNSUPPORTED: unsupported device or option";
+    }
+    return "PRNGD_?: unknown status";
+}
+
+const char *prngd_last_error(void) { return g_err; }
+
+int prngd_abi_version(void) { return PRNGD_ABI_VERSION; }
+
+prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
+    g_err[0] = 0;
+    if (!p || !out) return fail(PRNGD_EINVAL, "null argument");
+    *out = nullptr;
+    const uint32_t w = p->w;
+    if (w < 1 || w > 32) return fail(PRNGD_EINVAL, "w=%u outside [1, 32]", w);
+    if (p->a > 0xFFFFFFFFull) return fail(PRNGD_EINVAL, "a=%llu does not fit 32 bits",
+                                          (unsigned long long)p->a);
+    if (p->a0 >= p->a || p->a - p->a0 < 2)
+        return fail(PRNGD_EINVAL, "need a - a0 >= 2 (got a0=%llu, a=%llu): no x1 strictly inside",
+                    (unsigned long long)p->a0, (unsigned long long)p->a);
+    if (p->b0 != 0) return fail(PRNGD_EINVAL, "b0 must be 0 (x2 fills its draw width, R5)");
+    if (p->b == 0 || p->b > 0xFFFFFFFFull || ((p->b + 1) & p->b) != 0)
+        return fail(PRNGD_EINVAL, "b + 1 must be a power of two <= 2^32 (R5), got b=%llu",
+                    (unsigned long long)p->b);
+    if (p->b >= (1ull << w))
+        return fail(PRNGD_EINVAL, "need b < 2^w so that k*(b - b0) < 1 (b=%llu, w=%u)",
+                    (unsigned long long)p->b, w);
+    if (p->n_streams == 0 || p->n_per_stream == 0)
+        return fail(PRNGD_EINVAL, "n_streams and n_per_stream must be >= 1");
+    if (p->n_per_stream >= (1ull << 32))
+        return fail(PRNGD_EINVAL, "n_per_stream must be < 2^32");
+    if (p->n_streams > (1ull << 62) / p->n_per_stream)
+        return fail(PRNGD_EINVAL, "n_streams * n_per_stream overflows (limit 2^62)");
+    if (p->stream_begin > ~0ull - p->n_streams)
+        return fail(PRNGD_EINVAL, "stream_begin + n_streams overflows 64 bits");
+    const uint32_t known = PRNGD_FLAG_IEEE_DIV | PRNGD_FLAG_NO_TMA | PRNGD_FLAG_ALG1;
+    if (p->flags & ~known) return fail(PRNGD_EUNSUPPORTED, "unknown flag bits 0x%x", p->flags & ~known);
+
+    prngd_handle *h = new (std::nothrow) prngd_handle();
+    if (!h) return fail(PRNGD_ENOMEM, "host allocation of the handle failed");
+    h->p = *p;
+
+    // Eq.(3)/(4) constants in IEEE binary64 round-to-nearest, one rounding per operation (R7).
+    const double k = std::ldexp(1.0, -(int)w);
+    volatile double kb = k * (double)p->b;            // volatile: no contraction / reassociation
+    const double C = (double)p->a0 + kb;               // a0 + k*b          (Eq.(3))
+    volatile double kbb = k * ((double)p->b - (double)p->b0);
+    const double D = ((double)p->a - (double)p->a0) - kbb;  // a - a0 - k(b-b0) (Eq.(4))
+    prngd_info &I = h->info;
+    I.C = C;
+    I.D = D;
+    I.C_s = std::ldexp(C, (int)w);                     // exact power-of-two scaling (R10)
+    I.D_s = std::ldexp(D, (int)w);
+    I.y = 1.0 / I.D_s;                                 // RN(1/D_s)
+    I.sh1 = 32u - (uint32_t)bit_length(p->a);
+    I.sh2 = 32u - (uint32_t)bit_length(p->b);
+    // R11: the map is monotone, so the largest accepted pair (a-1, b) bounds every output.
+    {
+        const uint64_t v = ((p->a - 1) << w) | p->b;
+        volatile double n = (double)v - I.C_s;
+        const double qmax = n / I.D_s;
+        I.clamp = qmax >= 1.0 ? 1u : 0u;
+    }
+    // Rejection probability per attempt: (draw values outside (a0, a)) / 2^bitlen(a).
+    const double width = std::ldexp(1.0, bit_length(p->a));
+    const double p_rej = (width - (double)(p->a - p->a0 - 1)) / width;
+    // Speculate when a 512-pair warp batch is rejection-free with probability > 99%.
+    const bool alg1 = (p->flags & PRNGD_FLAG_ALG1) != 0;
+    I.speculative = (!alg1 && p_rej * 512.0 < 0.01) ? 1u : 0u;
+    I.n_outputs = p->n_streams * p->n_per_stream;
+    I.out_bytes = I.n_outputs * 8u;
+
+    GenArgs &g = h->args;
+    std::memset(&g, 0, sizeof(g));
+    g.seed = p->seed;
+    g.stream_begin = p->stream_begin;
+    g.n_streams = p->n_streams;
+    g.nps = p->n_per_stream;
+    g.Cs = I.C_s;
+    g.Ds = I.D_s;
+    g.y = I.y;
+    g.w = w;
+    g.sh1 = I.sh1;
+    g.sh2 = I.sh2;
+    g.lo = (uint32_t)(p->a0 + 1);
+    g.span = (uint32_t)(p->a - p->a0 - 1);
+
+    Plan &pl = h->plan;
+    pl.spec = I.speculative != 0;
+    pl.clamp = I.clamp != 0;
+    pl.ieee_div = (p->flags & PRNGD_FLAG_IEEE_DIV) != 0;
+    pl.alg1 = alg1;
+    pl.store = (p->flags & PRNGD_FLAG_NO_TMA) ? Store::STG16 : Store::TMA;
+    *out = h;
+    return PRNGD_OK;
+}
+
+prngd_status prngd_destroy(prngd_handle *h) {
+    if (!h) return PRNGD_OK;
+    if (h->scratch_dev >= 0) {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        cudaSetDevice(h->scratch_dev);
+        if (h->cons_scratch) cudaFree(h->cons_scratch);
+        for (int i = 0; i < 2; ++i) {
+            if (h->stage[i]) cudaFree(h->stage[i]);
+            if (h->ev_gen[i]) cudaEventDestroy(h->ev_gen[i]);
+            if (h->ev_copy[i]) cudaEventDestroy(h->ev_copy[i]);
+        }
+        if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+        if (cur >= 0) cudaSetDevice(cur);
+    }
+    delete h;
+    return PRNGD_OK;
+}
+
+prngd_status prngd_get_info(const prngd_handle *h, prngd_info *info) {
+    if (!h || !info) return fail(PRNGD_EINVAL, "null argument");
+    *info = h->info;
+    return PRNGD_OK;
+}
+
+uint32_t prngd_last_launches(const prngd_handle *h) { return h ? h->last_launches.load() : 0u; }
+
+static Plan plan_for(const prngd_handle *h, const void *out) {
+    Plan pl = h->plan;
+    const bool a16 = ((uintptr_t)out & 15u) == 0 && (h->p.n_per_stream & 1u) == 0;
+    const bool tma_ok = a16 && h->p.n_streams < (1ull << 31) && h->p.n_per_stream < (1ull << 31);
+    if (pl.store == Store::TMA && !tma_ok) pl.store = a16 ? Store::STG16 : Store::STG8;
+    if (pl.store == Store::STG16 && !a16) pl.store = Store::STG8;
+    return pl;
+}
+
+prngd_status prngd_generate(const prngd_handle *h, double *d_out, void *cuda_stream) {
+    if (!h || !d_out) return fail(PRNGD_EINVAL, "null handle or output pointer");
+    if ((uintptr_t)d_out & 7u) return fail(PRNGD_EINVAL, "d_out must be 8-byte aligned");
+    int sms = 0;
+    prngd_status s = device_ready(&sms);
+    if (s != PRNGD_OK) return s;
+    GenArgs g = h->args;
+    g.out = d_out;
+    cudaError_t e = prngd::launch_generate(g, plan_for(h, d_out), (cudaStream_t)cuda_stream, sms);
+    if (e != cudaSuccess) return cuda_fail(e, "generate kernel launch");
+    h->last_launches.store(1);
+    return PRNGD_OK;
+}
+
+static prngd_status ensure_device_scratch(prngd_handle *h) {
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (h->scratch_dev >= 0 && h->scratch_dev != dev)
+        return fail(PRNGD_EINVAL, "handle scratch lives on device %d, current device is %d",
+                    h->scratch_dev, dev);
+    h->scratch_dev = dev;
+    return PRNGD_OK;
+}
+
+prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64_t *d_hist,
+                                    double *d_pow, int64_t *d_count, void *cuda_stream) {
+    if (!hc || !d_hist || !d_pow || !d_count)
+        return fail(PRNGD_EINVAL, "null handle or accumulator pointer");
+    if (((uintptr_t)d_hist | (uintptr_t)d_pow | (uintptr_t)d_count) & 7u)
+        return fail(PRNGD_EINVAL, "accumulators must be 8-byte aligned");
+    if (d_out && ((uintptr_t)d_out & 7u)) return fail(PRNGD_EINVAL, "d_out must be 8-byte aligned");
+    int sms = 0;
+    prngd_status s = device_ready(&sms);
+    if (s != PRNGD_OK) return s;
+    prngd_handle *h = const_cast<prngd_handle *>(hc);  // scratch is internal, behind the mutex
+    std::lock_guard<std::mutex> lock(h->mu);
+    if ((s = ensure_device_scratch(h)) != PRNGD_OK) return s;
+    const size_t need = prngd::consume_scratch_bytes(sms);
+    if (h->cons_bytes < need) {
+        if (h->cons_scratch) cudaFree(h->cons_scratch);
+        h->cons_scratch = nullptr;
+        h->cons_bytes = 0;
+        cudaError_t e = cudaMalloc(&h->cons_scratch, need);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(PRNGD_ENOMEM, "consume scratch (%zu bytes): %s", need, cudaGetErrorString(e));
+        }
+        e = cudaMemset(h->cons_scratch, 0, need);  // the spill array must start at zero
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemset scratch");
+        h->cons_bytes = need;
+    }
+    int launches = 0;
+    cudaError_t e = prngd::launch_generate_consume(h->args, plan_for(h, d_out), d_out, d_hist,
+                                                   d_pow, d_count, h->cons_scratch,
+                                                   h->cons_bytes, (cudaStream_t)cuda_stream, sms,
+                                                   &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "generate_consume launch");
+    h->last_launches.store((uint32_t)launches);
+    return PRNGD_OK;
+}
+
+prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stream) {
+    if (!h || !h_out) return fail(PRNGD_EINVAL, "null handle or host pointer");
+    int sms = 0;
+    prngd_status s = device_ready(&sms);
+    if (s != PRNGD_OK) return s;
+    std::lock_guard<std::mutex> lock(h->mu);
+    if ((s = ensure_device_scratch(h)) != PRNGD_OK) return s;
+    const uint64_t nps = h->p.n_per_stream;
+    const uint64_t row_bytes = nps * 8u;
+    const uint64_t target = 256ull << 20;  // 256 MiB per chunk, two chunks in flight
+    uint64_t rows = target / row_bytes;
+    if (rows < 1) rows = 1;
+    rows = (rows + 31) / 32 * 32;          // whole warp tasks
+    if (rows > h->p.n_streams) rows = h->p.n_streams;
+    cudaError_t e;
+    if (h->stage_rows < rows) {
+        for (int i = 0; i < 2; ++i) {
+            if (h->stage[i]) cudaFree(h->stage[i]);
+            h->stage[i] = nullptr;
+        }
+        h->stage_rows = 0;
+        for (int i = 0; i < 2; ++i) {
+            e = cudaMalloc(&h->stage[i], rows * row_bytes);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return fail(PRNGD_ENOMEM, "staging buffer (%llu bytes): %s",
+                            (unsigned long long)(rows * row_bytes), cudaGetErrorString(e));
+            }
+        }
+        h->stage_rows = rows;
+    }
+    if (!h->copy_stream) {
+        if ((e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "cudaStreamCreate");
+        for (int i = 0; i < 2; ++i) {
+            if ((e = cudaEventCreateWithFlags(&h->ev_gen[i], cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&h->ev_copy[i], cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(e, "cudaEventCreate");
+        }
+    }
+    cudaStream_t gs = (cudaStream_t)cuda_stream;
+    uint32_t launches = 0;
+    bool used[2] = {false, false};
+    for (uint64_t r0 = 0, c = 0; r0 < h->p.n_streams; r0 += rows, ++c) {
+        const int b = (int)(c & 1u);
+        const uint64_t nr = (h->p.n_streams - r0) < rows ? (h->p.n_streams - r0) : rows;
+        if (used[b] && (e = cudaStreamWaitEvent(gs, h->ev_copy[b], 0)) != cudaSuccess)
+            return cuda_fail(e, "cudaStreamWaitEvent");
+        GenArgs g = h->args;
+        g.stream_begin = h->p.stream_begin + r0;
+        g.n_streams = nr;
+        g.out = h->stage[b];
+        if ((e = prngd::launch_generate(g, plan_for(h, h->stage[b]), gs, sms)) != cudaSuccess)
+            return cuda_fail(e, "generate kernel launch");
+        ++launches;
+        if ((e = cudaEventRecord(h->ev_gen[b], gs)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+        if ((e = cudaStreamWaitEvent(h->copy_stream, h->ev_gen[b], 0)) != cudaSuccess)
+            return cuda_fail(e, "cudaStreamWaitEvent");
+        if ((e = cudaMemcpyAsync(h_out + r0 * nps, h->stage[b], nr * row_bytes,
+                                 cudaMemcpyDeviceToHost, h->copy_stream)) != cudaSuccess)
+            return cuda_fail(e, "cudaMemcpyAsync D2H");
+        if ((e = cudaEventRecord(h->ev_copy[b], h->copy_stream)) != cudaSuccess)
+            return cuda_fail(e, "cudaEventRecord");
+        used[b] = true;
+    }
+    if ((e = cudaStreamSynchronize(h->copy_stream)) != cudaSuccess)
+        return cuda_fail(e, "device->host pipeline");
+    h->last_launches.store(launches);
+    return PRNGD_OK;
+}
+
+prngd_status prngd_debug_raw(const prngd_handle *h, uint32_t *d_raw, uint64_t draws,
+                             void *cuda_stream) {
+    if (!h || !d_raw || draws == 0) return fail(PRNGD_EINVAL, "null argument or zero draws");
+    int sms = 0;
+    prngd_status s = device_ready(&sms);
+    if (s != PRNGD_OK) return s;
+    cudaError_t e = prngd::launch_debug_raw(h->args, d_raw, draws, (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "debug_raw launch");
+    h->last_launches.store(1);
+    return PRNGD_OK;
+}
+
+prngd_status prngd_debug_pairs(const prngd_handle *h, uint32_t *d_pair_index,
+                               uint64_t *d_pairs_consumed, void *cuda_stream) {
+    if (!h) return fail(PRNGD_EINVAL, "null handle");
+    int sms = 0;
+    prngd_status s = device_ready(&sms);
+    if (s != PRNGD_OK) return s;
+    cudaError_t e = prngd::launch_debug_pairs(h->args, h->plan, d_pair_index, d_pairs_consumed,
+                                              (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "debug_pairs launch");
+    h->last_launches.store(1);
+    return PRNGD_OK;
+}
+
+prngd_status prngd_debug_map(const prngd_handle *h, const uint32_t *d_x1, const uint32_t *d_x2,
+                             double *d_z, uint64_t n, void *cuda_stream) {
+    if (!h) return fail(PRNGD_EINVAL, "null handle");
+    if (n && (!d_x1 || !d_x2 || !d_z)) return fail(PRNGD_EINVAL, "null array");
+    int sms = 0;
+    prngd_status s = device_ready(&sms);
+    if (s != PRNGD_OK) return s;
+    cudaError_t e = prngd::launch_debug_map(h->args, h->plan, d_x1, d_x2, d_z, n,
+                                            (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "debug_map launch");
+    h->last_launches.store(n ? 1 : 0);
+    return PRNGD_OK;
+}
+
+prngd_status prngd_debug_div_check(const prngd_handle *h, uint64_t n, uint64_t seed,
+                                   unsigned long long *d_mismatch, void *cuda_stream) {
+    if (!h || !d_mismatch) return fail(PRNGD_EINVAL, "null argument");
+    int sms = 0;
+    prngd_status s = device_ready(&sms);
+    if (s != PRNGD_OK) return s;
+    cudaError_t e = prngd::launch_debug_div_check(h->args, n, seed, d_mismatch,
+                                                  (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "debug_div_check launch");
+    h->last_launches.store(n ? 1 : 0);
+    return PRNGD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,54 @@
+// prngd_internal.h -- structures shared by the host runtime (prngd_host.cpp) and the sm_100a
+// kernels (prngd_kernels.cu).  Product code only; nothing here is shared with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/prngd.h"
+
+namespace prngd {
+
+// Everything a generator kernel needs, by value in the kernel parameter bank.
+struct GenArgs {
+    uint64_t seed;          // SplitMix64 seed (R6)
+    uint64_t stream_begin;  // global id of row 0
+    uint64_t n_streams;     // rows
+    uint64_t nps;           // n_per_stream, columns
+    double *out;            // row-major [n_streams][nps]; may be null in consume-only mode
+    double Cs, Ds, y;       // C*2^w, D*2^w, RN(1/D_s)   (R10)
+    uint32_t w;             // composition shift, v = (x1 << w) | x2
+    uint32_t sh1, sh2;      // draw widths, x = u >> sh (R4)
+    uint32_t lo, span;      // accept iff (x1 - lo) < span  <=>  a0 < x1 < a   (R3)
+    // consumer (S7)
+    uint32_t *hist_slab;    // [gridDim.x][32768] packed u16 pairs (consume kernels only)
+    int64_t *hist_spill;    // [65536] int64 carries of the packed counters
+    double *pow_slab;       // [gridDim.x][4]
+};
+
+enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2 };
+
+// Launch descriptors chosen by the host.
+struct Plan {
+    bool spec;      // speculative batch acceptance (rare rejection)
+    bool clamp;     // R11 clamp needed
+    bool ieee_div;  // PRNGD_FLAG_IEEE_DIV
+    bool alg1;      // PRNGD_FLAG_ALG1
+    Store store;
+};
+
+// Launchers (prngd_kernels.cu).  They return cudaGetLastError() of the launch.
+cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, int num_sms);
+cudaError_t launch_generate_consume(const GenArgs &g, const Plan &pl, double *d_out,
+                                    int64_t *d_hist, double *d_pow, int64_t *d_count,
+                                    void *scratch, size_t scratch_bytes, cudaStream_t st,
+                                    int num_sms, int *launches);
+size_t consume_scratch_bytes(int num_sms);
+cudaError_t launch_debug_raw(const GenArgs &g, uint32_t *d_raw, uint64_t draws, cudaStream_t st);
+cudaError_t launch_debug_pairs(const GenArgs &g, const Plan &pl, uint32_t *d_pidx,
+                               uint64_t *d_consumed, cudaStream_t st);
+cudaError_t launch_debug_map(const GenArgs &g, const Plan &pl, const uint32_t *x1,
+                             const uint32_t *x2, double *z, uint64_t n, cudaStream_t st);
+cudaError_t launch_debug_div_check(const GenArgs &g, uint64_t n, uint64_t seed,
+                                   unsigned long long *mismatch, cudaStream_t st);
+
+}  // namespace prngd

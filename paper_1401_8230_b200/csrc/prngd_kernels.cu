@@ -1,0 +1,610 @@
+// prngd_kernels.cu -- sm_100a kernels of the PRNGD hot path.
+//
+// Work decomposition: one warp owns 32 consecutive streams (rows of the [n_streams][nps]
+// output), one stream per lane; the xorshift128 state lives in 4 registers for the whole
+// stream.  A lane produces its stream's outputs in batches of kCols = 16 doubles (128 bytes,
+// one full cache line of its row).  The warp stages a 32 x 16 double tile in shared memory
+// (128B-swizzled so the per-lane 16-byte writes are bank-conflict-free) and writes it out
+// either with one TMA tensor store (cp.async.bulk.tensor.2d; the hardware clips the ragged
+// row/column tails) or with warp-coalesced 16-byte st.global (8 lanes per 128-byte row).
+// Rejection is handled per lane; with rare rejection (w = 32) the batch is computed
+// speculatively and recomputed exactly if any lane of the warp drew a rejected x1, so the
+// common path has no per-output branch.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "prngd_device.cuh"
+#include "prngd_internal.h"
+
+namespace prngd {
+
+constexpr int kCols = 16;                   // outputs per lane per batch (128 B of its row)
+constexpr int kTileBytes = 32 * kCols * 8;  // 4 KiB per warp tile
+constexpr int kNBuf = 2;                    // tiles per warp (double buffering)
+constexpr int kGenWarps = 4;                // warps per CTA, generate kernel
+constexpr int kConsWarpsWrite = 12;         // warps per CTA, consume kernel writing outputs
+constexpr int kConsWarpsNoWrite = 24;       // warps per CTA, consume-only kernel (<= 85 regs)
+constexpr int kHistWords = 32768;           // 65536 u16 counters packed in pairs (128 KiB)
+
+// ------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, uint32_t smem, int col,
+                                             int row) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+        "r"(smem), "r"(col), "r"(row)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void sts_v2(uint32_t addr, double a, double b) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
+}
+__device__ __forceinline__ void sts_f64(uint32_t addr, double a) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(a) : "memory");
+}
+__device__ __forceinline__ void lds_v2(uint32_t addr, double &a, double &b) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void stg_v2_cs(double *p, double a, double b) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+// Byte offset of element pair `chunk` (16 bytes) of row `row` in a 32 x 16 double tile, in the
+// TMA SWIZZLE_128B layout: chunk c of row r lives at chunk c ^ (r & 7).  Tiles are 1 KiB aligned.
+__device__ __forceinline__ uint32_t tile_off(uint32_t row, uint32_t chunk) {
+    return row * 128u + ((chunk ^ (row & 7u)) << 4);
+}
+
+// ------------------------------------------------------------------------------ consumer (S7)
+struct Consumer {
+    double s1, s2, s3, s4;
+    uint32_t *hist;   // shared: 32768 words, counter of bin b in half (b & 1) of word b >> 1
+    int64_t *spill;   // global: carries of the packed counters, [65536]
+    __device__ __forceinline__ void init(uint32_t *h, int64_t *sp) {
+        s1 = s2 = s3 = s4 = 0.0;
+        hist = h;
+        spill = sp;
+    }
+    // R16 for one output.  A word holds L + 65536*H (mod 2^32) exactly, as a sum of commutative
+    // increments.  The one thread whose atomicAdd carries the low field out (old low == 0xFFFF)
+    // or the word out of 32 bits (old + inc >= 2^32) records the carry in `spill`, which the
+    // finalize kernel adds back: L = low + 65536*cL, H = high + 65536*cW - cL.
+    __device__ __forceinline__ void add(double q) {
+        const double z2 = __dmul_rn(q, q);
+        s1 = __dadd_rn(s1, q);
+        s2 = __dadd_rn(s2, z2);
+        s3 = __dadd_rn(s3, __dmul_rn(z2, q));
+        s4 = __dadd_rn(s4, __dmul_rn(z2, z2));
+        const uint32_t bin = bin16(q);
+        const uint32_t inc = (bin & 1u) ? 0x10000u : 1u;
+        const uint32_t old = atomicAdd(&hist[bin >> 1], inc);
+        const bool carry_lo = (inc == 1u) && ((old & 0xFFFFu) == 0xFFFFu);
+        const bool carry_word = old > 0xFFFFFFFFu - inc;
+        if (__builtin_expect(carry_lo || carry_word, 0)) {
+            unsigned long long *sp = reinterpret_cast<unsigned long long *>(spill);
+            if (carry_lo) {
+                atomicAdd(&sp[bin], 65536ull);
+                atomicAdd(&sp[bin | 1u], 0xFFFFFFFFFFFFFFFFull);  // -1
+            }
+            if (carry_word) atomicAdd(&sp[bin | 1u], 65536ull);
+        }
+    }
+};
+
+struct NoConsumer {
+    __device__ __forceinline__ void init(uint32_t *, int64_t *) {}
+    __device__ __forceinline__ void add(double) {}
+};
+
+// ------------------------------------------------------------------------------ one batch
+// kCols outputs of this lane's stream into row `lane` of the tile at smem address `tile`.
+template <bool FULL32, bool SPEC, bool IEEE, bool ALG1>
+__device__ __forceinline__ void produce_batch(Xs128 &st, uint32_t tile, uint32_t lane,
+                                              const GenArgs &g) {
+    const uint32_t sh1 = FULL32 ? 0u : g.sh1;
+    const uint32_t sh2 = FULL32 ? 0u : g.sh2;
+    const uint32_t w = FULL32 ? 32u : g.w;
+    const uint32_t lo = FULL32 ? 1u : g.lo;
+    const uint32_t span = FULL32 ? 0xFFFFFFFEu : g.span;
+    bool done = false;
+    if (SPEC) {
+        // Speculative: compute the batch as if every x1 were accepted; one warp vote at the end.
+        const Xs128 saved = st;
+        bool rej = false;
+#pragma unroll
+        for (int c = 0; c < kCols / 2; ++c) {
+            const uint32_t a1 = draw(st) >> sh1;
+            const uint32_t a2 = draw(st) >> sh2;
+            const uint32_t b1 = draw(st) >> sh1;
+            const uint32_t b2 = draw(st) >> sh2;
+            rej |= !accepted(a1, lo, span);
+            rej |= !accepted(b1, lo, span);
+            sts_v2(tile + tile_off(lane, c), eq4_pair<IEEE, true>(a1, a2, w, g.Cs, g.Ds, g.y),
+                   eq4_pair<IEEE, true>(b1, b2, w, g.Cs, g.Ds, g.y));
+        }
+        done = !__any_sync(0xFFFFFFFFu, rej);
+        if (!done) st = saved;
+    }
+    if (!done) {
+#pragma unroll 1
+        for (int i = 0; i < kCols; ++i) {
+            uint32_t x1, x2;
+            if (ALG1) {  // NEXT-2: Alg. 1 redraws x1 alone, then draws x2
+                do {
+                    x1 = draw(st) >> sh1;
+                } while (!accepted(x1, lo, span));
+                x2 = draw(st) >> sh2;
+            } else {     // R2: a rejected x1 drops its whole pair
+                do {
+                    x1 = draw(st) >> sh1;
+                    x2 = draw(st) >> sh2;
+                } while (!accepted(x1, lo, span));
+            }
+            sts_f64(tile + tile_off(lane, (uint32_t)i >> 1) + ((uint32_t)i & 1u) * 8u,
+                    eq4_pair<IEEE, true>(x1, x2, w, g.Cs, g.Ds, g.y));
+        }
+    }
+}
+
+// Warp-coalesced flush of a 32 x 16 tile.  VEC16: 8 lanes per 128-byte row, 4 rows per
+// instruction (needs a 16-byte aligned output and even nps); else 16 lanes x 8 bytes per row.
+template <bool VEC16>
+__device__ __forceinline__ void flush_stg(uint32_t tile, uint32_t lane, const GenArgs &g,
+                                          uint64_t row0, uint64_t col0) {
+    if (VEC16) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t r = k * 4 + (lane >> 3), c = lane & 7u;
+            double a, b;
+            lds_v2(tile + tile_off(r, c), a, b);
+            const uint64_t row = row0 + r, col = col0 + 2 * c;
+            if (row < g.n_streams && col < g.nps) stg_v2_cs(g.out + row * g.nps + col, a, b);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t r = k * 2 + (lane >> 4), e = lane & 15u;
+            double a, b;
+            lds_v2(tile + tile_off(r, e >> 1), a, b);
+            const uint64_t row = row0 + r, col = col0 + e;
+            if (row < g.n_streams && col < g.nps) g.out[row * g.nps + col] = (e & 1u) ? b : a;
+        }
+    }
+}
+
+// One warp-task: streams [row0, row0 + 32), all nps columns.  `it` counts batches issued by
+// this warp (tile ring position).
+template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE, bool CONSUME,
+          class Cons>
+__device__ __forceinline__ void run_rows(const CUtensorMap *tmap, const GenArgs &g,
+                                         uint32_t tiles, uint32_t lane, uint64_t row0,
+                                         Cons &cons, uint32_t &it) {
+    Xs128 st = stream_start(g.seed, g.stream_begin + row0 + lane);
+    const bool live = (row0 + lane) < g.n_streams;  // ragged last warp: extra lanes not counted
+#pragma unroll 1
+    for (uint64_t col0 = 0; col0 < g.nps; col0 += kCols, ++it) {
+        const uint32_t tile = tiles + (it % kNBuf) * kTileBytes;
+        if (WRITE && ST == Store::TMA) {
+            if (lane == 0) bulk_wait_read<kNBuf - 1>();  // this tile's previous store read smem
+            __syncwarp();
+        }
+        produce_batch<FULL32, SPEC, IEEE, ALG1>(st, tile, lane, g);
+        if (CONSUME && live) {
+            // Outputs past nps in the last batch are computed but neither stored nor counted.
+            const uint32_t valid = (g.nps - col0) >= kCols ? kCols : (uint32_t)(g.nps - col0);
+            if (valid == kCols) {
+#pragma unroll
+                for (int c = 0; c < kCols / 2; ++c) {
+                    double a, b;
+                    lds_v2(tile + tile_off(lane, c), a, b);
+                    cons.add(a);
+                    cons.add(b);
+                }
+            } else {
+                for (uint32_t e = 0; e < valid; ++e) {
+                    double a, b;
+                    lds_v2(tile + tile_off(lane, e >> 1), a, b);
+                    cons.add((e & 1u) ? b : a);
+                }
+            }
+        }
+        if (WRITE) {
+            if (ST == Store::TMA) {
+                fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(tmap, tile, (int)col0, (int)row0);
+                    bulk_commit();
+                }
+            } else {
+                __syncwarp();
+                flush_stg<ST == Store::STG16>(tile, lane, g, row0, col0);
+                __syncwarp();  // tile reads done before the ring comes back to it
+            }
+        } else {
+            __syncwarp();
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t aligned_smem_base(uint8_t *raw) {
+    return (smem_u32(raw) + 1023u) & ~1023u;
+}
+
+// ------------------------------------------------------------------------------ kernels
+// S1-S6.  Grid: one warp per 32 streams, kGenWarps warps per CTA.
+template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST>
+__global__ void __launch_bounds__(kGenWarps * 32)
+    gen_kernel(const __grid_constant__ CUtensorMap tmap, const GenArgs g) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t tiles = aligned_smem_base(smem_raw) + warp * (kNBuf * kTileBytes);
+    const uint64_t row0 = ((uint64_t)blockIdx.x * kGenWarps + warp) * 32u;
+    if (row0 >= g.n_streams) return;
+    uint32_t it = 0;
+    NoConsumer nc;
+    run_rows<FULL32, SPEC, IEEE, ALG1, ST, true, false>(&tmap, g, tiles, lane, row0, nc, it);
+    if (ST == Store::TMA && lane == 0) bulk_wait_all();
+}
+
+// S1-S7, persistent: one CTA per SM owning a 128 KiB packed histogram; warps take 32-stream
+// tasks round-robin.  Writes per-CTA slabs that finalize_kernel reduces.
+template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE>
+__global__ void __launch_bounds__((WRITE ? kConsWarpsWrite : kConsWarpsNoWrite) * 32, 1)
+    consume_kernel(const __grid_constant__ CUtensorMap tmap, const GenArgs g) {
+    constexpr int kWarps = WRITE ? kConsWarpsWrite : kConsWarpsNoWrite;
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ double red[kWarps][4];
+    const uint32_t base = aligned_smem_base(smem_raw);
+    uint32_t *hist = reinterpret_cast<uint32_t *>(smem_raw + (base - smem_u32(smem_raw)));
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t tiles = base + kHistWords * 4u + warp * (kNBuf * kTileBytes);
+    for (uint32_t i = threadIdx.x; i < kHistWords; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    Consumer cons;
+    cons.init(hist, g.hist_spill);
+    uint32_t it = 0;
+    const uint64_t n_tasks = (g.n_streams + 31u) / 32u;
+#pragma unroll 1
+    for (uint64_t t = (uint64_t)blockIdx.x * kWarps + warp; t < n_tasks;
+         t += (uint64_t)gridDim.x * kWarps) {
+        run_rows<FULL32, SPEC, IEEE, ALG1, ST, WRITE, true>(&tmap, g, tiles, lane, t * 32u, cons,
+                                                             it);
+    }
+    if (WRITE && ST == Store::TMA && lane == 0) bulk_wait_all();
+    // moments: warp tree, then per-CTA in warp order (deterministic for a fixed grid)
+    double s[4] = {cons.s1, cons.s2, cons.s3, cons.s4};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        for (int o = 16; o > 0; o >>= 1) s[k] = __dadd_rn(s[k], __shfl_xor_sync(~0u, s[k], o));
+    if (lane == 0)
+        for (int k = 0; k < 4; ++k) red[warp][k] = s[k];
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double acc = 0.0;
+        for (int wi = 0; wi < kWarps; ++wi) acc = __dadd_rn(acc, red[wi][threadIdx.x]);
+        g.pow_slab[blockIdx.x * 4 + threadIdx.x] = acc;
+    }
+    uint4 *dst = reinterpret_cast<uint4 *>(g.hist_slab + (size_t)blockIdx.x * kHistWords);
+    const uint4 *src = reinterpret_cast<const uint4 *>(hist);
+    for (uint32_t i = threadIdx.x; i < kHistWords / 4; i += blockDim.x) dst[i] = src[i];
+}
+
+// Reduce the per-CTA slabs into the caller's accumulators; resets the spill array to zero.
+__global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int n_slabs,
+                                                       int64_t *spill, const double *pow_slab,
+                                                       int64_t *d_hist, double *d_pow,
+                                                       int64_t *d_count) {
+    __shared__ long long part[8];
+    long long local = 0;
+    for (uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x; wi < kHistWords;
+         wi += gridDim.x * blockDim.x) {
+        long long lo = 0, hi = 0;
+        for (int s = 0; s < n_slabs; ++s) {
+            const uint32_t v = slab[(size_t)s * kHistWords + wi];
+            lo += v & 0xFFFFu;
+            hi += v >> 16;
+        }
+        lo += spill[2 * wi];
+        hi += spill[2 * wi + 1];
+        spill[2 * wi] = 0;
+        spill[2 * wi + 1] = 0;
+        d_hist[2 * wi] += lo;
+        d_hist[2 * wi + 1] += hi;
+        local += lo + hi;
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(~0u, local, o);
+    if ((threadIdx.x & 31u) == 0) part[threadIdx.x >> 5] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
+        atomicAdd(reinterpret_cast<unsigned long long *>(d_count), (unsigned long long)t);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 4) {
+        double acc = 0.0;
+        for (int s = 0; s < n_slabs; ++s) acc = __dadd_rn(acc, pow_slab[s * 4 + threadIdx.x]);
+        d_pow[threadIdx.x] = __dadd_rn(d_pow[threadIdx.x], acc);
+    }
+}
+
+// ------------------------------------------------------------------------------ debug kernels
+__global__ void debug_raw_kernel(const GenArgs g, uint32_t *raw, uint64_t draws) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n_streams) return;
+    Xs128 st = stream_start(g.seed, g.stream_begin + i);
+    for (uint64_t d = 0; d < draws; ++d) raw[i * draws + d] = draw(st);
+}
+
+template <bool ALG1>
+__global__ void debug_pairs_kernel(const GenArgs g, uint32_t *pidx, uint64_t *consumed) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n_streams) return;
+    Xs128 st = stream_start(g.seed, g.stream_begin + i);
+    uint64_t p = 0;  // draws (ALG1) or pairs (R2) consumed
+    for (uint64_t j = 0; j < g.nps; ++j) {
+        uint32_t x1;
+        if (ALG1) {
+            do {
+                x1 = draw(st) >> g.sh1;
+                ++p;
+            } while (!accepted(x1, g.lo, g.span));
+            draw(st);
+            ++p;
+            if (pidx) pidx[i * g.nps + j] = (uint32_t)(p - 2);  // index of the accepted x1 draw
+        } else {
+            do {
+                x1 = draw(st) >> g.sh1;
+                draw(st);
+                ++p;
+            } while (!accepted(x1, g.lo, g.span));
+            if (pidx) pidx[i * g.nps + j] = (uint32_t)(p - 1);
+        }
+    }
+    if (consumed) consumed[i] = p;
+}
+
+template <bool IEEE>
+__global__ void debug_map_kernel(const GenArgs g, const uint32_t *x1, const uint32_t *x2,
+                                 double *z, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        z[i] = eq4_pair<IEEE, true>(x1[i], x2[i], g.w, g.Cs, g.Ds, g.y);
+}
+
+__global__ void debug_div_check_kernel(const GenArgs g, uint64_t n, uint64_t seed,
+                                       unsigned long long *mismatch) {
+    unsigned long long bad = 0;
+    const uint32_t m1 = g.sh1 >= 32 ? 0u : (0xFFFFFFFFu >> g.sh1);
+    const uint32_t m2 = g.sh2 >= 32 ? 0u : (0xFFFFFFFFu >> g.sh2);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = splitmix_finalize(seed + (i + 1) * kGamma);
+        uint32_t x1 = (uint32_t)h & m1, x2 = (uint32_t)(h >> 32) & m2;
+        // a quarter of the samples hug the top and bottom of x1 (where R11 and tiny q live)
+        if ((i & 3u) == 1u) x1 = m1 - (x1 & 7u);
+        if ((i & 3u) == 2u) x1 = x1 & 7u;
+        const uint64_t v = ((uint64_t)x1 << g.w) | (uint64_t)x2;
+        const double fast = eq4_scaled<false, false>(v, g.Cs, g.Ds, g.y);
+        const double ieee = eq4_scaled<true, false>(v, g.Cs, g.Ds, g.y);
+        bad += (__double_as_longlong(fast) != __double_as_longlong(ieee)) ? 1ull : 0ull;
+    }
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(~0u, bad, o);
+    if ((threadIdx.x & 31u) == 0 && bad) atomicAdd(mismatch, bad);
+}
+
+// ------------------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static std::once_flag once;
+    static EncodeTiledFn fn = nullptr;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// Tensor map over out[n_streams][nps] (doubles), box 16 columns x 32 rows, 128B swizzle.
+static cudaError_t make_tmap(CUtensorMap *m, double *out, uint64_t n_streams, uint64_t nps) {
+    std::memset(m, 0, sizeof(*m));
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {nps, n_streams};
+    const cuuint64_t strides[1] = {nps * 8u};
+    const cuuint32_t box[2] = {(cuuint32_t)kCols, 32u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, out, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <class K>
+static cudaError_t set_smem(K kernel, size_t bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST>
+static cudaError_t gen_launch(const CUtensorMap &m, const GenArgs &g, cudaStream_t st) {
+    auto k = gen_kernel<FULL32, SPEC, IEEE, ALG1, ST>;
+    const size_t smem = 1024 + (size_t)kGenWarps * kNBuf * kTileBytes;
+    cudaError_t e = set_smem(k, smem);
+    if (e != cudaSuccess) return e;
+    const uint64_t tasks = (g.n_streams + 31u) / 32u;
+    const uint64_t grid = (tasks + kGenWarps - 1) / kGenWarps;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    k<<<(unsigned)grid, kGenWarps * 32, smem, st>>>(m, g);
+    return cudaGetLastError();
+}
+
+template <Store ST>
+static cudaError_t gen_dispatch_store(const CUtensorMap &m, const GenArgs &g, const Plan &pl,
+                                      bool full32, cudaStream_t st) {
+    if (full32 && pl.spec && !pl.ieee_div && !pl.alg1)
+        return gen_launch<true, true, false, false, ST>(m, g, st);
+    if (pl.alg1)
+        return pl.ieee_div ? gen_launch<false, false, true, true, ST>(m, g, st)
+                           : gen_launch<false, false, false, true, ST>(m, g, st);
+    if (pl.spec)
+        return pl.ieee_div ? gen_launch<false, true, true, false, ST>(m, g, st)
+                           : gen_launch<false, true, false, false, ST>(m, g, st);
+    return pl.ieee_div ? gen_launch<false, false, true, false, ST>(m, g, st)
+                       : gen_launch<false, false, false, false, ST>(m, g, st);
+}
+
+static bool is_full32(const GenArgs &g) {
+    return g.w == 32 && g.sh1 == 0 && g.sh2 == 0 && g.lo == 1u && g.span == 0xFFFFFFFEu;
+}
+
+cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, int) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof(m));
+    Store s = pl.store;
+    if (s == Store::TMA && make_tmap(&m, g.out, g.n_streams, g.nps) != cudaSuccess)
+        s = Store::STG16;  // descriptor refused: fall back to coalesced st.global (same bits)
+    const bool f32 = is_full32(g);
+    switch (s) {
+        case Store::TMA: return gen_dispatch_store<Store::TMA>(m, g, pl, f32, st);
+        case Store::STG16: return gen_dispatch_store<Store::STG16>(m, g, pl, f32, st);
+        default: return gen_dispatch_store<Store::STG8>(m, g, pl, f32, st);
+    }
+}
+
+size_t consume_scratch_bytes(int num_sms) {
+    return (size_t)num_sms * kHistWords * 4u + 65536u * 8u + (size_t)num_sms * 4u * 8u;
+}
+
+template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE>
+static cudaError_t cons_launch(const CUtensorMap &m, const GenArgs &g, int grid,
+                               cudaStream_t st) {
+    constexpr int kWarps = WRITE ? kConsWarpsWrite : kConsWarpsNoWrite;
+    auto k = consume_kernel<FULL32, SPEC, IEEE, ALG1, ST, WRITE>;
+    const size_t smem = 1024 + (size_t)kHistWords * 4u + (WRITE ? (size_t)kWarps * kNBuf * kTileBytes : 0);
+    cudaError_t e = set_smem(k, smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, kWarps * 32, smem, st>>>(m, g);
+    return cudaGetLastError();
+}
+
+template <Store ST, bool WRITE>
+static cudaError_t cons_dispatch(const CUtensorMap &m, const GenArgs &g, const Plan &pl,
+                                 bool full32, int grid, cudaStream_t st) {
+    if (full32 && pl.spec && !pl.ieee_div && !pl.alg1)
+        return cons_launch<true, true, false, false, ST, WRITE>(m, g, grid, st);
+    if (pl.alg1)
+        return pl.ieee_div ? cons_launch<false, false, true, true, ST, WRITE>(m, g, grid, st)
+                           : cons_launch<false, false, false, true, ST, WRITE>(m, g, grid, st);
+    if (pl.spec)
+        return pl.ieee_div ? cons_launch<false, true, true, false, ST, WRITE>(m, g, grid, st)
+                           : cons_launch<false, true, false, false, ST, WRITE>(m, g, grid, st);
+    return pl.ieee_div ? cons_launch<false, false, true, false, ST, WRITE>(m, g, grid, st)
+                       : cons_launch<false, false, false, false, ST, WRITE>(m, g, grid, st);
+}
+
+cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d_out,
+                                    int64_t *d_hist, double *d_pow, int64_t *d_count,
+                                    void *scratch, size_t scratch_bytes, cudaStream_t st,
+                                    int num_sms, int *launches) {
+    *launches = 0;
+    if (scratch_bytes < consume_scratch_bytes(num_sms)) return cudaErrorInvalidValue;
+    GenArgs g = g0;
+    g.out = d_out;
+    uint8_t *sp = static_cast<uint8_t *>(scratch);
+    g.hist_slab = reinterpret_cast<uint32_t *>(sp);
+    g.hist_spill = reinterpret_cast<int64_t *>(sp + (size_t)num_sms * kHistWords * 4u);
+    g.pow_slab = reinterpret_cast<double *>(sp + (size_t)num_sms * kHistWords * 4u + 65536u * 8u);
+    const uint64_t tasks = (g.n_streams + 31u) / 32u;
+    const int kw = d_out ? kConsWarpsWrite : kConsWarpsNoWrite;
+    int grid = num_sms;
+    if ((uint64_t)grid * kw > tasks) grid = (int)((tasks + kw - 1) / kw);
+    if (grid < 1) grid = 1;
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof(m));
+    const bool f32 = is_full32(g);
+    cudaError_t e;
+    if (!d_out) {
+        e = cons_dispatch<Store::STG8, false>(m, g, pl, f32, grid, st);
+    } else {
+        Store s = pl.store;
+        if (s == Store::TMA && make_tmap(&m, d_out, g.n_streams, g.nps) != cudaSuccess)
+            s = Store::STG16;
+        switch (s) {
+            case Store::TMA: e = cons_dispatch<Store::TMA, true>(m, g, pl, f32, grid, st); break;
+            case Store::STG16: e = cons_dispatch<Store::STG16, true>(m, g, pl, f32, grid, st); break;
+            default: e = cons_dispatch<Store::STG8, true>(m, g, pl, f32, grid, st); break;
+        }
+    }
+    if (e != cudaSuccess) return e;
+    *launches = 1;
+    finalize_kernel<<<32, 256, 0, st>>>(g.hist_slab, grid, g.hist_spill, g.pow_slab, d_hist,
+                                         d_pow, d_count);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) *launches = 2;
+    return e;
+}
+
+cudaError_t launch_debug_raw(const GenArgs &g, uint32_t *d_raw, uint64_t draws, cudaStream_t st) {
+    const uint64_t blocks = (g.n_streams + 127) / 128;
+    debug_raw_kernel<<<(unsigned)blocks, 128, 0, st>>>(g, d_raw, draws);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_pairs(const GenArgs &g, const Plan &pl, uint32_t *d_pidx,
+                               uint64_t *d_consumed, cudaStream_t st) {
+    const uint64_t blocks = (g.n_streams + 127) / 128;
+    if (pl.alg1)
+        debug_pairs_kernel<true><<<(unsigned)blocks, 128, 0, st>>>(g, d_pidx, d_consumed);
+    else
+        debug_pairs_kernel<false><<<(unsigned)blocks, 128, 0, st>>>(g, d_pidx, d_consumed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_map(const GenArgs &g, const Plan &pl, const uint32_t *x1,
+                             const uint32_t *x2, double *z, uint64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    if (pl.ieee_div)
+        debug_map_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(g, x1, x2, z, n);
+    else
+        debug_map_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(g, x1, x2, z, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_div_check(const GenArgs &g, uint64_t n, uint64_t seed,
+                                   unsigned long long *mismatch, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    debug_div_check_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, n, seed, mismatch);
+    return cudaGetLastError();
+}
+
+}  // namespace prngd

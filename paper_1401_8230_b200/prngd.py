@@ -1,0 +1,250 @@
+"""Thin ctypes binding of libprngd_b200.so (include/prngd.h).
+
+Argument marshalling only: every step of the PRNGD path runs in the library's sm_100a kernels.
+Functions carry the C names; ``Generator`` is a convenience wrapper over them.  There is no CPU
+fallback: if the library is missing this module raises on import of the library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libprngd_b200.so")
+
+PRNGD_OK, PRNGD_EINVAL, PRNGD_ECUDA, PRNGD_ENOMEM, PRNGD_EUNSUPPORTED = range(5)
+PRNGD_FLAG_IEEE_DIV = 0x1
+PRNGD_FLAG_NO_TMA = 0x2
+PRNGD_FLAG_ALG1 = 0x4
+
+EXPORTS = (
+    "prngd_create", "prngd_destroy", "prngd_get_info", "prngd_generate", "prngd_generate_consume",
+    "prngd_generate_host", "prngd_last_launches", "prngd_status_string", "prngd_last_error",
+    "prngd_abi_version", "prngd_debug_raw", "prngd_debug_pairs", "prngd_debug_map",
+    "prngd_debug_div_check",
+)
+
+
+class prngd_params(C.Structure):
+    _fields_ = [("w", C.c_uint32), ("flags", C.c_uint32), ("a0", C.c_uint64), ("a", C.c_uint64),
+                ("b0", C.c_uint64), ("b", C.c_uint64), ("seed", C.c_uint64),
+                ("stream_begin", C.c_uint64), ("n_streams", C.c_uint64),
+                ("n_per_stream", C.c_uint64)]
+
+
+class prngd_info(C.Structure):
+    _fields_ = [("C", C.c_double), ("D", C.c_double), ("C_s", C.c_double), ("D_s", C.c_double),
+                ("y", C.c_double), ("sh1", C.c_uint32), ("sh2", C.c_uint32),
+                ("clamp", C.c_uint32), ("speculative", C.c_uint32), ("n_outputs", C.c_uint64),
+                ("out_bytes", C.c_uint64)]
+
+
+class PrngdError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{msg} [status {status}]")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load the native library (build it first with paper_1401_8230_b200.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1401_8230_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, u64, u32, st = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int
+        sig = {
+            "prngd_create": (st, [C.POINTER(prngd_params), C.POINTER(vp)]),
+            "prngd_destroy": (st, [vp]),
+            "prngd_get_info": (st, [vp, C.POINTER(prngd_info)]),
+            "prngd_generate": (st, [vp, vp, vp]),
+            "prngd_generate_consume": (st, [vp, vp, vp, vp, vp, vp]),
+            "prngd_generate_host": (st, [vp, vp, vp]),
+            "prngd_last_launches": (u32, [vp]),
+            "prngd_status_string": (C.c_char_p, [st]),
+            "prngd_last_error": (C.c_char_p, []),
+            "prngd_abi_version": (C.c_int, []),
+            "prngd_debug_raw": (st, [vp, vp, u64, vp]),
+            "prngd_debug_pairs": (st, [vp, vp, vp, vp]),
+            "prngd_debug_map": (st, [vp, vp, vp, vp, u64, vp]),
+            "prngd_debug_div_check": (st, [vp, u64, u64, vp, vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != PRNGD_OK:
+        detail = lib().prngd_last_error().decode(errors="replace")
+        name = lib().prngd_status_string(status).decode()
+        raise PrngdError(status, f"{what}: {name}: {detail}")
+
+
+def _ptr(t):
+    """Device/host pointer of a torch tensor or numpy array (None -> NULL)."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    return t.ctypes.data
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+# ---------------------------------------------------------------- C-named entry points
+
+def prngd_create(**kw) -> int:
+    p = prngd_params(**{k: int(v) for k, v in kw.items() if k in dict(prngd_params._fields_)})
+    h = C.c_void_p()
+    _check(lib().prngd_create(C.byref(p), C.byref(h)), "prngd_create")
+    return h.value
+
+
+def prngd_destroy(h: int):
+    _check(lib().prngd_destroy(h), "prngd_destroy")
+
+
+def prngd_get_info(h: int) -> dict:
+    i = prngd_info()
+    _check(lib().prngd_get_info(h, C.byref(i)), "prngd_get_info")
+    return {k: getattr(i, k) for k, _ in prngd_info._fields_}
+
+
+def prngd_generate(h: int, out, stream=None):
+    _check(lib().prngd_generate(h, _ptr(out), _stream_ptr(stream)), "prngd_generate")
+
+
+def prngd_generate_consume(h: int, out, hist, pw, count, stream=None):
+    _check(lib().prngd_generate_consume(h, _ptr(out), _ptr(hist), _ptr(pw), _ptr(count),
+                                        _stream_ptr(stream)), "prngd_generate_consume")
+
+
+def prngd_generate_host(h: int, host_out, stream=None):
+    _check(lib().prngd_generate_host(h, _ptr(host_out), _stream_ptr(stream)),
+           "prngd_generate_host")
+
+
+def prngd_last_launches(h: int) -> int:
+    return int(lib().prngd_last_launches(h))
+
+
+def prngd_debug_raw(h: int, raw, draws_per_stream: int, stream=None):
+    _check(lib().prngd_debug_raw(h, _ptr(raw), draws_per_stream, _stream_ptr(stream)),
+           "prngd_debug_raw")
+
+
+def prngd_debug_pairs(h: int, pair_index, consumed, stream=None):
+    _check(lib().prngd_debug_pairs(h, _ptr(pair_index), _ptr(consumed), _stream_ptr(stream)),
+           "prngd_debug_pairs")
+
+
+def prngd_debug_map(h: int, x1, x2, z, stream=None):
+    n = z.numel() if hasattr(z, "numel") else z.size
+    _check(lib().prngd_debug_map(h, _ptr(x1), _ptr(x2), _ptr(z), n, _stream_ptr(stream)),
+           "prngd_debug_map")
+
+
+def prngd_debug_div_check(h: int, n: int, seed: int, mismatch, stream=None):
+    _check(lib().prngd_debug_div_check(h, n, seed, _ptr(mismatch), _stream_ptr(stream)),
+           "prngd_debug_div_check")
+
+
+# ---------------------------------------------------------------- convenience wrapper
+
+class Generator:
+    """PRNGD(k = 2^-w, [a0;a], [b0;b]) over streams [stream_begin, stream_begin + n_streams)."""
+
+    def __init__(self, w, a0, a, b0, b, seed, n_streams, n_per_stream, stream_begin=0, flags=0,
+                 **_ignored):
+        self.params = dict(w=w, a0=a0, a=a, b0=b0, b=b, seed=seed, n_streams=n_streams,
+                           n_per_stream=n_per_stream, stream_begin=stream_begin, flags=flags)
+        self.handle = prngd_create(**self.params)
+        self.info = prngd_get_info(self.handle)
+
+    @classmethod
+    def from_params(cls, p: dict, **over):
+        q = dict(p)
+        q.update(over)
+        return cls(**q)
+
+    @property
+    def shape(self):
+        return (self.params["n_streams"], self.params["n_per_stream"])
+
+    def generate(self, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty(self.shape, dtype=torch.float64, device="cuda")
+        prngd_generate(self.handle, out, stream)
+        return out
+
+    def generate_consume(self, out=None, hist=None, pw=None, count=None, stream=None):
+        import torch
+        dev = "cuda"
+        hist = torch.zeros(65536, dtype=torch.int64, device=dev) if hist is None else hist
+        pw = torch.zeros(4, dtype=torch.float64, device=dev) if pw is None else pw
+        count = torch.zeros(1, dtype=torch.int64, device=dev) if count is None else count
+        prngd_generate_consume(self.handle, out, hist, pw, count, stream)
+        return out, hist, pw, count
+
+    def generate_host(self, host_out=None, stream=None):
+        import torch
+        if host_out is None:
+            host_out = torch.empty(self.shape, dtype=torch.float64, pin_memory=True)
+        prngd_generate_host(self.handle, host_out, stream)
+        return host_out
+
+    def raw(self, draws_per_stream, stream=None):
+        import torch
+        r = torch.empty((self.params["n_streams"], draws_per_stream), dtype=torch.int32,
+                        device="cuda")
+        prngd_debug_raw(self.handle, r, draws_per_stream, stream)
+        return r
+
+    def pairs(self, stream=None):
+        import torch
+        pidx = torch.empty(self.shape, dtype=torch.int32, device="cuda")
+        cons = torch.empty(self.params["n_streams"], dtype=torch.int64, device="cuda")
+        prngd_debug_pairs(self.handle, pidx, cons, stream)
+        return pidx, cons
+
+    def map(self, x1, x2, stream=None):
+        import torch
+        z = torch.empty(x1.shape, dtype=torch.float64, device="cuda")
+        prngd_debug_map(self.handle, x1, x2, z, stream)
+        return z
+
+    @property
+    def last_launches(self) -> int:
+        return prngd_last_launches(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            prngd_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

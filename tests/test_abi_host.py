@@ -1,0 +1,129 @@
+"""The C-ABI library builds, loads and exports every symbol include/prngd.h declares; host-side
+validation and constants (no GPU needed: prngd_create and prngd_get_info make no CUDA call)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_1401_8230_b200 import build as B
+from paper_1401_8230_b200 import prngd as P
+from paper_1401_8230_b200 import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    return P.lib()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "prngd.h")).read()
+    return sorted(set(re.findall(r"PRNGD_API\s+[\w\s\*]+?\b(prngd_\w+)\s*\(", src)))
+
+
+def test_header_and_binding_agree():
+    assert declared_symbols() == sorted(P.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", B.LIB], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (prngd_\w+)", out))
+    for name in declared_symbols():
+        assert name in exported, name
+        assert getattr(lib, name) is not None
+
+
+def test_library_is_sm100a_only(lib):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", B.LIB],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+def test_abi_version(lib):
+    assert lib.prngd_abi_version() == 1
+
+
+@pytest.mark.parametrize("bad,fragment", [
+    (dict(W.FULL32, w=0), "w=0"),
+    (dict(W.FULL32, w=33), "w=33"),
+    (dict(W.FULL32, a=2**32), "32 bits"),
+    (dict(W.FULL32, a0=2**32 - 2), "a - a0 >= 2"),
+    (dict(W.BYTE8, b0=1), "b0 must be 0"),
+    (dict(W.BYTE8, b=254), "power of two"),
+    (dict(W.BYTE8, b=511), "b < 2^w"),
+])
+def test_create_rejects_invalid(lib, bad, fragment):
+    with pytest.raises(P.PrngdError) as e:
+        P.prngd_create(**bad, seed=1, n_streams=1, n_per_stream=2)
+    assert e.value.status == P.PRNGD_EINVAL and fragment in str(e.value)
+
+
+@pytest.mark.parametrize("counts", [(0, 4), (4, 0), (2**40, 2**30), (1, 2**32)])
+def test_create_rejects_bad_counts(lib, counts):
+    with pytest.raises(P.PrngdError) as e:
+        P.prngd_create(**W.FULL32, seed=1, n_streams=counts[0], n_per_stream=counts[1])
+    assert e.value.status == P.PRNGD_EINVAL
+
+
+def test_create_rejects_unknown_flags(lib):
+    with pytest.raises(P.PrngdError) as e:
+        P.prngd_create(**W.FULL32, seed=1, n_streams=1, n_per_stream=2, flags=0x100)
+    assert e.value.status == P.PRNGD_EUNSUPPORTED
+
+
+def test_null_arguments(lib):
+    assert lib.prngd_create(None, None) == P.PRNGD_EINVAL
+    assert lib.prngd_destroy(None) == P.PRNGD_OK
+    assert lib.prngd_generate(None, None, None) == P.PRNGD_EINVAL
+    assert b"EINVAL" in lib.prngd_status_string(1)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg4"])
+def test_constants_match_oracle(lib, orc, name):
+    p = W.CONFIGS[name]
+    h = P.prngd_create(**p)
+    try:
+        i = P.prngd_get_info(h)
+    finally:
+        P.prngd_destroy(h)
+    C, D = orc.constants(p["w"], p["a0"], p["a"], p["b0"], p["b"])
+    assert (i["C"], i["D"]) == (C, D)
+    assert i["C_s"] == C * 2.0 ** p["w"] and i["D_s"] == D * 2.0 ** p["w"]
+    assert i["y"] == 1.0 / i["D_s"]
+    assert i["sh1"] == 32 - p["a"].bit_length() and i["sh2"] == 32 - p["b"].bit_length()
+    assert i["n_outputs"] == p["n_streams"] * p["n_per_stream"]
+
+
+@pytest.mark.parametrize("w,clamp", [(8, 0), (26, 0), (27, 1), (32, 1)])
+def test_clamp_flag_follows_R11(lib, w, clamp):
+    h = P.prngd_create(w=w, a0=0, a=2**w - 1, b0=0, b=2**w - 1, seed=1, n_streams=1, n_per_stream=2)
+    try:
+        assert P.prngd_get_info(h)["clamp"] == clamp
+    finally:
+        P.prngd_destroy(h)
+
+
+def test_speculation_only_for_rare_rejection(lib):
+    for p, spec in [(W.FULL32, 1), (W.ASYM, 1), (W.BYTE8, 0)]:
+        h = P.prngd_create(**p, seed=1, n_streams=1, n_per_stream=2)
+        assert P.prngd_get_info(h)["speculative"] == spec
+        P.prngd_destroy(h)
+    h = P.prngd_create(**W.FULL32, seed=1, n_streams=1, n_per_stream=2, flags=P.PRNGD_FLAG_ALG1)
+    assert P.prngd_get_info(h)["speculative"] == 0
+    P.prngd_destroy(h)
+
+
+def test_generate_without_gpu_fails_loudly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = P.prngd_create(**W.CONFIGS["cfg1"])
+    try:
+        st = lib.prngd_generate(h, 0x1000, None)
+        assert st in (P.PRNGD_ECUDA, P.PRNGD_EUNSUPPORTED)
+    finally:
+        P.prngd_destroy(h)

@@ -1,0 +1,291 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar (BASELINE north_star): bit-exact raw draws and pair indices, 0 ulp for the doubles (compared
+as int64 bit patterns), identical histograms/counts; FP64 power sums at relative 1e-12 (R16).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_1401_8230_b200 import prngd as P  # noqa: E402
+from paper_1401_8230_b200 import workloads as W  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def gpu():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    P.lib()  # fail loudly if the native library is missing
+    yield
+
+
+def bits(a):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
+
+
+def gen(p, **over):
+    q = dict(p)
+    q.update(over)
+    g = P.Generator(**q)
+    out = g.generate()
+    torch.cuda.synchronize()
+    assert g.last_launches == 1
+    return g, out
+
+
+def assert_same(gpu_out, ref):
+    gb, rb = bits(gpu_out).ravel(), bits(ref).ravel()
+    bad = np.nonzero(gb != rb)[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first at {bad[:5]}: " \
+        f"{bits(gpu_out).ravel()[bad[:3]]} vs {rb[bad[:3]]}"
+
+
+# ------------------------------------------------------------------ full-config parity
+
+@pytest.mark.parametrize("flags", [0, P.PRNGD_FLAG_NO_TMA, P.PRNGD_FLAG_IEEE_DIV])
+def test_cfg1_bitwise(orc, flags):
+    p = W.CONFIGS["cfg1"]
+    _, out = gen(p, flags=flags)
+    assert_same(out, orc.generate(p)["out"])
+
+
+@pytest.mark.parametrize("seed", [W.SEED, W.SEED2])
+def test_cfg2_bitwise_rejection_path(orc, seed):
+    p = W.config("cfg2", seed=seed)
+    _, out = gen(p)
+    assert_same(out, orc.generate(p)["out"])
+
+
+def test_cfg2_pair_indices_and_consumed(orc):
+    p = W.CONFIGS["cfg2"]
+    g = P.Generator(**p)
+    pidx, cons = g.pairs()
+    torch.cuda.synchronize()
+    r = orc.generate(p, want_out=False, want_pidx=True, want_consumed=True)
+    assert np.array_equal(pidx.cpu().numpy().view(np.uint32), r["pidx"])
+    assert np.array_equal(cons.cpu().numpy().view(np.uint64), r["consumed"])
+
+
+def test_raw_draws_bit_exact(orc):
+    p = W.CONFIGS["cfg1"]
+    g = P.Generator(**p)
+    raw = g.raw(64)
+    torch.cuda.synchronize()
+    assert np.array_equal(raw.cpu().numpy().view(np.uint32), orc.raw(p["seed"], 0, 1024, 64))
+
+
+def test_cfg4_asymmetric_sampled_streams(orc):
+    """cfg4 at full size (2^20 x 4096, 32 GiB) in the production launch; 48 streams spread over
+    the range compared bitwise with the oracle, and properties over all 2^32 outputs."""
+    p = W.CONFIGS["cfg4"]
+    _, out = gen(p)
+    rows = np.linspace(0, p["n_streams"] - 1, 48).astype(np.int64)
+    for r in rows[:8].tolist() + rows[8:].tolist():
+        ref = orc.generate(p, stream_begin=int(r), n_streams=1)["out"]
+        assert_same(out[r], ref[0])
+    assert bool((out > 0).all()) and bool((out < 1).all())
+    mx = out.max().item()
+    assert mx == float.fromhex("0x1.ffffffff00000p-1") or mx < 1.0
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_cfg3_full_size_sampled(orc):
+    """cfg3 exactly as bench.py launches it: 2^30 doubles; sampled streams bitwise, and global
+    properties (range, no 1.0, no 0) over every output."""
+    p = W.CONFIGS["cfg3"]
+    _, out = gen(p)
+    rows = np.linspace(0, p["n_streams"] - 1, 64).astype(np.int64)
+    ref = np.stack([orc.generate(p, stream_begin=int(r), n_streams=1)["out"][0] for r in rows])
+    assert_same(out[torch.from_numpy(rows).cuda()], ref)
+    assert bool((out > 0).all()) and bool((out < 1).all())
+    del out
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ ragged / edge shapes
+
+@pytest.mark.parametrize("ns,nps", [(1, 1), (1, 2), (31, 17), (33, 16), (1000, 1000),
+                                    (77, 999), (64, 3), (5, 4096 + 6)])
+@pytest.mark.parametrize("base", ["cfg1", "cfg2"])
+def test_ragged_shapes(orc, ns, nps, base):
+    p = W.config(base, n_streams=ns, n_per_stream=nps, stream_begin=12345)
+    _, out = gen(p)
+    assert_same(out, orc.generate(p)["out"])
+
+
+@pytest.mark.parametrize("flags", [0, P.PRNGD_FLAG_NO_TMA])
+def test_misaligned_output_pointer(orc, flags):
+    p = W.config("cfg1", n_streams=96, n_per_stream=64, flags=flags)
+    g = P.Generator(**p)
+    buf = torch.full((96 * 64 + 1,), -1.0, dtype=torch.float64, device="cuda")
+    P.prngd_generate(g.handle, buf[1:])   # 8-byte aligned only
+    torch.cuda.synchronize()
+    assert buf[0].item() == -1.0
+    assert_same(buf[1:], orc.generate(p)["out"])
+
+
+def test_no_out_of_bounds_writes(orc):
+    p = W.config("cfg1", n_streams=40, n_per_stream=30)
+    g = P.Generator(**p)
+    buf = torch.full((40 * 30 + 512,), -7.0, dtype=torch.float64, device="cuda")
+    g.generate(buf[:40 * 30].view(40, 30))
+    torch.cuda.synchronize()
+    assert bool((buf[40 * 30:] == -7.0).all())
+
+
+def test_general_ranges(orc):
+    for par in [dict(w=20, a0=5, a=2**20 - 3, b0=0, b=2**20 - 1),
+                dict(w=32, a0=1000, a=2**31 + 7, b0=0, b=2**16 - 1),
+                dict(w=12, a0=0, a=100, b0=0, b=63),
+                dict(w=1, a0=0, a=2, b0=0, b=1)]:
+        p = dict(par, seed=9, n_streams=100, n_per_stream=130)
+        _, out = gen(p)
+        assert_same(out, orc.generate(p)["out"])
+
+
+def test_sharding_equals_whole(orc):
+    p = W.config("cfg1", n_streams=256, n_per_stream=96)
+    _, whole = gen(p)
+    parts = [gen(W.shard(p, r, 4))[1] for r in range(4)]
+    assert_same(torch.cat(parts), whole.cpu().numpy())
+
+
+def test_determinism():
+    p = W.config("cfg1", n_streams=512)
+    _, a = gen(p)
+    _, b = gen(p)
+    assert torch.equal(a.view(torch.int64), b.view(torch.int64))
+
+
+def test_generate_host_matches_device(orc):
+    p = W.config("cfg1", n_streams=3000, n_per_stream=512)
+    g, dev = gen(p)
+    host = g.generate_host()
+    assert g.last_launches >= 1
+    assert_same(host, dev.cpu().numpy())
+
+
+# ------------------------------------------------------------------ the mapping alone
+
+def test_map_exhaustive_w8(orc):
+    p = W.BYTE8
+    g = P.Generator(**p, seed=1, n_streams=1, n_per_stream=2)
+    x1, x2 = np.meshgrid(np.arange(256, dtype=np.uint32), np.arange(256, dtype=np.uint32),
+                         indexing="ij")
+    z = g.map(torch.from_numpy(x1.ravel()).cuda(), torch.from_numpy(x2.ravel()).cuda())
+    torch.cuda.synchronize()
+    q, _ = orc.enumerate_pairs(p)
+    assert_same(z, q.ravel())
+
+
+def test_map_exhaustive_w16_closed_form():
+    """All 2^32 pairs at w=16 against the closed form RN(j/(2^16-1)^2) computed by torch's IEEE
+    division on the GPU (independent of the library's division)."""
+    p = dict(w=16, a0=0, a=65535, b0=0, b=65535)
+    g = P.Generator(**p, seed=1, n_streams=1, n_per_stream=2)
+    M = float(65535 ** 2)
+    x2 = torch.arange(65536, dtype=torch.int64, device="cuda")
+    for lo in range(1, 65535, 4096):
+        x1 = torch.arange(lo, min(lo + 4096, 65535), dtype=torch.int64, device="cuda")
+        X1, X2 = torch.meshgrid(x1, x2, indexing="ij")
+        z = g.map(X1.reshape(-1).to(torch.int32), X2.reshape(-1).to(torch.int32))
+        j = (X1 * 65536 + X2 - 65535).reshape(-1).to(torch.float64)
+        assert torch.equal(z.view(torch.int64), (j / M).view(torch.int64))
+
+
+def test_map_w32_edges_and_random(orc):
+    p = W.FULL32
+    g = P.Generator(**p, seed=1, n_streams=1, n_per_stream=2)
+    e1, e2 = W.edge_pairs(32, 32, span=24)
+    r1, r2 = W.random_pairs(11, 1 << 20, 32, 32)
+    x1 = np.concatenate([e1, r1, np.full(4096, 2**32 - 2, np.uint32)])
+    x2 = np.concatenate([e2, r2, (np.arange(4096, dtype=np.uint64) + 2**32 - 4096).astype(np.uint32)])
+    z = g.map(torch.from_numpy(x1.view(np.int32)).cuda(), torch.from_numpy(x2.view(np.int32)).cuda())
+    torch.cuda.synchronize()
+    assert_same(z, orc.map_pairs(p, x1, x2))
+    assert bool((z < 1.0).all())
+
+
+@pytest.mark.parametrize("par", [W.FULL32, W.ASYM, W.BYTE8,
+                                 dict(w=27, a0=0, a=2**27 - 1, b0=0, b=2**27 - 1),
+                                 dict(w=32, a0=1000, a=2**31 + 7, b0=0, b=2**16 - 1)])
+def test_fast_division_equals_ieee(par):
+    """R10 on the GPU: reciprocal + 2 FMA quotient == __ddiv_rn on 2^34 sampled numerators."""
+    g = P.Generator(**par, seed=1, n_streams=1, n_per_stream=2)
+    mism = torch.zeros(1, dtype=torch.int64, device="cuda")
+    P.prngd_debug_div_check(g.handle, 1 << 34, 0xC0FFEE, mism)
+    torch.cuda.synchronize()
+    assert mism.item() == 0
+
+
+# ------------------------------------------------------------------ fused consumer (S7)
+
+@pytest.mark.parametrize("write", [False, True])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_consume_matches_oracle(orc, name, write):
+    p = W.CONFIGS[name]
+    g = P.Generator(**p)
+    out = torch.empty(g.shape, dtype=torch.float64, device="cuda") if write else None
+    _, hist, pw, cnt = g.generate_consume(out)
+    torch.cuda.synchronize()
+    assert g.last_launches == 2
+    r = orc.generate(p, want_out=write, want_stats=True)
+    assert np.array_equal(hist.cpu().numpy(), r["hist"])
+    assert cnt.item() == r["count"] == p["n_streams"] * p["n_per_stream"]
+    assert np.allclose(pw.cpu().numpy(), r["pow"], rtol=1e-12, atol=0)
+    if write:
+        assert_same(out, r["out"])
+
+
+def test_consume_accumulates_across_shards(orc):
+    p = W.config("cfg4", n_streams=4096, n_per_stream=256)
+    hist = torch.zeros(65536, dtype=torch.int64, device="cuda")
+    pw = torch.zeros(4, dtype=torch.float64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for r in range(3):
+        P.Generator(**W.shard(p, r, 3)).generate_consume(None, hist, pw, cnt)
+    torch.cuda.synchronize()
+    ref = orc.generate(p, want_out=False, want_stats=True)
+    assert np.array_equal(hist.cpu().numpy(), ref["hist"]) and cnt.item() == ref["count"]
+    assert np.allclose(pw.cpu().numpy(), ref["pow"], rtol=1e-12, atol=0)
+
+
+def test_consume_packed_counter_carries():
+    """w=1, [0;2] x [0;1]: every output is 1/3 or 2/3, so two bins (one low, one high field of a
+    packed word) receive ~2^27 counts -- thousands of 16-bit carries per CTA.  The histogram must
+    equal the counts of the written outputs (torch bincount, independent of the consumer)."""
+    p = dict(w=1, a0=0, a=2, b0=0, b=1, seed=5, n_streams=4096, n_per_stream=65536)
+    g = P.Generator(**p)
+    out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+    _, hist, pw, cnt = g.generate_consume(out)
+    torch.cuda.synchronize()
+    b = torch.floor(out.view(-1) * 65536.0).to(torch.int64)
+    ref = torch.bincount(b, minlength=65536)
+    assert torch.equal(hist, ref)
+    assert cnt.item() == 4096 * 65536
+    nz = torch.nonzero(ref).view(-1).tolist()
+    assert nz == [21845, 43690]
+    assert ref.max().item() > 2 * 148 * 65536  # carries certainly happened
+
+
+def test_cfg4_histogram_full_size_consistent():
+    """cfg4 write + histogram in one fused call at full size: histogram == bincount of the
+    outputs it wrote, count == 2^32."""
+    p = W.CONFIGS["cfg4"]
+    g = P.Generator(**p)
+    out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+    _, hist, pw, cnt = g.generate_consume(out)
+    torch.cuda.synchronize()
+    ref = torch.zeros(65536, dtype=torch.int64, device="cuda")
+    flat = out.view(-1)
+    for lo in range(0, flat.numel(), 1 << 28):
+        ref += torch.bincount(torch.floor(flat[lo:lo + (1 << 28)] * 65536.0).to(torch.int64),
+                              minlength=65536)
+    assert torch.equal(hist, ref)
+    assert cnt.item() == 2**32
+    del out, flat
+    torch.cuda.empty_cache()
