@@ -271,6 +271,23 @@ def main():
             "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kern_ms,
             "frac_of_8TBs_nominal": achieved / 8000.0}
 
+    # -------------------------------------------------- pure-store ceiling on the same buffer
+    # (B13: torch fill_ and cudaMemset over the 8 GiB output; library kernels, context only)
+    if not consume:
+        best = 0.0
+        for fn in (lambda: out.fill_(0.5), lambda: out.zero_()):
+            for _ in range(3):
+                fn()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(20):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            best = max(best, 20 * bytes_launch / (a.elapsed_time(b) * 1e-3) / 1e9)
+        roof["write_ceiling_gbs"] = best
+        roof["frac_of_write_ceiling"] = achieved / best
+
     # -------------------------------------------------- end to end through the C ABI, host buffer
     e2e = None
     if args.e2e_steps > 0 and not consume:

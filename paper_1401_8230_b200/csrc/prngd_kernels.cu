@@ -24,7 +24,12 @@ namespace prngd {
 
 constexpr int kCols = 16;                   // outputs per lane per batch (128 B of its row)
 constexpr int kTileBytes = 32 * kCols * 8;  // 4 KiB per warp tile
-constexpr int kNBuf = 2;                    // tiles per warp (double buffering)
+constexpr int kNBufTma = 2;                 // tiles per warp when the TMA stores them (async)
+
+// Tiles per warp: the TMA store reads the tile asynchronously, so it gets a ring of two; the
+// st.global flush and the consume-only path read it synchronously and need one.
+template <Store ST, bool WRITE>
+constexpr int ring() { return (WRITE && ST == Store::TMA) ? kNBufTma : 1; }
 constexpr int kGenWarps = 4;                // warps per CTA, generate kernel
 constexpr int kConsWarpsWrite = 12;         // warps per CTA, consume kernel writing outputs
 constexpr int kConsWarpsNoWrite = 24;       // warps per CTA, consume-only kernel (<= 85 regs)
@@ -193,7 +198,7 @@ __device__ __forceinline__ void flush_stg(uint32_t tile, uint32_t lane, const Ge
 // One warp-task: streams [row0, row0 + 32), all nps columns.  `it` counts batches issued by
 // this warp (tile ring position).
 template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE, bool CONSUME,
-          class Cons>
+          int NB, class Cons>
 __device__ __forceinline__ void run_rows(const CUtensorMap *tmap, const GenArgs &g,
                                          uint32_t tiles, uint32_t lane, uint64_t row0,
                                          Cons &cons, uint32_t &it) {
@@ -201,9 +206,9 @@ __device__ __forceinline__ void run_rows(const CUtensorMap *tmap, const GenArgs 
     const bool live = (row0 + lane) < g.n_streams;  // ragged last warp: extra lanes not counted
 #pragma unroll 1
     for (uint64_t col0 = 0; col0 < g.nps; col0 += kCols, ++it) {
-        const uint32_t tile = tiles + (it % kNBuf) * kTileBytes;
+        const uint32_t tile = tiles + (NB == 1 ? 0u : (it % NB) * kTileBytes);
         if (WRITE && ST == Store::TMA) {
-            if (lane == 0) bulk_wait_read<kNBuf - 1>();  // this tile's previous store read smem
+            if (lane == 0) bulk_wait_read<NB - 1>();  // this tile's previous store read smem
             __syncwarp();
         }
         produce_batch<FULL32, SPEC, IEEE, ALG1>(st, tile, lane, g);
@@ -256,12 +261,13 @@ __global__ void __launch_bounds__(kGenWarps * 32)
     gen_kernel(const __grid_constant__ CUtensorMap tmap, const GenArgs g) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint32_t tiles = aligned_smem_base(smem_raw) + warp * (kNBuf * kTileBytes);
+    constexpr int NB = ring<ST, true>();
+    const uint32_t tiles = aligned_smem_base(smem_raw) + warp * (NB * kTileBytes);
     const uint64_t row0 = ((uint64_t)blockIdx.x * kGenWarps + warp) * 32u;
     if (row0 >= g.n_streams) return;
     uint32_t it = 0;
     NoConsumer nc;
-    run_rows<FULL32, SPEC, IEEE, ALG1, ST, true, false>(&tmap, g, tiles, lane, row0, nc, it);
+    run_rows<FULL32, SPEC, IEEE, ALG1, ST, true, false, NB>(&tmap, g, tiles, lane, row0, nc, it);
     if (ST == Store::TMA && lane == 0) bulk_wait_all();
 }
 
@@ -271,12 +277,13 @@ template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE>
 __global__ void __launch_bounds__((WRITE ? kConsWarpsWrite : kConsWarpsNoWrite) * 32, 1)
     consume_kernel(const __grid_constant__ CUtensorMap tmap, const GenArgs g) {
     constexpr int kWarps = WRITE ? kConsWarpsWrite : kConsWarpsNoWrite;
+    constexpr int NB = ring<ST, WRITE>();
     extern __shared__ uint8_t smem_raw[];
     __shared__ double red[kWarps][4];
     const uint32_t base = aligned_smem_base(smem_raw);
     uint32_t *hist = reinterpret_cast<uint32_t *>(smem_raw + (base - smem_u32(smem_raw)));
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint32_t tiles = base + kHistWords * 4u + warp * (kNBuf * kTileBytes);
+    const uint32_t tiles = base + kHistWords * 4u + warp * (NB * kTileBytes);
     for (uint32_t i = threadIdx.x; i < kHistWords; i += blockDim.x) hist[i] = 0u;
     __syncthreads();
     Consumer cons;
@@ -286,8 +293,8 @@ __global__ void __launch_bounds__((WRITE ? kConsWarpsWrite : kConsWarpsNoWrite) 
 #pragma unroll 1
     for (uint64_t t = (uint64_t)blockIdx.x * kWarps + warp; t < n_tasks;
          t += (uint64_t)gridDim.x * kWarps) {
-        run_rows<FULL32, SPEC, IEEE, ALG1, ST, WRITE, true>(&tmap, g, tiles, lane, t * 32u, cons,
-                                                             it);
+        run_rows<FULL32, SPEC, IEEE, ALG1, ST, WRITE, true, NB>(&tmap, g, tiles, lane, t * 32u,
+                                                                 cons, it);
     }
     if (WRITE && ST == Store::TMA && lane == 0) bulk_wait_all();
     // moments: warp tree, then per-CTA in warp order (deterministic for a fixed grid)
@@ -454,7 +461,7 @@ static cudaError_t set_smem(K kernel, size_t bytes) {
 template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST>
 static cudaError_t gen_launch(const CUtensorMap &m, const GenArgs &g, cudaStream_t st) {
     auto k = gen_kernel<FULL32, SPEC, IEEE, ALG1, ST>;
-    const size_t smem = 1024 + (size_t)kGenWarps * kNBuf * kTileBytes;
+    const size_t smem = 1024 + (size_t)kGenWarps * ring<ST, true>() * kTileBytes;
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
     const uint64_t tasks = (g.n_streams + 31u) / 32u;
@@ -506,7 +513,7 @@ static cudaError_t cons_launch(const CUtensorMap &m, const GenArgs &g, int grid,
                                cudaStream_t st) {
     constexpr int kWarps = WRITE ? kConsWarpsWrite : kConsWarpsNoWrite;
     auto k = consume_kernel<FULL32, SPEC, IEEE, ALG1, ST, WRITE>;
-    const size_t smem = 1024 + (size_t)kHistWords * 4u + (WRITE ? (size_t)kWarps * kNBuf * kTileBytes : 0);
+    const size_t smem = 1024 + (size_t)kHistWords * 4u + (size_t)kWarps * ring<ST, WRITE>() * kTileBytes;
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
     k<<<grid, kWarps * 32, smem, st>>>(m, g);

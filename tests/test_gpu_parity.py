@@ -184,7 +184,8 @@ def test_map_exhaustive_w8(orc):
 
 def test_map_exhaustive_w16_closed_form():
     """All 2^32 pairs at w=16 against the closed form RN(j/(2^16-1)^2) computed by torch's IEEE
-    division on the GPU (independent of the library's division)."""
+    tensor/tensor division on the GPU (independent of the library's division; a Python-scalar
+    divisor would make torch multiply by a rounded reciprocal instead)."""
     p = dict(w=16, a0=0, a=65535, b0=0, b=65535)
     g = P.Generator(**p, seed=1, n_streams=1, n_per_stream=2)
     M = float(65535 ** 2)
@@ -194,7 +195,7 @@ def test_map_exhaustive_w16_closed_form():
         X1, X2 = torch.meshgrid(x1, x2, indexing="ij")
         z = g.map(X1.reshape(-1).to(torch.int32), X2.reshape(-1).to(torch.int32))
         j = (X1 * 65536 + X2 - 65535).reshape(-1).to(torch.float64)
-        assert torch.equal(z.view(torch.int64), (j / M).view(torch.int64))
+        assert torch.equal(z.view(torch.int64), (j / torch.full_like(j, M)).view(torch.int64))
 
 
 def test_map_w32_edges_and_random(orc):
