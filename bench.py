@@ -148,6 +148,30 @@ def cpu_baseline(p: dict, target_s: float = 12.0) -> dict:
                       f"({n} doubles, {dt:.1f} s, outputs written to host RAM)"}
 
 
+def write_ceiling(out, stream, torch) -> dict:
+    import ctypes
+    try:
+        from paper_1401_8230_b200 import build as B
+        L = ctypes.CDLL(B.build_tools())
+    except Exception as e:  # measurement aid only
+        return {"write_ceiling_gbs": None, "write_ceiling_note": f"unavailable: {e}"}
+    L.wc_store.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64,
+                           ctypes.c_void_p]
+    n = out.numel()
+    res = {}
+    for vec in (2, 4):
+        for k in range(3):
+            L.wc_store(out.data_ptr(), n, vec, k, stream.cuda_stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for k in range(20):
+            L.wc_store(out.data_ptr(), n, vec, 100 + k, stream.cuda_stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        res[f"store{8 * vec}B_gbs"] = 20 * 8 * n / (a.elapsed_time(b) * 1e-3) / 1e9
+    return {"write_ceiling_gbs": max(res.values()), "write_ceiling_detail": res}
+
+
 def run_reference(args, rank, world):
     """Reference arm = the CPU oracle (this tier has no upstream code)."""
     if rank != 0:
@@ -272,21 +296,11 @@ def main():
             "frac_of_8TBs_nominal": achieved / 8000.0}
 
     # -------------------------------------------------- pure-store ceiling on the same buffer
-    # (B13: torch fill_ and cudaMemset over the 8 GiB output; library kernels, context only)
+    # (B13, tools/write_ceiling.cu: incompressible values, 16/32-byte coalesced stores)
     if not consume:
-        best = 0.0
-        for fn in (lambda: out.fill_(0.5), lambda: out.zero_()):
-            for _ in range(3):
-                fn()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for _ in range(20):
-                fn()
-            b.record(stream)
-            torch.cuda.synchronize()
-            best = max(best, 20 * bytes_launch / (a.elapsed_time(b) * 1e-3) / 1e9)
-        roof["write_ceiling_gbs"] = best
-        roof["frac_of_write_ceiling"] = achieved / best
+        roof.update(write_ceiling(out, stream, torch))
+        if roof.get("write_ceiling_gbs"):
+            roof["frac_of_write_ceiling"] = achieved / roof["write_ceiling_gbs"]
 
     # -------------------------------------------------- end to end through the C ABI, host buffer
     e2e = None

@@ -55,8 +55,12 @@ typedef enum {
 /* flags */
 #define PRNGD_FLAG_IEEE_DIV   0x1u  /* use the IEEE division instruction sequence instead of the
                                        reciprocal + 2 FMA correction (R10); same bits, slower */
-#define PRNGD_FLAG_NO_TMA     0x2u  /* store through the warp-coalesced st.global path even when
-                                       the TMA tensor-store path is eligible */
+#define PRNGD_FLAG_NO_TMA     0x2u  /* store path A/B: stage each warp batch in shared memory and
+                                       write it with warp-coalesced 16-byte st.global */
+#define PRNGD_FLAG_STORE_TMA  0x8u  /* store path A/B: stage in shared memory and write with one
+                                       TMA tensor store (cp.async.bulk.tensor.2d) per warp batch.
+                                       Default (neither flag): each lane writes its own row with
+                                       32-byte st.global.v4 straight from registers */
 #define PRNGD_FLAG_ALG1       0x4u  /* NEXT-2 reading of Alg. 1: a rejected x1 is
                                        redrawn alone (x2 is drawn only after acceptance) */
 

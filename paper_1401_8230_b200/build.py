@@ -60,9 +60,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+TOOL_SRC = os.path.join(ROOT, "tools", "write_ceiling.cu")
+TOOL_LIB = os.path.join(ROOT, "tools", "libwriteceil.so")
+
+
+def build_tools(force: bool = False) -> str:
+    """B13 write-roofline microbenchmark used by bench.py (measurement only)."""
+    if force or not os.path.exists(TOOL_LIB) or os.path.getmtime(TOOL_LIB) < os.path.getmtime(TOOL_SRC):
+        cmd = [NVCC, *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-cudart",
+               "shared", "-o", TOOL_LIB, TOOL_SRC]
+        subprocess.check_call(cmd)
+    return TOOL_LIB
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     a = ap.parse_args()
     print(build(force=a.force, verbose=a.verbose))
+    print(build_tools(force=a.force))

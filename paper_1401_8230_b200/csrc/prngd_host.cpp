@@ -114,7 +114,8 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         return fail(PRNGD_EINVAL, "n_streams * n_per_stream overflows (limit 2^62)");
     if (p->stream_begin > ~0ull - p->n_streams)
         return fail(PRNGD_EINVAL, "stream_begin + n_streams overflows 64 bits");
-    const uint32_t known = PRNGD_FLAG_IEEE_DIV | PRNGD_FLAG_NO_TMA | PRNGD_FLAG_ALG1;
+    const uint32_t known =
+        PRNGD_FLAG_IEEE_DIV | PRNGD_FLAG_NO_TMA | PRNGD_FLAG_ALG1 | PRNGD_FLAG_STORE_TMA;
     if (p->flags & ~known) return fail(PRNGD_EUNSUPPORTED, "unknown flag bits 0x%x", p->flags & ~known);
 
     prngd_handle *h = new (std::nothrow) prngd_handle();
@@ -165,13 +166,16 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     g.sh2 = I.sh2;
     g.lo = (uint32_t)(p->a0 + 1);
     g.span = (uint32_t)(p->a - p->a0 - 1);
+    g.span_fast = g.span - I.clamp;
 
     Plan &pl = h->plan;
     pl.spec = I.speculative != 0;
     pl.clamp = I.clamp != 0;
     pl.ieee_div = (p->flags & PRNGD_FLAG_IEEE_DIV) != 0;
     pl.alg1 = alg1;
-    pl.store = (p->flags & PRNGD_FLAG_NO_TMA) ? Store::STG16 : Store::TMA;
+    pl.store = (p->flags & PRNGD_FLAG_NO_TMA)      ? Store::STG16
+               : (p->flags & PRNGD_FLAG_STORE_TMA) ? Store::TMA
+                                                   : Store::DIRECT;
     *out = h;
     return PRNGD_OK;
 }
@@ -203,10 +207,16 @@ prngd_status prngd_get_info(const prngd_handle *h, prngd_info *info) {
 
 uint32_t prngd_last_launches(const prngd_handle *h) { return h ? h->last_launches.load() : 0u; }
 
+// Store path for this output pointer: the requested one when its alignment rules hold, else
+// the next one that is legal (same bits whichever path writes them).
 static Plan plan_for(const prngd_handle *h, const void *out) {
     Plan pl = h->plan;
-    const bool a16 = ((uintptr_t)out & 15u) == 0 && (h->p.n_per_stream & 1u) == 0;
-    const bool tma_ok = a16 && h->p.n_streams < (1ull << 31) && h->p.n_per_stream < (1ull << 31);
+    const uintptr_t a = (uintptr_t)out;
+    const uint64_t nps = h->p.n_per_stream;
+    const bool a32 = (a & 31u) == 0 && (nps & 3u) == 0;
+    const bool a16 = (a & 15u) == 0 && (nps & 1u) == 0;
+    const bool tma_ok = a16 && h->p.n_streams < (1ull << 31) && nps < (1ull << 31);
+    if (pl.store == Store::DIRECT && !a32) pl.store = a16 ? Store::STG16 : Store::STG8;
     if (pl.store == Store::TMA && !tma_ok) pl.store = a16 ? Store::STG16 : Store::STG8;
     if (pl.store == Store::STG16 && !a16) pl.store = Store::STG8;
     return pl;

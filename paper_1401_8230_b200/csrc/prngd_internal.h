@@ -19,13 +19,18 @@ struct GenArgs {
     uint32_t w;             // composition shift, v = (x1 << w) | x2
     uint32_t sh1, sh2;      // draw widths, x = u >> sh (R4)
     uint32_t lo, span;      // accept iff (x1 - lo) < span  <=>  a0 < x1 < a   (R3)
+    uint32_t span_fast;     // span - clamp: speculative band excluding x1 = a - 1 when R11 applies
     // consumer (S7)
     uint32_t *hist_slab;    // [gridDim.x][32768] packed u16 pairs (consume kernels only)
     int64_t *hist_spill;    // [65536] int64 carries of the packed counters
     double *pow_slab;       // [gridDim.x][4]
 };
 
-enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2 };
+// How a warp's 32 x 16 batch reaches HBM:
+//   DIRECT: each lane stores its row segment from registers, 4 x 32-byte st.global.v4.f64
+//   TMA:    smem tile (128B swizzle) + one cp.async.bulk.tensor.2d store per warp batch
+//   STG16:  smem tile + warp-coalesced 16-byte st.global;  STG8: same with 8-byte stores
+enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3 };
 
 // Launch descriptors chosen by the host.
 struct Plan {

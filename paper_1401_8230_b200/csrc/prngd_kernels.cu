@@ -27,12 +27,18 @@ constexpr int kTileBytes = 32 * kCols * 8;  // 4 KiB per warp tile
 constexpr int kNBufTma = 2;                 // tiles per warp when the TMA stores them (async)
 
 // Tiles per warp: the TMA store reads the tile asynchronously, so it gets a ring of two; the
-// st.global flush and the consume-only path read it synchronously and need one.
+// smem-staged st.global flush reads it synchronously and needs one; the direct path and the
+// consume-only path keep the batch in registers and need none.
 template <Store ST, bool WRITE>
-constexpr int ring() { return (WRITE && ST == Store::TMA) ? kNBufTma : 1; }
+constexpr int ring() {
+    return !WRITE || ST == Store::DIRECT ? 0 : (ST == Store::TMA ? kNBufTma : 1);
+}
 constexpr int kGenWarps = 4;                // warps per CTA, generate kernel
-constexpr int kConsWarpsWrite = 12;         // warps per CTA, consume kernel writing outputs
-constexpr int kConsWarpsNoWrite = 24;       // warps per CTA, consume-only kernel (<= 85 regs)
+constexpr int kConsWarpsTiles = 12;         // warps per CTA, consume kernel staging tiles in smem
+constexpr int kConsWarpsRegs = 24;          // warps per CTA, consume kernel without tiles (<= 85 regs)
+
+template <Store ST, bool WRITE>
+constexpr int cons_warps() { return ring<ST, WRITE>() > 0 ? kConsWarpsTiles : kConsWarpsRegs; }
 constexpr int kHistWords = 32768;           // 65536 u16 counters packed in pairs (128 KiB)
 
 // ------------------------------------------------------------------------------ PTX helpers
@@ -120,53 +126,60 @@ struct NoConsumer {
 };
 
 // ------------------------------------------------------------------------------ one batch
-// kCols outputs of this lane's stream into row `lane` of the tile at smem address `tile`.
+// One pair of the exact path: draw until accepted, then Eq.(1)+(4) with the clamp.
+template <bool IEEE, bool ALG1>
+__device__ __forceinline__ double exact_output(Xs128 &st, uint32_t sh1, uint32_t sh2, uint32_t w,
+                                               uint32_t lo, uint32_t span, const GenArgs &g) {
+    uint32_t x1, x2;
+    if (ALG1) {  // NEXT-2: Alg. 1 redraws x1 alone, then draws x2
+        do {
+            x1 = draw(st) >> sh1;
+        } while (!accepted(x1, lo, span));
+        x2 = draw(st) >> sh2;
+    } else {     // R2: a rejected x1 drops its whole pair
+        do {
+            x1 = draw(st) >> sh1;
+            x2 = draw(st) >> sh2;
+        } while (!accepted(x1, lo, span));
+    }
+    return eq4_pair<IEEE, true>(x1, x2, w, g.Cs, g.Ds, g.y);
+}
+
+// kCols consecutive outputs of this lane's stream, into registers q[0..kCols).
 template <bool FULL32, bool SPEC, bool IEEE, bool ALG1>
-__device__ __forceinline__ void produce_batch(Xs128 &st, uint32_t tile, uint32_t lane,
-                                              const GenArgs &g) {
+__device__ __forceinline__ void produce_batch(Xs128 &st, double (&q)[kCols], const GenArgs &g) {
     const uint32_t sh1 = FULL32 ? 0u : g.sh1;
     const uint32_t sh2 = FULL32 ? 0u : g.sh2;
     const uint32_t w = FULL32 ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo;
     const uint32_t span = FULL32 ? 0xFFFFFFFEu : g.span;
-    bool done = false;
     if (SPEC) {
-        // Speculative: compute the batch as if every x1 were accepted; one warp vote at the end.
+        // Fast-path band: x1 = a - 1 is the only row whose pairs can round to 1.0 (R11, monotone
+        // map), so when the clamp is needed that row goes to the exact path with the rejections.
+        const uint32_t span_fast = FULL32 ? 0xFFFFFFFDu : g.span_fast;
+        // Speculative: compute the batch as if every x1 were accepted and below a - 1; one warp
+        // vote at the end decides whether the exact path (reject loop + clamp) redoes it.
         const Xs128 saved = st;
         bool rej = false;
 #pragma unroll
-        for (int c = 0; c < kCols / 2; ++c) {
-            const uint32_t a1 = draw(st) >> sh1;
-            const uint32_t a2 = draw(st) >> sh2;
-            const uint32_t b1 = draw(st) >> sh1;
-            const uint32_t b2 = draw(st) >> sh2;
-            rej |= !accepted(a1, lo, span);
-            rej |= !accepted(b1, lo, span);
-            sts_v2(tile + tile_off(lane, c), eq4_pair<IEEE, true>(a1, a2, w, g.Cs, g.Ds, g.y),
-                   eq4_pair<IEEE, true>(b1, b2, w, g.Cs, g.Ds, g.y));
-        }
-        done = !__any_sync(0xFFFFFFFFu, rej);
-        if (!done) st = saved;
-    }
-    if (!done) {
-#pragma unroll 1
         for (int i = 0; i < kCols; ++i) {
-            uint32_t x1, x2;
-            if (ALG1) {  // NEXT-2: Alg. 1 redraws x1 alone, then draws x2
-                do {
-                    x1 = draw(st) >> sh1;
-                } while (!accepted(x1, lo, span));
-                x2 = draw(st) >> sh2;
-            } else {     // R2: a rejected x1 drops its whole pair
-                do {
-                    x1 = draw(st) >> sh1;
-                    x2 = draw(st) >> sh2;
-                } while (!accepted(x1, lo, span));
-            }
-            sts_f64(tile + tile_off(lane, (uint32_t)i >> 1) + ((uint32_t)i & 1u) * 8u,
-                    eq4_pair<IEEE, true>(x1, x2, w, g.Cs, g.Ds, g.y));
+            const uint32_t x1 = draw(st) >> sh1;
+            const uint32_t x2 = draw(st) >> sh2;
+            rej |= !accepted(x1, lo, span_fast);
+            q[i] = eq4_pair<IEEE, false>(x1, x2, w, g.Cs, g.Ds, g.y);
         }
+        if (__builtin_expect(!__any_sync(0xFFFFFFFFu, rej), 1)) return;
+        st = saved;
     }
+#pragma unroll
+    for (int i = 0; i < kCols; ++i) q[i] = exact_output<IEEE, ALG1>(st, sh1, sh2, w, lo, span, g);
+}
+
+__device__ __forceinline__ void stg_v4_cs(double *p, double a, double b, double c, double d) {
+    // one full 32-byte sector per lane (sm_100 256-bit store)
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+                 "d"(d)
+                 : "memory");
 }
 
 // Warp-coalesced flush of a 32 x 16 tile.  VEC16: 8 lanes per 128-byte row, 4 rows per
@@ -204,48 +217,58 @@ __device__ __forceinline__ void run_rows(const CUtensorMap *tmap, const GenArgs 
                                          Cons &cons, uint32_t &it) {
     Xs128 st = stream_start(g.seed, g.stream_begin + row0 + lane);
     const bool live = (row0 + lane) < g.n_streams;  // ragged last warp: extra lanes not counted
+    double *row_out = (WRITE && ST == Store::DIRECT) ? g.out + (row0 + lane) * g.nps : nullptr;
 #pragma unroll 1
     for (uint64_t col0 = 0; col0 < g.nps; col0 += kCols, ++it) {
-        const uint32_t tile = tiles + (NB == 1 ? 0u : (it % NB) * kTileBytes);
-        if (WRITE && ST == Store::TMA) {
+        double q[kCols];
+        produce_batch<FULL32, SPEC, IEEE, ALG1>(st, q, g);
+        // Outputs past nps in the last batch are computed but neither stored nor counted.
+        const bool full = g.nps - col0 >= (uint64_t)kCols;
+        const uint32_t valid = full ? (uint32_t)kCols : (uint32_t)(g.nps - col0);
+        if (CONSUME && live) {
+            if (full) {
+#pragma unroll
+                for (int i = 0; i < kCols; ++i) cons.add(q[i]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < kCols; ++i)
+                    if ((uint32_t)i < valid) cons.add(q[i]);
+            }
+        }
+        if constexpr (!WRITE) continue;
+        if constexpr (ST == Store::DIRECT) {
+            // Each lane writes its own row: 4 x 32-byte full-sector stores per batch.
+            if (live) {
+                if (full) {
+#pragma unroll
+                    for (int i = 0; i < kCols; i += 4)
+                        stg_v4_cs(row_out + col0 + i, q[i], q[i + 1], q[i + 2], q[i + 3]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kCols; ++i)
+                        if ((uint32_t)i < valid) row_out[col0 + i] = q[i];
+                }
+            }
+        } else {
+        const uint32_t tile = tiles + (NB <= 1 ? 0u : (it % NB) * kTileBytes);
+        if constexpr (ST == Store::TMA) {
             if (lane == 0) bulk_wait_read<NB - 1>();  // this tile's previous store read smem
             __syncwarp();
         }
-        produce_batch<FULL32, SPEC, IEEE, ALG1>(st, tile, lane, g);
-        if (CONSUME && live) {
-            // Outputs past nps in the last batch are computed but neither stored nor counted.
-            const uint32_t valid = (g.nps - col0) >= kCols ? kCols : (uint32_t)(g.nps - col0);
-            if (valid == kCols) {
 #pragma unroll
-                for (int c = 0; c < kCols / 2; ++c) {
-                    double a, b;
-                    lds_v2(tile + tile_off(lane, c), a, b);
-                    cons.add(a);
-                    cons.add(b);
-                }
-            } else {
-                for (uint32_t e = 0; e < valid; ++e) {
-                    double a, b;
-                    lds_v2(tile + tile_off(lane, e >> 1), a, b);
-                    cons.add((e & 1u) ? b : a);
-                }
-            }
-        }
-        if (WRITE) {
-            if (ST == Store::TMA) {
-                fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store_2d(tmap, tile, (int)col0, (int)row0);
-                    bulk_commit();
-                }
-            } else {
-                __syncwarp();
-                flush_stg<ST == Store::STG16>(tile, lane, g, row0, col0);
-                __syncwarp();  // tile reads done before the ring comes back to it
+        for (int c = 0; c < kCols / 2; ++c) sts_v2(tile + tile_off(lane, c), q[2 * c], q[2 * c + 1]);
+        if constexpr (ST == Store::TMA) {
+            fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(tmap, tile, (int)col0, (int)row0);
+                bulk_commit();
             }
         } else {
             __syncwarp();
+            flush_stg<ST == Store::STG16>(tile, lane, g, row0, col0);
+            __syncwarp();  // tile reads done before the ring comes back to it
+        }
         }
     }
 }
@@ -268,15 +291,17 @@ __global__ void __launch_bounds__(kGenWarps * 32)
     uint32_t it = 0;
     NoConsumer nc;
     run_rows<FULL32, SPEC, IEEE, ALG1, ST, true, false, NB>(&tmap, g, tiles, lane, row0, nc, it);
-    if (ST == Store::TMA && lane == 0) bulk_wait_all();
+    if constexpr (ST == Store::TMA) {
+        if (lane == 0) bulk_wait_all();
+    }
 }
 
 // S1-S7, persistent: one CTA per SM owning a 128 KiB packed histogram; warps take 32-stream
 // tasks round-robin.  Writes per-CTA slabs that finalize_kernel reduces.
 template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE>
-__global__ void __launch_bounds__((WRITE ? kConsWarpsWrite : kConsWarpsNoWrite) * 32, 1)
+__global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     consume_kernel(const __grid_constant__ CUtensorMap tmap, const GenArgs g) {
-    constexpr int kWarps = WRITE ? kConsWarpsWrite : kConsWarpsNoWrite;
+    constexpr int kWarps = cons_warps<ST, WRITE>();
     constexpr int NB = ring<ST, WRITE>();
     extern __shared__ uint8_t smem_raw[];
     __shared__ double red[kWarps][4];
@@ -296,7 +321,9 @@ __global__ void __launch_bounds__((WRITE ? kConsWarpsWrite : kConsWarpsNoWrite) 
         run_rows<FULL32, SPEC, IEEE, ALG1, ST, WRITE, true, NB>(&tmap, g, tiles, lane, t * 32u,
                                                                  cons, it);
     }
-    if (WRITE && ST == Store::TMA && lane == 0) bulk_wait_all();
+    if constexpr (WRITE && ST == Store::TMA) {
+        if (lane == 0) bulk_wait_all();
+    }
     // moments: warp tree, then per-CTA in warp order (deterministic for a fixed grid)
     double s[4] = {cons.s1, cons.s2, cons.s3, cons.s4};
 #pragma unroll
@@ -498,6 +525,7 @@ cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, i
         s = Store::STG16;  // descriptor refused: fall back to coalesced st.global (same bits)
     const bool f32 = is_full32(g);
     switch (s) {
+        case Store::DIRECT: return gen_dispatch_store<Store::DIRECT>(m, g, pl, f32, st);
         case Store::TMA: return gen_dispatch_store<Store::TMA>(m, g, pl, f32, st);
         case Store::STG16: return gen_dispatch_store<Store::STG16>(m, g, pl, f32, st);
         default: return gen_dispatch_store<Store::STG8>(m, g, pl, f32, st);
@@ -511,7 +539,7 @@ size_t consume_scratch_bytes(int num_sms) {
 template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE>
 static cudaError_t cons_launch(const CUtensorMap &m, const GenArgs &g, int grid,
                                cudaStream_t st) {
-    constexpr int kWarps = WRITE ? kConsWarpsWrite : kConsWarpsNoWrite;
+    constexpr int kWarps = cons_warps<ST, WRITE>();
     auto k = consume_kernel<FULL32, SPEC, IEEE, ALG1, ST, WRITE>;
     const size_t smem = 1024 + (size_t)kHistWords * 4u + (size_t)kWarps * ring<ST, WRITE>() * kTileBytes;
     cudaError_t e = set_smem(k, smem);
@@ -548,7 +576,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
     g.hist_spill = reinterpret_cast<int64_t *>(sp + (size_t)num_sms * kHistWords * 4u);
     g.pow_slab = reinterpret_cast<double *>(sp + (size_t)num_sms * kHistWords * 4u + 65536u * 8u);
     const uint64_t tasks = (g.n_streams + 31u) / 32u;
-    const int kw = d_out ? kConsWarpsWrite : kConsWarpsNoWrite;
+    const int kw = kConsWarpsTiles;  // grid sizing: the smaller CTA bounds the task count
     int grid = num_sms;
     if ((uint64_t)grid * kw > tasks) grid = (int)((tasks + kw - 1) / kw);
     if (grid < 1) grid = 1;
@@ -563,6 +591,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
         if (s == Store::TMA && make_tmap(&m, d_out, g.n_streams, g.nps) != cudaSuccess)
             s = Store::STG16;
         switch (s) {
+            case Store::DIRECT: e = cons_dispatch<Store::DIRECT, true>(m, g, pl, f32, grid, st); break;
             case Store::TMA: e = cons_dispatch<Store::TMA, true>(m, g, pl, f32, grid, st); break;
             case Store::STG16: e = cons_dispatch<Store::STG16, true>(m, g, pl, f32, grid, st); break;
             default: e = cons_dispatch<Store::STG8, true>(m, g, pl, f32, grid, st); break;

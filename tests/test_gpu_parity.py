@@ -45,7 +45,8 @@ def assert_same(gpu_out, ref):
 
 # ------------------------------------------------------------------ full-config parity
 
-@pytest.mark.parametrize("flags", [0, P.PRNGD_FLAG_NO_TMA, P.PRNGD_FLAG_IEEE_DIV])
+@pytest.mark.parametrize("flags", [0, P.PRNGD_FLAG_NO_TMA, P.PRNGD_FLAG_STORE_TMA,
+                                   P.PRNGD_FLAG_IEEE_DIV])
 def test_cfg1_bitwise(orc, flags):
     p = W.CONFIGS["cfg1"]
     _, out = gen(p, flags=flags)
@@ -117,15 +118,25 @@ def test_ragged_shapes(orc, ns, nps, base):
     assert_same(out, orc.generate(p)["out"])
 
 
-@pytest.mark.parametrize("flags", [0, P.PRNGD_FLAG_NO_TMA])
-def test_misaligned_output_pointer(orc, flags):
+@pytest.mark.parametrize("flags", [0, P.PRNGD_FLAG_NO_TMA, P.PRNGD_FLAG_STORE_TMA])
+@pytest.mark.parametrize("offset", [1, 2, 3])
+def test_misaligned_output_pointer(orc, flags, offset):
+    """8-, 16- and 24-byte offsets: each store path falls back to the next legal one."""
     p = W.config("cfg1", n_streams=96, n_per_stream=64, flags=flags)
     g = P.Generator(**p)
-    buf = torch.full((96 * 64 + 1,), -1.0, dtype=torch.float64, device="cuda")
-    P.prngd_generate(g.handle, buf[1:])   # 8-byte aligned only
+    buf = torch.full((96 * 64 + offset,), -1.0, dtype=torch.float64, device="cuda")
+    P.prngd_generate(g.handle, buf[offset:])
     torch.cuda.synchronize()
-    assert buf[0].item() == -1.0
-    assert_same(buf[1:], orc.generate(p)["out"])
+    assert bool((buf[:offset] == -1.0).all())
+    assert_same(buf[offset:], orc.generate(p)["out"])
+
+
+@pytest.mark.parametrize("flags", [0, P.PRNGD_FLAG_NO_TMA, P.PRNGD_FLAG_STORE_TMA])
+@pytest.mark.parametrize("name", ["cfg2", "cfg4"])
+def test_store_paths_bitwise(orc, flags, name):
+    p = W.config(name, n_streams=200, n_per_stream=100, flags=flags)
+    _, out = gen(p)
+    assert_same(out, orc.generate(p)["out"])
 
 
 def test_no_out_of_bounds_writes(orc):
@@ -225,10 +236,13 @@ def test_fast_division_equals_ieee(par):
 
 # ------------------------------------------------------------------ fused consumer (S7)
 
+@pytest.mark.parametrize("flags", [0, P.PRNGD_FLAG_NO_TMA, P.PRNGD_FLAG_STORE_TMA])
 @pytest.mark.parametrize("write", [False, True])
 @pytest.mark.parametrize("name", ["cfg1", "cfg2"])
-def test_consume_matches_oracle(orc, name, write):
-    p = W.CONFIGS[name]
+def test_consume_matches_oracle(orc, name, write, flags):
+    if flags and not write:
+        pytest.skip("store flags only matter when outputs are written")
+    p = W.config(name, flags=flags)
     g = P.Generator(**p)
     out = torch.empty(g.shape, dtype=torch.float64, device="cuda") if write else None
     _, hist, pw, cnt = g.generate_consume(out)
