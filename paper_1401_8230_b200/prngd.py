@@ -16,6 +16,7 @@ PRNGD_OK, PRNGD_EINVAL, PRNGD_ECUDA, PRNGD_ENOMEM, PRNGD_EUNSUPPORTED = range(5)
 PRNGD_FLAG_IEEE_DIV = 0x1
 PRNGD_FLAG_NO_TMA = 0x2
 PRNGD_FLAG_ALG1 = 0x4
+PRNGD_FLAG_STORE_TMA = 0x8
 
 EXPORTS = (
     "prngd_create", "prngd_destroy", "prngd_get_info", "prngd_generate", "prngd_generate_consume",
