@@ -284,15 +284,44 @@ __global__ void __launch_bounds__(kGenWarps * 32)
     gen_kernel(const __grid_constant__ CUtensorMap tmap, const GenArgs g) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    constexpr int NB = ring<ST, true>();
-    const uint32_t tiles = aligned_smem_base(smem_raw) + warp * (NB * kTileBytes);
     const uint64_t row0 = ((uint64_t)blockIdx.x * kGenWarps + warp) * 32u;
-    if (row0 >= g.n_streams) return;
-    uint32_t it = 0;
-    NoConsumer nc;
-    run_rows<FULL32, SPEC, IEEE, ALG1, ST, true, false, NB>(&tmap, g, tiles, lane, row0, nc, it);
     if constexpr (ST == Store::TMA) {
-        if (lane == 0) bulk_wait_all();
+        // CTA-level staging: the 4 warps fill one 128-row x 16-column slab (16 KiB, two slots)
+        // and thread 0 writes it with ONE tensor store per batch.  Warps past n_streams keep
+        // computing (their rows are clipped by the TMA) so every thread reaches the barrier.
+        const uint32_t slab0 = aligned_smem_base(smem_raw);
+        const uint32_t my_tile = slab0 + warp * kTileBytes;
+        const uint64_t cta_row0 = (uint64_t)blockIdx.x * kGenWarps * 32u;
+        Xs128 st = stream_start(g.seed, g.stream_begin + row0 + lane);
+        uint32_t slot = 0;
+#pragma unroll 1
+        for (uint64_t col0 = 0; col0 < g.nps; col0 += kCols, slot ^= 1u) {
+            double q[kCols];
+            produce_batch<FULL32, SPEC, IEEE, ALG1>(st, q, g);
+            const uint32_t tile = my_tile + slot * (kGenWarps * kTileBytes);
+#pragma unroll
+            for (int c = 0; c < kCols / 2; ++c)
+                sts_v2(tile + tile_off(lane, c), q[2 * c], q[2 * c + 1]);
+            fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
+            // The other slot's store (previous batch) must have read its smem before the next
+            // batch overwrites it; thread 0 owns the bulk groups, the barrier publishes it.
+            if (threadIdx.x == 0) bulk_wait_read<0>();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                tma_store_2d(&tmap, slab0 + slot * (kGenWarps * kTileBytes), (int)col0,
+                             (int)cta_row0);
+                bulk_commit();
+            }
+        }
+        if (threadIdx.x == 0) bulk_wait_all();
+    } else {
+        constexpr int NB = ring<ST, true>();
+        const uint32_t tiles = aligned_smem_base(smem_raw) + warp * (NB * kTileBytes);
+        if (row0 >= g.n_streams) return;
+        uint32_t it = 0;
+        NoConsumer nc;
+        run_rows<FULL32, SPEC, IEEE, ALG1, ST, true, false, NB>(&tmap, g, tiles, lane, row0, nc,
+                                                                it);
     }
 }
 
@@ -465,14 +494,15 @@ static EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// Tensor map over out[n_streams][nps] (doubles), box 16 columns x 32 rows, 128B swizzle.
-static cudaError_t make_tmap(CUtensorMap *m, double *out, uint64_t n_streams, uint64_t nps) {
+// Tensor map over out[n_streams][nps] (doubles), box 16 columns x box_rows rows, 128B swizzle.
+static cudaError_t make_tmap(CUtensorMap *m, double *out, uint64_t n_streams, uint64_t nps,
+                             uint32_t box_rows) {
     std::memset(m, 0, sizeof(*m));
     EncodeTiledFn enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
     const cuuint64_t dims[2] = {nps, n_streams};
     const cuuint64_t strides[1] = {nps * 8u};
-    const cuuint32_t box[2] = {(cuuint32_t)kCols, 32u};
+    const cuuint32_t box[2] = {(cuuint32_t)kCols, box_rows};
     const cuuint32_t estr[2] = {1u, 1u};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, out, dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -521,7 +551,7 @@ cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, i
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
     Store s = pl.store;
-    if (s == Store::TMA && make_tmap(&m, g.out, g.n_streams, g.nps) != cudaSuccess)
+    if (s == Store::TMA && make_tmap(&m, g.out, g.n_streams, g.nps, 32u * kGenWarps) != cudaSuccess)
         s = Store::STG16;  // descriptor refused: fall back to coalesced st.global (same bits)
     const bool f32 = is_full32(g);
     switch (s) {
@@ -588,7 +618,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
         e = cons_dispatch<Store::STG8, false>(m, g, pl, f32, grid, st);
     } else {
         Store s = pl.store;
-        if (s == Store::TMA && make_tmap(&m, d_out, g.n_streams, g.nps) != cudaSuccess)
+        if (s == Store::TMA && make_tmap(&m, d_out, g.n_streams, g.nps, 32u) != cudaSuccess)
             s = Store::STG16;
         switch (s) {
             case Store::DIRECT: e = cons_dispatch<Store::DIRECT, true>(m, g, pl, f32, grid, st); break;

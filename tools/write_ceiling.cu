@@ -1,35 +1,93 @@
-// write_ceiling.cu -- B13 store-roofline microbenchmark (measurement tool, not the product).
-// Streams incompressible 64-bit values (a per-element hash, so L2 compression cannot shrink the
-// DRAM traffic) over a buffer with 16- or 32-byte coalesced stores, grid = 148 x occupancy.
+// write_ceiling.cu -- B13 store-roofline microbenchmarks (measurement tool, not the product).
+// All modes write incompressible 64-bit values (a cheap per-element hash, so L2 compression
+// cannot shrink the DRAM traffic) into an n-double buffer:
+//   mode 0  contiguous, grid-stride, 16-byte st.global.v2 (148 x 8 CTAs of 256)
+//   mode 1  contiguous, grid-stride, 32-byte st.global.v4
+//   mode 2  the generator's access pattern without its arithmetic: buffer viewed as
+//           [rows][cols], one warp per 32 rows, 128 bytes of each row per step, warp-coalesced
+//           16-byte stores (4 rows x 128 B per instruction), 4 warps per CTA, one CTA per 128 rows
+//   mode 3  contiguous 16 KiB cp.async.bulk (TMA bulk) stores from shared memory
 #include <cstdint>
 #include <cuda_runtime.h>
 
-__device__ __forceinline__ uint64_t h64(uint64_t v) {
-    v ^= v >> 33; v *= 0xff51afd7ed558ccdull; v ^= v >> 33; return v;
+__device__ __forceinline__ double hval(uint64_t i, uint64_t salt) {
+    uint32_t lo = (uint32_t)(i + salt) * 0x9E3779B1u;
+    uint32_t hi = (lo ^ (lo >> 15)) * 0x85EBCA77u;
+    return __hiloint2double((int)(hi & 0x3FEFFFFFu), (int)lo);
 }
 
 template <int VEC>
-__global__ void __launch_bounds__(256) store_kernel(double *p, uint64_t n, uint64_t salt) {
+__global__ void __launch_bounds__(256) contiguous(double *p, uint64_t n, uint64_t salt) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * VEC;
-    for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * VEC; i + VEC <= n; i += stride) {
-        double v[VEC];
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) v[k] = __longlong_as_double((long long)(h64(i + k + salt) >> 12));
+    for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * VEC; i + VEC <= n;
+         i += stride) {
         if (VEC == 2)
-            asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" :: "l"(p + i), "d"(v[0]), "d"(v[1]) : "memory");
+            asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p + i), "d"(hval(i, salt)),
+                         "d"(hval(i + 1, salt))
+                         : "memory");
         else
-            asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" :: "l"(p + i), "d"(v[0]), "d"(v[1]),
-                         "d"(v[VEC > 2 ? 2 : 0]), "d"(v[VEC > 3 ? 3 : 0]) : "memory");
+            asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p + i),
+                         "d"(hval(i, salt)), "d"(hval(i + 1, salt)), "d"(hval(i + 2, salt)),
+                         "d"(hval(i + 3, salt))
+                         : "memory");
     }
 }
 
-extern "C" __attribute__((visibility("default"))) int wc_store(double *p, uint64_t n, int vec,
+__global__ void __launch_bounds__(128) row_tiles(double *p, uint64_t rows, uint64_t cols,
+                                                 uint64_t salt) {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint64_t row0 = ((uint64_t)blockIdx.x * 4 + warp) * 32;
+    if (row0 >= rows) return;
+    for (uint64_t c0 = 0; c0 + 16 <= cols; c0 += 16) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint64_t r = row0 + k * 4 + (lane >> 3), c = c0 + 2 * (lane & 7u);
+            double *q = p + r * cols + c;
+            asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(q), "d"(hval(r * cols + c, salt)),
+                         "d"(hval(r * cols + c + 1, salt))
+                         : "memory");
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128) bulk_contiguous(double *p, uint64_t n, uint64_t salt) {
+    constexpr int kChunk = 16384;  // bytes per bulk store
+    __shared__ alignas(128) double buf[2][kChunk / 8];
+    for (int i = threadIdx.x; i < 2 * kChunk / 8; i += blockDim.x)
+        (&buf[0][0])[i] = hval(blockIdx.x * 4096u + i, salt);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const uint64_t chunks = n * 8 / kChunk;
+    int k = 0;
+    for (uint64_t c = blockIdx.x; c < chunks; c += gridDim.x, k ^= 1) {
+        const uint32_t s = (uint32_t)__cvta_generic_to_shared(&buf[k][0]);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         p + c * (kChunk / 8)),
+                     "r"(s), "n"(kChunk)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 8;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+extern "C" __attribute__((visibility("default"))) int wc_store(double *p, uint64_t n, int mode,
                                                                uint64_t salt, void *stream) {
     int sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = sms * 8;
-    if (vec == 4) store_kernel<4><<<grid, 256, 0, (cudaStream_t)stream>>>(p, n, salt);
-    else store_kernel<2><<<grid, 256, 0, (cudaStream_t)stream>>>(p, n, salt);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (mode) {
+        case 0: contiguous<2><<<sms * 8, 256, 0, st>>>(p, n, salt); break;
+        case 1: contiguous<4><<<sms * 8, 256, 0, st>>>(p, n, salt); break;
+        case 2: {  // rows x 1024 columns, like cfg3
+            const uint64_t cols = 1024, rows = n / cols;
+            row_tiles<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(p, rows, cols, salt);
+            break;
+        }
+        case 3: bulk_contiguous<<<sms * 4, 128, 0, st>>>(p, n, salt); break;
+        default: return -1;
+    }
     return (int)cudaGetLastError();
 }
