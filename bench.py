@@ -42,7 +42,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--flags", type=int, default=0, help="prngd flags (A/B of store paths)")
+    ap.add_argument("--flags", type=int, default=0, help="extra prngd flags")
+    ap.add_argument("--store", default="row", choices=["row", "tma", "tile", "direct"],
+                    help="store path A/B (include/prngd.h PRNGD_FLAG_STORE_*)")
     return ap.parse_args()
 
 
@@ -223,7 +225,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     p = workload_params(args.workload, rank, world)
-    p["flags"] = args.flags
+    p["flags"] = args.flags | P.STORE_FLAGS[args.store]
     consume = args.workload == "cfg5"
     g = P.Generator(**p)
     nout = p["n_streams"] * p["n_per_stream"]
@@ -293,7 +295,8 @@ def main():
     achieved = bytes_launch / (kern_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-            "kernel": "gen_kernel<FULL32,SPEC,TMA>" if not consume else "consume_kernel+finalize",
+            "kernel": f"gen_kernel<FULL32,SPEC,{args.store.upper()}>" if not consume
+                      else "consume_kernel+finalize",
             "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kern_ms,
             "frac_of_8TBs_nominal": achieved / 8000.0}
 
@@ -343,7 +346,7 @@ def main():
                        "seed": p["seed"], "bytes_written_per_step_per_gpu": 8 * nout,
                        "l2": "inputs none; 8 B/output written, >126 MB L2 per step (no flush)",
                        "parallelism": f"stream-range shards x{world}",
-                       "flags": args.flags},
+                       "flags": p["flags"], "store": args.store},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -55,12 +55,21 @@ typedef enum {
 /* flags */
 #define PRNGD_FLAG_IEEE_DIV   0x1u  /* use the IEEE division instruction sequence instead of the
                                        reciprocal + 2 FMA correction (R10); same bits, slower */
-#define PRNGD_FLAG_NO_TMA     0x2u  /* store path A/B: stage each warp batch in shared memory and
-                                       write it with warp-coalesced 16-byte st.global */
-#define PRNGD_FLAG_STORE_TMA  0x8u  /* store path A/B: stage in shared memory and write with one
-                                       TMA tensor store (cp.async.bulk.tensor.2d) per warp batch.
-                                       Default (neither flag): each lane writes its own row with
-                                       32-byte st.global.v4 straight from registers */
+/* Store-path selection, bits 3..5 (an A/B switch; every path writes the same bits):
+ *   ROW    (default) each warp stages 32 rows x 64 outputs in shared memory and writes every row
+ *          as one 512-byte burst (32 lanes x 16-byte st.global) -- DRAM-friendly row bursts
+ *   TMA    32 x 16-output warp tiles, one cp.async.bulk.tensor.2d store per 128-row CTA slab
+ *   TILE   32 x 16-output warp tiles written with warp-coalesced 16-byte st.global
+ *   DIRECT every lane writes its own row from registers with 32-byte st.global.v4
+ * A path whose alignment rules the output pointer / n_per_stream break falls back to the next
+ * legal one (ROW, TMA, TILE: 16-byte aligned output and even n_per_stream; DIRECT: 32-byte and
+ * n_per_stream % 4 == 0; otherwise 8-byte stores). */
+#define PRNGD_STORE_SHIFT        3
+#define PRNGD_STORE_MASK         (7u << PRNGD_STORE_SHIFT)
+#define PRNGD_FLAG_STORE_ROW     (0u << PRNGD_STORE_SHIFT)
+#define PRNGD_FLAG_STORE_TMA     (1u << PRNGD_STORE_SHIFT)
+#define PRNGD_FLAG_STORE_TILE    (2u << PRNGD_STORE_SHIFT)
+#define PRNGD_FLAG_STORE_DIRECT  (3u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_ALG1       0x4u  /* NEXT-2 reading of Alg. 1: a rejected x1 is
                                        redrawn alone (x2 is drawn only after acceptance) */
 

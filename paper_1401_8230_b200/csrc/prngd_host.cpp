@@ -114,9 +114,11 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         return fail(PRNGD_EINVAL, "n_streams * n_per_stream overflows (limit 2^62)");
     if (p->stream_begin > ~0ull - p->n_streams)
         return fail(PRNGD_EINVAL, "stream_begin + n_streams overflows 64 bits");
-    const uint32_t known =
-        PRNGD_FLAG_IEEE_DIV | PRNGD_FLAG_NO_TMA | PRNGD_FLAG_ALG1 | PRNGD_FLAG_STORE_TMA;
+    const uint32_t known = PRNGD_FLAG_IEEE_DIV | PRNGD_FLAG_ALG1 | PRNGD_STORE_MASK;
     if (p->flags & ~known) return fail(PRNGD_EUNSUPPORTED, "unknown flag bits 0x%x", p->flags & ~known);
+    if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 3)
+        return fail(PRNGD_EUNSUPPORTED, "unknown store path %u",
+                    (p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT);
 
     prngd_handle *h = new (std::nothrow) prngd_handle();
     if (!h) return fail(PRNGD_ENOMEM, "host allocation of the handle failed");
@@ -173,9 +175,12 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     pl.clamp = I.clamp != 0;
     pl.ieee_div = (p->flags & PRNGD_FLAG_IEEE_DIV) != 0;
     pl.alg1 = alg1;
-    pl.store = (p->flags & PRNGD_FLAG_NO_TMA)      ? Store::STG16
-               : (p->flags & PRNGD_FLAG_STORE_TMA) ? Store::TMA
-                                                   : Store::DIRECT;
+    switch (p->flags & PRNGD_STORE_MASK) {
+        case PRNGD_FLAG_STORE_TMA: pl.store = Store::TMA; break;
+        case PRNGD_FLAG_STORE_TILE: pl.store = Store::STG16; break;
+        case PRNGD_FLAG_STORE_DIRECT: pl.store = Store::DIRECT; break;
+        default: pl.store = Store::ROW; break;
+    }
     *out = h;
     return PRNGD_OK;
 }
@@ -217,6 +222,7 @@ static Plan plan_for(const prngd_handle *h, const void *out) {
     const bool a16 = (a & 15u) == 0 && (nps & 1u) == 0;
     const bool tma_ok = a16 && h->p.n_streams < (1ull << 31) && nps < (1ull << 31);
     if (pl.store == Store::DIRECT && !a32) pl.store = a16 ? Store::STG16 : Store::STG8;
+    if (pl.store == Store::ROW && !a16) pl.store = Store::STG8;
     if (pl.store == Store::TMA && !tma_ok) pl.store = a16 ? Store::STG16 : Store::STG8;
     if (pl.store == Store::STG16 && !a16) pl.store = Store::STG8;
     return pl;

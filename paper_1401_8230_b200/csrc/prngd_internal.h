@@ -26,11 +26,12 @@ struct GenArgs {
     double *pow_slab;       // [gridDim.x][4]
 };
 
-// How a warp's 32 x 16 batch reaches HBM:
+// How a warp's outputs reach HBM (include/prngd.h PRNGD_FLAG_STORE_*):
+//   ROW:    32 rows x 64 outputs staged in smem, each row written as one 512 B burst
 //   DIRECT: each lane stores its row segment from registers, 4 x 32-byte st.global.v4.f64
-//   TMA:    smem tile (128B swizzle) + one cp.async.bulk.tensor.2d store per warp batch
-//   STG16:  smem tile + warp-coalesced 16-byte st.global;  STG8: same with 8-byte stores
-enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3 };
+//   TMA:    32 x 16 smem tiles (128B swizzle) + one cp.async.bulk.tensor.2d store per CTA slab
+//   STG16:  32 x 16 smem tile + warp-coalesced 16-byte st.global;  STG8: 8-byte stores
+enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3, ROW = 4 };
 
 // Launch descriptors chosen by the host.
 struct Plan {

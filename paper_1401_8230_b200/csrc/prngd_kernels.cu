@@ -31,14 +31,28 @@ constexpr int kNBufTma = 2;                 // tiles per warp when the TMA store
 // consume-only path keep the batch in registers and need none.
 template <Store ST, bool WRITE>
 constexpr int ring() {
-    return !WRITE || ST == Store::DIRECT ? 0 : (ST == Store::TMA ? kNBufTma : 1);
+    return !WRITE || ST == Store::DIRECT || ST == Store::ROW ? 0 : (ST == Store::TMA ? kNBufTma : 1);
 }
-constexpr int kGenWarps = 4;                // warps per CTA, generate kernel
+constexpr int kGenWarps = 4;                // warps per CTA, generate kernel (tile paths)
+constexpr int kRowCols = 64;                // ROW path: outputs per row per burst (512 B)
+constexpr int kRowTileBytes = 32 * kRowCols * 8;  // 16 KiB per warp
+
+template <Store ST>
+constexpr int gen_warps() { return ST == Store::ROW ? 1 : kGenWarps; }
+template <Store ST>
+constexpr size_t gen_smem() {
+    return ST == Store::ROW ? 1024 + (size_t)kRowTileBytes
+                            : 1024 + (size_t)kGenWarps * (ST == Store::TMA ? 2 : 1) * kTileBytes;
+}
 constexpr int kConsWarpsTiles = 12;         // warps per CTA, consume kernel staging tiles in smem
 constexpr int kConsWarpsRegs = 24;          // warps per CTA, consume kernel without tiles (<= 85 regs)
 
+constexpr int kConsWarpsRow = 6;            // consume + ROW store: 6 x 16 KiB tiles + histogram
 template <Store ST, bool WRITE>
-constexpr int cons_warps() { return ring<ST, WRITE>() > 0 ? kConsWarpsTiles : kConsWarpsRegs; }
+constexpr int cons_warps() {
+    return (WRITE && ST == Store::ROW) ? kConsWarpsRow
+                                       : (ring<ST, WRITE>() > 0 ? kConsWarpsTiles : kConsWarpsRegs);
+}
 constexpr int kHistWords = 32768;           // 65536 u16 counters packed in pairs (128 KiB)
 
 // ------------------------------------------------------------------------------ PTX helpers
@@ -273,6 +287,51 @@ __device__ __forceinline__ void run_rows(const CUtensorMap *tmap, const GenArgs 
     }
 }
 
+// ROW store path: the warp stages kRowCols outputs of each of its 32 rows in a 16 KiB tile
+// (row r, 16-byte chunk c stored at chunk c ^ r: conflict-free both for the per-lane writes and
+// for the per-row reads), then writes every row as ONE 512-byte burst: 32 lanes x 16 bytes of
+// the same row per st.global.  Long per-row bursts are what keeps HBM writes efficient with
+// 2^20 independent row fronts (tools/pattern_sweep.py).
+template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, bool CONSUME, class Cons>
+__device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, uint32_t lane,
+                                               uint64_t row0, Cons &cons) {
+    Xs128 st = stream_start(g.seed, g.stream_begin + row0 + lane);
+    const bool live = (row0 + lane) < g.n_streams;
+    const uint32_t nrows = (g.n_streams - row0) < 32u ? (uint32_t)(g.n_streams - row0) : 32u;
+    const uint32_t my_row = tile + lane * (kRowCols * 8u);
+#pragma unroll 1
+    for (uint64_t col0 = 0; col0 < g.nps; col0 += kRowCols) {
+#pragma unroll 1
+        for (uint32_t b = 0; b < kRowCols / kCols; ++b) {
+            double q[kCols];
+            produce_batch<FULL32, SPEC, IEEE, ALG1>(st, q, g);
+            if (CONSUME && live) {
+                const uint64_t base = col0 + b * kCols;
+#pragma unroll
+                for (int i = 0; i < kCols; ++i)
+                    if (base + i < g.nps) cons.add(q[i]);
+            }
+#pragma unroll
+            for (int c = 0; c < kCols / 2; ++c) {
+                const uint32_t chunk = b * (kCols / 2) + c;  // logical 16-byte chunk of the row
+                sts_v2(my_row + ((chunk ^ lane) << 4), q[2 * c], q[2 * c + 1]);
+            }
+        }
+        __syncwarp();
+        const uint64_t col = col0 + 2 * lane;
+        if (col < g.nps) {
+            double *dst = g.out + row0 * g.nps + col;
+#pragma unroll 4
+            for (uint32_t r = 0; r < nrows; ++r) {
+                double a, b2;
+                lds_v2(tile + r * (kRowCols * 8u) + ((lane ^ r) << 4), a, b2);
+                stg_v2_cs(dst + (uint64_t)r * g.nps, a, b2);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 __device__ __forceinline__ uint32_t aligned_smem_base(uint8_t *raw) {
     return (smem_u32(raw) + 1023u) & ~1023u;
 }
@@ -280,12 +339,16 @@ __device__ __forceinline__ uint32_t aligned_smem_base(uint8_t *raw) {
 // ------------------------------------------------------------------------------ kernels
 // S1-S6.  Grid: one warp per 32 streams, kGenWarps warps per CTA.
 template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST>
-__global__ void __launch_bounds__(kGenWarps * 32)
+__global__ void __launch_bounds__(gen_warps<ST>() * 32)
     gen_kernel(const __grid_constant__ CUtensorMap tmap, const GenArgs g) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const uint64_t row0 = ((uint64_t)blockIdx.x * kGenWarps + warp) * 32u;
-    if constexpr (ST == Store::TMA) {
+    const uint64_t row0 = ((uint64_t)blockIdx.x * gen_warps<ST>() + warp) * 32u;
+    if constexpr (ST == Store::ROW) {
+        NoConsumer nc;
+        run_rows_burst<FULL32, SPEC, IEEE, ALG1, false>(g, aligned_smem_base(smem_raw), lane, row0,
+                                                        nc);
+    } else if constexpr (ST == Store::TMA) {
         // CTA-level staging: the 4 warps fill one 128-row x 16-column slab (16 KiB, two slots)
         // and thread 0 writes it with ONE tensor store per batch.  Warps past n_streams keep
         // computing (their rows are clipped by the TMA) so every thread reaches the barrier.
@@ -347,8 +410,12 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
 #pragma unroll 1
     for (uint64_t t = (uint64_t)blockIdx.x * kWarps + warp; t < n_tasks;
          t += (uint64_t)gridDim.x * kWarps) {
-        run_rows<FULL32, SPEC, IEEE, ALG1, ST, WRITE, true, NB>(&tmap, g, tiles, lane, t * 32u,
-                                                                 cons, it);
+        if constexpr (WRITE && ST == Store::ROW)
+            run_rows_burst<FULL32, SPEC, IEEE, ALG1, true>(
+                g, base + kHistWords * 4u + warp * kRowTileBytes, lane, t * 32u, cons);
+        else
+            run_rows<FULL32, SPEC, IEEE, ALG1, ST, WRITE, true, NB>(&tmap, g, tiles, lane, t * 32u,
+                                                                     cons, it);
     }
     if constexpr (WRITE && ST == Store::TMA) {
         if (lane == 0) bulk_wait_all();
@@ -518,13 +585,13 @@ static cudaError_t set_smem(K kernel, size_t bytes) {
 template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST>
 static cudaError_t gen_launch(const CUtensorMap &m, const GenArgs &g, cudaStream_t st) {
     auto k = gen_kernel<FULL32, SPEC, IEEE, ALG1, ST>;
-    const size_t smem = 1024 + (size_t)kGenWarps * ring<ST, true>() * kTileBytes;
+    const size_t smem = gen_smem<ST>();
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
     const uint64_t tasks = (g.n_streams + 31u) / 32u;
-    const uint64_t grid = (tasks + kGenWarps - 1) / kGenWarps;
+    const uint64_t grid = (tasks + gen_warps<ST>() - 1) / gen_warps<ST>();
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    k<<<(unsigned)grid, kGenWarps * 32, smem, st>>>(m, g);
+    k<<<(unsigned)grid, gen_warps<ST>() * 32, smem, st>>>(m, g);
     return cudaGetLastError();
 }
 
@@ -555,6 +622,7 @@ cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, i
         s = Store::STG16;  // descriptor refused: fall back to coalesced st.global (same bits)
     const bool f32 = is_full32(g);
     switch (s) {
+        case Store::ROW: return gen_dispatch_store<Store::ROW>(m, g, pl, f32, st);
         case Store::DIRECT: return gen_dispatch_store<Store::DIRECT>(m, g, pl, f32, st);
         case Store::TMA: return gen_dispatch_store<Store::TMA>(m, g, pl, f32, st);
         case Store::STG16: return gen_dispatch_store<Store::STG16>(m, g, pl, f32, st);
@@ -571,7 +639,9 @@ static cudaError_t cons_launch(const CUtensorMap &m, const GenArgs &g, int grid,
                                cudaStream_t st) {
     constexpr int kWarps = cons_warps<ST, WRITE>();
     auto k = consume_kernel<FULL32, SPEC, IEEE, ALG1, ST, WRITE>;
-    const size_t smem = 1024 + (size_t)kHistWords * 4u + (size_t)kWarps * ring<ST, WRITE>() * kTileBytes;
+    const size_t smem = 1024 + (size_t)kHistWords * 4u +
+                        (WRITE && ST == Store::ROW ? (size_t)kWarps * kRowTileBytes
+                                                   : (size_t)kWarps * ring<ST, WRITE>() * kTileBytes);
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
     k<<<grid, kWarps * 32, smem, st>>>(m, g);
@@ -606,7 +676,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
     g.hist_spill = reinterpret_cast<int64_t *>(sp + (size_t)num_sms * kHistWords * 4u);
     g.pow_slab = reinterpret_cast<double *>(sp + (size_t)num_sms * kHistWords * 4u + 65536u * 8u);
     const uint64_t tasks = (g.n_streams + 31u) / 32u;
-    const int kw = kConsWarpsTiles;  // grid sizing: the smaller CTA bounds the task count
+    const int kw = kConsWarpsRow;  // grid sizing: the smallest CTA bounds the task count
     int grid = num_sms;
     if ((uint64_t)grid * kw > tasks) grid = (int)((tasks + kw - 1) / kw);
     if (grid < 1) grid = 1;
@@ -621,6 +691,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
         if (s == Store::TMA && make_tmap(&m, d_out, g.n_streams, g.nps, 32u) != cudaSuccess)
             s = Store::STG16;
         switch (s) {
+            case Store::ROW: e = cons_dispatch<Store::ROW, true>(m, g, pl, f32, grid, st); break;
             case Store::DIRECT: e = cons_dispatch<Store::DIRECT, true>(m, g, pl, f32, grid, st); break;
             case Store::TMA: e = cons_dispatch<Store::TMA, true>(m, g, pl, f32, grid, st); break;
             case Store::STG16: e = cons_dispatch<Store::STG16, true>(m, g, pl, f32, grid, st); break;

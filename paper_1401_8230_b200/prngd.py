@@ -14,9 +14,13 @@ LIB_PATH = os.path.join(PKG, "libprngd_b200.so")
 
 PRNGD_OK, PRNGD_EINVAL, PRNGD_ECUDA, PRNGD_ENOMEM, PRNGD_EUNSUPPORTED = range(5)
 PRNGD_FLAG_IEEE_DIV = 0x1
-PRNGD_FLAG_NO_TMA = 0x2
 PRNGD_FLAG_ALG1 = 0x4
-PRNGD_FLAG_STORE_TMA = 0x8
+PRNGD_FLAG_STORE_ROW = 0 << 3
+PRNGD_FLAG_STORE_TMA = 1 << 3
+PRNGD_FLAG_STORE_TILE = 2 << 3
+PRNGD_FLAG_STORE_DIRECT = 3 << 3
+STORE_FLAGS = {"row": PRNGD_FLAG_STORE_ROW, "tma": PRNGD_FLAG_STORE_TMA,
+               "tile": PRNGD_FLAG_STORE_TILE, "direct": PRNGD_FLAG_STORE_DIRECT}
 
 EXPORTS = (
     "prngd_create", "prngd_destroy", "prngd_get_info", "prngd_generate", "prngd_generate_consume",

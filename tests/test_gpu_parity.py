@@ -45,8 +45,7 @@ def assert_same(gpu_out, ref):
 
 # ------------------------------------------------------------------ full-config parity
 
-@pytest.mark.parametrize("flags", [0, P.PRNGD_FLAG_NO_TMA, P.PRNGD_FLAG_STORE_TMA,
-                                   P.PRNGD_FLAG_IEEE_DIV])
+@pytest.mark.parametrize("flags", list(P.STORE_FLAGS.values()) + [P.PRNGD_FLAG_IEEE_DIV])
 def test_cfg1_bitwise(orc, flags):
     p = W.CONFIGS["cfg1"]
     _, out = gen(p, flags=flags)
@@ -118,7 +117,7 @@ def test_ragged_shapes(orc, ns, nps, base):
     assert_same(out, orc.generate(p)["out"])
 
 
-@pytest.mark.parametrize("flags", [0, P.PRNGD_FLAG_NO_TMA, P.PRNGD_FLAG_STORE_TMA])
+@pytest.mark.parametrize("flags", list(P.STORE_FLAGS.values()))
 @pytest.mark.parametrize("offset", [1, 2, 3])
 def test_misaligned_output_pointer(orc, flags, offset):
     """8-, 16- and 24-byte offsets: each store path falls back to the next legal one."""
@@ -131,7 +130,7 @@ def test_misaligned_output_pointer(orc, flags, offset):
     assert_same(buf[offset:], orc.generate(p)["out"])
 
 
-@pytest.mark.parametrize("flags", [0, P.PRNGD_FLAG_NO_TMA, P.PRNGD_FLAG_STORE_TMA])
+@pytest.mark.parametrize("flags", list(P.STORE_FLAGS.values()))
 @pytest.mark.parametrize("name", ["cfg2", "cfg4"])
 def test_store_paths_bitwise(orc, flags, name):
     p = W.config(name, n_streams=200, n_per_stream=100, flags=flags)
@@ -236,7 +235,7 @@ def test_fast_division_equals_ieee(par):
 
 # ------------------------------------------------------------------ fused consumer (S7)
 
-@pytest.mark.parametrize("flags", [0, P.PRNGD_FLAG_NO_TMA, P.PRNGD_FLAG_STORE_TMA])
+@pytest.mark.parametrize("flags", list(P.STORE_FLAGS.values()))
 @pytest.mark.parametrize("write", [False, True])
 @pytest.mark.parametrize("name", ["cfg1", "cfg2"])
 def test_consume_matches_oracle(orc, name, write, flags):

@@ -72,6 +72,40 @@ __global__ void __launch_bounds__(128) bulk_contiguous(double *p, uint64_t n, ui
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// The generator's row-major [rows][1024] layout, one warp per 32 rows, but each row receives
+// `burst` contiguous bytes at a time (the warp writes one row's burst back to back, 512 B per
+// instruction), so DRAM sees bursts of that size per row.  Occupancy can be limited with
+// dynamic shared memory padding.
+__global__ void __launch_bounds__(128) row_bursts(double *p, uint64_t rows, uint64_t cols,
+                                                  uint32_t burst_doubles, uint64_t salt) {
+    extern __shared__ uint8_t pad[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint64_t row0 = ((uint64_t)blockIdx.x * 4 + warp) * 32;
+    if (row0 >= rows) return;
+    if (salt == ~0ull) pad[threadIdx.x] = 0;  // keep the smem allocation alive
+    for (uint64_t c0 = 0; c0 < cols; c0 += burst_doubles) {
+        for (uint32_t r = 0; r < 32; ++r) {
+            for (uint32_t k = 2 * lane; k < burst_doubles; k += 64) {
+                const uint64_t e = (row0 + r) * cols + c0 + k;
+                asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p + e), "d"(hval(e, salt)),
+                             "d"(hval(e + 1, salt))
+                             : "memory");
+            }
+        }
+    }
+}
+
+extern "C" __attribute__((visibility("default"))) int wc_pattern(double *p, uint64_t n,
+                                                                 uint32_t burst_bytes,
+                                                                 uint32_t smem_pad, uint64_t salt,
+                                                                 void *stream) {
+    const uint64_t cols = 1024, rows = n / cols;
+    cudaFuncSetAttribute(row_bursts, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    row_bursts<<<(unsigned)((rows + 127) / 128), 128, smem_pad, (cudaStream_t)stream>>>(
+        p, rows, cols, burst_bytes / 8, salt);
+    return (int)cudaGetLastError();
+}
+
 extern "C" __attribute__((visibility("default"))) int wc_store(double *p, uint64_t n, int mode,
                                                                uint64_t salt, void *stream) {
     int sms = 0, dev = 0;
