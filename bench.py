@@ -41,9 +41,11 @@ def parse():
     ap.add_argument("--workload", default="cfg3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-write", action="store_true",
+                    help="consume workloads: fused histogram/moments only, outputs not stored")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flags", type=int, default=0, help="extra prngd flags")
-    ap.add_argument("--store", default="row", choices=["row", "tma", "tile", "direct"],
+    ap.add_argument("--store", default="row", choices=["row", "row1k", "tma", "tile", "direct"],
                     help="store path A/B (include/prngd.h PRNGD_FLAG_STORE_*)")
     return ap.parse_args()
 
@@ -239,7 +241,8 @@ def main():
     def step():
         if consume:
             hist.zero_(), pw.zero_(), cnt.zero_()
-            P.prngd_generate_consume(g.handle, out, hist, pw, cnt, stream)
+            P.prngd_generate_consume(g.handle, None if args.no_write else out, hist, pw, cnt,
+                                     stream)
             if world > 1:
                 dist.all_reduce(hist)
                 dist.all_reduce(pw)
@@ -346,7 +349,8 @@ def main():
                        "seed": p["seed"], "bytes_written_per_step_per_gpu": 8 * nout,
                        "l2": "inputs none; 8 B/output written, >126 MB L2 per step (no flush)",
                        "parallelism": f"stream-range shards x{world}",
-                       "flags": p["flags"], "store": args.store},
+                       "flags": p["flags"], "store": args.store,
+                       "write_outputs": not (consume and args.no_write)},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -70,6 +70,7 @@ typedef enum {
 #define PRNGD_FLAG_STORE_TMA     (1u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_TILE    (2u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_DIRECT  (3u << PRNGD_STORE_SHIFT)
+#define PRNGD_FLAG_STORE_ROW1K   (4u << PRNGD_STORE_SHIFT)  /* ROW with 1 KiB bursts (A/B) */
 #define PRNGD_FLAG_ALG1       0x4u  /* NEXT-2 reading of Alg. 1: a rejected x1 is
                                        redrawn alone (x2 is drawn only after acceptance) */
 

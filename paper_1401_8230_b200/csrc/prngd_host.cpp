@@ -116,7 +116,7 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         return fail(PRNGD_EINVAL, "stream_begin + n_streams overflows 64 bits");
     const uint32_t known = PRNGD_FLAG_IEEE_DIV | PRNGD_FLAG_ALG1 | PRNGD_STORE_MASK;
     if (p->flags & ~known) return fail(PRNGD_EUNSUPPORTED, "unknown flag bits 0x%x", p->flags & ~known);
-    if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 3)
+    if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 4)
         return fail(PRNGD_EUNSUPPORTED, "unknown store path %u",
                     (p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT);
 
@@ -179,6 +179,7 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         case PRNGD_FLAG_STORE_TMA: pl.store = Store::TMA; break;
         case PRNGD_FLAG_STORE_TILE: pl.store = Store::STG16; break;
         case PRNGD_FLAG_STORE_DIRECT: pl.store = Store::DIRECT; break;
+        case PRNGD_FLAG_STORE_ROW1K: pl.store = Store::ROW1K; break;
         default: pl.store = Store::ROW; break;
     }
     *out = h;
@@ -222,7 +223,7 @@ static Plan plan_for(const prngd_handle *h, const void *out) {
     const bool a16 = (a & 15u) == 0 && (nps & 1u) == 0;
     const bool tma_ok = a16 && h->p.n_streams < (1ull << 31) && nps < (1ull << 31);
     if (pl.store == Store::DIRECT && !a32) pl.store = a16 ? Store::STG16 : Store::STG8;
-    if (pl.store == Store::ROW && !a16) pl.store = Store::STG8;
+    if ((pl.store == Store::ROW || pl.store == Store::ROW1K) && !a16) pl.store = Store::STG8;
     if (pl.store == Store::TMA && !tma_ok) pl.store = a16 ? Store::STG16 : Store::STG8;
     if (pl.store == Store::STG16 && !a16) pl.store = Store::STG8;
     return pl;

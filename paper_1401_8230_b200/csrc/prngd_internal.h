@@ -31,7 +31,8 @@ struct GenArgs {
 //   DIRECT: each lane stores its row segment from registers, 4 x 32-byte st.global.v4.f64
 //   TMA:    32 x 16 smem tiles (128B swizzle) + one cp.async.bulk.tensor.2d store per CTA slab
 //   STG16:  32 x 16 smem tile + warp-coalesced 16-byte st.global;  STG8: 8-byte stores
-enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3, ROW = 4 };
+//   ROW1K:  as ROW with 128 outputs (1 KiB bursts) per row
+enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3, ROW = 4, ROW1K = 5 };
 
 // Launch descriptors chosen by the host.
 struct Plan {

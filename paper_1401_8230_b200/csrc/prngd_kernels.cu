@@ -31,18 +31,24 @@ constexpr int kNBufTma = 2;                 // tiles per warp when the TMA store
 // consume-only path keep the batch in registers and need none.
 template <Store ST, bool WRITE>
 constexpr int ring() {
-    return !WRITE || ST == Store::DIRECT || ST == Store::ROW ? 0 : (ST == Store::TMA ? kNBufTma : 1);
+    return !WRITE || ST == Store::DIRECT || ST == Store::ROW || ST == Store::ROW1K
+               ? 0
+               : (ST == Store::TMA ? kNBufTma : 1);
 }
 constexpr int kGenWarps = 4;                // warps per CTA, generate kernel (tile paths)
 constexpr int kRowCols = 64;                // ROW path: outputs per row per burst (512 B)
 constexpr int kRowTileBytes = 32 * kRowCols * 8;  // 16 KiB per warp
 
 template <Store ST>
-constexpr int gen_warps() { return ST == Store::ROW ? 1 : kGenWarps; }
+constexpr bool is_row() { return ST == Store::ROW || ST == Store::ROW1K; }
+template <Store ST>
+constexpr int row_cols() { return ST == Store::ROW1K ? 2 * kRowCols : kRowCols; }
+template <Store ST>
+constexpr int gen_warps() { return is_row<ST>() ? 1 : kGenWarps; }
 template <Store ST>
 constexpr size_t gen_smem() {
-    return ST == Store::ROW ? 1024 + (size_t)kRowTileBytes
-                            : 1024 + (size_t)kGenWarps * (ST == Store::TMA ? 2 : 1) * kTileBytes;
+    return is_row<ST>() ? 1024 + (size_t)32 * row_cols<ST>() * 8
+                        : 1024 + (size_t)kGenWarps * (ST == Store::TMA ? 2 : 1) * kTileBytes;
 }
 constexpr int kConsWarpsTiles = 12;         // warps per CTA, consume kernel staging tiles in smem
 constexpr int kConsWarpsRegs = 24;          // warps per CTA, consume kernel without tiles (<= 85 regs)
@@ -292,17 +298,18 @@ __device__ __forceinline__ void run_rows(const CUtensorMap *tmap, const GenArgs 
 // for the per-row reads), then writes every row as ONE 512-byte burst: 32 lanes x 16 bytes of
 // the same row per st.global.  Long per-row bursts are what keeps HBM writes efficient with
 // 2^20 independent row fronts (tools/pattern_sweep.py).
-template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, bool CONSUME, class Cons>
+template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, bool CONSUME, int RC = kRowCols,
+          class Cons>
 __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, uint32_t lane,
                                                uint64_t row0, Cons &cons) {
     Xs128 st = stream_start(g.seed, g.stream_begin + row0 + lane);
     const bool live = (row0 + lane) < g.n_streams;
     const uint32_t nrows = (g.n_streams - row0) < 32u ? (uint32_t)(g.n_streams - row0) : 32u;
-    const uint32_t my_row = tile + lane * (kRowCols * 8u);
+    const uint32_t my_row = tile + lane * (RC * 8u);
 #pragma unroll 1
-    for (uint64_t col0 = 0; col0 < g.nps; col0 += kRowCols) {
+    for (uint64_t col0 = 0; col0 < g.nps; col0 += RC) {
 #pragma unroll 1
-        for (uint32_t b = 0; b < kRowCols / kCols; ++b) {
+        for (uint32_t b = 0; b < RC / kCols; ++b) {
             double q[kCols];
             produce_batch<FULL32, SPEC, IEEE, ALG1>(st, q, g);
             if (CONSUME && live) {
@@ -318,14 +325,17 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
             }
         }
         __syncwarp();
-        const uint64_t col = col0 + 2 * lane;
-        if (col < g.nps) {
-            double *dst = g.out + row0 * g.nps + col;
+#pragma unroll
+        for (uint32_t h = 0; h < RC / kRowCols; ++h) {  // 512-byte halves of a 1 KiB burst
+            const uint64_t col = col0 + h * kRowCols + 2 * lane;
+            if (col < g.nps) {
+                double *dst = g.out + row0 * g.nps + col;
 #pragma unroll 4
-            for (uint32_t r = 0; r < nrows; ++r) {
-                double a, b2;
-                lds_v2(tile + r * (kRowCols * 8u) + ((lane ^ r) << 4), a, b2);
-                stg_v2_cs(dst + (uint64_t)r * g.nps, a, b2);
+                for (uint32_t r = 0; r < nrows; ++r) {
+                    double a, b2;
+                    lds_v2(tile + r * (RC * 8u) + (((h * 32u + lane) ^ r) << 4), a, b2);
+                    stg_v2_cs(dst + (uint64_t)r * g.nps, a, b2);
+                }
             }
         }
         __syncwarp();
@@ -344,10 +354,10 @@ __global__ void __launch_bounds__(gen_warps<ST>() * 32)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint64_t row0 = ((uint64_t)blockIdx.x * gen_warps<ST>() + warp) * 32u;
-    if constexpr (ST == Store::ROW) {
+    if constexpr (is_row<ST>()) {
         NoConsumer nc;
-        run_rows_burst<FULL32, SPEC, IEEE, ALG1, false>(g, aligned_smem_base(smem_raw), lane, row0,
-                                                        nc);
+        run_rows_burst<FULL32, SPEC, IEEE, ALG1, false, row_cols<ST>()>(
+            g, aligned_smem_base(smem_raw), lane, row0, nc);
     } else if constexpr (ST == Store::TMA) {
         // CTA-level staging: the 4 warps fill one 128-row x 16-column slab (16 KiB, two slots)
         // and thread 0 writes it with ONE tensor store per batch.  Warps past n_streams keep
@@ -623,6 +633,7 @@ cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, i
     const bool f32 = is_full32(g);
     switch (s) {
         case Store::ROW: return gen_dispatch_store<Store::ROW>(m, g, pl, f32, st);
+        case Store::ROW1K: return gen_dispatch_store<Store::ROW1K>(m, g, pl, f32, st);
         case Store::DIRECT: return gen_dispatch_store<Store::DIRECT>(m, g, pl, f32, st);
         case Store::TMA: return gen_dispatch_store<Store::TMA>(m, g, pl, f32, st);
         case Store::STG16: return gen_dispatch_store<Store::STG16>(m, g, pl, f32, st);
@@ -691,7 +702,8 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
         if (s == Store::TMA && make_tmap(&m, d_out, g.n_streams, g.nps, 32u) != cudaSuccess)
             s = Store::STG16;
         switch (s) {
-            case Store::ROW: e = cons_dispatch<Store::ROW, true>(m, g, pl, f32, grid, st); break;
+            case Store::ROW:
+            case Store::ROW1K: e = cons_dispatch<Store::ROW, true>(m, g, pl, f32, grid, st); break;
             case Store::DIRECT: e = cons_dispatch<Store::DIRECT, true>(m, g, pl, f32, grid, st); break;
             case Store::TMA: e = cons_dispatch<Store::TMA, true>(m, g, pl, f32, grid, st); break;
             case Store::STG16: e = cons_dispatch<Store::STG16, true>(m, g, pl, f32, grid, st); break;

@@ -19,8 +19,10 @@ PRNGD_FLAG_STORE_ROW = 0 << 3
 PRNGD_FLAG_STORE_TMA = 1 << 3
 PRNGD_FLAG_STORE_TILE = 2 << 3
 PRNGD_FLAG_STORE_DIRECT = 3 << 3
+PRNGD_FLAG_STORE_ROW1K = 4 << 3
 STORE_FLAGS = {"row": PRNGD_FLAG_STORE_ROW, "tma": PRNGD_FLAG_STORE_TMA,
-               "tile": PRNGD_FLAG_STORE_TILE, "direct": PRNGD_FLAG_STORE_DIRECT}
+               "tile": PRNGD_FLAG_STORE_TILE, "direct": PRNGD_FLAG_STORE_DIRECT,
+               "row1k": PRNGD_FLAG_STORE_ROW1K}
 
 EXPORTS = (
     "prngd_create", "prngd_destroy", "prngd_get_info", "prngd_generate", "prngd_generate_consume",
