@@ -290,7 +290,7 @@ def main():
     bytes_launch = 8 * nout
     tr = traffic_per_launch()
     traffic = None
-    if tr and tr.get("workload") == args.workload:
+    if tr and tr.get("workload") == args.workload and tr.get("store") == args.store:
         traffic = tr.get("dram_bytes_per_launch")
     if consume:
         # dominant kernel = fused generate+consume; its own duration needs the launch list.
