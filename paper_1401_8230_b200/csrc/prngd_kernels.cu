@@ -53,7 +53,8 @@ constexpr size_t gen_smem() {
 constexpr int kConsWarpsTiles = 12;         // warps per CTA, consume kernel staging tiles in smem
 constexpr int kConsWarpsRegs = 24;          // warps per CTA, consume kernel without tiles (<= 85 regs)
 
-constexpr int kConsWarpsRow = 6;            // consume + ROW store: 6 x 16 KiB tiles + histogram
+constexpr int kConsWarpsRow = 12;           // consume + ROW store: 12 x 8 KiB tiles + histogram
+constexpr int kConsRowCols = 32;            // consume + ROW store: 256-byte row bursts
 template <Store ST, bool WRITE>
 constexpr int cons_warps() {
     return (WRITE && ST == Store::ROW) ? kConsWarpsRow
@@ -115,27 +116,29 @@ struct Consumer {
         spill = sp;
     }
     // R16 for one output.  A word holds L + 65536*H (mod 2^32) exactly, as a sum of commutative
-    // increments.  The one thread whose atomicAdd carries the low field out (old low == 0xFFFF)
-    // or the word out of 32 bits (old + inc >= 2^32) records the carry in `spill`, which the
-    // finalize kernel adds back: L = low + 65536*cL, H = high + 65536*cW - cL.
+    // increments.  The one thread whose atomicAdd wraps the field it increments (that field of
+    // the new word is 0) records the carry in `spill`, which the finalize kernel adds back:
+    //   low field wrapped:  L gains 65536, the carry went into H (H -1), and if H was 0xFFFF the
+    //                       word wrapped too (H +65536);   high field wrapped: H gains 65536.
     __device__ __forceinline__ void add(double q) {
+        // power sums: the FMAs round once per term (compared at relative 1e-12, R16)
         const double z2 = __dmul_rn(q, q);
         s1 = __dadd_rn(s1, q);
         s2 = __dadd_rn(s2, z2);
-        s3 = __dadd_rn(s3, __dmul_rn(z2, q));
-        s4 = __dadd_rn(s4, __dmul_rn(z2, z2));
+        s3 = __fma_rn(z2, q, s3);
+        s4 = __fma_rn(z2, z2, s4);
         const uint32_t bin = bin16(q);
-        const uint32_t inc = (bin & 1u) ? 0x10000u : 1u;
-        const uint32_t old = atomicAdd(&hist[bin >> 1], inc);
-        const bool carry_lo = (inc == 1u) && ((old & 0xFFFFu) == 0xFFFFu);
-        const bool carry_word = old > 0xFFFFFFFFu - inc;
-        if (__builtin_expect(carry_lo || carry_word, 0)) {
-            unsigned long long *sp = reinterpret_cast<unsigned long long *>(spill);
-            if (carry_lo) {
-                atomicAdd(&sp[bin], 65536ull);
-                atomicAdd(&sp[bin | 1u], 0xFFFFFFFFFFFFFFFFull);  // -1
-            }
-            if (carry_word) atomicAdd(&sp[bin | 1u], 65536ull);
+        const uint32_t sh = (bin & 1u) << 4;
+        const uint32_t inc = 1u << sh;
+        const uint32_t nw = atomicAdd(&hist[bin >> 1], inc) + inc;
+        if (__builtin_expect(((nw >> sh) & 0xFFFFu) == 0u, 0)) carry(bin, nw);
+    }
+    __device__ __noinline__ void carry(uint32_t bin, uint32_t nw) {
+        unsigned long long *sp = reinterpret_cast<unsigned long long *>(spill);
+        atomicAdd(&sp[bin], 65536ull);
+        if ((bin & 1u) == 0u) {
+            atomicAdd(&sp[bin | 1u], 0xFFFFFFFFFFFFFFFFull);  // -1: the carry went into H
+            if (nw == 0u) atomicAdd(&sp[bin | 1u], 65536ull);  // ... and wrapped the word
         }
     }
 };
@@ -302,6 +305,7 @@ template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, bool CONSUME, int RC = k
           class Cons>
 __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, uint32_t lane,
                                                uint64_t row0, Cons &cons) {
+    constexpr uint32_t CPR = RC / 2;  // 16-byte chunks per row segment
     Xs128 st = stream_start(g.seed, g.stream_begin + row0 + lane);
     const bool live = (row0 + lane) < g.n_streams;
     const uint32_t nrows = (g.n_streams - row0) < 32u ? (uint32_t)(g.n_streams - row0) : 32u;
@@ -314,27 +318,48 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
             produce_batch<FULL32, SPEC, IEEE, ALG1>(st, q, g);
             if (CONSUME && live) {
                 const uint64_t base = col0 + b * kCols;
+                if (base + kCols <= g.nps) {
 #pragma unroll
-                for (int i = 0; i < kCols; ++i)
-                    if (base + i < g.nps) cons.add(q[i]);
+                    for (int i = 0; i < kCols; ++i) cons.add(q[i]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kCols; ++i)
+                        if (base + i < g.nps) cons.add(q[i]);
+                }
             }
 #pragma unroll
             for (int c = 0; c < kCols / 2; ++c) {
                 const uint32_t chunk = b * (kCols / 2) + c;  // logical 16-byte chunk of the row
-                sts_v2(my_row + ((chunk ^ lane) << 4), q[2 * c], q[2 * c + 1]);
+                sts_v2(my_row + ((chunk ^ (lane & (CPR - 1))) << 4), q[2 * c], q[2 * c + 1]);
             }
         }
         __syncwarp();
+        if constexpr (CPR >= 32) {
+            // one row per instruction: 32 lanes x 16 B = 512 B of the same row
 #pragma unroll
-        for (uint32_t h = 0; h < RC / kRowCols; ++h) {  // 512-byte halves of a 1 KiB burst
-            const uint64_t col = col0 + h * kRowCols + 2 * lane;
-            if (col < g.nps) {
-                double *dst = g.out + row0 * g.nps + col;
+            for (uint32_t h = 0; h < CPR / 32; ++h) {
+                const uint64_t col = col0 + 2 * (h * 32 + lane);
+                if (col < g.nps) {
+                    double *dst = g.out + row0 * g.nps + col;
 #pragma unroll 4
-                for (uint32_t r = 0; r < nrows; ++r) {
+                    for (uint32_t r = 0; r < nrows; ++r) {
+                        double a, b2;
+                        lds_v2(tile + r * (RC * 8u) + (((h * 32u + lane) ^ r) << 4), a, b2);
+                        stg_v2_cs(dst + (uint64_t)r * g.nps, a, b2);
+                    }
+                }
+            }
+        } else {
+            // 32 / CPR rows per instruction, CPR lanes per row
+            const uint32_t c = lane % CPR, rsub = lane / CPR;
+            const uint64_t col = col0 + 2 * c;
+#pragma unroll 4
+            for (uint32_t r0 = 0; r0 < 32; r0 += 32 / CPR) {
+                const uint32_t r = r0 + rsub;
+                if (r < nrows && col < g.nps) {
                     double a, b2;
-                    lds_v2(tile + r * (RC * 8u) + (((h * 32u + lane) ^ r) << 4), a, b2);
-                    stg_v2_cs(dst + (uint64_t)r * g.nps, a, b2);
+                    lds_v2(tile + r * (RC * 8u) + ((c ^ (r & (CPR - 1))) << 4), a, b2);
+                    stg_v2_cs(g.out + (row0 + r) * g.nps + col, a, b2);
                 }
             }
         }
@@ -421,8 +446,8 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     for (uint64_t t = (uint64_t)blockIdx.x * kWarps + warp; t < n_tasks;
          t += (uint64_t)gridDim.x * kWarps) {
         if constexpr (WRITE && ST == Store::ROW)
-            run_rows_burst<FULL32, SPEC, IEEE, ALG1, true>(
-                g, base + kHistWords * 4u + warp * kRowTileBytes, lane, t * 32u, cons);
+            run_rows_burst<FULL32, SPEC, IEEE, ALG1, true, kConsRowCols>(
+                g, base + kHistWords * 4u + warp * (32u * kConsRowCols * 8u), lane, t * 32u, cons);
         else
             run_rows<FULL32, SPEC, IEEE, ALG1, ST, WRITE, true, NB>(&tmap, g, tiles, lane, t * 32u,
                                                                      cons, it);
@@ -651,7 +676,7 @@ static cudaError_t cons_launch(const CUtensorMap &m, const GenArgs &g, int grid,
     constexpr int kWarps = cons_warps<ST, WRITE>();
     auto k = consume_kernel<FULL32, SPEC, IEEE, ALG1, ST, WRITE>;
     const size_t smem = 1024 + (size_t)kHistWords * 4u +
-                        (WRITE && ST == Store::ROW ? (size_t)kWarps * kRowTileBytes
+                        (WRITE && ST == Store::ROW ? (size_t)kWarps * 32 * kConsRowCols * 8
                                                    : (size_t)kWarps * ring<ST, WRITE>() * kTileBytes);
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
