@@ -215,8 +215,11 @@ uint32_t prngd_last_launches(const prngd_handle *h) { return h ? h->last_launche
 
 // Store path for this output pointer: the requested one when its alignment rules hold, else
 // the next one that is legal (same bits whichever path writes them).
-static Plan plan_for(const prngd_handle *h, const void *out) {
+static Plan plan_for(const prngd_handle *h, const void *out, bool consume = false) {
     Plan pl = h->plan;
+    // Fused consumer + outputs: the smem histogram leaves no room for row tiles at full
+    // occupancy, so the default there is the register (DIRECT) store (measured best).
+    if (consume && (h->p.flags & PRNGD_STORE_MASK) == PRNGD_FLAG_STORE_ROW) pl.store = Store::DIRECT;
     const uintptr_t a = (uintptr_t)out;
     const uint64_t nps = h->p.n_per_stream;
     const bool a32 = (a & 31u) == 0 && (nps & 3u) == 0;
@@ -281,7 +284,7 @@ prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64
         h->cons_bytes = need;
     }
     int launches = 0;
-    cudaError_t e = prngd::launch_generate_consume(h->args, plan_for(h, d_out), d_out, d_hist,
+    cudaError_t e = prngd::launch_generate_consume(h->args, plan_for(h, d_out, true), d_out, d_hist,
                                                    d_pow, d_count, h->cons_scratch,
                                                    h->cons_bytes, (cudaStream_t)cuda_stream, sms,
                                                    &launches);
