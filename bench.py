@@ -56,10 +56,9 @@ def dist_env():
 
 
 def workload_params(name: str, rank: int, world: int) -> dict:
-    p = W.config(name)
-    # per-GPU shard of the global stream space: rank r owns [r*n, (r+1)*n)
-    p["stream_begin"] = rank * p["n_streams"]
-    return p
+    from paper_1401_8230_b200 import dist as D
+    # per-GPU shard of the global stream space: rank r owns [r*n, (r+1)*n) (weak scaling)
+    return D.shard_params(W.config(name), rank, world, D.WEAK)
 
 
 def peaks():
@@ -217,6 +216,7 @@ def main():
 
     import torch
     import torch.distributed as dist
+    from paper_1401_8230_b200 import dist as D
     from paper_1401_8230_b200 import prngd as P
 
     if not torch.cuda.is_available():
@@ -243,10 +243,8 @@ def main():
             hist.zero_(), pw.zero_(), cnt.zero_()
             P.prngd_generate_consume(g.handle, None if args.no_write else out, hist, pw, cnt,
                                      stream)
-            if world > 1:
-                dist.all_reduce(hist)
-                dist.all_reduce(pw)
-                dist.all_reduce(cnt)
+            if world > 1:  # the path's only exchange: NCCL all-reduce of the statistics
+                D.allreduce_stats(hist, pw, cnt)
         else:
             P.prngd_generate(g.handle, out, stream)
 
