@@ -15,7 +15,7 @@ _CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-
 __all__ = [
     "build", "lib", "mix64", "splitmix64_output", "xs128_sequence", "stream_state", "constants",
     "map_pairs", "map_pairs_noclamp", "accept", "generate", "raw", "enumerate_pairs",
-    "map_eq5", "map_eq6", "GAMMA",
+    "map_eq5", "map_eq6", "map_kind", "GAMMA",
 ]
 
 GAMMA = 0x9E3779B97F4A7C15
@@ -62,6 +62,11 @@ def lib():
         L.oracle_generate.restype = i32
         L.oracle_generate.argtypes = [u32, u64, u64, u64, u64, u64, u64, u64, u64,
                                       vp, vp, vp, vp, vp, vp]
+        L.oracle_generate_ex.restype = i32
+        L.oracle_generate_ex.argtypes = [u32, u64, u64, u64, u64, u64, u64, u64, u64, i32, i32, i32,
+                                         vp, vp, vp, vp, vp, vp]
+        L.oracle_map_kind.restype = dbl
+        L.oracle_map_kind.argtypes = [i32, i32, u32, u64, u64, u64, u64, u32, u32]
         L.oracle_raw.restype = None
         L.oracle_raw.argtypes = [u64, u64, u64, u64, vp]
         L.oracle_enumerate.restype = i32
@@ -121,8 +126,14 @@ def accept(p: dict, x1: int) -> bool:
 
 
 def generate(p: dict, stream_begin: int | None = None, n_streams: int | None = None,
-             want_out=True, want_pidx=False, want_consumed=False, want_stats=False) -> dict:
-    """Run the whole oracle path on streams [stream_begin, stream_begin+n_streams)."""
+             want_out=True, want_pidx=False, want_consumed=False, want_stats=False,
+             kind: int | None = None, alg1: bool | None = None, open_interval: bool | None = None
+             ) -> dict:
+    """Run the whole oracle path on streams [stream_begin, stream_begin+n_streams).
+    kind / alg1 / open_interval default to p["map"] (4), p["alg1"], p["open"] (False)."""
+    kind = p.get("map", 4) if kind is None else kind
+    alg1 = p.get("alg1", False) if alg1 is None else alg1
+    open_interval = p.get("open", False) if open_interval is None else open_interval
     sb = p.get("stream_begin", 0) if stream_begin is None else stream_begin
     ns = p["n_streams"] if n_streams is None else n_streams
     nps = p["n_per_stream"]
@@ -133,8 +144,10 @@ def generate(p: dict, stream_begin: int | None = None, n_streams: int | None = N
     hist = np.zeros(65536, dtype=np.int64) if want_stats else None
     pw = np.zeros(4, dtype=np.float64) if want_stats else None
     cnt = np.zeros(1, dtype=np.int64) if want_stats else None
-    rc = lib().oracle_generate(p["w"], p["a0"], p["a"], p["b0"], p["b"], p["seed"], sb, ns, nps,
-                               _ptr(out), _ptr(pidx), _ptr(cons), _ptr(hist), _ptr(pw), _ptr(cnt))
+    rc = lib().oracle_generate_ex(p["w"], p["a0"], p["a"], p["b0"], p["b"], p["seed"], sb, ns, nps,
+                                  int(kind), int(bool(alg1)), int(bool(open_interval)),
+                                  _ptr(out), _ptr(pidx), _ptr(cons), _ptr(hist), _ptr(pw),
+                                  _ptr(cnt))
     if rc:
         raise ValueError("invalid parameters")
     if want_out:
@@ -164,6 +177,14 @@ def enumerate_pairs(p: dict):
     if rc:
         raise ValueError("invalid parameters or widths too large")
     return q.reshape(n1, n2), acc.reshape(n1, n2).astype(bool)
+
+
+def map_kind(p: dict, kind: int, x1, x2, open_interval: bool = False) -> np.ndarray:
+    x1 = np.asarray(x1, dtype=np.uint32).ravel()
+    x2 = np.asarray(x2, dtype=np.uint32).ravel()
+    f = lib().oracle_map_kind
+    return np.array([f(kind, int(open_interval), p["w"], p["a0"], p["a"], p["b0"], p["b"],
+                       int(a), int(b)) for a, b in zip(x1, x2)], dtype=np.float64)
 
 
 def map_eq5(p: dict, x1: int, x2: int) -> float:

@@ -119,32 +119,62 @@ int oracle_accept(uint64_t a0, uint64_t a, uint32_t x1)
     return (uint64_t)x1 > a0 && (uint64_t)x1 < a;
 }
 
-int oracle_generate(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64_t b,
-                    uint64_t seed, uint64_t stream_begin, uint64_t n_streams, uint64_t n_per_stream,
-                    double *out, uint32_t *pidx, uint64_t *consumed,
-                    int64_t *hist, double *pw, int64_t *count)
+double oracle_map_kind(int kind, int open_interval, uint32_t w, uint64_t a0, uint64_t a,
+                       uint64_t b0, uint64_t b, uint32_t x1, uint32_t x2)
+{
+    double q;
+    if (kind == 5) q = oracle_map_eq5(w, a0, a, b0, b, x1, x2);
+    else if (kind == 6) q = oracle_map_eq6(w, x1, x2);
+    else q = oracle_map_noclamp(w, a0, a, b0, b, x1, x2);
+    if (q >= 1.0) q = 0x1.fffffffffffffp-1;   /* R11 for every mapping */
+    if (open_interval) q = 1.0 - q;           /* P:159-161 "use 1-z instead of z" */
+    return q;
+}
+
+int oracle_generate_ex(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64_t b,
+                       uint64_t seed, uint64_t stream_begin, uint64_t n_streams,
+                       uint64_t n_per_stream, int kind, int alg1, int open_interval,
+                       double *out, uint32_t *pidx, uint64_t *consumed,
+                       int64_t *hist, double *pw, int64_t *count)
 {
     if (!valid(w, a0, a, b0, b)) return 1;
+    if (kind != 4 && kind != 5 && kind != 6) return 1;
+    if (kind == 6 && !(a0 == 0 && b0 == 0 && a == (1ull << w) - 1 && b == a)) return 1;
     int sh1 = 32 - bitlen(a); /* R4: x = top bits of the 32-bit draw */
     int sh2 = 32 - bitlen(b);
     for (uint64_t i = 0; i < n_streams; i++) {
         uint32_t st[4];
         oracle_stream_state(seed, stream_begin + i, st);
-        uint64_t p = 0; /* pairs consumed so far */
+        uint64_t p = 0; /* pairs (R2) or draws (Alg. 1) consumed so far */
         for (uint64_t j = 0; j < n_per_stream; j++) {
             uint32_t x1, x2;
-            do { /* R2: pair-drop -- a rejected x1 discards its whole pair */
-                uint32_t u1 = oracle_xs128_next(st);
-                uint32_t u2 = oracle_xs128_next(st);
-                x1 = u1 >> sh1;
-                x2 = u2 >> sh2;
+            if (alg1) {
+                /* NEXT-2, Alg. 1: redraw R1 alone until accepted, then draw R2 */
+                do {
+                    x1 = oracle_xs128_next(st) >> sh1;
+                    p++;
+                } while (!oracle_accept(a0, a, x1));
+                x2 = oracle_xs128_next(st) >> sh2;
                 p++;
-            } while (!oracle_accept(a0, a, x1));
-            double q = oracle_map(w, a0, a, b0, b, x1, x2);
+            } else {
+                do { /* R2: pair-drop -- a rejected x1 discards its whole pair */
+                    uint32_t u1 = oracle_xs128_next(st);
+                    uint32_t u2 = oracle_xs128_next(st);
+                    x1 = u1 >> sh1;
+                    x2 = u2 >> sh2;
+                    p++;
+                } while (!oracle_accept(a0, a, x1));
+            }
+            double q = oracle_map_kind(kind, open_interval, w, a0, a, b0, b, x1, x2);
             uint64_t o = i * n_per_stream + j; /* R15: stream-major layout */
             if (out) out[o] = q;
-            if (pidx) pidx[o] = (uint32_t)(p - 1);
-            if (hist) hist[(uint32_t)(q * 65536.0)]++;         /* R16 */
+            /* pair index (R2), or index of the accepted x1 draw (Alg. 1) */
+            if (pidx) pidx[o] = (uint32_t)(alg1 ? p - 2 : p - 1);
+            if (hist) {
+                uint32_t bin = (uint32_t)(q * 65536.0);              /* R16 */
+                if (bin > 65535u) bin = 65535u;                      /* R18: q = 1 (open) */
+                hist[bin]++;
+            }
             if (pw) {
                 double z2 = q * q;
                 pw[0] += q;
@@ -157,6 +187,15 @@ int oracle_generate(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64_t b
         if (consumed) consumed[i] = p;
     }
     return 0;
+}
+
+int oracle_generate(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64_t b,
+                    uint64_t seed, uint64_t stream_begin, uint64_t n_streams, uint64_t n_per_stream,
+                    double *out, uint32_t *pidx, uint64_t *consumed,
+                    int64_t *hist, double *pw, int64_t *count)
+{
+    return oracle_generate_ex(w, a0, a, b0, b, seed, stream_begin, n_streams, n_per_stream,
+                              4, 0, 0, out, pidx, consumed, hist, pw, count);
 }
 
 void oracle_raw(uint64_t seed, uint64_t stream_begin, uint64_t n_streams, uint64_t draws,

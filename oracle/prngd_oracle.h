@@ -75,6 +75,19 @@ int oracle_generate(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64_t b
                     double *out, uint32_t *pidx, uint64_t *consumed,
                     int64_t *hist, double *pw, int64_t *count);
 
+/* Generalised whole path: kind = 4 (Eq.(4)), 5 (Eq.(5)) or 6 (Eq.(6), P:149-157,
+ * full unit-interval range only); alg1 != 0 consumes draws as Alg. 1 does (redraw x1 alone,
+ * P:115-120; consumed[] then counts draws and pidx[] holds the accepted x1's draw index);
+ * open_interval != 0 returns 1 - z'.  Histogram bin of q = 1.0 is 65535 (R18). */
+int oracle_generate_ex(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64_t b,
+                       uint64_t seed, uint64_t stream_begin, uint64_t n_streams,
+                       uint64_t n_per_stream, int kind, int alg1, int open_interval,
+                       double *out, uint32_t *pidx, uint64_t *consumed,
+                       int64_t *hist, double *pw, int64_t *count);
+/* One pair through mapping `kind` (4/5/6) + clamp (R11) [+ 1 - z' when open_interval]. */
+double oracle_map_kind(int kind, int open_interval, uint32_t w, uint64_t a0, uint64_t a,
+                       uint64_t b0, uint64_t b, uint32_t x1, uint32_t x2);
+
 /* Raw base draws: raw[i][d] = d-th xorshift128 output of global stream stream_begin+i. */
 void oracle_raw(uint64_t seed, uint64_t stream_begin, uint64_t n_streams, uint64_t draws,
                 uint32_t *raw);

@@ -357,3 +357,75 @@ def test_eq5_eq6_exact_rational(orc, w):
             assert abs(Fraction(q5) - E) <= tol and abs(Fraction(q6) - E) <= 2 * tol
     assert orc.map_eq5(p, 1, 0) == 0.0
     assert orc.map_eq5(p, n - 2, n - 1) == float(1 - kp)
+
+
+# ----------------------------------------------------------------------------- NEXT-1/2 whole path
+
+def test_alg1_z_formula_is_eq4():
+    """Alg. 1's Z with min/max equals Eq.(4) with a0 = b0 = min, a = b = max (R2 note)."""
+    import random
+    rnd = random.Random(3)
+    for w in (3, 8, 32):
+        k = Fraction(1, 2**w)
+        mn, mx = 0, 2**w - 1
+        p = dict(w=w, a0=mn, a=mx, b0=mn, b=mx)
+        for _ in range(200):
+            r1, r2 = rnd.randrange(1, mx), rnd.randrange(0, mx + 1)
+            z_alg1 = (r1 + k * r2 - (mn + k * mx)) / ((mx - mn) * (1 - k))
+            assert z_alg1 == exact_eq4(p, r1, r2)
+
+
+def test_alg1_consumption_matches_raw_draws(orc):
+    """Alg. 1: x1 is redrawn alone until accepted, then one x2 is drawn."""
+    p = W.config("cfg2", n_streams=4, n_per_stream=200, alg1=True)
+    r = orc.generate(p, want_pidx=True, want_consumed=True)
+    raw = orc.raw(p["seed"], 0, 4, int(r["consumed"].max()))
+    for s in range(4):
+        d, outs, idx = 0, [], []
+        while len(outs) < 200:
+            x1 = raw[s, d] >> 24
+            if 0 < x1 < 255:
+                x2 = raw[s, d + 1] >> 24
+                outs.append(((int(x1) << 8) + int(x2) - 255) / 65025.0)
+                idx.append(d)
+                d += 2
+            else:
+                d += 1
+        assert np.array_equal(r["out"][s], np.array(outs)) and list(r["pidx"][s]) == idx
+        assert r["consumed"][s] == d
+
+
+@pytest.mark.parametrize("kind", [5, 6])
+def test_eq5_eq6_whole_path_uses_the_mapping(orc, kind):
+    p = W.config("cfg2", n_streams=8, n_per_stream=100, map=kind)
+    r = orc.generate(p, want_pidx=True)
+    raw = orc.raw(p["seed"], 0, 8, 2 * (int(r["pidx"].max()) + 1))
+    for s in range(8):
+        x1 = raw[s, 2 * r["pidx"][s]] >> 24
+        x2 = raw[s, 2 * r["pidx"][s] + 1] >> 24
+        assert np.array_equal(r["out"][s], orc.map_kind(p, kind, x1, x2))
+    # Eq.(5)/(6) include z' = 0 (P:133-134) and stay below 1
+    q, acc = orc.enumerate_pairs(W.BYTE8)
+    x1, x2 = np.nonzero(acc)
+    v = orc.map_kind(W.BYTE8, kind, x1, x2)
+    assert v.min() == 0.0 and v.max() < 1.0 and np.unique(v).size == 65024
+
+
+def test_open_interval_never_zero(orc):
+    """P:159-161: 1 - z' excludes 0; exact (Sterbenz) for z' >= 1/2."""
+    q, acc = orc.enumerate_pairs(W.BYTE8)
+    x1, x2 = np.nonzero(acc)
+    for kind in (4, 5):
+        z = orc.map_kind(W.BYTE8, kind, x1, x2)
+        o = orc.map_kind(W.BYTE8, kind, x1, x2, open_interval=True)
+        assert o.min() > 0.0 and o.max() <= 1.0
+        big = z >= 0.5
+        assert np.array_equal(o[big], 1.0 - z[big])
+    assert orc.map_kind(W.BYTE8, 5, [1], [0], open_interval=True)[0] == 1.0
+
+
+def test_eq5_w32_reaches_one_and_is_clamped(orc):
+    """At w=32 (1 - k') rounds to 1, so Eq.(5)'s top pair needs the R11 clamp as well."""
+    top = 2**32 - 1
+    assert orc.map_eq5(W.FULL32, top - 1, top) == 1.0
+    assert orc.map_kind(W.FULL32, 5, [top - 1], [top])[0] == float.fromhex("0x1.fffffffffffffp-1")
