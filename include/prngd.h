@@ -71,6 +71,16 @@ typedef enum {
 #define PRNGD_FLAG_STORE_TILE    (2u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_DIRECT  (3u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_ROW1K   (4u << PRNGD_STORE_SHIFT)  /* ROW with 1 KiB bursts (A/B) */
+/* Mapping selection, bits 6..7 (NEXT-1): Eq.(4) (default), Eq.(5) discrete-grid normalisation
+ * onto [0; 1-k'], or Eq.(6) unit-interval form (requires a0 = b0 = 0 and
+ * a = b = 2^w - 1).  All three are followed by the R11 clamp (z' <= 1 - 2^-53). */
+#define PRNGD_MAP_SHIFT          6
+#define PRNGD_MAP_MASK           (3u << PRNGD_MAP_SHIFT)
+#define PRNGD_FLAG_MAP_EQ4       (0u << PRNGD_MAP_SHIFT)
+#define PRNGD_FLAG_MAP_EQ5       (1u << PRNGD_MAP_SHIFT)
+#define PRNGD_FLAG_MAP_EQ6       (2u << PRNGD_MAP_SHIFT)
+#define PRNGD_FLAG_OPEN          0x100u  /* return 1 - z': never 0; the histogram puts
+                                            1.0 in bin 65535 (R18) */
 #define PRNGD_FLAG_ALG1       0x4u  /* NEXT-2 reading of Alg. 1: a rejected x1 is
                                        redrawn alone (x2 is drawn only after acceptance) */
 

@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "prngd_internal.h"
+
 namespace prngd {
 
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;      // SplitMix64 increment
@@ -75,9 +77,35 @@ __device__ __forceinline__ double eq4_pair(uint32_t x1, uint32_t x2, uint32_t w,
     return eq4_scaled<IEEE_DIV, CLAMP>(((uint64_t)x1 << w) | (uint64_t)x2, Cs, Ds, y);
 }
 
+// ---- S5 for every mapping the library offers (runtime-uniform selection) -------------------
+//   kind 4  Eq.(4):  q = RN(RN(v) - C_s) / D_s                         v = x1*2^w + x2
+//   kind 5  Eq.(5):  q = RN(RN(v5) / D_s) * RN(1 - k^2)                  v5 = (x1-a0-1)*2^w + x2
+//   kind 6  Eq.(6):  q = RN(RN(1 - k^2) * RN(RN(v) - 2^w)) / D_s
+// each followed by the R11 clamp and, for the open interval, 1 - q.  Every 2^w
+// rescaling is exact, so each is bit-identical to the literal unscaled evaluation.
+
+template <bool IEEE_DIV, bool CLAMP>
+__device__ __forceinline__ double map_pair(uint32_t x1, uint32_t x2, const MapArgs &m) {
+    const uint64_t v = ((uint64_t)(x1 - m.sub) << m.w) | (uint64_t)x2;
+    double n = __dsub_rn(__ull2double_rn(v), m.Cs);
+    if (m.kind == 6) n = __dmul_rn(n, m.scale);
+    double q;
+    if (IEEE_DIV) {
+        q = __ddiv_rn(n, m.Ds);
+    } else {
+        const double q0 = __dmul_rn(n, m.y);
+        const double r = __fma_rn(-q0, m.Ds, n);
+        q = __fma_rn(r, m.y, q0);
+    }
+    if (m.kind == 5) q = __dmul_rn(q, m.scale);
+    if (CLAMP) q = fmin(q, kBelowOne);
+    if (m.open) q = __dsub_rn(1.0, q);
+    return q;
+}
+
 // ---- S7: bin of the 2^16-bin histogram (R16): exact scaling by 2^16, truncation -------------
 __device__ __forceinline__ uint32_t bin16(double q) {
-    return (uint32_t)__double2uint_rz(__dmul_rn(q, 65536.0));
+    return min((uint32_t)__double2uint_rz(__dmul_rn(q, 65536.0)), 65535u);  // R18: q = 1 (open)
 }
 
 }  // namespace prngd

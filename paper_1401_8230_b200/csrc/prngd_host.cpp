@@ -114,8 +114,13 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         return fail(PRNGD_EINVAL, "n_streams * n_per_stream overflows (limit 2^62)");
     if (p->stream_begin > ~0ull - p->n_streams)
         return fail(PRNGD_EINVAL, "stream_begin + n_streams overflows 64 bits");
-    const uint32_t known = PRNGD_FLAG_IEEE_DIV | PRNGD_FLAG_ALG1 | PRNGD_STORE_MASK;
+    const uint32_t known = PRNGD_FLAG_IEEE_DIV | PRNGD_FLAG_ALG1 | PRNGD_STORE_MASK |
+                           PRNGD_MAP_MASK | PRNGD_FLAG_OPEN;
     if (p->flags & ~known) return fail(PRNGD_EUNSUPPORTED, "unknown flag bits 0x%x", p->flags & ~known);
+    const uint32_t map_code = (p->flags & PRNGD_MAP_MASK) >> PRNGD_MAP_SHIFT;
+    if (map_code > 2) return fail(PRNGD_EUNSUPPORTED, "unknown mapping code %u", map_code);
+    if (map_code == 2 && !(p->a0 == 0 && p->b0 == 0 && p->a == (1ull << w) - 1 && p->b == p->a))
+        return fail(PRNGD_EINVAL, "Eq.(6) needs the unit-interval range a0=b0=0, a=b=2^w-1");
     if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 4)
         return fail(PRNGD_EUNSUPPORTED, "unknown store path %u",
                     (p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT);
@@ -138,11 +143,34 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     I.y = 1.0 / I.D_s;                                 // RN(1/D_s)
     I.sh1 = 32u - (uint32_t)bit_length(p->a);
     I.sh2 = 32u - (uint32_t)bit_length(p->b);
-    // R11: the map is monotone, so the largest accepted pair (a-1, b) bounds every output.
+
+    // Mapping constants (scaled by 2^w, R10) for Eq.(4), Eq.(5) or Eq.(6).
+    const uint32_t kind = map_code == 1 ? 5u : (map_code == 2 ? 6u : 4u);
+    volatile double kk = k * k;                          // k' = k^2 (exact)
+    const double scale = 1.0 - kk;                       // RN(1 - k')
+    double Ds = I.D_s, Cs = I.C_s;
+    uint32_t sub = 0;
+    if (kind == 5) {  // den = trunc[(a-a0-2k)/k] + b - b0, in units of k
+        volatile double kb5 = k * ((double)p->b - (double)p->b0);
+        const double den = (double)(p->a - p->a0 - 2) + kb5;
+        Ds = std::ldexp(den, (int)w);
+        Cs = 0.0;
+        sub = (uint32_t)(p->a0 + 1);
+    } else if (kind == 6) {  // den = trunc[1/k] - 2 - k
+        volatile double d1 = std::ldexp(1.0, (int)w) - 2.0;
+        const double den = d1 - k;
+        Ds = std::ldexp(den, (int)w);
+        Cs = std::ldexp(1.0, (int)w);                    // the "- 1" of Eq.(6), scaled
+    }
+    const double y = 1.0 / Ds;                           // RN(1/D_s)
+    if (kind == 4) I.y = y;
+    // R11: every mapping is monotone, so the largest accepted pair (a-1, b) bounds every output.
     {
-        const uint64_t v = ((p->a - 1) << w) | p->b;
-        volatile double n = (double)v - I.C_s;
-        const double qmax = n / I.D_s;
+        const uint64_t v = ((p->a - 1 - sub) << w) | p->b;
+        volatile double n = (double)v - Cs;
+        if (kind == 6) n = n * scale;
+        volatile double qmax = n / Ds;
+        if (kind == 5) qmax = qmax * scale;
         I.clamp = qmax >= 1.0 ? 1u : 0u;
     }
     // Rejection probability per attempt: (draw values outside (a0, a)) / 2^bitlen(a).
@@ -169,6 +197,14 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     g.lo = (uint32_t)(p->a0 + 1);
     g.span = (uint32_t)(p->a - p->a0 - 1);
     g.span_fast = g.span - I.clamp;
+    g.map.Cs = Cs;
+    g.map.Ds = Ds;
+    g.map.y = y;
+    g.map.scale = scale;
+    g.map.w = w;
+    g.map.sub = sub;
+    g.map.kind = kind;
+    g.map.open = (p->flags & PRNGD_FLAG_OPEN) ? 1u : 0u;
 
     Plan &pl = h->plan;
     pl.spec = I.speculative != 0;

@@ -8,6 +8,13 @@
 
 namespace prngd {
 
+// Mapping constants of the generic kernels (prngd_device.cuh map_pair): Eq.(4)/(5)/(6) scaled by
+// 2^w (R10) plus the open-interval switch.
+struct MapArgs {
+    double Cs, Ds, y, scale;
+    uint32_t w, sub, kind, open;
+};
+
 // Everything a generator kernel needs, by value in the kernel parameter bank.
 struct GenArgs {
     uint64_t seed;          // SplitMix64 seed (R6)
@@ -20,6 +27,7 @@ struct GenArgs {
     uint32_t sh1, sh2;      // draw widths, x = u >> sh (R4)
     uint32_t lo, span;      // accept iff (x1 - lo) < span  <=>  a0 < x1 < a   (R3)
     uint32_t span_fast;     // span - clamp: speculative band excluding x1 = a - 1 when R11 applies
+    MapArgs map;            // mapping of the generic kernels (Eq.(4)/(5)/(6), open interval)
     // consumer (S7)
     uint32_t *hist_slab;    // [gridDim.x][32768] packed u16 pairs (consume kernels only)
     int64_t *hist_spill;    // [65536] int64 carries of the packed counters

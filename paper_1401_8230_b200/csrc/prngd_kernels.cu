@@ -165,7 +165,7 @@ __device__ __forceinline__ double exact_output(Xs128 &st, uint32_t sh1, uint32_t
             x2 = draw(st) >> sh2;
         } while (!accepted(x1, lo, span));
     }
-    return eq4_pair<IEEE, true>(x1, x2, w, g.Cs, g.Ds, g.y);
+    return map_pair<IEEE, true>(x1, x2, g.map);
 }
 
 // kCols consecutive outputs of this lane's stream, into registers q[0..kCols).
@@ -189,7 +189,8 @@ __device__ __forceinline__ void produce_batch(Xs128 &st, double (&q)[kCols], con
             const uint32_t x1 = draw(st) >> sh1;
             const uint32_t x2 = draw(st) >> sh2;
             rej |= !accepted(x1, lo, span_fast);
-            q[i] = eq4_pair<IEEE, false>(x1, x2, w, g.Cs, g.Ds, g.y);
+            q[i] = FULL32 ? eq4_pair<IEEE, false>(x1, x2, 32u, g.Cs, g.Ds, g.y)
+                          : map_pair<IEEE, false>(x1, x2, g.map);
         }
         if (__builtin_expect(!__any_sync(0xFFFFFFFFu, rej), 1)) return;
         st = saved;
@@ -552,7 +553,7 @@ __global__ void debug_map_kernel(const GenArgs g, const uint32_t *x1, const uint
                                  double *z, uint64_t n) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
-        z[i] = eq4_pair<IEEE, true>(x1[i], x2[i], g.w, g.Cs, g.Ds, g.y);
+        z[i] = map_pair<IEEE, true>(x1[i], x2[i], g.map);
 }
 
 __global__ void debug_div_check_kernel(const GenArgs g, uint64_t n, uint64_t seed,
@@ -646,7 +647,8 @@ static cudaError_t gen_dispatch_store(const CUtensorMap &m, const GenArgs &g, co
 }
 
 static bool is_full32(const GenArgs &g) {
-    return g.w == 32 && g.sh1 == 0 && g.sh2 == 0 && g.lo == 1u && g.span == 0xFFFFFFFEu;
+    return g.w == 32 && g.sh1 == 0 && g.sh2 == 0 && g.lo == 1u && g.span == 0xFFFFFFFEu &&
+           g.map.kind == 4 && g.map.open == 0 && g.span_fast == 0xFFFFFFFDu;
 }
 
 cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, int) {

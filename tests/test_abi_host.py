@@ -71,7 +71,7 @@ def test_create_rejects_bad_counts(lib, counts):
 
 def test_create_rejects_unknown_flags(lib):
     with pytest.raises(P.PrngdError) as e:
-        P.prngd_create(**W.FULL32, seed=1, n_streams=1, n_per_stream=2, flags=0x100)
+        P.prngd_create(**W.FULL32, seed=1, n_streams=1, n_per_stream=2, flags=0x10000)
     assert e.value.status == P.PRNGD_EUNSUPPORTED
 
 
@@ -127,3 +127,24 @@ def test_generate_without_gpu_fails_loudly(lib):
         assert st in (P.PRNGD_ECUDA, P.PRNGD_EUNSUPPORTED)
     finally:
         P.prngd_destroy(h)
+
+
+def test_eq6_requires_unit_interval(lib):
+    with pytest.raises(P.PrngdError) as e:
+        P.prngd_create(**W.ASYM, seed=1, n_streams=1, n_per_stream=2, flags=P.PRNGD_FLAG_MAP_EQ6)
+    assert e.value.status == P.PRNGD_EINVAL
+    h = P.prngd_create(**W.FULL32, seed=1, n_streams=1, n_per_stream=2, flags=P.PRNGD_FLAG_MAP_EQ6)
+    P.prngd_destroy(h)
+
+
+@pytest.mark.parametrize("kind,w,clamp", [(5, 8, 0), (5, 32, 1), (6, 8, 0), (6, 32, 1)])
+def test_clamp_flag_for_eq5_eq6(lib, orc, kind, w, clamp):
+    p = dict(w=w, a0=0, a=2**w - 1, b0=0, b=2**w - 1)
+    h = P.prngd_create(**p, seed=1, n_streams=1, n_per_stream=2, flags=P.MAP_FLAGS[kind])
+    try:
+        assert P.prngd_get_info(h)["clamp"] == clamp
+    finally:
+        P.prngd_destroy(h)
+    top = 2**w - 1
+    raw = orc.map_eq5(p, top - 1, top) if kind == 5 else orc.map_eq6(w, top - 1, top)
+    assert (raw >= 1.0) == bool(clamp)

@@ -303,3 +303,59 @@ def test_cfg4_histogram_full_size_consistent():
     assert cnt.item() == 2**32
     del out, flat
     torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ NEXT-1 / NEXT-2 variants
+
+VARIANTS = [(k, o) for k in (4, 5, 6) for o in (False, True)]
+
+
+@pytest.mark.parametrize("kind,open_", VARIANTS)
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_mappings_bitwise(orc, name, kind, open_):
+    """Eq.(5)/(6) and the open interval 1 - z' through the whole path."""
+    flags = P.MAP_FLAGS[kind] | (P.PRNGD_FLAG_OPEN if open_ else 0)
+    p = W.config(name, n_streams=512, n_per_stream=256)
+    _, out = gen(p, flags=flags)
+    ref = orc.generate(p, kind=kind, open_interval=open_)["out"]
+    assert_same(out, ref)
+    if open_:
+        assert bool((out > 0).all()) and bool((out <= 1).all())
+    else:
+        assert bool((out >= 0).all()) and bool((out < 1).all())
+
+
+@pytest.mark.parametrize("kind,open_", VARIANTS)
+def test_mappings_exhaustive_w8(orc, kind, open_):
+    flags = P.MAP_FLAGS[kind] | (P.PRNGD_FLAG_OPEN if open_ else 0)
+    g = P.Generator(**W.BYTE8, seed=1, n_streams=1, n_per_stream=2, flags=flags)
+    x1, x2 = np.meshgrid(np.arange(1, 255, dtype=np.uint32), np.arange(256, dtype=np.uint32),
+                         indexing="ij")
+    z = g.map(torch.from_numpy(x1.ravel()).cuda(), torch.from_numpy(x2.ravel()).cuda())
+    torch.cuda.synchronize()
+    assert_same(z, orc.map_kind(W.BYTE8, kind, x1.ravel(), x2.ravel(), open_interval=open_))
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_alg1_consumption_bitwise(orc, name):
+    p = W.config(name, n_streams=512, n_per_stream=256, flags=P.PRNGD_FLAG_ALG1)
+    g, out = gen(p)
+    ref = orc.generate(p, alg1=True, want_pidx=True, want_consumed=True)
+    assert_same(out, ref["out"])
+    pidx, cons = g.pairs()
+    torch.cuda.synchronize()
+    assert np.array_equal(pidx.cpu().numpy().view(np.uint32), ref["pidx"])
+    assert np.array_equal(cons.cpu().numpy().view(np.uint64), ref["consumed"])
+
+
+@pytest.mark.parametrize("kind", [5, 4])
+def test_open_interval_histogram_top_bin(orc, kind):
+    """R18: with 1 - z' the value 1.0 (from z' = 0 in Eq.(5)) lands in bin 65535."""
+    flags = P.MAP_FLAGS[kind] | P.PRNGD_FLAG_OPEN
+    p = W.config("cfg2", n_streams=1024, n_per_stream=512, flags=flags)
+    g = P.Generator(**p)
+    _, hist, pw, cnt = g.generate_consume()
+    torch.cuda.synchronize()
+    ref = orc.generate(p, kind=kind, open_interval=True, want_out=False, want_stats=True)
+    assert np.array_equal(hist.cpu().numpy(), ref["hist"]) and cnt.item() == ref["count"]
+    assert np.allclose(pw.cpu().numpy(), ref["pow"], rtol=1e-12, atol=0)
