@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--workload", default="cfg3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--consume", action="store_true",
+                    help="add the fused consumer (S7) to a write workload (cfg5 always has it)")
     ap.add_argument("--no-write", action="store_true",
                     help="consume workloads: fused histogram/moments only, outputs not stored")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -228,7 +230,7 @@ def main():
 
     p = workload_params(args.workload, rank, world)
     p["flags"] = args.flags | P.STORE_FLAGS[args.store]
-    consume = args.workload == "cfg5"
+    consume = args.workload == "cfg5" or args.consume
     g = P.Generator(**p)
     nout = p["n_streams"] * p["n_per_stream"]
     out = torch.empty((p["n_streams"], p["n_per_stream"]), dtype=torch.float64, device="cuda")
