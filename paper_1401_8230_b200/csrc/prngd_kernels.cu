@@ -150,7 +150,7 @@ struct NoConsumer {
 
 // ------------------------------------------------------------------------------ one batch
 // One pair of the exact path: draw until accepted, then Eq.(1)+(4) with the clamp.
-template <bool IEEE, bool ALG1>
+template <bool EQ4, bool IEEE, bool ALG1>
 __device__ __forceinline__ double exact_output(Xs128 &st, uint32_t sh1, uint32_t sh2, uint32_t w,
                                                uint32_t lo, uint32_t span, const GenArgs &g) {
     uint32_t x1, x2;
@@ -165,12 +165,16 @@ __device__ __forceinline__ double exact_output(Xs128 &st, uint32_t sh1, uint32_t
             x2 = draw(st) >> sh2;
         } while (!accepted(x1, lo, span));
     }
-    return map_pair<IEEE, true>(x1, x2, g.map);
+    return EQ4 ? eq4_pair<IEEE, true>(x1, x2, w, g.Cs, g.Ds, g.y) : map_pair<IEEE, true>(x1, x2, g.map);
 }
 
 // kCols consecutive outputs of this lane's stream, into registers q[0..kCols).
-template <bool FULL32, bool SPEC, bool IEEE, bool ALG1>
+template <int MODE, bool SPEC, bool IEEE, bool ALG1>
 __device__ __forceinline__ void produce_batch(Xs128 &st, double (&q)[kCols], const GenArgs &g) {
+    // MODE 2: w = 32 full range, Eq.(4) closed (every constant compiled in); MODE 1: Eq.(4)
+    // closed with runtime ranges; MODE 0: any mapping (runtime-uniform selection).
+    constexpr bool FULL32 = MODE == 2;
+    constexpr bool EQ4 = MODE >= 1;
     const uint32_t sh1 = FULL32 ? 0u : g.sh1;
     const uint32_t sh2 = FULL32 ? 0u : g.sh2;
     const uint32_t w = FULL32 ? 32u : g.w;
@@ -189,14 +193,14 @@ __device__ __forceinline__ void produce_batch(Xs128 &st, double (&q)[kCols], con
             const uint32_t x1 = draw(st) >> sh1;
             const uint32_t x2 = draw(st) >> sh2;
             rej |= !accepted(x1, lo, span_fast);
-            q[i] = FULL32 ? eq4_pair<IEEE, false>(x1, x2, 32u, g.Cs, g.Ds, g.y)
-                          : map_pair<IEEE, false>(x1, x2, g.map);
+            q[i] = EQ4 ? eq4_pair<IEEE, false>(x1, x2, w, g.Cs, g.Ds, g.y)
+                       : map_pair<IEEE, false>(x1, x2, g.map);
         }
         if (__builtin_expect(!__any_sync(0xFFFFFFFFu, rej), 1)) return;
         st = saved;
     }
 #pragma unroll
-    for (int i = 0; i < kCols; ++i) q[i] = exact_output<IEEE, ALG1>(st, sh1, sh2, w, lo, span, g);
+    for (int i = 0; i < kCols; ++i) q[i] = exact_output<EQ4, IEEE, ALG1>(st, sh1, sh2, w, lo, span, g);
 }
 
 __device__ __forceinline__ void stg_v4_cs(double *p, double a, double b, double c, double d) {
@@ -234,7 +238,7 @@ __device__ __forceinline__ void flush_stg(uint32_t tile, uint32_t lane, const Ge
 
 // One warp-task: streams [row0, row0 + 32), all nps columns.  `it` counts batches issued by
 // this warp (tile ring position).
-template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE, bool CONSUME,
+template <int MODE, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE, bool CONSUME,
           int NB, class Cons>
 __device__ __forceinline__ void run_rows(const CUtensorMap *tmap, const GenArgs &g,
                                          uint32_t tiles, uint32_t lane, uint64_t row0,
@@ -245,7 +249,7 @@ __device__ __forceinline__ void run_rows(const CUtensorMap *tmap, const GenArgs 
 #pragma unroll 1
     for (uint64_t col0 = 0; col0 < g.nps; col0 += kCols, ++it) {
         double q[kCols];
-        produce_batch<FULL32, SPEC, IEEE, ALG1>(st, q, g);
+        produce_batch<MODE, SPEC, IEEE, ALG1>(st, q, g);
         // Outputs past nps in the last batch are computed but neither stored nor counted.
         const bool full = g.nps - col0 >= (uint64_t)kCols;
         const uint32_t valid = full ? (uint32_t)kCols : (uint32_t)(g.nps - col0);
@@ -302,7 +306,7 @@ __device__ __forceinline__ void run_rows(const CUtensorMap *tmap, const GenArgs 
 // for the per-row reads), then writes every row as ONE 512-byte burst: 32 lanes x 16 bytes of
 // the same row per st.global.  Long per-row bursts are what keeps HBM writes efficient with
 // 2^20 independent row fronts (tools/pattern_sweep.py).
-template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, bool CONSUME, int RC = kRowCols,
+template <int MODE, bool SPEC, bool IEEE, bool ALG1, bool CONSUME, int RC = kRowCols,
           class Cons>
 __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, uint32_t lane,
                                                uint64_t row0, Cons &cons) {
@@ -316,7 +320,7 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
 #pragma unroll 1
         for (uint32_t b = 0; b < RC / kCols; ++b) {
             double q[kCols];
-            produce_batch<FULL32, SPEC, IEEE, ALG1>(st, q, g);
+            produce_batch<MODE, SPEC, IEEE, ALG1>(st, q, g);
             if (CONSUME && live) {
                 const uint64_t base = col0 + b * kCols;
                 if (base + kCols <= g.nps) {
@@ -374,7 +378,7 @@ __device__ __forceinline__ uint32_t aligned_smem_base(uint8_t *raw) {
 
 // ------------------------------------------------------------------------------ kernels
 // S1-S6.  Grid: one warp per 32 streams, kGenWarps warps per CTA.
-template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST>
+template <int MODE, bool SPEC, bool IEEE, bool ALG1, Store ST>
 __global__ void __launch_bounds__(gen_warps<ST>() * 32)
     gen_kernel(const __grid_constant__ CUtensorMap tmap, const GenArgs g) {
     extern __shared__ uint8_t smem_raw[];
@@ -382,7 +386,7 @@ __global__ void __launch_bounds__(gen_warps<ST>() * 32)
     const uint64_t row0 = ((uint64_t)blockIdx.x * gen_warps<ST>() + warp) * 32u;
     if constexpr (is_row<ST>()) {
         NoConsumer nc;
-        run_rows_burst<FULL32, SPEC, IEEE, ALG1, false, row_cols<ST>()>(
+        run_rows_burst<MODE, SPEC, IEEE, ALG1, false, row_cols<ST>()>(
             g, aligned_smem_base(smem_raw), lane, row0, nc);
     } else if constexpr (ST == Store::TMA) {
         // CTA-level staging: the 4 warps fill one 128-row x 16-column slab (16 KiB, two slots)
@@ -396,7 +400,7 @@ __global__ void __launch_bounds__(gen_warps<ST>() * 32)
 #pragma unroll 1
         for (uint64_t col0 = 0; col0 < g.nps; col0 += kCols, slot ^= 1u) {
             double q[kCols];
-            produce_batch<FULL32, SPEC, IEEE, ALG1>(st, q, g);
+            produce_batch<MODE, SPEC, IEEE, ALG1>(st, q, g);
             const uint32_t tile = my_tile + slot * (kGenWarps * kTileBytes);
 #pragma unroll
             for (int c = 0; c < kCols / 2; ++c)
@@ -419,14 +423,14 @@ __global__ void __launch_bounds__(gen_warps<ST>() * 32)
         if (row0 >= g.n_streams) return;
         uint32_t it = 0;
         NoConsumer nc;
-        run_rows<FULL32, SPEC, IEEE, ALG1, ST, true, false, NB>(&tmap, g, tiles, lane, row0, nc,
+        run_rows<MODE, SPEC, IEEE, ALG1, ST, true, false, NB>(&tmap, g, tiles, lane, row0, nc,
                                                                 it);
     }
 }
 
 // S1-S7, persistent: one CTA per SM owning a 128 KiB packed histogram; warps take 32-stream
 // tasks round-robin.  Writes per-CTA slabs that finalize_kernel reduces.
-template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE>
+template <int MODE, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE>
 __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     consume_kernel(const __grid_constant__ CUtensorMap tmap, const GenArgs g) {
     constexpr int kWarps = cons_warps<ST, WRITE>();
@@ -447,10 +451,10 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     for (uint64_t t = (uint64_t)blockIdx.x * kWarps + warp; t < n_tasks;
          t += (uint64_t)gridDim.x * kWarps) {
         if constexpr (WRITE && ST == Store::ROW)
-            run_rows_burst<FULL32, SPEC, IEEE, ALG1, true, kConsRowCols>(
+            run_rows_burst<MODE, SPEC, IEEE, ALG1, true, kConsRowCols>(
                 g, base + kHistWords * 4u + warp * (32u * kConsRowCols * 8u), lane, t * 32u, cons);
         else
-            run_rows<FULL32, SPEC, IEEE, ALG1, ST, WRITE, true, NB>(&tmap, g, tiles, lane, t * 32u,
+            run_rows<MODE, SPEC, IEEE, ALG1, ST, WRITE, true, NB>(&tmap, g, tiles, lane, t * 32u,
                                                                      cons, it);
     }
     if constexpr (WRITE && ST == Store::TMA) {
@@ -618,9 +622,9 @@ static cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST>
+template <int MODE, bool SPEC, bool IEEE, bool ALG1, Store ST>
 static cudaError_t gen_launch(const CUtensorMap &m, const GenArgs &g, cudaStream_t st) {
-    auto k = gen_kernel<FULL32, SPEC, IEEE, ALG1, ST>;
+    auto k = gen_kernel<MODE, SPEC, IEEE, ALG1, ST>;
     const size_t smem = gen_smem<ST>();
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
@@ -633,22 +637,27 @@ static cudaError_t gen_launch(const CUtensorMap &m, const GenArgs &g, cudaStream
 
 template <Store ST>
 static cudaError_t gen_dispatch_store(const CUtensorMap &m, const GenArgs &g, const Plan &pl,
-                                      bool full32, cudaStream_t st) {
-    if (full32 && pl.spec && !pl.ieee_div && !pl.alg1)
-        return gen_launch<true, true, false, false, ST>(m, g, st);
+                                      int mode, cudaStream_t st) {
+    if (pl.spec && !pl.ieee_div && !pl.alg1) {
+        if (mode == 2) return gen_launch<2, true, false, false, ST>(m, g, st);
+        if (mode == 1) return gen_launch<1, true, false, false, ST>(m, g, st);
+    }
     if (pl.alg1)
-        return pl.ieee_div ? gen_launch<false, false, true, true, ST>(m, g, st)
-                           : gen_launch<false, false, false, true, ST>(m, g, st);
+        return pl.ieee_div ? gen_launch<0, false, true, true, ST>(m, g, st)
+                           : gen_launch<0, false, false, true, ST>(m, g, st);
     if (pl.spec)
-        return pl.ieee_div ? gen_launch<false, true, true, false, ST>(m, g, st)
-                           : gen_launch<false, true, false, false, ST>(m, g, st);
-    return pl.ieee_div ? gen_launch<false, false, true, false, ST>(m, g, st)
-                       : gen_launch<false, false, false, false, ST>(m, g, st);
+        return pl.ieee_div ? gen_launch<0, true, true, false, ST>(m, g, st)
+                           : gen_launch<0, true, false, false, ST>(m, g, st);
+    return pl.ieee_div ? gen_launch<0, false, true, false, ST>(m, g, st)
+                       : gen_launch<0, false, false, false, ST>(m, g, st);
 }
 
-static bool is_full32(const GenArgs &g) {
-    return g.w == 32 && g.sh1 == 0 && g.sh2 == 0 && g.lo == 1u && g.span == 0xFFFFFFFEu &&
-           g.map.kind == 4 && g.map.open == 0 && g.span_fast == 0xFFFFFFFDu;
+// Kernel specialisation: 2 = w = 32 full range Eq.(4) closed, 1 = Eq.(4) closed, 0 = generic.
+static int kernel_mode(const GenArgs &g) {
+    const bool eq4 = g.map.kind == 4 && g.map.open == 0;
+    const bool full32 = eq4 && g.w == 32 && g.sh1 == 0 && g.sh2 == 0 && g.lo == 1u &&
+                        g.span == 0xFFFFFFFEu && g.span_fast == 0xFFFFFFFDu;
+    return full32 ? 2 : (eq4 ? 1 : 0);
 }
 
 cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, int) {
@@ -657,7 +666,7 @@ cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, i
     Store s = pl.store;
     if (s == Store::TMA && make_tmap(&m, g.out, g.n_streams, g.nps, 32u * kGenWarps) != cudaSuccess)
         s = Store::STG16;  // descriptor refused: fall back to coalesced st.global (same bits)
-    const bool f32 = is_full32(g);
+    const int f32 = kernel_mode(g);
     switch (s) {
         case Store::ROW: return gen_dispatch_store<Store::ROW>(m, g, pl, f32, st);
         case Store::ROW1K: return gen_dispatch_store<Store::ROW1K>(m, g, pl, f32, st);
@@ -672,11 +681,11 @@ size_t consume_scratch_bytes(int num_sms) {
     return (size_t)num_sms * kHistWords * 4u + 65536u * 8u + (size_t)num_sms * 4u * 8u;
 }
 
-template <bool FULL32, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE>
+template <int MODE, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE>
 static cudaError_t cons_launch(const CUtensorMap &m, const GenArgs &g, int grid,
                                cudaStream_t st) {
     constexpr int kWarps = cons_warps<ST, WRITE>();
-    auto k = consume_kernel<FULL32, SPEC, IEEE, ALG1, ST, WRITE>;
+    auto k = consume_kernel<MODE, SPEC, IEEE, ALG1, ST, WRITE>;
     const size_t smem = 1024 + (size_t)kHistWords * 4u +
                         (WRITE && ST == Store::ROW ? (size_t)kWarps * 32 * kConsRowCols * 8
                                                    : (size_t)kWarps * ring<ST, WRITE>() * kTileBytes);
@@ -688,17 +697,19 @@ static cudaError_t cons_launch(const CUtensorMap &m, const GenArgs &g, int grid,
 
 template <Store ST, bool WRITE>
 static cudaError_t cons_dispatch(const CUtensorMap &m, const GenArgs &g, const Plan &pl,
-                                 bool full32, int grid, cudaStream_t st) {
-    if (full32 && pl.spec && !pl.ieee_div && !pl.alg1)
-        return cons_launch<true, true, false, false, ST, WRITE>(m, g, grid, st);
+                                 int mode, int grid, cudaStream_t st) {
+    if (pl.spec && !pl.ieee_div && !pl.alg1) {
+        if (mode == 2) return cons_launch<2, true, false, false, ST, WRITE>(m, g, grid, st);
+        if (mode == 1) return cons_launch<1, true, false, false, ST, WRITE>(m, g, grid, st);
+    }
     if (pl.alg1)
-        return pl.ieee_div ? cons_launch<false, false, true, true, ST, WRITE>(m, g, grid, st)
-                           : cons_launch<false, false, false, true, ST, WRITE>(m, g, grid, st);
+        return pl.ieee_div ? cons_launch<0, false, true, true, ST, WRITE>(m, g, grid, st)
+                           : cons_launch<0, false, false, true, ST, WRITE>(m, g, grid, st);
     if (pl.spec)
-        return pl.ieee_div ? cons_launch<false, true, true, false, ST, WRITE>(m, g, grid, st)
-                           : cons_launch<false, true, false, false, ST, WRITE>(m, g, grid, st);
-    return pl.ieee_div ? cons_launch<false, false, true, false, ST, WRITE>(m, g, grid, st)
-                       : cons_launch<false, false, false, false, ST, WRITE>(m, g, grid, st);
+        return pl.ieee_div ? cons_launch<0, true, true, false, ST, WRITE>(m, g, grid, st)
+                           : cons_launch<0, true, false, false, ST, WRITE>(m, g, grid, st);
+    return pl.ieee_div ? cons_launch<0, false, true, false, ST, WRITE>(m, g, grid, st)
+                       : cons_launch<0, false, false, false, ST, WRITE>(m, g, grid, st);
 }
 
 cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d_out,
@@ -720,7 +731,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
     if (grid < 1) grid = 1;
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
-    const bool f32 = is_full32(g);
+    const int f32 = kernel_mode(g);
     cudaError_t e;
     if (!d_out) {
         e = cons_dispatch<Store::STG8, false>(m, g, pl, f32, grid, st);
