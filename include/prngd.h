@@ -81,6 +81,13 @@ typedef enum {
 #define PRNGD_FLAG_MAP_EQ6       (2u << PRNGD_MAP_SHIFT)
 #define PRNGD_FLAG_OPEN          0x100u  /* return 1 - z': never 0; the histogram puts
                                             1.0 in bin 65535 (R18) */
+/* NEXT-3 intra-stream parallelism: one warp per stream, lanes start at draws 0, 64, 128, ... of
+ * the stream via GF(2) jump-ahead of xorshift128 and a warp scan of accepted counts places every
+ * output exactly where the sequential order puts it.  Chosen automatically by prngd_generate
+ * when there are too few streams to fill the GPU (n_streams < 16384 and n_per_stream >= 512,
+ * pair-drop consumption); these flags force it on or off. */
+#define PRNGD_FLAG_JUMP          0x200u
+#define PRNGD_FLAG_NO_JUMP       0x400u
 #define PRNGD_FLAG_ALG1       0x4u  /* NEXT-2 reading of Alg. 1: a rejected x1 is
                                        redrawn alone (x2 is drawn only after acceptance) */
 
@@ -162,6 +169,12 @@ PRNGD_API prngd_status prngd_debug_pairs(const prngd_handle *h, uint32_t *d_pair
  * device mapping as the generator (no acceptance test).  n may be 0. */
 PRNGD_API prngd_status prngd_debug_map(const prngd_handle *h, const uint32_t *d_x1, const uint32_t *d_x2,
                              double *d_z, uint64_t n, void *cuda_stream);
+
+/* Host-only check of the jump-ahead: out = T^n_draws * in for the xorshift128 state
+ * (x, y, z, w) = in[0..3].  lane_table >= 0 applies instead the byte table the GPU uses for lane
+ * `lane_table` (= T^(64 * lane_table)); n_draws is then ignored.  No CUDA call. */
+PRNGD_API prngd_status prngd_debug_jump(uint64_t n_draws, const uint32_t *in, uint32_t *out,
+                                        int lane_table);
 
 /* d_mismatch[0] += number of n_s in the sample for which the reciprocal + 2 FMA quotient
  * differs from the IEEE division (R10).  Samples: n = RN(v) - C_s for v = x1*2^w + x2 with

@@ -115,7 +115,9 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     if (p->stream_begin > ~0ull - p->n_streams)
         return fail(PRNGD_EINVAL, "stream_begin + n_streams overflows 64 bits");
     const uint32_t known = PRNGD_FLAG_IEEE_DIV | PRNGD_FLAG_ALG1 | PRNGD_STORE_MASK |
-                           PRNGD_MAP_MASK | PRNGD_FLAG_OPEN;
+                           PRNGD_MAP_MASK | PRNGD_FLAG_OPEN | PRNGD_FLAG_JUMP | PRNGD_FLAG_NO_JUMP;
+    if ((p->flags & PRNGD_FLAG_JUMP) && (p->flags & (PRNGD_FLAG_NO_JUMP | PRNGD_FLAG_ALG1)))
+        return fail(PRNGD_EUNSUPPORTED, "jump-ahead needs pair-drop consumption and no NO_JUMP");
     if (p->flags & ~known) return fail(PRNGD_EUNSUPPORTED, "unknown flag bits 0x%x", p->flags & ~known);
     const uint32_t map_code = (p->flags & PRNGD_MAP_MASK) >> PRNGD_MAP_SHIFT;
     if (map_code > 2) return fail(PRNGD_EUNSUPPORTED, "unknown mapping code %u", map_code);
@@ -211,6 +213,9 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     pl.clamp = I.clamp != 0;
     pl.ieee_div = (p->flags & PRNGD_FLAG_IEEE_DIV) != 0;
     pl.alg1 = alg1;
+    pl.jump = (p->flags & PRNGD_FLAG_JUMP) ||
+              (!(p->flags & PRNGD_FLAG_NO_JUMP) && !alg1 && p->n_streams < 16384 &&
+               p->n_per_stream >= 512);
     switch (p->flags & PRNGD_STORE_MASK) {
         case PRNGD_FLAG_STORE_TMA: pl.store = Store::TMA; break;
         case PRNGD_FLAG_STORE_TILE: pl.store = Store::STG16; break;
@@ -276,7 +281,14 @@ prngd_status prngd_generate(const prngd_handle *h, double *d_out, void *cuda_str
     if (s != PRNGD_OK) return s;
     GenArgs g = h->args;
     g.out = d_out;
-    cudaError_t e = prngd::launch_generate(g, plan_for(h, d_out), (cudaStream_t)cuda_stream, sms);
+    cudaError_t e;
+    if (h->plan.jump) {
+        const void *tables = nullptr;
+        if ((e = prngd::jump_tables(&tables)) != cudaSuccess) return cuda_fail(e, "jump tables");
+        e = prngd::launch_generate_jump(g, h->plan, tables, (cudaStream_t)cuda_stream);
+    } else {
+        e = prngd::launch_generate(g, plan_for(h, d_out), (cudaStream_t)cuda_stream, sms);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "generate kernel launch");
     h->last_launches.store(1);
     return PRNGD_OK;
@@ -436,6 +448,13 @@ prngd_status prngd_debug_map(const prngd_handle *h, const uint32_t *d_x1, const 
                                             (cudaStream_t)cuda_stream);
     if (e != cudaSuccess) return cuda_fail(e, "debug_map launch");
     h->last_launches.store(n ? 1 : 0);
+    return PRNGD_OK;
+}
+
+prngd_status prngd_debug_jump(uint64_t n_draws, const uint32_t *in, uint32_t *out,
+                              int lane_table) {
+    if (!in || !out || lane_table > 31) return fail(PRNGD_EINVAL, "null state or lane > 31");
+    prngd::jump_host(n_draws, in, out, lane_table);
     return PRNGD_OK;
 }
 

@@ -48,8 +48,15 @@ struct Plan {
     bool clamp;     // R11 clamp needed
     bool ieee_div;  // PRNGD_FLAG_IEEE_DIV
     bool alg1;      // PRNGD_FLAG_ALG1
+    bool jump;      // NEXT-3 intra-stream kernel (one warp per stream)
     Store store;
 };
+
+// NEXT-3 jump-ahead (prngd_jump.cpp): lane l of a warp starts a round at draw l*kJumpDraws of
+// its stream (kJumpDraws / 2 pairs per lane per round, 32 lanes per stream).
+constexpr uint64_t kJumpDraws = 64;
+cudaError_t jump_tables(const void **out);  // device byte tables [32][16][256] x uint4, cached
+void jump_host(uint64_t n_draws, const uint32_t in[4], uint32_t out[4], int lane_table);
 
 // Launchers (prngd_kernels.cu).  They return cudaGetLastError() of the launch.
 cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, int num_sms);
@@ -58,6 +65,8 @@ cudaError_t launch_generate_consume(const GenArgs &g, const Plan &pl, double *d_
                                     void *scratch, size_t scratch_bytes, cudaStream_t st,
                                     int num_sms, int *launches);
 size_t consume_scratch_bytes(int num_sms);
+cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *tables,
+                                 cudaStream_t st);
 cudaError_t launch_debug_raw(const GenArgs &g, uint32_t *d_raw, uint64_t draws, cudaStream_t st);
 cudaError_t launch_debug_pairs(const GenArgs &g, const Plan &pl, uint32_t *d_pidx,
                                uint64_t *d_consumed, cudaStream_t st);

@@ -1,0 +1,145 @@
+// prngd_jump.cpp -- GF(2) jump-ahead for xorshift128 (NEXT-3: intra-stream parallelism).
+//
+// xorshift128 (Marsaglia 2003) is linear over GF(2): one draw maps the 128-bit state
+// s = (x, y, z, w) to T*s.  Advancing a stream by n draws is the matrix power T^n, so the 32
+// lanes of a warp can start at draws 0, 64, 128, ... of the same stream.  The device applies
+// J_l = T^(64 l) with byte tables: tab[l][b][v] = J_l * (v << 8b), so J_l * s is the XOR of 16
+// table entries (16 x 16-byte loads).  Product code; independent of oracle/.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "prngd_internal.h"
+
+namespace prngd {
+
+namespace {
+
+struct Vec128 {
+    uint32_t w[4];  // w[0] = x, w[1] = y, w[2] = z, w[3] = w
+};
+
+// One xorshift128 step on a state vector: the linear map T.
+Vec128 step(const Vec128 &s) {
+    const uint32_t t = s.w[0] ^ (s.w[0] << 11);
+    Vec128 r;
+    r.w[0] = s.w[1];
+    r.w[1] = s.w[2];
+    r.w[2] = s.w[3];
+    r.w[3] = s.w[3] ^ (s.w[3] >> 19) ^ t ^ (t >> 8);
+    return r;
+}
+
+struct Mat128 {
+    Vec128 col[128];  // column j = image of basis vector e_j (bit j%32 of word j/32)
+};
+
+Vec128 apply(const Mat128 &m, const Vec128 &v) {
+    Vec128 r = {{0, 0, 0, 0}};
+    for (int j = 0; j < 128; ++j)
+        if ((v.w[j >> 5] >> (j & 31)) & 1u)
+            for (int k = 0; k < 4; ++k) r.w[k] ^= m.col[j].w[k];
+    return r;
+}
+
+Mat128 mul(const Mat128 &a, const Mat128 &b) {  // (a*b) v = a (b v)
+    Mat128 c;
+    for (int j = 0; j < 128; ++j) c.col[j] = apply(a, b.col[j]);
+    return c;
+}
+
+Mat128 identity() {
+    Mat128 m;
+    std::memset(&m, 0, sizeof(m));
+    for (int j = 0; j < 128; ++j) m.col[j].w[j >> 5] = 1u << (j & 31);
+    return m;
+}
+
+Mat128 t_matrix() {
+    Mat128 m;
+    for (int j = 0; j < 128; ++j) {
+        Vec128 e = {{0, 0, 0, 0}};
+        e.w[j >> 5] = 1u << (j & 31);
+        m.col[j] = step(e);
+    }
+    return m;
+}
+
+Mat128 t_power(uint64_t n) {  // T^n by square-and-multiply
+    Mat128 r = identity(), p = t_matrix();
+    while (n) {
+        if (n & 1u) r = mul(p, r);
+        n >>= 1;
+        if (n) p = mul(p, p);
+    }
+    return r;
+}
+
+// Byte tables of the 32 lane matrices J_l = T^(kJumpDraws * l), [l][b][v] -> 4 words.
+std::vector<uint32_t> build_tables() {
+    std::vector<uint32_t> tab((size_t)32 * 16 * 256 * 4, 0u);
+    const Mat128 step_lane = t_power(kJumpDraws);
+    Mat128 j = identity();
+    for (int l = 0; l < 32; ++l) {
+        for (int b = 0; b < 16; ++b)
+            for (int v = 0; v < 256; ++v) {
+                uint32_t *e = &tab[(((size_t)l * 16 + b) * 256 + v) * 4];
+                for (int t = 0; t < 8; ++t)
+                    if ((v >> t) & 1)
+                        for (int k = 0; k < 4; ++k) e[k] ^= j.col[8 * b + t].w[k];
+            }
+        j = mul(step_lane, j);
+    }
+    return tab;
+}
+
+std::mutex g_mu;
+std::map<int, void *> g_dev_tables;  // device -> table pointer (process lifetime)
+
+}  // namespace
+
+cudaError_t jump_tables(const void **out) {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(g_mu);
+    auto it = g_dev_tables.find(dev);
+    if (it != g_dev_tables.end()) {
+        *out = it->second;
+        return cudaSuccess;
+    }
+    static std::vector<uint32_t> host = build_tables();
+    void *d = nullptr;
+    if ((e = cudaMalloc(&d, host.size() * 4)) != cudaSuccess) return e;
+    if ((e = cudaMemcpy(d, host.data(), host.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) {
+        cudaFree(d);
+        return e;
+    }
+    g_dev_tables[dev] = d;
+    *out = d;
+    return cudaSuccess;
+}
+
+void jump_host(uint64_t n_draws, const uint32_t in[4], uint32_t out[4], int lane_table) {
+    Vec128 v;
+    std::memcpy(v.w, in, 16);
+    Vec128 r;
+    if (lane_table >= 0) {  // through the byte table of lane `lane_table` (what the GPU reads)
+        static std::vector<uint32_t> tab = build_tables();
+        std::memset(r.w, 0, 16);
+        for (int b = 0; b < 16; ++b) {
+            const uint32_t byte = (v.w[b >> 2] >> (8 * (b & 3))) & 0xFFu;
+            const uint32_t *e = &tab[(((size_t)lane_table * 16 + b) * 256 + byte) * 4];
+            for (int k = 0; k < 4; ++k) r.w[k] ^= e[k];
+        }
+    } else {
+        r = apply(t_power(n_draws), v);
+    }
+    std::memcpy(out, r.w, 16);
+}
+
+}  // namespace prngd

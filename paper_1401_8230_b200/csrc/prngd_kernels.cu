@@ -516,6 +516,111 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
     }
 }
 
+// ------------------------------------------------------------------------------ NEXT-3 jump kernel
+// One warp per stream.  Each round, lane l jumps the stream state by l * kJumpDraws draws
+// (J_l = T^(64 l), byte tables) and produces kJumpPairs = 32 consecutive pairs; a warp scan of
+// the per-lane accepted counts places every accepted output (pair-drop, R2), so the layout is
+// exactly the sequential one.  Lane 31's final state starts the next round.
+constexpr int kJumpPairs = (int)(kJumpDraws / 2);
+constexpr int kJumpWarps = 4;
+
+__device__ __forceinline__ Xs128 jump_state(const uint4 *__restrict__ tab, const Xs128 &s) {
+    const uint32_t words[4] = {s.x, s.y, s.z, s.w};
+    uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        const uint32_t v = (words[b >> 2] >> (8 * (b & 3))) & 0xFFu;
+        const uint4 t = __ldg(&tab[b * 256 + v]);
+        r0 ^= t.x;
+        r1 ^= t.y;
+        r2 ^= t.z;
+        r3 ^= t.w;
+    }
+    return Xs128{r0, r1, r2, r3};
+}
+
+// staging: row = lane (32 doubles = 16 chunks of 16 B), chunk c stored at c ^ (row & 15)
+__device__ __forceinline__ uint32_t jstage_off(uint32_t row, uint32_t j) {
+    return row * 256u + ((((j >> 1) ^ (row & 15u))) << 4) + (j & 1u) * 8u;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kJumpWarps * 32)
+    gen_jump_kernel(const GenArgs g, const uint4 *__restrict__ tabs) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint64_t row = (uint64_t)blockIdx.x * kJumpWarps + warp;
+    if (row >= g.n_streams) return;
+    constexpr bool FULL32 = MODE == 2;
+    const uint32_t sh1 = FULL32 ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
+    const uint32_t w = FULL32 ? 32u : g.w;
+    const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
+    const uint32_t stage = aligned_smem_base(smem_raw) + warp * (32u * kJumpPairs * 8u);
+    const uint4 *my_tab = tabs + (size_t)lane * 16 * 256;
+    double *row_out = g.out + row * g.nps;
+    Xs128 S = stream_start(g.seed, g.stream_begin + row);
+    uint64_t base = 0;
+#pragma unroll 1
+    while (base < g.nps) {
+        Xs128 st = lane ? jump_state(my_tab, S) : S;
+        uint32_t mask = 0;
+#pragma unroll
+        for (int half = 0; half < kJumpPairs / kCols; ++half) {
+            double q[kCols];
+#pragma unroll
+            for (int i = 0; i < kCols; ++i) {
+                const uint32_t x1 = draw(st) >> sh1;
+                const uint32_t x2 = draw(st) >> sh2;
+                mask |= (accepted(x1, lo, span) ? 1u : 0u) << (half * kCols + i);
+                q[i] = MODE >= 1 ? eq4_pair<false, true>(x1, x2, w, g.Cs, g.Ds, g.y)
+                                 : map_pair<false, true>(x1, x2, g.map);
+            }
+#pragma unroll
+            for (int c = 0; c < kCols / 2; ++c)
+                sts_v2(stage + jstage_off(lane, half * kCols + 2 * c), q[2 * c], q[2 * c + 1]);
+        }
+        const uint32_t cnt = __popc(mask);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += t;
+        }
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        __syncwarp();
+        if (total == 32u * kJumpPairs) {
+            // no rejection this round: the staging tile is already in output order
+#pragma unroll 4
+            for (uint32_t k = 0; k < (uint32_t)kJumpPairs; ++k) {
+                const uint64_t pos = base + k * 32u + lane;
+                if (pos < g.nps) {
+                    double v;
+                    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(stage + jstage_off(k, lane)));
+                    row_out[pos] = v;
+                }
+            }
+        } else {
+            uint64_t pos = base + incl - cnt;
+            for (uint32_t j = 0; j < (uint32_t)kJumpPairs; ++j) {
+                if ((mask >> j) & 1u) {
+                    if (pos < g.nps) {
+                        double v;
+                        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(stage + jstage_off(lane, j)));
+                        row_out[pos] = v;
+                    }
+                    ++pos;
+                }
+            }
+        }
+        __syncwarp();
+        S.x = __shfl_sync(0xFFFFFFFFu, st.x, 31);
+        S.y = __shfl_sync(0xFFFFFFFFu, st.y, 31);
+        S.z = __shfl_sync(0xFFFFFFFFu, st.z, 31);
+        S.w = __shfl_sync(0xFFFFFFFFu, st.w, 31);
+        base += total;
+    }
+}
+
 // ------------------------------------------------------------------------------ debug kernels
 __global__ void debug_raw_kernel(const GenArgs g, uint32_t *raw, uint64_t draws) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -755,6 +860,28 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
     e = cudaGetLastError();
     if (e == cudaSuccess) *launches = 2;
     return e;
+}
+
+cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *tables,
+                                 cudaStream_t st) {
+    (void)pl;
+    const size_t smem = 1024 + (size_t)kJumpWarps * 32 * kJumpPairs * 8;
+    const uint64_t grid = (g.n_streams + kJumpWarps - 1) / kJumpWarps;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    const uint4 *t = static_cast<const uint4 *>(tables);
+    const int mode = kernel_mode(g);
+    cudaError_t e;
+    if (mode == 2) {
+        if ((e = set_smem(gen_jump_kernel<2>, smem)) != cudaSuccess) return e;
+        gen_jump_kernel<2><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);
+    } else if (mode == 1) {
+        if ((e = set_smem(gen_jump_kernel<1>, smem)) != cudaSuccess) return e;
+        gen_jump_kernel<1><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);
+    } else {
+        if ((e = set_smem(gen_jump_kernel<0>, smem)) != cudaSuccess) return e;
+        gen_jump_kernel<0><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_debug_raw(const GenArgs &g, uint32_t *d_raw, uint64_t draws, cudaStream_t st) {

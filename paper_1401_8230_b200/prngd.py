@@ -24,6 +24,8 @@ PRNGD_FLAG_MAP_EQ4 = 0 << 6
 PRNGD_FLAG_MAP_EQ5 = 1 << 6
 PRNGD_FLAG_MAP_EQ6 = 2 << 6
 PRNGD_FLAG_OPEN = 0x100
+PRNGD_FLAG_JUMP = 0x200
+PRNGD_FLAG_NO_JUMP = 0x400
 MAP_FLAGS = {4: PRNGD_FLAG_MAP_EQ4, 5: PRNGD_FLAG_MAP_EQ5, 6: PRNGD_FLAG_MAP_EQ6}
 STORE_FLAGS = {"row": PRNGD_FLAG_STORE_ROW, "tma": PRNGD_FLAG_STORE_TMA,
                "tile": PRNGD_FLAG_STORE_TILE, "direct": PRNGD_FLAG_STORE_DIRECT,
@@ -33,7 +35,7 @@ EXPORTS = (
     "prngd_create", "prngd_destroy", "prngd_get_info", "prngd_generate", "prngd_generate_consume",
     "prngd_generate_host", "prngd_last_launches", "prngd_status_string", "prngd_last_error",
     "prngd_abi_version", "prngd_debug_raw", "prngd_debug_pairs", "prngd_debug_map",
-    "prngd_debug_div_check",
+    "prngd_debug_div_check", "prngd_debug_jump",
 )
 
 
@@ -84,6 +86,7 @@ def lib():
             "prngd_debug_pairs": (st, [vp, vp, vp, vp]),
             "prngd_debug_map": (st, [vp, vp, vp, vp, u64, vp]),
             "prngd_debug_div_check": (st, [vp, u64, u64, vp, vp]),
+            "prngd_debug_jump": (st, [u64, vp, vp, C.c_int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -173,6 +176,15 @@ def prngd_debug_map(h: int, x1, x2, z, stream=None):
 def prngd_debug_div_check(h: int, n: int, seed: int, mismatch, stream=None):
     _check(lib().prngd_debug_div_check(h, n, seed, _ptr(mismatch), _stream_ptr(stream)),
            "prngd_debug_div_check")
+
+
+def prngd_debug_jump(n_draws: int, state, lane_table: int = -1):
+    import numpy as np
+    a = np.ascontiguousarray(state, dtype=np.uint32)
+    o = np.zeros(4, dtype=np.uint32)
+    _check(lib().prngd_debug_jump(n_draws, a.ctypes.data, o.ctypes.data, lane_table),
+           "prngd_debug_jump")
+    return tuple(int(v) for v in o)
 
 
 # ---------------------------------------------------------------- convenience wrapper

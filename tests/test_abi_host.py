@@ -148,3 +148,24 @@ def test_clamp_flag_for_eq5_eq6(lib, orc, kind, w, clamp):
     top = 2**w - 1
     raw = orc.map_eq5(p, top - 1, top) if kind == 5 else orc.map_eq6(w, top - 1, top)
     assert (raw >= 1.0) == bool(clamp)
+
+
+def test_jump_ahead_matches_sequential_draws(lib, orc):
+    """NEXT-3: T^n (GF(2) matrix power) and the GPU's byte tables reproduce n sequential
+    xorshift128 draws of the oracle (Marsaglia recurrence)."""
+    for seed, s in [(1, 0), (7, 12345), (W.SEED2, 2**40 + 3)]:
+        st = orc.stream_state(seed, s)
+        seq = orc.xs128_sequence(st, 64 * 31 + 4)   # outputs = successive w words
+        for n in (1, 2, 3, 4, 5, 63, 64, 65, 1000, 64 * 31):
+            got = P.prngd_debug_jump(n, st)
+            # the state after n draws holds the last four outputs (x, y, z, w)
+            assert got == tuple(seq[n - 4:n]) if n >= 4 else got[3] == seq[n - 1]
+        for lane in (0, 1, 2, 17, 31):
+            assert P.prngd_debug_jump(0, st, lane) == P.prngd_debug_jump(64 * lane, st) if lane \
+                else P.prngd_debug_jump(0, st, 0) == st
+
+
+def test_jump_flag_rules(lib):
+    with pytest.raises(P.PrngdError):
+        P.prngd_create(**W.FULL32, seed=1, n_streams=1, n_per_stream=2,
+                       flags=P.PRNGD_FLAG_JUMP | P.PRNGD_FLAG_ALG1)

@@ -359,3 +359,37 @@ def test_open_interval_histogram_top_bin(orc, kind):
     ref = orc.generate(p, kind=kind, open_interval=True, want_out=False, want_stats=True)
     assert np.array_equal(hist.cpu().numpy(), ref["hist"]) and cnt.item() == ref["count"]
     assert np.allclose(pw.cpu().numpy(), ref["pow"], rtol=1e-12, atol=0)
+
+
+# ------------------------------------------------------------------ NEXT-3 jump-ahead kernel
+
+@pytest.mark.parametrize("jump", [P.PRNGD_FLAG_JUMP, P.PRNGD_FLAG_NO_JUMP])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_jump_and_sequential_kernels_bitwise(orc, name, jump):
+    p = W.config(name, flags=jump)
+    _, out = gen(p)
+    assert_same(out, orc.generate(p)["out"])
+
+
+@pytest.mark.parametrize("ns,nps", [(1, 1), (3, 5), (33, 1000), (5, 2049), (100, 4096 + 7)])
+@pytest.mark.parametrize("base", ["cfg1", "cfg2", "cfg4"])
+def test_jump_ragged(orc, base, ns, nps):
+    p = W.config(base, n_streams=ns, n_per_stream=nps, stream_begin=777, flags=P.PRNGD_FLAG_JUMP)
+    _, out = gen(p)
+    assert_same(out, orc.generate(p)["out"])
+
+
+@pytest.mark.parametrize("kind,open_", [(5, False), (6, True), (4, True)])
+def test_jump_with_mappings(orc, kind, open_):
+    flags = P.PRNGD_FLAG_JUMP | P.MAP_FLAGS[kind] | (P.PRNGD_FLAG_OPEN if open_ else 0)
+    p = W.config("cfg2", n_streams=64, n_per_stream=3000, flags=flags)
+    _, out = gen(p)
+    assert_same(out, orc.generate(p, kind=kind, open_interval=open_)["out"])
+
+
+def test_jump_general_ranges(orc):
+    for par in [dict(w=12, a0=0, a=100, b0=0, b=63), dict(w=1, a0=0, a=2, b0=0, b=1),
+                dict(w=32, a0=1000, a=2**31 + 7, b0=0, b=2**16 - 1)]:
+        p = dict(par, seed=9, n_streams=37, n_per_stream=2500, flags=P.PRNGD_FLAG_JUMP)
+        _, out = gen(p)
+        assert_same(out, orc.generate(p)["out"])
