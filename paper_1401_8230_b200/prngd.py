@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libprngd_b200.so")
+# PRNGD_LIB: load an alternative build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("PRNGD_LIB") or os.path.join(PKG, "libprngd_b200.so")
 
 PRNGD_OK, PRNGD_EINVAL, PRNGD_ECUDA, PRNGD_ENOMEM, PRNGD_EUNSUPPORTED = range(5)
 PRNGD_FLAG_IEEE_DIV = 0x1
@@ -20,6 +21,7 @@ PRNGD_FLAG_STORE_TMA = 1 << 3
 PRNGD_FLAG_STORE_TILE = 2 << 3
 PRNGD_FLAG_STORE_DIRECT = 3 << 3
 PRNGD_FLAG_STORE_ROW1K = 4 << 3
+PRNGD_FLAG_STORE_ROWJ = 5 << 3
 PRNGD_FLAG_MAP_EQ4 = 0 << 6
 PRNGD_FLAG_MAP_EQ5 = 1 << 6
 PRNGD_FLAG_MAP_EQ6 = 2 << 6
@@ -29,7 +31,7 @@ PRNGD_FLAG_NO_JUMP = 0x400
 MAP_FLAGS = {4: PRNGD_FLAG_MAP_EQ4, 5: PRNGD_FLAG_MAP_EQ5, 6: PRNGD_FLAG_MAP_EQ6}
 STORE_FLAGS = {"row": PRNGD_FLAG_STORE_ROW, "tma": PRNGD_FLAG_STORE_TMA,
                "tile": PRNGD_FLAG_STORE_TILE, "direct": PRNGD_FLAG_STORE_DIRECT,
-               "row1k": PRNGD_FLAG_STORE_ROW1K}
+               "row1k": PRNGD_FLAG_STORE_ROW1K, "rowj": PRNGD_FLAG_STORE_ROWJ}
 
 EXPORTS = (
     "prngd_create", "prngd_destroy", "prngd_get_info", "prngd_generate", "prngd_generate_consume",
