@@ -47,7 +47,7 @@ def parse():
                     help="consume workloads: fused histogram/moments only, outputs not stored")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flags", type=int, default=0, help="extra prngd flags")
-    ap.add_argument("--store", default="row", choices=["row", "row1k", "rowj", "tma", "tile", "direct"],
+    ap.add_argument("--store", default="row", choices=["row", "row1k", "tma", "tile", "direct"],
                     help="store path A/B (include/prngd.h PRNGD_FLAG_STORE_*)")
     return ap.parse_args()
 

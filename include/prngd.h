@@ -71,8 +71,6 @@ typedef enum {
 #define PRNGD_FLAG_STORE_TILE    (2u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_DIRECT  (3u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_ROW1K   (4u << PRNGD_STORE_SHIFT)  /* ROW with 1 KiB bursts (A/B) */
-#define PRNGD_FLAG_STORE_ROWJ    (5u << PRNGD_STORE_SHIFT)  /* 2 lanes/stream via jump-ahead,
-                                                              1 KiB bursts (A/B) */
 /* Mapping selection, bits 6..7 (NEXT-1): Eq.(4) (default), Eq.(5) discrete-grid normalisation
  * onto [0; 1-k'], or Eq.(6) unit-interval form (requires a0 = b0 = 0 and
  * a = b = 2^w - 1).  All three are followed by the R11 clamp (z' <= 1 - 2^-53). */

@@ -123,7 +123,7 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     if (map_code > 2) return fail(PRNGD_EUNSUPPORTED, "unknown mapping code %u", map_code);
     if (map_code == 2 && !(p->a0 == 0 && p->b0 == 0 && p->a == (1ull << w) - 1 && p->b == p->a))
         return fail(PRNGD_EINVAL, "Eq.(6) needs the unit-interval range a0=b0=0, a=b=2^w-1");
-    if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 5)
+    if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 4)
         return fail(PRNGD_EUNSUPPORTED, "unknown store path %u",
                     (p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT);
 
@@ -221,7 +221,6 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         case PRNGD_FLAG_STORE_TILE: pl.store = Store::STG16; break;
         case PRNGD_FLAG_STORE_DIRECT: pl.store = Store::DIRECT; break;
         case PRNGD_FLAG_STORE_ROW1K: pl.store = Store::ROW1K; break;
-        case PRNGD_FLAG_STORE_ROWJ: pl.store = Store::ROWJ; break;
         default: pl.store = Store::ROW; break;
     }
     *out = h;
@@ -268,10 +267,6 @@ static Plan plan_for(const prngd_handle *h, const void *out, bool consume = fals
     const bool a16 = (a & 15u) == 0 && (nps & 1u) == 0;
     const bool tma_ok = a16 && h->p.n_streams < (1ull << 31) && nps < (1ull << 31);
     if (pl.store == Store::DIRECT && !a32) pl.store = a16 ? Store::STG16 : Store::STG8;
-    // ROWJ: rare-rejection Eq.(4)-closed configurations only (speculative rounds)
-    const bool rowj_ok = pl.spec && !pl.ieee_div && !pl.alg1 && h->args.map.kind == 4 &&
-                         !h->args.map.open && a16;
-    if (pl.store == Store::ROWJ && !rowj_ok) pl.store = Store::ROW;
     if ((pl.store == Store::ROW || pl.store == Store::ROW1K) && !a16) pl.store = Store::STG8;
     if (pl.store == Store::TMA && !tma_ok) pl.store = a16 ? Store::STG16 : Store::STG8;
     if (pl.store == Store::STG16 && !a16) pl.store = Store::STG8;
@@ -288,11 +283,10 @@ prngd_status prngd_generate(const prngd_handle *h, double *d_out, void *cuda_str
     g.out = d_out;
     cudaError_t e;
     const Plan pl = plan_for(h, d_out);
-    if (h->plan.jump || pl.store == Store::ROWJ) {
+    if (h->plan.jump) {
         const void *tables = nullptr;
         if ((e = prngd::jump_tables(&tables)) != cudaSuccess) return cuda_fail(e, "jump tables");
-        e = h->plan.jump ? prngd::launch_generate_jump(g, h->plan, tables, (cudaStream_t)cuda_stream)
-                         : prngd::launch_generate_rowj(g, tables, (cudaStream_t)cuda_stream);
+        e = prngd::launch_generate_jump(g, h->plan, tables, (cudaStream_t)cuda_stream);
     } else {
         e = prngd::launch_generate(g, pl, (cudaStream_t)cuda_stream, sms);
     }

@@ -40,8 +40,7 @@ struct GenArgs {
 //   TMA:    32 x 16 smem tiles (128B swizzle) + one cp.async.bulk.tensor.2d store per CTA slab
 //   STG16:  32 x 16 smem tile + warp-coalesced 16-byte st.global;  STG8: 8-byte stores
 //   ROW1K:  as ROW with 128 outputs (1 KiB bursts) per row
-//   ROWJ:   two lanes per stream (jump-ahead), 1 KiB bursts at the ROW smem budget
-enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3, ROW = 4, ROW1K = 5, ROWJ = 6 };
+enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3, ROW = 4, ROW1K = 5 };
 
 // Launch descriptors chosen by the host.
 struct Plan {
@@ -68,7 +67,6 @@ cudaError_t launch_generate_consume(const GenArgs &g, const Plan &pl, double *d_
 size_t consume_scratch_bytes(int num_sms);
 cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *tables,
                                  cudaStream_t st);
-cudaError_t launch_generate_rowj(const GenArgs &g, const void *tables, cudaStream_t st);
 cudaError_t launch_debug_raw(const GenArgs &g, uint32_t *d_raw, uint64_t draws, cudaStream_t st);
 cudaError_t launch_debug_pairs(const GenArgs &g, const Plan &pl, uint32_t *d_pidx,
                                uint64_t *d_consumed, cudaStream_t st);

@@ -625,121 +625,6 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
     }
 }
 
-// ------------------------------------------------------------------------------ ROWJ kernel
-// ROW store with 1 KiB row bursts at the same shared-memory budget: two lanes per stream.  Lane
-// 2s+j owns stream s of the warp's 16; each round lane j produces pairs [64 j, 64 j + 64) of
-// the stream's next 128 (lane 1 jumps its copy of the round-start state by T^128, GF(2) table),
-// and the warp writes every stream's 128 outputs as ONE 1 KiB burst (two 512 B instructions).
-// Rare events (a rejected x1, or x1 = a - 1 when the R11 clamp may apply) make the warp redo
-// the round exactly: with pair-drop (R2) a round's pair range is fixed, so each lane re-draws
-// its 64 pairs from the saved state, drops the rejected ones, clamps, and writes its accepted
-// outputs after its partner's (scalar stores); an odd output count also sends later rounds of
-// that warp through this path (16-byte stores need an even column).
-constexpr int kRowjPairs = 64;  // pairs per lane per round
-
-template <int MODE>
-__global__ void __launch_bounds__(32) gen_rowj_kernel(const GenArgs g,
-                                                      const uint4 *__restrict__ t128) {
-    extern __shared__ uint8_t smem_raw[];
-    constexpr bool FULL32 = MODE == 2;
-    const uint32_t lane = threadIdx.x & 31u, s = lane >> 1, j = lane & 1u;
-    const uint64_t row = (uint64_t)blockIdx.x * 16u + s;
-    const bool live = row < g.n_streams;
-    const uint32_t sh1 = FULL32 ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
-    const uint32_t w = FULL32 ? 32u : g.w;
-    const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
-    const uint32_t span_fast = FULL32 ? 0xFFFFFFFDu : g.span_fast;
-    const uint32_t tile = aligned_smem_base(smem_raw);
-    const uint32_t my_row = tile + lane * (kRowjPairs * 8u);
-    const uint32_t nstreams_here =
-        (g.n_streams - (uint64_t)blockIdx.x * 16u) < 16u ? (uint32_t)(g.n_streams - (uint64_t)blockIdx.x * 16u) : 16u;
-    Xs128 S = stream_start(g.seed, g.stream_begin + (live ? row : 0));
-    uint64_t base = 0;  // outputs of this lane's stream written so far
-#pragma unroll 1
-    while (__any_sync(0xFFFFFFFFu, live && base < g.nps)) {
-        Xs128 st = j ? jump_state(t128, S) : S;
-        const Xs128 saved = st;
-        bool rare = false;
-#pragma unroll 1
-        for (uint32_t b = 0; b < kRowjPairs / kCols; ++b) {
-            double q[kCols];
-#pragma unroll
-            for (int i = 0; i < kCols; ++i) {
-                const uint32_t x1 = draw(st) >> sh1;
-                const uint32_t x2 = draw(st) >> sh2;
-                rare |= !accepted(x1, lo, span_fast);
-                q[i] = eq4_pair<false, false>(x1, x2, w, g.Cs, g.Ds, g.y);
-            }
-#pragma unroll
-            for (int c = 0; c < kCols / 2; ++c) {
-                const uint32_t chunk = b * (kCols / 2) + c;
-                sts_v2(my_row + ((chunk ^ lane) << 4), q[2 * c], q[2 * c + 1]);
-            }
-        }
-        const bool exact = __any_sync(0xFFFFFFFFu, rare) || (base & 1u);
-        uint32_t produced = 2u * kRowjPairs;
-        if (!exact) {
-            __syncwarp();
-            // fast: stream s's 128 outputs = rows 2s, 2s+1 of the tile, one 1 KiB burst
-            for (uint32_t ss = 0; ss < nstreams_here; ++ss) {
-                const uint64_t b0 = __shfl_sync(0xFFFFFFFFu, base, 2 * ss);
-                double *dst = g.out + ((uint64_t)blockIdx.x * 16u + ss) * g.nps + b0;
-#pragma unroll
-                for (uint32_t h = 0; h < 2; ++h) {
-                    const uint64_t col = b0 + h * kRowjPairs + 2 * lane;
-                    if (col < g.nps) {
-                        double a, c2;
-                        const uint32_t r = 2 * ss + h;
-                        lds_v2(tile + r * (kRowjPairs * 8u) + ((lane ^ r) << 4), a, c2);
-                        stg_v2_cs(dst + h * kRowjPairs + 2 * lane, a, c2);
-                    }
-                }
-            }
-            __syncwarp();
-        } else {
-            // exact round: same pair range, rejected pairs dropped, clamp applied
-            st = saved;
-            uint32_t mask0 = 0, mask1 = 0;
-            for (uint32_t i = 0; i < (uint32_t)kRowjPairs; ++i) {
-                const uint32_t x1 = draw(st) >> sh1;
-                const uint32_t x2 = draw(st) >> sh2;
-                if (accepted(x1, lo, span)) {
-                    if (i < 32) mask0 |= 1u << i; else mask1 |= 1u << (i - 32);
-                    sts_f64(my_row + (((i >> 1) ^ lane) << 4) + (i & 1u) * 8u,
-                            eq4_pair<false, true>(x1, x2, w, g.Cs, g.Ds, g.y));
-                }
-            }
-            const uint32_t cnt = __popc(mask0) + __popc(mask1);
-            const uint32_t cnt0 = __shfl_sync(0xFFFFFFFFu, cnt, lane & ~1u);
-            produced = cnt0 + __shfl_sync(0xFFFFFFFFu, cnt, lane | 1u);
-            uint64_t pos = base + (j ? cnt0 : 0u);
-            if (live) {
-                double *dst = g.out + row * g.nps;
-                for (uint32_t i = 0; i < (uint32_t)kRowjPairs; ++i) {
-                    const uint32_t bit = i < 32 ? (mask0 >> i) & 1u : (mask1 >> (i - 32)) & 1u;
-                    if (bit) {
-                        if (pos < g.nps) {
-                            double v;
-                            asm volatile("ld.shared.f64 %0, [%1];"
-                                         : "=d"(v)
-                                         : "r"(my_row + (((i >> 1) ^ lane) << 4) + (i & 1u) * 8u));
-                            dst[pos] = v;
-                        }
-                        ++pos;
-                    }
-                }
-            }
-            __syncwarp();
-        }
-        // next round starts where lane j = 1 stopped
-        S.x = __shfl_sync(0xFFFFFFFFu, st.x, lane | 1u);
-        S.y = __shfl_sync(0xFFFFFFFFu, st.y, lane | 1u);
-        S.z = __shfl_sync(0xFFFFFFFFu, st.z, lane | 1u);
-        S.w = __shfl_sync(0xFFFFFFFFu, st.w, lane | 1u);
-        base += produced;
-    }
-}
-
 // ------------------------------------------------------------------------------ debug kernels
 __global__ void debug_raw_kernel(const GenArgs g, uint32_t *raw, uint64_t draws) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -999,23 +884,6 @@ cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *t
     } else {
         if ((e = set_smem(gen_jump_kernel<0>, smem)) != cudaSuccess) return e;
         gen_jump_kernel<0><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);
-    }
-    return cudaGetLastError();
-}
-
-cudaError_t launch_generate_rowj(const GenArgs &g, const void *tables, cudaStream_t st) {
-    const size_t smem = 1024 + (size_t)32 * kRowjPairs * 8;
-    const uint64_t grid = (g.n_streams + 15) / 16;
-    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    // lane table 2 = T^(2 * 64) = 64 pairs (kJumpDraws = 64 draws per lane table step)
-    const uint4 *t = static_cast<const uint4 *>(tables) + (size_t)2 * 16 * 256;
-    cudaError_t e;
-    if (kernel_mode(g) == 2) {
-        if ((e = set_smem(gen_rowj_kernel<2>, smem)) != cudaSuccess) return e;
-        gen_rowj_kernel<2><<<(unsigned)grid, 32, smem, st>>>(g, t);
-    } else {
-        if ((e = set_smem(gen_rowj_kernel<1>, smem)) != cudaSuccess) return e;
-        gen_rowj_kernel<1><<<(unsigned)grid, 32, smem, st>>>(g, t);
     }
     return cudaGetLastError();
 }

@@ -393,27 +393,3 @@ def test_jump_general_ranges(orc):
         p = dict(par, seed=9, n_streams=37, n_per_stream=2500, flags=P.PRNGD_FLAG_JUMP)
         _, out = gen(p)
         assert_same(out, orc.generate(p)["out"])
-
-
-# ------------------------------------------------------------------ ROWJ store path (jump-ahead)
-
-@pytest.mark.parametrize("par,ns,nps", [
-    (W.FULL32, 1000, 1024), (W.FULL32, 33, 130), (W.ASYM, 100, 4096 + 6),
-    (dict(w=18, a0=0, a=2**18 - 1, b0=0, b=2**18 - 1), 512, 2000),      # rejections every ~60 rounds
-    (dict(w=27, a0=0, a=2**27 - 1, b0=0, b=2**27 - 1), 300, 1024),      # clamp row, R11
-])
-def test_rowj_bitwise(orc, par, ns, nps):
-    p = dict(par, seed=3, n_streams=ns, n_per_stream=nps,
-             flags=P.PRNGD_FLAG_STORE_ROWJ | P.PRNGD_FLAG_NO_JUMP)
-    _, out = gen(p)
-    assert_same(out, orc.generate(p)["out"])
-
-
-def test_rowj_full_size_sampled(orc):
-    p = W.config("cfg3", flags=P.PRNGD_FLAG_STORE_ROWJ)
-    _, out = gen(p)
-    rows = np.linspace(0, p["n_streams"] - 1, 32).astype(np.int64)
-    ref = np.stack([orc.generate(p, stream_begin=int(r), n_streams=1)["out"][0] for r in rows])
-    assert_same(out[torch.from_numpy(rows).cuda()], ref)
-    del out
-    torch.cuda.empty_cache()
