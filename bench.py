@@ -47,6 +47,8 @@ def parse():
                     help="consume workloads: fused histogram/moments only, outputs not stored")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flags", type=int, default=0, help="extra prngd flags")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="override streams per GPU (experiments; the config names it)")
     ap.add_argument("--store", default="row", choices=["row", "row1k", "tma", "tile", "direct"],
                     help="store path A/B (include/prngd.h PRNGD_FLAG_STORE_*)")
     return ap.parse_args()
@@ -229,6 +231,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     p = workload_params(args.workload, rank, world)
+    if args.streams:
+        p["stream_begin"] = rank * args.streams
+        p["n_streams"] = args.streams
     p["flags"] = args.flags | P.STORE_FLAGS[args.store]
     consume = args.workload == "cfg5" or args.consume
     g = P.Generator(**p)
