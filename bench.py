@@ -235,6 +235,8 @@ def main():
         p["stream_begin"] = rank * args.streams
         p["n_streams"] = args.streams
     p["flags"] = args.flags | P.STORE_FLAGS[args.store]
+    if p.get("mrg"):
+        p["flags"] |= P.PRNGD_FLAG_MRG32K3A
     consume = args.workload == "cfg5" or args.consume
     g = P.Generator(**p)
     nout = p["n_streams"] * p["n_per_stream"]

@@ -86,6 +86,12 @@ typedef enum {
  * output exactly where the sequential order puts it.  Chosen automatically by prngd_generate
  * when there are too few streams to fill the GPU (n_streams < 16384 and n_per_stream >= 512,
  * pair-drop consumption); these flags force it on or off. */
+/* NEXT-2: MRG32k3a base generator (L'Ecuyer 1999; P:165 names it) instead of xorshift128.
+ * x1 and x2 are uniform bitlen(a)- and bitlen(b)-bit values obtained from MRG32k3a outputs by
+ * reduce-to-width rejection (both widths <= 31); each stream's state comes from SplitMix64
+ * outputs #3s..#3s+2.  prngd_generate only (pair-drop, ROW store: 16-byte aligned output and
+ * even n_per_stream); EUNSUPPORTED elsewhere. */
+#define PRNGD_FLAG_MRG32K3A      0x800u
 #define PRNGD_FLAG_JUMP          0x200u
 #define PRNGD_FLAG_NO_JUMP       0x400u
 #define PRNGD_FLAG_ALG1       0x4u  /* NEXT-2 reading of Alg. 1: a rejected x1 is

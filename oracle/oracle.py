@@ -15,7 +15,7 @@ _CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-
 __all__ = [
     "build", "lib", "mix64", "splitmix64_output", "xs128_sequence", "stream_state", "constants",
     "map_pairs", "map_pairs_noclamp", "accept", "generate", "raw", "enumerate_pairs",
-    "map_eq5", "map_eq6", "map_kind", "GAMMA",
+    "map_eq5", "map_eq6", "map_kind", "mrg_sequence", "mrg_stream_state", "GAMMA",
 ]
 
 GAMMA = 0x9E3779B97F4A7C15
@@ -65,6 +65,13 @@ def lib():
         L.oracle_generate_ex.restype = i32
         L.oracle_generate_ex.argtypes = [u32, u64, u64, u64, u64, u64, u64, u64, u64, i32, i32, i32,
                                          vp, vp, vp, vp, vp, vp]
+        L.oracle_generate_gen.restype = i32
+        L.oracle_generate_gen.argtypes = [u32, u64, u64, u64, u64, u64, u64, u64, u64, i32, i32,
+                                          i32, i32, vp, vp, vp, vp, vp, vp]
+        L.oracle_mrg_next.restype = u32
+        L.oracle_mrg_next.argtypes = [vp]
+        L.oracle_mrg_stream_state.restype = None
+        L.oracle_mrg_stream_state.argtypes = [u64, u64, vp]
         L.oracle_map_kind.restype = dbl
         L.oracle_map_kind.argtypes = [i32, i32, u32, u64, u64, u64, u64, u32, u32]
         L.oracle_raw.restype = None
@@ -132,6 +139,7 @@ def generate(p: dict, stream_begin: int | None = None, n_streams: int | None = N
     """Run the whole oracle path on streams [stream_begin, stream_begin+n_streams).
     kind / alg1 / open_interval default to p["map"] (4), p["alg1"], p["open"] (False)."""
     kind = p.get("map", 4) if kind is None else kind
+    mrg = bool(p.get("mrg", False))
     alg1 = p.get("alg1", False) if alg1 is None else alg1
     open_interval = p.get("open", False) if open_interval is None else open_interval
     sb = p.get("stream_begin", 0) if stream_begin is None else stream_begin
@@ -144,10 +152,10 @@ def generate(p: dict, stream_begin: int | None = None, n_streams: int | None = N
     hist = np.zeros(65536, dtype=np.int64) if want_stats else None
     pw = np.zeros(4, dtype=np.float64) if want_stats else None
     cnt = np.zeros(1, dtype=np.int64) if want_stats else None
-    rc = lib().oracle_generate_ex(p["w"], p["a0"], p["a"], p["b0"], p["b"], p["seed"], sb, ns, nps,
-                                  int(kind), int(bool(alg1)), int(bool(open_interval)),
-                                  _ptr(out), _ptr(pidx), _ptr(cons), _ptr(hist), _ptr(pw),
-                                  _ptr(cnt))
+    rc = lib().oracle_generate_gen(p["w"], p["a0"], p["a"], p["b0"], p["b"], p["seed"], sb, ns,
+                                   nps, int(kind), int(bool(alg1)), int(bool(open_interval)),
+                                   int(mrg), _ptr(out), _ptr(pidx), _ptr(cons), _ptr(hist),
+                                   _ptr(pw), _ptr(cnt))
     if rc:
         raise ValueError("invalid parameters")
     if want_out:
@@ -177,6 +185,17 @@ def enumerate_pairs(p: dict):
     if rc:
         raise ValueError("invalid parameters or widths too large")
     return q.reshape(n1, n2), acc.reshape(n1, n2).astype(bool)
+
+
+def mrg_sequence(state6, n: int) -> list[int]:
+    st = np.array(state6, dtype=np.int64)
+    return [lib().oracle_mrg_next(st.ctypes.data) for _ in range(n)]
+
+
+def mrg_stream_state(seed: int, s: int) -> tuple:
+    st = np.zeros(6, dtype=np.int64)
+    lib().oracle_mrg_stream_state(seed, s, st.ctypes.data)
+    return tuple(int(v) for v in st)
 
 
 def map_kind(p: dict, kind: int, x1, x2, open_interval: bool = False) -> np.ndarray:

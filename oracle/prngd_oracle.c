@@ -54,6 +54,56 @@ void oracle_stream_state(uint64_t seed, uint64_t s, uint32_t st[4])
     st[3] = (uint32_t)(o1 >> 32);
 }
 
+/* ---- NEXT-2: MRG32k3a (L'Ecuyer 1999, "Good parameters and implementations for combined
+ * multiple recursive random number generators", Oper. Res. 47(1)), named by P:165. ---------- */
+#define MRG_M1 4294967087ll   /* 2^32 - 209   */
+#define MRG_M2 4294944443ll   /* 2^32 - 22853 */
+
+uint32_t oracle_mrg_next(int64_t s[6])
+{
+    /* component 1: x_n = (1403580 x_{n-2} - 810728 x_{n-3}) mod m1 */
+    int64_t p1 = (1403580ll * s[1] - 810728ll * s[0]) % MRG_M1;
+    if (p1 < 0) p1 += MRG_M1;
+    s[0] = s[1]; s[1] = s[2]; s[2] = p1;
+    /* component 2: y_n = (527612 y_{n-1} - 1370589 y_{n-3}) mod m2 */
+    int64_t p2 = (527612ll * s[5] - 1370589ll * s[3]) % MRG_M2;
+    if (p2 < 0) p2 += MRG_M2;
+    s[3] = s[4]; s[4] = s[5]; s[5] = p2;
+    /* combination: z = (x - y) mod m1, with 0 reported as m1 -> u in [1, m1] (R21) */
+    int64_t z = p1 - p2;
+    if (z <= 0) z += MRG_M1;
+    return (uint32_t)z;
+}
+
+void oracle_mrg_stream_state(uint64_t seed, uint64_t s, int64_t st[6])
+{
+    /* R22: SplitMix64 outputs #3s, #3s+1, #3s+2 -> six 32-bit words (lo, hi, ...), the first
+     * three reduced mod m1, the last three mod m2; an all-zero component gets a 1. */
+    uint32_t wd[6];
+    for (int i = 0; i < 3; i++) {
+        uint64_t o = oracle_splitmix64_output(seed, 3u * s + (uint64_t)i);
+        wd[2 * i] = (uint32_t)(o & 0xFFFFFFFFu);
+        wd[2 * i + 1] = (uint32_t)(o >> 32);
+    }
+    for (int i = 0; i < 3; i++) st[i] = (int64_t)wd[i] % MRG_M1;
+    for (int i = 0; i < 3; i++) st[3 + i] = (int64_t)wd[3 + i] % MRG_M2;
+    if (!st[0] && !st[1] && !st[2]) st[0] = 1;
+    if (!st[3] && !st[4] && !st[5]) st[3] = 1;
+}
+
+/* R23: a uniform `width`-bit value from MRG32k3a (SPEC's reduce_to_width): with
+ * T = floor(m1 / 2^width) * 2^width, draws u with u - 1 >= T are discarded, else (u-1) mod 2^width. */
+uint32_t oracle_mrg_reduced(int64_t st[6], int width, uint64_t *draws)
+{
+    uint64_t span = 1ull << width;
+    uint64_t T = ((uint64_t)MRG_M1 / span) * span;
+    for (;;) {
+        uint64_t u = oracle_mrg_next(st);
+        (*draws)++;
+        if (u - 1u < T) return (uint32_t)((u - 1u) & (span - 1u));
+    }
+}
+
 static int bitlen(uint64_t v)
 {
     int n = 0;
@@ -137,18 +187,39 @@ int oracle_generate_ex(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64_
                        double *out, uint32_t *pidx, uint64_t *consumed,
                        int64_t *hist, double *pw, int64_t *count)
 {
+    return oracle_generate_gen(w, a0, a, b0, b, seed, stream_begin, n_streams, n_per_stream, kind,
+                               alg1, open_interval, 0, out, pidx, consumed, hist, pw, count);
+}
+
+int oracle_generate_gen(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64_t b,
+                        uint64_t seed, uint64_t stream_begin, uint64_t n_streams,
+                        uint64_t n_per_stream, int kind, int alg1, int open_interval, int mrg,
+                        double *out, uint32_t *pidx, uint64_t *consumed,
+                        int64_t *hist, double *pw, int64_t *count)
+{
     if (!valid(w, a0, a, b0, b)) return 1;
+    if (mrg && (alg1 || bitlen(a) > 31 || bitlen(b) > 31)) return 1;
     if (kind != 4 && kind != 5 && kind != 6) return 1;
     if (kind == 6 && !(a0 == 0 && b0 == 0 && a == (1ull << w) - 1 && b == a)) return 1;
     int sh1 = 32 - bitlen(a); /* R4: x = top bits of the 32-bit draw */
     int sh2 = 32 - bitlen(b);
     for (uint64_t i = 0; i < n_streams; i++) {
         uint32_t st[4];
-        oracle_stream_state(seed, stream_begin + i, st);
+        int64_t ms[6];
+        uint64_t mdraws = 0; /* MRG32k3a outputs consumed (NEXT-2) */
+        if (mrg) oracle_mrg_stream_state(seed, stream_begin + i, ms);
+        else oracle_stream_state(seed, stream_begin + i, st);
         uint64_t p = 0; /* pairs (R2) or draws (Alg. 1) consumed so far */
         for (uint64_t j = 0; j < n_per_stream; j++) {
             uint32_t x1, x2;
-            if (alg1) {
+            if (mrg) {
+                /* pair-drop (R2) over pairs of reduced MRG32k3a values (R23) */
+                do {
+                    x1 = oracle_mrg_reduced(ms, bitlen(a), &mdraws);
+                    x2 = oracle_mrg_reduced(ms, bitlen(b), &mdraws);
+                    p++;
+                } while (!oracle_accept(a0, a, x1));
+            } else if (alg1) {
                 /* NEXT-2, Alg. 1: redraw R1 alone until accepted, then draw R2 */
                 do {
                     x1 = oracle_xs128_next(st) >> sh1;
@@ -184,7 +255,7 @@ int oracle_generate_ex(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64_
             }
             if (count) (*count)++;
         }
-        if (consumed) consumed[i] = p;
+        if (consumed) consumed[i] = mrg ? mdraws : p;
     }
     return 0;
 }

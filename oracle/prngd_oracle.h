@@ -84,6 +84,20 @@ int oracle_generate_ex(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64_
                        uint64_t n_per_stream, int kind, int alg1, int open_interval,
                        double *out, uint32_t *pidx, uint64_t *consumed,
                        int64_t *hist, double *pw, int64_t *count);
+/* NEXT-2 base generator MRG32k3a (L'Ecuyer 1999): integer output u in [1, m1] (R21),
+ * per-stream state from SplitMix64 (R22), reduced uniform width-bit values (R23). */
+uint32_t oracle_mrg_next(int64_t s[6]);
+void oracle_mrg_stream_state(uint64_t seed, uint64_t s, int64_t st[6]);
+uint32_t oracle_mrg_reduced(int64_t st[6], int width, uint64_t *draws);
+/* oracle_generate_ex with a base-generator switch: mrg != 0 draws x1, x2 as reduced MRG32k3a
+ * values of bitlen(a), bitlen(b) bits (both <= 31; pair-drop only); consumed[] then counts MRG
+ * outputs. */
+int oracle_generate_gen(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64_t b,
+                        uint64_t seed, uint64_t stream_begin, uint64_t n_streams,
+                        uint64_t n_per_stream, int kind, int alg1, int open_interval, int mrg,
+                        double *out, uint32_t *pidx, uint64_t *consumed,
+                        int64_t *hist, double *pw, int64_t *count);
+
 /* One pair through mapping `kind` (4/5/6) + clamp (R11) [+ 1 - z' when open_interval]. */
 double oracle_map_kind(int kind, int open_interval, uint32_t w, uint64_t a0, uint64_t a,
                        uint64_t b0, uint64_t b, uint32_t x1, uint32_t x2);

@@ -36,6 +36,68 @@ __device__ __forceinline__ Xs128 stream_start(uint64_t seed, uint64_t s) {
     return r;
 }
 
+// ---- NEXT-2: MRG32k3a (L'Ecuyer 1999), integer form -------------------------------------------
+constexpr uint32_t kM1 = 4294967087u;  // 2^32 - 209
+constexpr uint32_t kM2 = 4294944443u;  // 2^32 - 22853
+
+struct Mrg32k3a {
+    uint32_t s0, s1, s2;  // component 1, oldest first
+    uint32_t t0, t1, t2;  // component 2
+};
+
+// t mod m for t < 2^54 and m = 2^32 - c: fold the high word twice (2^32 = c mod m).
+template <uint32_t C, uint32_t M>
+__device__ __forceinline__ uint32_t mod_fold(uint64_t t) {
+    uint64_t r = (t >> 32) * C + (t & 0xFFFFFFFFull);
+    r = (r >> 32) * C + (r & 0xFFFFFFFFull);
+    return (uint32_t)(r >= M ? r - M : r);
+}
+
+// One MRG32k3a output u in [1, m1] (R21): x_n = 1403580 x_{n-2} - 810728 x_{n-3} mod m1,
+// y_n = 527612 y_{n-1} - 1370589 y_{n-3} mod m2, u = (x_n - y_n) mod m1 with 0 -> m1.  The
+// negative terms are written as +a (m - s), so every intermediate is a nonnegative u64 < 2^54.
+__device__ __forceinline__ uint32_t mrg_next(Mrg32k3a &m) {
+    const uint32_t p1 = mod_fold<209u, kM1>(1403580ull * m.s1 + 810728ull * (kM1 - m.s0));
+    m.s0 = m.s1;
+    m.s1 = m.s2;
+    m.s2 = p1;
+    const uint32_t p2 = mod_fold<22853u, kM2>(527612ull * m.t2 + 1370589ull * (kM2 - m.t0));
+    m.t0 = m.t1;
+    m.t1 = m.t2;
+    m.t2 = p2;
+    return p1 > p2 ? p1 - p2 : p1 + (kM1 - p2);
+}
+
+// R23: uniform width-bit value: discard u with u - 1 >= T = floor(m1 / 2^width) * 2^width.
+__device__ __forceinline__ uint32_t mrg_reduced(Mrg32k3a &m, uint32_t T, uint32_t mask) {
+    uint32_t u;
+    do {
+        u = mrg_next(m) - 1u;
+    } while (u >= T);
+    return u & mask;
+}
+
+// R22: stream s starts from SplitMix64 outputs #3s, #3s+1, #3s+2 (six 32-bit words).
+__device__ __forceinline__ Mrg32k3a mrg_stream_start(uint64_t seed, uint64_t s) {
+    uint32_t wd[6];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const uint64_t o = splitmix_finalize(seed + (3 * s + i + 1) * kGamma);
+        wd[2 * i] = (uint32_t)o;
+        wd[2 * i + 1] = (uint32_t)(o >> 32);
+    }
+    Mrg32k3a m;
+    m.s0 = wd[0] >= kM1 ? wd[0] - kM1 : wd[0];
+    m.s1 = wd[1] >= kM1 ? wd[1] - kM1 : wd[1];
+    m.s2 = wd[2] >= kM1 ? wd[2] - kM1 : wd[2];
+    m.t0 = wd[3] >= kM2 ? wd[3] - kM2 : wd[3];
+    m.t1 = wd[4] >= kM2 ? wd[4] - kM2 : wd[4];
+    m.t2 = wd[5] >= kM2 ? wd[5] - kM2 : wd[5];
+    if ((m.s0 | m.s1 | m.s2) == 0u) m.s0 = 1u;
+    if ((m.t0 | m.t1 | m.t2) == 0u) m.t0 = 1u;
+    return m;
+}
+
 // ---- S2: base draw, Marsaglia xor128 (Alg. 1 "r <- PRNG()") ---------------------
 __device__ __forceinline__ uint32_t draw(Xs128 &s) {
     const uint32_t t = s.x ^ (s.x << 11);

@@ -115,7 +115,13 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     if (p->stream_begin > ~0ull - p->n_streams)
         return fail(PRNGD_EINVAL, "stream_begin + n_streams overflows 64 bits");
     const uint32_t known = PRNGD_FLAG_IEEE_DIV | PRNGD_FLAG_ALG1 | PRNGD_STORE_MASK |
-                           PRNGD_MAP_MASK | PRNGD_FLAG_OPEN | PRNGD_FLAG_JUMP | PRNGD_FLAG_NO_JUMP;
+                           PRNGD_MAP_MASK | PRNGD_FLAG_OPEN | PRNGD_FLAG_JUMP | PRNGD_FLAG_NO_JUMP |
+                           PRNGD_FLAG_MRG32K3A;
+    const bool mrg = (p->flags & PRNGD_FLAG_MRG32K3A) != 0;
+    if (mrg && (bit_length(p->a) > 31 || bit_length(p->b) > 31))
+        return fail(PRNGD_EINVAL, "MRG32k3a draws are at most 31 bits wide (bitlen(a), bitlen(b) <= 31)");
+    if (mrg && (p->flags & (PRNGD_FLAG_ALG1 | PRNGD_FLAG_JUMP)))
+        return fail(PRNGD_EUNSUPPORTED, "MRG32k3a supports pair-drop consumption without jump-ahead");
     if ((p->flags & PRNGD_FLAG_JUMP) && (p->flags & (PRNGD_FLAG_NO_JUMP | PRNGD_FLAG_ALG1)))
         return fail(PRNGD_EUNSUPPORTED, "jump-ahead needs pair-drop consumption and no NO_JUMP");
     if (p->flags & ~known) return fail(PRNGD_EUNSUPPORTED, "unknown flag bits 0x%x", p->flags & ~known);
@@ -213,9 +219,20 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     pl.clamp = I.clamp != 0;
     pl.ieee_div = (p->flags & PRNGD_FLAG_IEEE_DIV) != 0;
     pl.alg1 = alg1;
-    pl.jump = (p->flags & PRNGD_FLAG_JUMP) ||
-              (!(p->flags & PRNGD_FLAG_NO_JUMP) && !alg1 && p->n_streams < 16384 &&
-               p->n_per_stream >= 512);
+    pl.mrg = mrg;
+    if (mrg) {  // R23 thresholds: T = floor(m1 / 2^width) * 2^width
+        const uint64_t m1 = 4294967087ull;
+        const uint64_t s1 = 1ull << bit_length(p->a), s2 = 1ull << bit_length(p->b);
+        g.mrg_t1 = (uint32_t)(m1 / s1 * s1);
+        g.mrg_t2 = (uint32_t)(m1 / s2 * s2);
+        g.mrg_mask1 = (uint32_t)(s1 - 1);
+        g.mrg_mask2 = (uint32_t)(s2 - 1);
+        I.speculative = 0;
+        pl.spec = false;
+    }
+    pl.jump = !mrg && ((p->flags & PRNGD_FLAG_JUMP) ||
+                       (!(p->flags & PRNGD_FLAG_NO_JUMP) && !alg1 && p->n_streams < 16384 &&
+                        p->n_per_stream >= 512));
     switch (p->flags & PRNGD_STORE_MASK) {
         case PRNGD_FLAG_STORE_TMA: pl.store = Store::TMA; break;
         case PRNGD_FLAG_STORE_TILE: pl.store = Store::STG16; break;
@@ -283,7 +300,11 @@ prngd_status prngd_generate(const prngd_handle *h, double *d_out, void *cuda_str
     g.out = d_out;
     cudaError_t e;
     const Plan pl = plan_for(h, d_out);
-    if (h->plan.jump) {
+    if (h->plan.mrg) {
+        if (pl.store != Store::ROW && pl.store != Store::ROW1K)
+            return fail(PRNGD_EUNSUPPORTED, "MRG32k3a needs a 16-byte aligned output and even n_per_stream");
+        e = prngd::launch_generate_mrg(g, (cudaStream_t)cuda_stream);
+    } else if (h->plan.jump) {
         const void *tables = nullptr;
         if ((e = prngd::jump_tables(&tables)) != cudaSuccess) return cuda_fail(e, "jump tables");
         e = prngd::launch_generate_jump(g, h->plan, tables, (cudaStream_t)cuda_stream);
@@ -309,6 +330,7 @@ prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64
                                     double *d_pow, int64_t *d_count, void *cuda_stream) {
     if (!hc || !d_hist || !d_pow || !d_count)
         return fail(PRNGD_EINVAL, "null handle or accumulator pointer");
+    if (hc->plan.mrg) return fail(PRNGD_EUNSUPPORTED, "the fused consumer runs on xorshift128 only");
     if (((uintptr_t)d_hist | (uintptr_t)d_pow | (uintptr_t)d_count) & 7u)
         return fail(PRNGD_EINVAL, "accumulators must be 8-byte aligned");
     if (d_out && ((uintptr_t)d_out & 7u)) return fail(PRNGD_EINVAL, "d_out must be 8-byte aligned");
@@ -344,6 +366,7 @@ prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64
 
 prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stream) {
     if (!h || !h_out) return fail(PRNGD_EINVAL, "null handle or host pointer");
+    if (h->plan.mrg) return fail(PRNGD_EUNSUPPORTED, "generate_host runs on xorshift128 only");
     int sms = 0;
     prngd_status s = device_ready(&sms);
     if (s != PRNGD_OK) return s;
@@ -416,6 +439,7 @@ prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stre
 prngd_status prngd_debug_raw(const prngd_handle *h, uint32_t *d_raw, uint64_t draws,
                              void *cuda_stream) {
     if (!h || !d_raw || draws == 0) return fail(PRNGD_EINVAL, "null argument or zero draws");
+    if (h->plan.mrg) return fail(PRNGD_EUNSUPPORTED, "debug_raw dumps xorshift128 draws only");
     int sms = 0;
     prngd_status s = device_ready(&sms);
     if (s != PRNGD_OK) return s;
@@ -428,6 +452,7 @@ prngd_status prngd_debug_raw(const prngd_handle *h, uint32_t *d_raw, uint64_t dr
 prngd_status prngd_debug_pairs(const prngd_handle *h, uint32_t *d_pair_index,
                                uint64_t *d_pairs_consumed, void *cuda_stream) {
     if (!h) return fail(PRNGD_EINVAL, "null handle");
+    if (h->plan.mrg) return fail(PRNGD_EUNSUPPORTED, "debug_pairs follows xorshift128 only");
     int sms = 0;
     prngd_status s = device_ready(&sms);
     if (s != PRNGD_OK) return s;

@@ -28,6 +28,8 @@ struct GenArgs {
     uint32_t lo, span;      // accept iff (x1 - lo) < span  <=>  a0 < x1 < a   (R3)
     uint32_t span_fast;     // span - clamp: speculative band excluding x1 = a - 1 when R11 applies
     MapArgs map;            // mapping of the generic kernels (Eq.(4)/(5)/(6), open interval)
+    uint32_t mrg_t1, mrg_t2;        // NEXT-2: reduce-to-width thresholds for bitlen(a), bitlen(b)
+    uint32_t mrg_mask1, mrg_mask2;  //         and the width masks
     // consumer (S7)
     uint32_t *hist_slab;    // [gridDim.x][32768] packed u16 pairs (consume kernels only)
     int64_t *hist_spill;    // [65536] int64 carries of the packed counters
@@ -49,6 +51,7 @@ struct Plan {
     bool ieee_div;  // PRNGD_FLAG_IEEE_DIV
     bool alg1;      // PRNGD_FLAG_ALG1
     bool jump;      // NEXT-3 intra-stream kernel (one warp per stream)
+    bool mrg;       // NEXT-2 MRG32k3a base generator
     Store store;
 };
 
@@ -65,6 +68,7 @@ cudaError_t launch_generate_consume(const GenArgs &g, const Plan &pl, double *d_
                                     void *scratch, size_t scratch_bytes, cudaStream_t st,
                                     int num_sms, int *launches);
 size_t consume_scratch_bytes(int num_sms);
+cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st);
 cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *tables,
                                  cudaStream_t st);
 cudaError_t launch_debug_raw(const GenArgs &g, uint32_t *d_raw, uint64_t draws, cudaStream_t st);

@@ -310,12 +310,38 @@ __device__ __forceinline__ void run_rows(const CUtensorMap *tmap, const GenArgs 
 // for the per-row reads), then writes every row as ONE 512-byte burst: 32 lanes x 16 bytes of
 // the same row per st.global.  Long per-row bursts are what keeps HBM writes efficient with
 // 2^20 independent row fronts (tools/pattern_sweep.py).
-template <int MODE, bool SPEC, bool IEEE, bool ALG1, bool CONSUME, int RC = kRowCols,
-          class Cons>
+// Batch producers: kCols consecutive outputs of one stream into registers.
+template <int MODE, bool SPEC, bool IEEE, bool ALG1>
+struct XsProducer {  // xorshift128 base generator (S1-S5)
+    Xs128 st;
+    __device__ __forceinline__ XsProducer(const GenArgs &g, uint64_t s)
+        : st(stream_start(g.seed, s)) {}
+    __device__ __forceinline__ void operator()(double (&q)[kCols], const GenArgs &g) {
+        produce_batch<MODE, SPEC, IEEE, ALG1>(st, q, g);
+    }
+};
+
+struct MrgProducer {  // NEXT-2: MRG32k3a base generator, reduced draws (R21-R23), pair-drop
+    Mrg32k3a st;
+    __device__ __forceinline__ MrgProducer(const GenArgs &g, uint64_t s)
+        : st(mrg_stream_start(g.seed, s)) {}
+    __device__ __forceinline__ void operator()(double (&q)[kCols], const GenArgs &g) {
+#pragma unroll
+        for (int i = 0; i < kCols; ++i) {
+            uint32_t x1, x2;
+            do {
+                x1 = mrg_reduced(st, g.mrg_t1, g.mrg_mask1);
+                x2 = mrg_reduced(st, g.mrg_t2, g.mrg_mask2);
+            } while (!accepted(x1, g.lo, g.span));
+            q[i] = map_pair<false, true>(x1, x2, g.map);
+        }
+    }
+};
+
+template <bool CONSUME, int RC, class Prod, class Cons>
 __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, uint32_t lane,
-                                               uint64_t row0, Cons &cons) {
+                                               uint64_t row0, Prod &prod, Cons &cons) {
     constexpr uint32_t CPR = RC / 2;  // 16-byte chunks per row segment
-    Xs128 st = stream_start(g.seed, g.stream_begin + row0 + lane);
     const bool live = (row0 + lane) < g.n_streams;
     const uint32_t nrows = (g.n_streams - row0) < 32u ? (uint32_t)(g.n_streams - row0) : 32u;
     const uint32_t my_row = tile + lane * (RC * 8u);
@@ -324,7 +350,7 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
 #pragma unroll 1
         for (uint32_t b = 0; b < RC / kCols; ++b) {
             double q[kCols];
-            produce_batch<MODE, SPEC, IEEE, ALG1>(st, q, g);
+            prod(q, g);
             if (CONSUME && live) {
                 const uint64_t base = col0 + b * kCols;
                 if (base + kCols <= g.nps) {
@@ -390,8 +416,9 @@ __global__ void __launch_bounds__(gen_warps<ST>() * 32)
     const uint64_t row0 = ((uint64_t)blockIdx.x * gen_warps<ST>() + warp) * 32u;
     if constexpr (is_row<ST>()) {
         NoConsumer nc;
-        run_rows_burst<MODE, SPEC, IEEE, ALG1, false, row_cols<ST>()>(
-            g, aligned_smem_base(smem_raw), lane, row0, nc);
+        XsProducer<MODE, SPEC, IEEE, ALG1> prod(g, g.stream_begin + row0 + lane);
+        run_rows_burst<false, row_cols<ST>()>(g, aligned_smem_base(smem_raw), lane, row0, prod,
+                                              nc);
     } else if constexpr (ST == Store::TMA) {
         // CTA-level staging: the 4 warps fill one 128-row x 16-column slab (16 KiB, two slots)
         // and thread 0 writes it with ONE tensor store per batch.  Warps past n_streams keep
@@ -454,9 +481,12 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
 #pragma unroll 1
     for (uint64_t t = (uint64_t)blockIdx.x * kWarps + warp; t < n_tasks;
          t += (uint64_t)gridDim.x * kWarps) {
-        if constexpr (WRITE && ST == Store::ROW)
-            run_rows_burst<MODE, SPEC, IEEE, ALG1, true, kConsRowCols>(
-                g, base + kHistWords * 4u + warp * (32u * kConsRowCols * 8u), lane, t * 32u, cons);
+        if constexpr (WRITE && ST == Store::ROW) {
+            XsProducer<MODE, SPEC, IEEE, ALG1> prod(g, g.stream_begin + t * 32u + lane);
+            run_rows_burst<true, kConsRowCols>(
+                g, base + kHistWords * 4u + warp * (32u * kConsRowCols * 8u), lane, t * 32u, prod,
+                cons);
+        }
         else
             run_rows<MODE, SPEC, IEEE, ALG1, ST, WRITE, true, NB>(&tmap, g, tiles, lane, t * 32u,
                                                                      cons, it);
@@ -518,6 +548,17 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
         for (int s = 0; s < n_slabs; ++s) acc = __dadd_rn(acc, pow_slab[s * 4 + threadIdx.x]);
         d_pow[threadIdx.x] = __dadd_rn(d_pow[threadIdx.x], acc);
     }
+}
+
+// ------------------------------------------------------------------------------ NEXT-2 MRG32k3a
+// Same ROW burst store, MRG32k3a base draws (ALU-bound: ~2 x 25 integer ops per draw).
+__global__ void __launch_bounds__(32) gen_mrg_kernel(const GenArgs g) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t row0 = (uint64_t)blockIdx.x * 32u;
+    NoConsumer nc;
+    MrgProducer prod(g, g.stream_begin + row0 + lane);
+    run_rows_burst<false, kRowCols>(g, aligned_smem_base(smem_raw), lane, row0, prod, nc);
 }
 
 // ------------------------------------------------------------------------------ NEXT-3 jump kernel
@@ -864,6 +905,16 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
     e = cudaGetLastError();
     if (e == cudaSuccess) *launches = 2;
     return e;
+}
+
+cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st) {
+    const size_t smem = 1024 + (size_t)kRowTileBytes;
+    const uint64_t grid = (g.n_streams + 31) / 32;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    cudaError_t e = set_smem(gen_mrg_kernel, smem);
+    if (e != cudaSuccess) return e;
+    gen_mrg_kernel<<<(unsigned)grid, 32, smem, st>>>(g);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *tables,

@@ -23,6 +23,9 @@ CONFIGS = {
     "cfg3": dict(FULL32, seed=SEED, stream_begin=0, n_streams=2**20, n_per_stream=1024),
     "cfg4": dict(ASYM, seed=SEED, stream_begin=0, n_streams=2**20, n_per_stream=4096),
     "cfg5": dict(FULL32, seed=SEED, stream_begin=0, n_streams=2**20, n_per_stream=2048),
+    # NEXT-2 (not a BASELINE config): cfg3's shape on the MRG32k3a base generator, 26-bit draws
+    "mrg26": dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1, seed=SEED, stream_begin=0,
+                  n_streams=2**20, n_per_stream=1024, mrg=True),
 }
 
 DESCRIPTIONS = {
@@ -31,6 +34,7 @@ DESCRIPTIONS = {
     "cfg3": "w=32 full range, 2^20 streams x 1024 = 2^30 doubles (8 GiB) single-GPU bulk",
     "cfg4": "x1 in [1,2^32-1], x2 in [0,2^31-1], k=2^-32, 2^20 x 4096, write + histogram",
     "cfg5": "w=32 full range, 2^23 global streams, 2^20 x 2048 per GPU, write + hist + moments",
+    "mrg26": "NEXT-2: MRG32k3a base generator, w=26 full range, 2^20 streams x 1024",
 }
 
 

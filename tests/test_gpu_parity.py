@@ -393,3 +393,26 @@ def test_jump_general_ranges(orc):
         p = dict(par, seed=9, n_streams=37, n_per_stream=2500, flags=P.PRNGD_FLAG_JUMP)
         _, out = gen(p)
         assert_same(out, orc.generate(p)["out"])
+
+
+# ------------------------------------------------------------------ NEXT-2 MRG32k3a base generator
+
+@pytest.mark.parametrize("par", [dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1),
+                                 dict(w=31, a0=0, a=2**31 - 1, b0=0, b=2**31 - 1),
+                                 dict(w=16, a0=3, a=40000, b0=0, b=2**12 - 1)])
+@pytest.mark.parametrize("kind", [4, 5])
+def test_mrg32k3a_bitwise(orc, par, kind):
+    p = dict(par, seed=11, n_streams=300, n_per_stream=130,
+             flags=P.PRNGD_FLAG_MRG32K3A | P.MAP_FLAGS[kind], mrg=True)
+    _, out = gen(p)
+    assert_same(out, orc.generate(p, kind=kind)["out"])
+
+
+def test_mrg32k3a_unsupported_calls():
+    p = dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1, seed=1, n_streams=32, n_per_stream=64,
+             flags=P.PRNGD_FLAG_MRG32K3A)
+    g = P.Generator(**p)
+    with pytest.raises(P.PrngdError):
+        g.generate_consume()
+    with pytest.raises(P.PrngdError):
+        g.raw(4)

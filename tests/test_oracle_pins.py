@@ -429,3 +429,49 @@ def test_eq5_w32_reaches_one_and_is_clamped(orc):
     top = 2**32 - 1
     assert orc.map_eq5(W.FULL32, top - 1, top) == 1.0
     assert orc.map_kind(W.FULL32, 5, [top - 1], [top])[0] == float.fromhex("0x1.fffffffffffffp-1")
+
+
+# ----------------------------------------------------------------------------- NEXT-2 MRG32k3a
+
+M1, M2 = 2**32 - 209, 2**32 - 22853
+
+
+def test_mrg32k3a_definition_first_outputs(orc):
+    """L'Ecuyer (1999) MRG32k3a: x_n = (1403580 x_{n-2} - 810728 x_{n-3}) mod m1,
+    y_n = (527612 y_{n-1} - 1370589 y_{n-3}) mod m2, u = (x_n - y_n) mod m1 (0 -> m1).
+    From the all-12345 seed the first output is 545508589 (hand-checked: p1 = 592852*12345 mod m1
+    = 3023790853, p2 = -842977*12345 mod m2 = 2478282264)."""
+    seq = orc.mrg_sequence([12345] * 6, 200)
+    assert seq[0] == 3023790853 - 2478282264 == 545508589
+    x, y = [12345] * 3, [12345] * 3
+    for u in seq:
+        x.append((1403580 * x[-2] - 810728 * x[-3]) % M1)
+        y.append((527612 * y[-1] - 1370589 * y[-3]) % M2)
+        z = (x[-1] - y[-1]) % M1
+        assert u == (z if z else M1) and 1 <= u <= M1
+
+
+def test_mrg_stream_states_in_range(orc):
+    for s in range(300):
+        st = orc.mrg_stream_state(1, s)
+        assert all(0 <= v < M1 for v in st[:3]) and all(0 <= v < M2 for v in st[3:])
+        assert any(st[:3]) and any(st[3:])
+
+
+def test_mrg_reduced_draws_uniform_and_rejection_rate(orc):
+    """R23: reduce-to-width keeps exactly T = floor(m1/2^w)*2^w of the m1 values."""
+    p = dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1, seed=1, n_streams=64,
+             n_per_stream=2000, mrg=True)
+    r = orc.generate(p, want_consumed=True, want_pidx=True)
+    pairs = int(r["pidx"][:, -1].sum() + 64)
+    draws = int(r["consumed"].sum())
+    T = (M1 // 2**26) * 2**26
+    keep = T / M1
+    # each pair needs 2 kept draws: draws ~ 2*pairs/keep
+    expected = 2 * pairs / keep
+    assert abs(draws - expected) < 6 * np.sqrt(expected * (1 - keep)) + 10
+    v = r["out"].ravel()
+    assert v.min() > 0 and v.max() < 1
+    h = np.histogram(v, bins=64, range=(0, 1))[0]
+    e = v.size / 64
+    assert ((h - e) ** 2 / e).sum() < 64 + 8 * np.sqrt(2 * 64)   # chi2 sanity, 63 dof
