@@ -551,14 +551,19 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
 }
 
 // ------------------------------------------------------------------------------ NEXT-2 MRG32k3a
-// Same ROW burst store, MRG32k3a base draws (ALU-bound: ~2 x 25 integer ops per draw).
+// Same ROW burst store, MRG32k3a base draws (ALU/latency-bound: ~2 x 25 integer ops per draw),
+// so shorter bursts (smaller tiles) buy occupancy.
+#ifndef PRNGD_MRG_RC
+#define PRNGD_MRG_RC 16  // A/B on cfg3 shape: 16 -> 136, 32 -> 129, 64 -> 119 Gd/s
+#endif
+constexpr int kMrgCols = PRNGD_MRG_RC;
 __global__ void __launch_bounds__(32) gen_mrg_kernel(const GenArgs g) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t row0 = (uint64_t)blockIdx.x * 32u;
     NoConsumer nc;
     MrgProducer prod(g, g.stream_begin + row0 + lane);
-    run_rows_burst<false, kRowCols>(g, aligned_smem_base(smem_raw), lane, row0, prod, nc);
+    run_rows_burst<false, kMrgCols>(g, aligned_smem_base(smem_raw), lane, row0, prod, nc);
 }
 
 // ------------------------------------------------------------------------------ NEXT-3 jump kernel
@@ -908,7 +913,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
 }
 
 cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st) {
-    const size_t smem = 1024 + (size_t)kRowTileBytes;
+    const size_t smem = 1024 + (size_t)32 * kMrgCols * 8;
     const uint64_t grid = (g.n_streams + 31) / 32;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     cudaError_t e = set_smem(gen_mrg_kernel, smem);
