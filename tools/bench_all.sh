@@ -9,4 +9,5 @@ run --workload cfg4 --steps 50
 run --workload cfg4 --steps 50 --consume
 run --workload cfg5 --steps 50
 run --workload cfg5 --steps 50 --no-write
+run --workload mrg26 --steps 50
 echo done
