@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--flags", type=int, default=0, help="extra prngd flags")
     ap.add_argument("--streams", type=int, default=0,
                     help="override streams per GPU (experiments; the config names it)")
-    ap.add_argument("--store", default="row", choices=["row", "row1k", "rowreg", "tma", "tile", "direct"],
+    ap.add_argument("--store", default="row", choices=["row", "row1k", "tma", "tile", "direct"],
                     help="store path A/B (include/prngd.h PRNGD_FLAG_STORE_*)")
     return ap.parse_args()
 

@@ -71,8 +71,6 @@ typedef enum {
 #define PRNGD_FLAG_STORE_TILE    (2u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_DIRECT  (3u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_ROW1K   (4u << PRNGD_STORE_SHIFT)  /* ROW with 1 KiB bursts (A/B) */
-#define PRNGD_FLAG_STORE_ROWREG  (5u << PRNGD_STORE_SHIFT)  /* 1 KiB per row: 512 B from smem +
-                                                              512 B from registers (A/B) */
 /* Mapping selection, bits 6..7 (NEXT-1): Eq.(4) (default), Eq.(5) discrete-grid normalisation
  * onto [0; 1-k'], or Eq.(6) unit-interval form (requires a0 = b0 = 0 and
  * a = b = 2^w - 1).  All three are followed by the R11 clamp (z' <= 1 - 2^-53). */

@@ -129,7 +129,7 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     if (map_code > 2) return fail(PRNGD_EUNSUPPORTED, "unknown mapping code %u", map_code);
     if (map_code == 2 && !(p->a0 == 0 && p->b0 == 0 && p->a == (1ull << w) - 1 && p->b == p->a))
         return fail(PRNGD_EINVAL, "Eq.(6) needs the unit-interval range a0=b0=0, a=b=2^w-1");
-    if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 5)
+    if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 4)
         return fail(PRNGD_EUNSUPPORTED, "unknown store path %u",
                     (p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT);
 
@@ -238,7 +238,6 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         case PRNGD_FLAG_STORE_TILE: pl.store = Store::STG16; break;
         case PRNGD_FLAG_STORE_DIRECT: pl.store = Store::DIRECT; break;
         case PRNGD_FLAG_STORE_ROW1K: pl.store = Store::ROW1K; break;
-        case PRNGD_FLAG_STORE_ROWREG: pl.store = Store::ROWREG; break;
         default: pl.store = Store::ROW; break;
     }
     *out = h;
@@ -285,7 +284,6 @@ static Plan plan_for(const prngd_handle *h, const void *out, bool consume = fals
     const bool a16 = (a & 15u) == 0 && (nps & 1u) == 0;
     const bool tma_ok = a16 && h->p.n_streams < (1ull << 31) && nps < (1ull << 31);
     if (pl.store == Store::DIRECT && !a32) pl.store = a16 ? Store::STG16 : Store::STG8;
-    if (pl.store == Store::ROWREG && !a32) pl.store = Store::ROW;
     if ((pl.store == Store::ROW || pl.store == Store::ROW1K) && !a16) pl.store = Store::STG8;
     if (pl.store == Store::TMA && !tma_ok) pl.store = a16 ? Store::STG16 : Store::STG8;
     if (pl.store == Store::STG16 && !a16) pl.store = Store::STG8;

@@ -42,8 +42,7 @@ struct GenArgs {
 //   TMA:    32 x 16 smem tiles (128B swizzle) + one cp.async.bulk.tensor.2d store per CTA slab
 //   STG16:  32 x 16 smem tile + warp-coalesced 16-byte st.global;  STG8: 8-byte stores
 //   ROW1K:  as ROW with 128 outputs (1 KiB bursts) per row
-//   ROWREG: 1 KiB per row per flush: 512 B staged in smem + 512 B held in registers
-enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3, ROW = 4, ROW1K = 5, ROWREG = 6 };
+enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3, ROW = 4, ROW1K = 5 };
 
 // Launch descriptors chosen by the host.
 struct Plan {

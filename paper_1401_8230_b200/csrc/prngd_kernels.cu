@@ -44,11 +44,10 @@ constexpr bool is_row() { return ST == Store::ROW || ST == Store::ROW1K; }
 template <Store ST>
 constexpr int row_cols() { return ST == Store::ROW1K ? 2 * kRowCols : kRowCols; }
 template <Store ST>
-constexpr int gen_warps() { return is_row<ST>() || ST == Store::ROWREG ? 1 : kGenWarps; }
+constexpr int gen_warps() { return is_row<ST>() ? 1 : kGenWarps; }
 template <Store ST>
 constexpr size_t gen_smem() {
-    return ST == Store::ROWREG ? 1024 + (size_t)kRowTileBytes
-           : is_row<ST>()      ? 1024 + (size_t)32 * row_cols<ST>() * 8
+    return is_row<ST>() ? 1024 + (size_t)32 * row_cols<ST>() * 8
                         : 1024 + (size_t)kGenWarps * (ST == Store::TMA ? 2 : 1) * kTileBytes;
 }
 constexpr int kConsWarpsTiles = 12;         // warps per CTA, consume kernel staging tiles in smem
@@ -403,65 +402,6 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
     }
 }
 
-// ROWREG store path (A/B): 1 KiB per row per flush at the ROW shared-memory budget.  The first
-// 64 outputs of each row segment are staged in the 16 KiB smem tile and leave as warp-coalesced
-// 512 B row bursts; the next 64 stay in registers (128 per lane) and each lane writes them
-// right after, as 16 x 32-byte stores into its own row, so every row's 1 KiB reaches the L2
-// within one flush.
-template <int MODE, bool SPEC, bool IEEE, bool ALG1>
-__device__ __forceinline__ void run_rows_rowreg(const GenArgs &g, uint32_t tile, uint32_t lane,
-                                                uint64_t row0) {
-    constexpr uint32_t RC = 2 * kRowCols;  // outputs per row per flush
-    XsProducer<MODE, SPEC, IEEE, ALG1> prod(g, g.stream_begin + row0 + lane);
-    const bool live = (row0 + lane) < g.n_streams;
-    const uint32_t nrows = (g.n_streams - row0) < 32u ? (uint32_t)(g.n_streams - row0) : 32u;
-    const uint32_t my_row = tile + lane * (kRowCols * 8u);
-    double *row_out = g.out + (row0 + lane) * g.nps;
-#pragma unroll 1
-    for (uint64_t col0 = 0; col0 < g.nps; col0 += RC) {
-#pragma unroll 1
-        for (uint32_t b = 0; b < kRowCols / kCols; ++b) {
-            double q[kCols];
-            prod(q, g);
-#pragma unroll
-            for (int c = 0; c < kCols / 2; ++c)
-                sts_v2(my_row + (((b * (kCols / 2) + c) ^ lane) << 4), q[2 * c], q[2 * c + 1]);
-        }
-        double r[kRowCols];
-#pragma unroll
-        for (uint32_t b = 0; b < kRowCols / kCols; ++b) {
-            double q[kCols];
-            prod(q, g);
-#pragma unroll
-            for (int i = 0; i < kCols; ++i) r[b * kCols + i] = q[i];
-        }
-        __syncwarp();
-        const uint64_t col = col0 + 2 * lane;
-        if (col < g.nps) {
-            double *dst = g.out + row0 * g.nps + col;
-#pragma unroll 4
-            for (uint32_t rr = 0; rr < nrows; ++rr) {
-                double a, b2;
-                lds_v2(tile + rr * (kRowCols * 8u) + ((lane ^ rr) << 4), a, b2);
-                stg_v2_cs(dst + (uint64_t)rr * g.nps, a, b2);
-            }
-        }
-        if (live) {
-            const uint64_t c1 = col0 + kRowCols;
-            if (c1 + kRowCols <= g.nps) {
-#pragma unroll
-                for (int i = 0; i < kRowCols; i += 4)
-                    stg_v4_cs(row_out + c1 + i, r[i], r[i + 1], r[i + 2], r[i + 3]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < kRowCols; ++i)
-                    if (c1 + i < g.nps) row_out[c1 + i] = r[i];
-            }
-        }
-        __syncwarp();
-    }
-}
-
 __device__ __forceinline__ uint32_t aligned_smem_base(uint8_t *raw) {
     return (smem_u32(raw) + 1023u) & ~1023u;
 }
@@ -474,9 +414,7 @@ __global__ void __launch_bounds__(gen_warps<ST>() * 32)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint64_t row0 = ((uint64_t)blockIdx.x * gen_warps<ST>() + warp) * 32u;
-    if constexpr (ST == Store::ROWREG) {
-        run_rows_rowreg<MODE, SPEC, IEEE, ALG1>(g, aligned_smem_base(smem_raw), lane, row0);
-    } else if constexpr (is_row<ST>()) {
+    if constexpr (is_row<ST>()) {
         NoConsumer nc;
         XsProducer<MODE, SPEC, IEEE, ALG1> prod(g, g.stream_begin + row0 + lane);
         run_rows_burst<false, row_cols<ST>()>(g, aligned_smem_base(smem_raw), lane, row0, prod,
@@ -887,7 +825,6 @@ cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, i
     switch (s) {
         case Store::ROW: return gen_dispatch_store<Store::ROW>(m, g, pl, f32, st);
         case Store::ROW1K: return gen_dispatch_store<Store::ROW1K>(m, g, pl, f32, st);
-        case Store::ROWREG: return gen_dispatch_store<Store::ROWREG>(m, g, pl, f32, st);
         case Store::DIRECT: return gen_dispatch_store<Store::DIRECT>(m, g, pl, f32, st);
         case Store::TMA: return gen_dispatch_store<Store::TMA>(m, g, pl, f32, st);
         case Store::STG16: return gen_dispatch_store<Store::STG16>(m, g, pl, f32, st);
@@ -959,8 +896,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
             s = Store::STG16;
         switch (s) {
             case Store::ROW:
-            case Store::ROW1K:
-            case Store::ROWREG: e = cons_dispatch<Store::ROW, true>(m, g, pl, f32, grid, st); break;
+            case Store::ROW1K: e = cons_dispatch<Store::ROW, true>(m, g, pl, f32, grid, st); break;
             case Store::DIRECT: e = cons_dispatch<Store::DIRECT, true>(m, g, pl, f32, grid, st); break;
             case Store::TMA: e = cons_dispatch<Store::TMA, true>(m, g, pl, f32, grid, st); break;
             case Store::STG16: e = cons_dispatch<Store::STG16, true>(m, g, pl, f32, grid, st); break;

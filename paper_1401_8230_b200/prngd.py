@@ -21,7 +21,6 @@ PRNGD_FLAG_STORE_TMA = 1 << 3
 PRNGD_FLAG_STORE_TILE = 2 << 3
 PRNGD_FLAG_STORE_DIRECT = 3 << 3
 PRNGD_FLAG_STORE_ROW1K = 4 << 3
-PRNGD_FLAG_STORE_ROWREG = 5 << 3
 PRNGD_FLAG_MAP_EQ4 = 0 << 6
 PRNGD_FLAG_MAP_EQ5 = 1 << 6
 PRNGD_FLAG_MAP_EQ6 = 2 << 6
@@ -32,7 +31,7 @@ PRNGD_FLAG_NO_JUMP = 0x400
 MAP_FLAGS = {4: PRNGD_FLAG_MAP_EQ4, 5: PRNGD_FLAG_MAP_EQ5, 6: PRNGD_FLAG_MAP_EQ6}
 STORE_FLAGS = {"row": PRNGD_FLAG_STORE_ROW, "tma": PRNGD_FLAG_STORE_TMA,
                "tile": PRNGD_FLAG_STORE_TILE, "direct": PRNGD_FLAG_STORE_DIRECT,
-               "row1k": PRNGD_FLAG_STORE_ROW1K, "rowreg": PRNGD_FLAG_STORE_ROWREG}
+               "row1k": PRNGD_FLAG_STORE_ROW1K}
 
 EXPORTS = (
     "prngd_create", "prngd_destroy", "prngd_get_info", "prngd_generate", "prngd_generate_consume",
