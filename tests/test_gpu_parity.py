@@ -416,3 +416,61 @@ def test_mrg32k3a_unsupported_calls():
         g.generate_consume()
     with pytest.raises(P.PrngdError):
         g.raw(4)
+
+
+# ------------------------------------------------------------------ guard bands (no sanitizer here)
+
+GUARD = 4096  # doubles of sentinel before and after the output
+
+
+def _guarded(shape):
+    n = shape[0] * shape[1]
+    buf = torch.full((n + 2 * GUARD,), -3.25, dtype=torch.float64, device="cuda")
+    return buf, buf[GUARD:GUARD + n].view(shape)
+
+
+def _guards_intact(buf, n):
+    return bool((buf[:GUARD] == -3.25).all()) and bool((buf[GUARD + n:] == -3.25).all())
+
+
+@pytest.mark.parametrize("flags", list(P.STORE_FLAGS.values()) +
+                         [P.PRNGD_FLAG_JUMP, P.PRNGD_FLAG_MAP_EQ6 | P.PRNGD_FLAG_OPEN])
+@pytest.mark.parametrize("ns,nps", [(45, 70), (31, 1030), (1, 6)])
+def test_guard_bands_generate(orc, flags, ns, nps):
+    p = W.config("cfg1", n_streams=ns, n_per_stream=nps, flags=flags)
+    g = P.Generator(**p)
+    buf, out = _guarded(g.shape)
+    g.generate(out)
+    torch.cuda.synchronize()
+    assert _guards_intact(buf, ns * nps)
+    kind = 6 if flags & P.PRNGD_FLAG_MAP_EQ6 else 4
+    assert_same(out, orc.generate(p, kind=kind, open_interval=bool(flags & P.PRNGD_FLAG_OPEN))["out"])
+
+
+@pytest.mark.parametrize("flags", [P.PRNGD_FLAG_STORE_ROW, P.PRNGD_FLAG_STORE_TMA,
+                                   P.PRNGD_FLAG_STORE_TILE, P.PRNGD_FLAG_STORE_DIRECT])
+def test_guard_bands_consume(orc, flags):
+    p = W.config("cfg2", n_streams=77, n_per_stream=130, flags=flags)
+    g = P.Generator(**p)
+    buf, out = _guarded(g.shape)
+    hbuf = torch.full((65536 + 2 * GUARD,), -7, dtype=torch.int64, device="cuda")
+    hist = hbuf[GUARD:GUARD + 65536]
+    hist.zero_()
+    g.generate_consume(out, hist)
+    torch.cuda.synchronize()
+    assert _guards_intact(buf, 77 * 130)
+    assert bool((hbuf[:GUARD] == -7).all()) and bool((hbuf[GUARD + 65536:] == -7).all())
+    ref = orc.generate(p, want_stats=True)
+    assert np.array_equal(hist.cpu().numpy(), ref["hist"])
+    assert_same(out, ref["out"])
+
+
+def test_guard_bands_mrg(orc):
+    p = dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1, seed=2, n_streams=45, n_per_stream=70,
+             flags=P.PRNGD_FLAG_MRG32K3A, mrg=True)
+    g = P.Generator(**p)
+    buf, out = _guarded(g.shape)
+    g.generate(out)
+    torch.cuda.synchronize()
+    assert _guards_intact(buf, 45 * 70)
+    assert_same(out, orc.generate(p)["out"])
