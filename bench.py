@@ -31,6 +31,8 @@ from paper_1401_8230_b200 import workloads as W  # noqa: E402
 
 METRIC = "Gdoubles/s generated (1/2/4/8 B200) and % of HBM-write roofline"
 FALLBACK_HBM = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+KERNELS = {0: "gen_kernel", 1: "gen_seg_kernel", 2: "gen_jump_kernel", 3: "gen_mrg_kernel"}
+STORES = {0: "TMA", 1: "TILE", 2: "STG8", 3: "DIRECT", 4: "ROW", 5: "ROW1K", 6: "SEG"}
 
 
 def parse():
@@ -49,7 +51,8 @@ def parse():
     ap.add_argument("--flags", type=int, default=0, help="extra prngd flags")
     ap.add_argument("--streams", type=int, default=0,
                     help="override streams per GPU (experiments; the config names it)")
-    ap.add_argument("--store", default="row", choices=["row", "row1k", "tma", "tile", "direct"],
+    ap.add_argument("--store", default="auto",
+                    choices=["auto", "seg", "row", "row1k", "tma", "tile", "direct"],
                     help="store path A/B (include/prngd.h PRNGD_FLAG_STORE_*)")
     return ap.parse_args()
 
@@ -315,8 +318,8 @@ def main():
     achieved = bytes_launch / (kern_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-            "kernel": f"gen_kernel<FULL32,SPEC,{args.store.upper()}>" if not consume
-                      else "consume_kernel+finalize",
+            "kernel": KERNELS[g.info["kernel"]] + f" (store path {STORES[g.info['store']]})"
+                      if not consume else "consume_kernel+finalize",
             "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kern_ms,
             "frac_of_8TBs_nominal": achieved / 8000.0}
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count

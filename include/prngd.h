@@ -56,7 +56,12 @@ typedef enum {
 #define PRNGD_FLAG_IEEE_DIV   0x1u  /* use the IEEE division instruction sequence instead of the
                                        reciprocal + 2 FMA correction (R10); same bits, slower */
 /* Store-path selection, bits 3..5 (an A/B switch; every path writes the same bits):
- *   ROW    (default) each warp stages 32 rows x 64 outputs in shared memory and writes every row
+ *   AUTO   (default, 0) SEG where it applies, else ROW; the fused consumer uses DIRECT
+ *   SEG    row segments: n_per_stream / 128 lanes share a row, lane j starts at pair 128 j of
+ *          its stream by GF(2) jump-ahead and owns that 1 KiB segment; each flush writes 512-byte
+ *          chunks of every segment.  Needs rare rejection (prngd_info.speculative), pair-drop
+ *          consumption and n_per_stream = 128 * 2^m <= 4096; otherwise ROW is used
+ *   ROW    each warp stages 32 rows x 64 outputs in shared memory and writes every row
  *          as one 512-byte burst (32 lanes x 16-byte st.global) -- DRAM-friendly row bursts
  *   TMA    32 x 16-output warp tiles, one cp.async.bulk.tensor.2d store per 128-row CTA slab
  *   TILE   32 x 16-output warp tiles written with warp-coalesced 16-byte st.global
@@ -66,7 +71,9 @@ typedef enum {
  * n_per_stream % 4 == 0; otherwise 8-byte stores). */
 #define PRNGD_STORE_SHIFT        3
 #define PRNGD_STORE_MASK         (7u << PRNGD_STORE_SHIFT)
-#define PRNGD_FLAG_STORE_ROW     (0u << PRNGD_STORE_SHIFT)
+#define PRNGD_FLAG_STORE_AUTO    (0u << PRNGD_STORE_SHIFT)
+#define PRNGD_FLAG_STORE_ROW     (5u << PRNGD_STORE_SHIFT)
+#define PRNGD_FLAG_STORE_SEG     (6u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_TMA     (1u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_TILE    (2u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_DIRECT  (3u << PRNGD_STORE_SHIFT)
@@ -84,7 +91,7 @@ typedef enum {
 /* NEXT-3 intra-stream parallelism: one warp per stream, lanes start at draws 0, 64, 128, ... of
  * the stream via GF(2) jump-ahead of xorshift128 and a warp scan of accepted counts places every
  * output exactly where the sequential order puts it.  Chosen automatically by prngd_generate
- * when there are too few streams to fill the GPU (n_streams < 16384 and n_per_stream >= 512,
+ * when there are too few streams to fill the GPU (AUTO store path, n_streams < 16384 and n_per_stream >= 512,
  * pair-drop consumption); these flags force it on or off. */
 /* NEXT-2: MRG32k3a base generator (L'Ecuyer 1999; P:165 names it) instead of xorshift128.
  * x1 and x2 are uniform bitlen(a)- and bitlen(b)-bit values obtained from MRG32k3a outputs by
@@ -119,6 +126,11 @@ typedef struct {
     uint32_t speculative;   /* 1 if the kernel checks acceptance once per batch (rare rejection) */
     uint64_t n_outputs;     /* n_streams * n_per_stream                                      */
     uint64_t out_bytes;     /* 8 * n_outputs                                                 */
+    uint32_t kernel;        /* kernel prngd_generate launches for a 256-byte aligned output:
+                               0 gen_kernel (one lane per stream), 1 gen_seg_kernel (SEG),
+                               2 gen_jump_kernel (NEXT-3), 3 gen_mrg_kernel (NEXT-2)         */
+    uint32_t store;         /* its store path: 0 TMA, 1 TILE, 2 8-byte, 3 DIRECT, 4 ROW,
+                               5 ROW1K, 6 SEG                                                 */
 } prngd_info;
 
 /* Validate *p and build an immutable handle (host only: no CUDA call, no device memory).
@@ -178,7 +190,8 @@ PRNGD_API prngd_status prngd_debug_map(const prngd_handle *h, const uint32_t *d_
 
 /* Host-only check of the jump-ahead: out = T^n_draws * in for the xorshift128 state
  * (x, y, z, w) = in[0..3].  lane_table >= 0 applies instead the byte table the GPU uses for lane
- * `lane_table` (= T^(64 * lane_table)); n_draws is then ignored.  No CUDA call. */
+ * `lane_table` (= T^(d * lane_table)) with per-lane distance d = n_draws, or d = 64 (the NEXT-3
+ * jump kernel's tables) when n_draws is 0; the SEG store path uses d = 256.  No CUDA call. */
 PRNGD_API prngd_status prngd_debug_jump(uint64_t n_draws, const uint32_t *in, uint32_t *out,
                                         int lane_table);
 

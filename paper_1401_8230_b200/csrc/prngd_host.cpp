@@ -129,7 +129,7 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     if (map_code > 2) return fail(PRNGD_EUNSUPPORTED, "unknown mapping code %u", map_code);
     if (map_code == 2 && !(p->a0 == 0 && p->b0 == 0 && p->a == (1ull << w) - 1 && p->b == p->a))
         return fail(PRNGD_EINVAL, "Eq.(6) needs the unit-interval range a0=b0=0, a=b=2^w-1");
-    if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 4)
+    if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 6)
         return fail(PRNGD_EUNSUPPORTED, "unknown store path %u",
                     (p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT);
 
@@ -230,15 +230,19 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         I.speculative = 0;
         pl.spec = false;
     }
+    // The NEXT-3 jump kernel when forced, or by default (AUTO store) for too few streams to
+    // fill the GPU; an explicit store path is honoured.
+    const bool store_auto = (p->flags & PRNGD_STORE_MASK) == PRNGD_FLAG_STORE_AUTO;
     pl.jump = !mrg && ((p->flags & PRNGD_FLAG_JUMP) ||
-                       (!(p->flags & PRNGD_FLAG_NO_JUMP) && !alg1 && p->n_streams < 16384 &&
-                        p->n_per_stream >= 512));
+                       (!(p->flags & PRNGD_FLAG_NO_JUMP) && !alg1 && store_auto &&
+                        p->n_streams < 16384 && p->n_per_stream >= 512));
     switch (p->flags & PRNGD_STORE_MASK) {
         case PRNGD_FLAG_STORE_TMA: pl.store = Store::TMA; break;
         case PRNGD_FLAG_STORE_TILE: pl.store = Store::STG16; break;
         case PRNGD_FLAG_STORE_DIRECT: pl.store = Store::DIRECT; break;
         case PRNGD_FLAG_STORE_ROW1K: pl.store = Store::ROW1K; break;
-        default: pl.store = Store::ROW; break;
+        case PRNGD_FLAG_STORE_ROW: pl.store = Store::ROW; break;
+        default: pl.store = Store::SEG; break;  // AUTO and SEG: SEG where plan_for allows it
     }
     *out = h;
     return PRNGD_OK;
@@ -263,9 +267,14 @@ prngd_status prngd_destroy(prngd_handle *h) {
     return PRNGD_OK;
 }
 
+static Plan plan_for(const prngd_handle *h, const void *out, bool consume = false);
+
 prngd_status prngd_get_info(const prngd_handle *h, prngd_info *info) {
     if (!h || !info) return fail(PRNGD_EINVAL, "null argument");
     *info = h->info;
+    const Plan pl = plan_for(h, reinterpret_cast<const void *>(uintptr_t{256}));
+    info->store = (uint32_t)pl.store;
+    info->kernel = h->plan.mrg ? 3u : h->plan.jump ? 2u : pl.store == Store::SEG ? 1u : 0u;
     return PRNGD_OK;
 }
 
@@ -273,21 +282,40 @@ uint32_t prngd_last_launches(const prngd_handle *h) { return h ? h->last_launche
 
 // Store path for this output pointer: the requested one when its alignment rules hold, else
 // the next one that is legal (same bits whichever path writes them).
-static Plan plan_for(const prngd_handle *h, const void *out, bool consume = false) {
+static Plan plan_for(const prngd_handle *h, const void *out, bool consume) {
     Plan pl = h->plan;
     // Fused consumer + outputs: the smem histogram leaves no room for row tiles at full
     // occupancy, so the default there is the register (DIRECT) store (measured best).
-    if (consume && (h->p.flags & PRNGD_STORE_MASK) == PRNGD_FLAG_STORE_ROW) pl.store = Store::DIRECT;
+    if (consume && pl.store == Store::SEG) pl.store = Store::DIRECT;
     const uintptr_t a = (uintptr_t)out;
     const uint64_t nps = h->p.n_per_stream;
     const bool a32 = (a & 31u) == 0 && (nps & 3u) == 0;
     const bool a16 = (a & 15u) == 0 && (nps & 1u) == 0;
+    // SEG: rare rejection (speculative), pair-drop, nps = 128 * S with S a power of two <= 32,
+    // and 16-byte stores; otherwise the ROW path.
+    if (pl.store == Store::SEG) {
+        const uint64_t S = nps / prngd::kSegOut;
+        const bool seg_ok = pl.spec && !pl.alg1 && a16 && nps % prngd::kSegOut == 0 && S >= 1 &&
+                            S <= 32 && (S & (S - 1)) == 0;
+        if (!seg_ok) pl.store = Store::ROW;
+    }
     const bool tma_ok = a16 && h->p.n_streams < (1ull << 31) && nps < (1ull << 31);
     if (pl.store == Store::DIRECT && !a32) pl.store = a16 ? Store::STG16 : Store::STG8;
     if ((pl.store == Store::ROW || pl.store == Store::ROW1K) && !a16) pl.store = Store::STG8;
     if (pl.store == Store::TMA && !tma_ok) pl.store = a16 ? Store::STG16 : Store::STG8;
     if (pl.store == Store::STG16 && !a16) pl.store = Store::STG8;
     return pl;
+}
+
+// Row-parallel generate kernels (one lane per stream, or per 1 KiB stream segment for SEG).
+static cudaError_t launch_rows(const GenArgs &g, const Plan &pl, cudaStream_t st, int sms) {
+    if (pl.store == Store::SEG) {
+        const void *tables = nullptr;
+        cudaError_t e = prngd::jump_tables(prngd::kSegDraws, &tables);
+        if (e != cudaSuccess) return e;
+        return prngd::launch_generate_seg(g, pl, tables, st);
+    }
+    return prngd::launch_generate(g, pl, st, sms);
 }
 
 prngd_status prngd_generate(const prngd_handle *h, double *d_out, void *cuda_stream) {
@@ -306,10 +334,11 @@ prngd_status prngd_generate(const prngd_handle *h, double *d_out, void *cuda_str
         e = prngd::launch_generate_mrg(g, (cudaStream_t)cuda_stream);
     } else if (h->plan.jump) {
         const void *tables = nullptr;
-        if ((e = prngd::jump_tables(&tables)) != cudaSuccess) return cuda_fail(e, "jump tables");
+        if ((e = prngd::jump_tables(prngd::kJumpDraws, &tables)) != cudaSuccess)
+            return cuda_fail(e, "jump tables");
         e = prngd::launch_generate_jump(g, h->plan, tables, (cudaStream_t)cuda_stream);
     } else {
-        e = prngd::launch_generate(g, pl, (cudaStream_t)cuda_stream, sms);
+        e = launch_rows(g, pl, (cudaStream_t)cuda_stream, sms);
     }
     if (e != cudaSuccess) return cuda_fail(e, "generate kernel launch");
     h->last_launches.store(1);
@@ -417,7 +446,7 @@ prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stre
         g.stream_begin = h->p.stream_begin + r0;
         g.n_streams = nr;
         g.out = h->stage[b];
-        if ((e = prngd::launch_generate(g, plan_for(h, h->stage[b]), gs, sms)) != cudaSuccess)
+        if ((e = launch_rows(g, plan_for(h, h->stage[b]), gs, sms)) != cudaSuccess)
             return cuda_fail(e, "generate kernel launch");
         ++launches;
         if ((e = cudaEventRecord(h->ev_gen[b], gs)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");

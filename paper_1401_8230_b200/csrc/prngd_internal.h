@@ -42,7 +42,8 @@ struct GenArgs {
 //   TMA:    32 x 16 smem tiles (128B swizzle) + one cp.async.bulk.tensor.2d store per CTA slab
 //   STG16:  32 x 16 smem tile + warp-coalesced 16-byte st.global;  STG8: 8-byte stores
 //   ROW1K:  as ROW with 128 outputs (1 KiB bursts) per row
-enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3, ROW = 4, ROW1K = 5 };
+//   SEG:    nps/128 lanes per row (jump-ahead), each lane a 1 KiB segment; 512 B bursts
+enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3, ROW = 4, ROW1K = 5, SEG = 6 };
 
 // Launch descriptors chosen by the host.
 struct Plan {
@@ -58,7 +59,12 @@ struct Plan {
 // NEXT-3 jump-ahead (prngd_jump.cpp): lane l of a warp starts a round at draw l*kJumpDraws of
 // its stream (kJumpDraws / 2 pairs per lane per round, 32 lanes per stream).
 constexpr uint64_t kJumpDraws = 64;
-cudaError_t jump_tables(const void **out);  // device byte tables [32][16][256] x uint4, cached
+// SEG store path: a lane owns a 1 KiB segment (kSegOut outputs = pairs) of its stream's row and
+// starts at draw j * kSegDraws (segment j) via the same byte tables built for that distance.
+constexpr uint64_t kSegOut = 128;
+constexpr uint64_t kSegDraws = 2 * kSegOut;
+// device byte tables [32][16][256] x uint4 of J_l = T^(lane_draws * l), cached per device
+cudaError_t jump_tables(uint64_t lane_draws, const void **out);
 void jump_host(uint64_t n_draws, const uint32_t in[4], uint32_t out[4], int lane_table);
 
 // Launchers (prngd_kernels.cu).  They return cudaGetLastError() of the launch.
@@ -71,6 +77,8 @@ size_t consume_scratch_bytes(int num_sms);
 cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st);
 cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *tables,
                                  cudaStream_t st);
+cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *tables,
+                                cudaStream_t st);
 cudaError_t launch_debug_raw(const GenArgs &g, uint32_t *d_raw, uint64_t draws, cudaStream_t st);
 cudaError_t launch_debug_pairs(const GenArgs &g, const Plan &pl, uint32_t *d_pidx,
                                uint64_t *d_consumed, cudaStream_t st);

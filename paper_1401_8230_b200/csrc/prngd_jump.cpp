@@ -79,10 +79,10 @@ Mat128 t_power(uint64_t n) {  // T^n by square-and-multiply
     return r;
 }
 
-// Byte tables of the 32 lane matrices J_l = T^(kJumpDraws * l), [l][b][v] -> 4 words.
-std::vector<uint32_t> build_tables() {
+// Byte tables of the 32 lane matrices J_l = T^(lane_draws * l), [l][b][v] -> 4 words.
+std::vector<uint32_t> build_tables(uint64_t lane_draws) {
     std::vector<uint32_t> tab((size_t)32 * 16 * 256 * 4, 0u);
-    const Mat128 step_lane = t_power(kJumpDraws);
+    const Mat128 step_lane = t_power(lane_draws);
     Mat128 j = identity();
     for (int l = 0; l < 32; ++l) {
         for (int b = 0; b < 16; ++b)
@@ -98,28 +98,36 @@ std::vector<uint32_t> build_tables() {
 }
 
 std::mutex g_mu;
-std::map<int, void *> g_dev_tables;  // device -> table pointer (process lifetime)
+std::map<std::pair<int, uint64_t>, void *> g_dev_tables;  // (device, lane_draws) -> tables
+std::map<uint64_t, std::vector<uint32_t>> g_host_tables;   // lane_draws -> host copy
+
+const std::vector<uint32_t> &host_tables(uint64_t lane_draws) {  // call with g_mu held
+    auto it = g_host_tables.find(lane_draws);
+    if (it == g_host_tables.end())
+        it = g_host_tables.emplace(lane_draws, build_tables(lane_draws)).first;
+    return it->second;
+}
 
 }  // namespace
 
-cudaError_t jump_tables(const void **out) {
+cudaError_t jump_tables(uint64_t lane_draws, const void **out) {
     int dev = -1;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lock(g_mu);
-    auto it = g_dev_tables.find(dev);
+    auto it = g_dev_tables.find({dev, lane_draws});
     if (it != g_dev_tables.end()) {
         *out = it->second;
         return cudaSuccess;
     }
-    static std::vector<uint32_t> host = build_tables();
+    const std::vector<uint32_t> &host = host_tables(lane_draws);
     void *d = nullptr;
     if ((e = cudaMalloc(&d, host.size() * 4)) != cudaSuccess) return e;
     if ((e = cudaMemcpy(d, host.data(), host.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) {
         cudaFree(d);
         return e;
     }
-    g_dev_tables[dev] = d;
+    g_dev_tables[{dev, lane_draws}] = d;
     *out = d;
     return cudaSuccess;
 }
@@ -128,8 +136,11 @@ void jump_host(uint64_t n_draws, const uint32_t in[4], uint32_t out[4], int lane
     Vec128 v;
     std::memcpy(v.w, in, 16);
     Vec128 r;
-    if (lane_table >= 0) {  // through the byte table of lane `lane_table` (what the GPU reads)
-        static std::vector<uint32_t> tab = build_tables();
+    if (lane_table >= 0) {  // through the byte table of lane `lane_table` (what the GPU reads):
+                            // J = T^(lane_draws * lane_table), lane_draws = n_draws or kJumpDraws
+        const uint64_t lane_draws = n_draws ? n_draws : kJumpDraws;
+        std::lock_guard<std::mutex> lock(g_mu);
+        const std::vector<uint32_t> &tab = host_tables(lane_draws);
         std::memset(r.w, 0, 16);
         for (int b = 0; b < 16; ++b) {
             const uint32_t byte = (v.w[b >> 2] >> (8 * (b & 3))) & 0xFFu;

@@ -671,6 +671,127 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
     }
 }
 
+// ------------------------------------------------------------------------------ SEG store path
+// Row segments: a lane owns one 1 KiB segment (kSegOut = 128 outputs) of a row, so the S =
+// nps / 128 lanes of a row write it side by side and each flush puts S 512-byte chunks, 1 KiB
+// apart, into the same row (tools/segment_sweep.py: 7.09 vs 6.73 TB/s for cfg3's rows, 6.9 vs
+// 6.2 TB/s for cfg4's).  Lane j of a row starts at pair j*128 = draw j*kSegDraws of its stream
+// through the jump tables T^(256 l).  Under pair-drop that pair range is fixed whatever the
+// earlier lanes reject, but the output positions are not: the fast path assumes no rejection
+// (and no x1 = a - 1, the only row the R11 clamp can touch) and a warp vote at the end sends
+// the whole warp to seg_exact(), which rewrites every output of its rows exactly.
+constexpr int kSegHalf = 64;  // outputs per lane per flush (one 512-byte chunk)
+
+template <int MODE, bool IEEE>
+__device__ __forceinline__ void seg_exact(const GenArgs &g, Xs128 st, uint32_t j, uint32_t S,
+                                          uint64_t row, bool live) {
+    constexpr bool FULL32 = MODE == 2;
+    constexpr bool EQ4 = MODE >= 1;
+    const uint32_t sh1 = FULL32 ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
+    const uint32_t w = FULL32 ? 32u : g.w;
+    const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
+    const Xs128 seg0 = st;
+    // pass 1: accepted pairs among this lane's kSegOut pairs
+    uint32_t cnt = 0;
+#pragma unroll 1
+    for (uint32_t i = 0; i < kSegOut; ++i) {
+        const uint32_t x1 = draw(st) >> sh1;
+        draw(st);
+        cnt += accepted(x1, lo, span) ? 1u : 0u;
+    }
+    // exclusive scan over the S lanes of the row: first output position of this segment
+    uint32_t incl = cnt;
+    for (uint32_t o = 1; o < S; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o, S);
+        if (j >= o) incl += t;
+    }
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, S - 1, S);
+    // pass 2: each accepted pair at its sequential position (the R11 clamp included)
+    st = seg0;
+    uint32_t pos = incl - cnt;
+    double *row_out = g.out + row * g.nps;
+#pragma unroll 1
+    for (uint32_t i = 0; i < kSegOut; ++i) {
+        const uint32_t x1 = draw(st) >> sh1;
+        const uint32_t x2 = draw(st) >> sh2;
+        if (accepted(x1, lo, span)) {
+            const double q = EQ4 ? eq4_pair<IEEE, true>(x1, x2, w, g.Cs, g.Ds, g.y)
+                                 : map_pair<IEEE, true>(x1, x2, g.map);
+            if (live) row_out[pos] = q;
+            ++pos;
+        }
+    }
+    // the row's last lane continues the sequence past pair nps for the outputs still missing
+    if (j == S - 1) {
+#pragma unroll 1
+        for (uint64_t p = total; p < g.nps; ++p) {
+            const double q = exact_output<EQ4, IEEE, false>(st, sh1, sh2, w, lo, span, g);
+            if (live) row_out[p] = q;
+        }
+    }
+}
+
+template <int MODE, bool IEEE>
+__global__ void __launch_bounds__(32)
+    gen_seg_kernel(const GenArgs g, const uint4 *__restrict__ tabs, uint32_t log2S) {
+    extern __shared__ uint8_t smem_raw[];
+    constexpr bool FULL32 = MODE == 2;
+    constexpr bool EQ4 = MODE >= 1;
+    const uint32_t sh1 = FULL32 ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
+    const uint32_t w = FULL32 ? 32u : g.w;
+    const uint32_t lo = FULL32 ? 1u : g.lo;
+    const uint32_t span_fast = FULL32 ? 0xFFFFFFFDu : g.span_fast;
+    const uint32_t lane = threadIdx.x;
+    const uint32_t S = 1u << log2S;            // lanes (segments) per row
+    const uint32_t j = lane & (S - 1u);        // this lane's segment
+    const uint32_t rows_per_warp = 32u >> log2S;
+    const uint64_t row0 = (uint64_t)blockIdx.x * rows_per_warp;
+    const uint64_t row = row0 + (lane >> log2S);
+    const bool live = row < g.n_streams;
+    const uint32_t tile = aligned_smem_base(smem_raw);
+    const uint32_t my = tile + lane * (kSegHalf * 8u);  // this lane's 512-byte tile row
+    Xs128 st = stream_start(g.seed, g.stream_begin + row);
+    if (j) st = jump_state(tabs + (size_t)j * 16 * 256, st);
+    const Xs128 seg0 = st;
+    bool rej = false;
+#pragma unroll 1
+    for (uint32_t h = 0; h < kSegOut / kSegHalf; ++h) {
+#pragma unroll 1
+        for (uint32_t b = 0; b < kSegHalf / kCols; ++b) {
+            double q[kCols];
+#pragma unroll
+            for (int i = 0; i < kCols; ++i) {
+                const uint32_t x1 = draw(st) >> sh1;
+                const uint32_t x2 = draw(st) >> sh2;
+                rej |= !accepted(x1, lo, span_fast);
+                q[i] = EQ4 ? eq4_pair<IEEE, false>(x1, x2, w, g.Cs, g.Ds, g.y)
+                           : map_pair<IEEE, false>(x1, x2, g.map);
+            }
+            // 16-byte chunk c of tile row r at chunk c ^ r: conflict-free writes and reads
+#pragma unroll
+            for (int c = 0; c < kCols / 2; ++c)
+                sts_v2(my + (((b * (kCols / 2) + c) ^ lane) << 4), q[2 * c], q[2 * c + 1]);
+        }
+        __syncwarp();
+        // flush: tile row r -> 512 contiguous bytes of row(r), segment j(r), half h
+#pragma unroll 4
+        for (uint32_t r = 0; r < 32u; ++r) {
+            const uint64_t rr = row0 + (r >> log2S);
+            if (rr < g.n_streams) {
+                double a, b2;
+                lds_v2(tile + r * (kSegHalf * 8u) + ((lane ^ r) << 4), a, b2);
+                stg_v2_cs(g.out + rr * g.nps + (r & (S - 1u)) * kSegOut + h * kSegHalf + 2 * lane,
+                          a, b2);
+            }
+        }
+        __syncwarp();
+    }
+    if (__builtin_expect(__any_sync(0xFFFFFFFFu, rej), 0)) {
+        __syncwarp();  // the speculative stores above are ordered before the exact rewrite
+        seg_exact<MODE, IEEE>(g, seg0, j, S, row, live);
+    }
+}
+
 // ------------------------------------------------------------------------------ debug kernels
 __global__ void debug_raw_kernel(const GenArgs g, uint32_t *raw, uint64_t draws) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -941,6 +1062,37 @@ cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *t
         if ((e = set_smem(gen_jump_kernel<0>, smem)) != cudaSuccess) return e;
         gen_jump_kernel<0><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *tables,
+                                cudaStream_t st) {
+    const uint64_t S = g.nps / kSegOut;  // host checked: nps = 128 * S, S a power of two <= 32
+    uint32_t log2S = 0;
+    while ((1ull << log2S) < S) ++log2S;
+    const uint64_t rows_per_warp = 32u >> log2S;
+    const uint64_t grid = (g.n_streams + rows_per_warp - 1) / rows_per_warp;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    const size_t smem = 1024 + (size_t)32 * kSegHalf * 8;
+    const uint4 *t = static_cast<const uint4 *>(tables);
+    const int mode = kernel_mode(g);
+    cudaError_t e;
+#define PRNGD_SEG_LAUNCH(M, I)                                                                  \
+    do {                                                                                        \
+        if ((e = set_smem(gen_seg_kernel<M, I>, smem)) != cudaSuccess) return e;                \
+        gen_seg_kernel<M, I><<<(unsigned)grid, 32, smem, st>>>(g, t, log2S);                   \
+    } while (0)
+    if (pl.ieee_div) {
+        if (mode >= 1) PRNGD_SEG_LAUNCH(1, true);
+        else PRNGD_SEG_LAUNCH(0, true);
+    } else if (mode == 2) {
+        PRNGD_SEG_LAUNCH(2, false);
+    } else if (mode == 1) {
+        PRNGD_SEG_LAUNCH(1, false);
+    } else {
+        PRNGD_SEG_LAUNCH(0, false);
+    }
+#undef PRNGD_SEG_LAUNCH
     return cudaGetLastError();
 }
 

@@ -16,7 +16,9 @@ LIB_PATH = os.environ.get("PRNGD_LIB") or os.path.join(PKG, "libprngd_b200.so")
 PRNGD_OK, PRNGD_EINVAL, PRNGD_ECUDA, PRNGD_ENOMEM, PRNGD_EUNSUPPORTED = range(5)
 PRNGD_FLAG_IEEE_DIV = 0x1
 PRNGD_FLAG_ALG1 = 0x4
-PRNGD_FLAG_STORE_ROW = 0 << 3
+PRNGD_FLAG_STORE_AUTO = 0 << 3
+PRNGD_FLAG_STORE_ROW = 5 << 3
+PRNGD_FLAG_STORE_SEG = 6 << 3
 PRNGD_FLAG_STORE_TMA = 1 << 3
 PRNGD_FLAG_STORE_TILE = 2 << 3
 PRNGD_FLAG_STORE_DIRECT = 3 << 3
@@ -29,7 +31,8 @@ PRNGD_FLAG_JUMP = 0x200
 PRNGD_FLAG_MRG32K3A = 0x800
 PRNGD_FLAG_NO_JUMP = 0x400
 MAP_FLAGS = {4: PRNGD_FLAG_MAP_EQ4, 5: PRNGD_FLAG_MAP_EQ5, 6: PRNGD_FLAG_MAP_EQ6}
-STORE_FLAGS = {"row": PRNGD_FLAG_STORE_ROW, "tma": PRNGD_FLAG_STORE_TMA,
+STORE_FLAGS = {"auto": PRNGD_FLAG_STORE_AUTO, "seg": PRNGD_FLAG_STORE_SEG,
+               "row": PRNGD_FLAG_STORE_ROW, "tma": PRNGD_FLAG_STORE_TMA,
                "tile": PRNGD_FLAG_STORE_TILE, "direct": PRNGD_FLAG_STORE_DIRECT,
                "row1k": PRNGD_FLAG_STORE_ROW1K}
 
@@ -52,7 +55,7 @@ class prngd_info(C.Structure):
     _fields_ = [("C", C.c_double), ("D", C.c_double), ("C_s", C.c_double), ("D_s", C.c_double),
                 ("y", C.c_double), ("sh1", C.c_uint32), ("sh2", C.c_uint32),
                 ("clamp", C.c_uint32), ("speculative", C.c_uint32), ("n_outputs", C.c_uint64),
-                ("out_bytes", C.c_uint64)]
+                ("out_bytes", C.c_uint64), ("kernel", C.c_uint32), ("store", C.c_uint32)]
 
 
 class PrngdError(RuntimeError):

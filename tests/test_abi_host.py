@@ -163,6 +163,10 @@ def test_jump_ahead_matches_sequential_draws(lib, orc):
         for lane in (0, 1, 2, 17, 31):
             assert P.prngd_debug_jump(0, st, lane) == P.prngd_debug_jump(64 * lane, st) if lane \
                 else P.prngd_debug_jump(0, st, 0) == st
+        # SEG store path tables: lane j of a row starts at draw 256 j (pair 128 j)
+        seq = orc.xs128_sequence(st, 256 * 31)
+        for lane in (1, 2, 7, 15, 31):
+            assert P.prngd_debug_jump(256, st, lane) == tuple(seq[256 * lane - 4:256 * lane])
 
 
 def test_jump_flag_rules(lib):

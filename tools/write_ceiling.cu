@@ -125,3 +125,43 @@ extern "C" __attribute__((visibility("default"))) int wc_store(double *p, uint64
     }
     return (int)cudaGetLastError();
 }
+
+// Segmented rows: the buffer is [rows][cols]; a one-warp CTA owns 32/S rows, each split into S
+// segments (lane = row_local * S + seg owns one segment).  Each flush writes `chunk` bytes of
+// every segment (32 chunks per flush, 512 B per instruction walking the chunks in lane order),
+// so S = 1, chunk = 512 is the ROW kernel's pattern and S = 32, chunk = cols*8/32 writes one
+// whole row per flush.  Occupancy is set by the dynamic smem pad (the real tile size).
+__global__ void __launch_bounds__(32) row_segments(double *p, uint64_t rows, uint64_t cols,
+                                                   uint32_t S, uint32_t chunk_doubles,
+                                                   uint64_t salt) {
+    extern __shared__ uint8_t pad[];
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t rpw = 32u / S;
+    const uint64_t row0 = (uint64_t)blockIdx.x * rpw;
+    if (row0 >= rows) return;
+    if (salt == ~0ull) pad[threadIdx.x] = 0;
+    const uint64_t seg_len = cols / S;
+    const uint32_t per_flush = 32u * chunk_doubles;  // doubles per flush
+    for (uint64_t v = 0; v * chunk_doubles < seg_len; ++v) {
+        for (uint32_t off = 2 * lane; off < per_flush; off += 64) {
+            const uint32_t c = off / chunk_doubles, within = off % chunk_doubles;
+            const uint64_t r = row0 + c / S, seg = c % S;
+            const uint64_t e = r * cols + seg * seg_len + v * chunk_doubles + within;
+            asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p + e), "d"(hval(e, salt)),
+                         "d"(hval(e + 1, salt))
+                         : "memory");
+        }
+    }
+}
+
+extern "C" __attribute__((visibility("default"))) int wc_segments(double *p, uint64_t n,
+                                                                  uint32_t S, uint32_t chunk_bytes,
+                                                                  uint32_t smem_pad, uint64_t salt,
+                                                                  void *stream, uint64_t cols) {
+    const uint64_t rows = n / cols;
+    cudaFuncSetAttribute(row_segments, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const uint32_t rpw = 32u / S;
+    row_segments<<<(unsigned)((rows + rpw - 1) / rpw), 32, smem_pad, (cudaStream_t)stream>>>(
+        p, rows, cols, S, chunk_bytes / 8, salt);
+    return (int)cudaGetLastError();
+}
