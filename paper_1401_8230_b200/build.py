@@ -6,8 +6,10 @@ from __future__ import annotations
 
 import argparse
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -37,8 +39,9 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     if not (force or out or _stale()):
         return LIB
     objs = []
+    objdir = tempfile.mkdtemp(prefix="prngd_build_")  # per build: variant builds may run in parallel
     for src in SOURCES:
-        obj = os.path.join(CSRC, os.path.basename(src) + ".o")
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
@@ -58,8 +61,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
     os.replace(tmp, lib)
-    for o in objs:
-        os.remove(o)
+    shutil.rmtree(objdir, ignore_errors=True)
     return lib
 
 

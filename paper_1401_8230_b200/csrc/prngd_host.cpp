@@ -242,8 +242,10 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         case PRNGD_FLAG_STORE_DIRECT: pl.store = Store::DIRECT; break;
         case PRNGD_FLAG_STORE_ROW1K: pl.store = Store::ROW1K; break;
         case PRNGD_FLAG_STORE_ROW: pl.store = Store::ROW; break;
-        default: pl.store = Store::SEG; break;  // AUTO and SEG: SEG where plan_for allows it
+        case PRNGD_FLAG_STORE_SEG: pl.store = Store::SEG; break;
+        default: pl.store = Store::ROW; break;  // AUTO: ROW; plan_for may pick SEG (below)
     }
+    pl.store_auto = store_auto;
     *out = h;
     return PRNGD_OK;
 }
@@ -274,7 +276,7 @@ prngd_status prngd_get_info(const prngd_handle *h, prngd_info *info) {
     *info = h->info;
     const Plan pl = plan_for(h, reinterpret_cast<const void *>(uintptr_t{256}));
     info->store = (uint32_t)pl.store;
-    info->kernel = h->plan.mrg ? 3u : h->plan.jump ? 2u : pl.store == Store::SEG ? 1u : 0u;
+    info->kernel = pl.mrg ? 3u : pl.jump ? 2u : pl.store == Store::SEG ? 1u : 0u;
     return PRNGD_OK;
 }
 
@@ -286,18 +288,23 @@ static Plan plan_for(const prngd_handle *h, const void *out, bool consume) {
     Plan pl = h->plan;
     // Fused consumer + outputs: the smem histogram leaves no room for row tiles at full
     // occupancy, so the default there is the register (DIRECT) store (measured best).
-    if (consume && pl.store == Store::SEG) pl.store = Store::DIRECT;
+    if (consume && (pl.store == Store::SEG || pl.store_auto)) pl.store = Store::DIRECT;
     const uintptr_t a = (uintptr_t)out;
     const uint64_t nps = h->p.n_per_stream;
     const bool a32 = (a & 31u) == 0 && (nps & 3u) == 0;
     const bool a16 = (a & 15u) == 0 && (nps & 1u) == 0;
     // SEG: rare rejection (speculative), pair-drop, nps = 128 * S with S a power of two <= 32,
-    // and 16-byte stores; otherwise the ROW path.
-    if (pl.store == Store::SEG) {
-        const uint64_t S = nps / prngd::kSegOut;
-        const bool seg_ok = pl.spec && !pl.alg1 && a16 && nps % prngd::kSegOut == 0 && S >= 1 &&
-                            S <= 32 && (S & (S - 1)) == 0;
-        if (!seg_ok) pl.store = Store::ROW;
+    // and 16-byte stores; otherwise the ROW path.  AUTO takes SEG instead of the NEXT-3 jump
+    // kernel for few-stream generate calls (cfg1: 76 vs 64 Gd/s); for bulk shapes ROW stays
+    // ahead (cfg3: 790 vs 645 Gd/s: the per-segment jump costs more than the store pattern
+    // gains).
+    const uint64_t S = nps / prngd::kSegOut;
+    const bool seg_ok = !pl.mrg && pl.spec && !pl.alg1 && a16 && nps % prngd::kSegOut == 0 &&
+                        S >= 1 && S <= 32 && (S & (S - 1)) == 0;
+    if (pl.store == Store::SEG && !seg_ok) pl.store = Store::ROW;
+    if (!consume && pl.store_auto && pl.jump && !(h->p.flags & PRNGD_FLAG_JUMP) && seg_ok) {
+        pl.jump = false;
+        pl.store = Store::SEG;
     }
     const bool tma_ok = a16 && h->p.n_streams < (1ull << 31) && nps < (1ull << 31);
     if (pl.store == Store::DIRECT && !a32) pl.store = a16 ? Store::STG16 : Store::STG8;
@@ -328,11 +335,11 @@ prngd_status prngd_generate(const prngd_handle *h, double *d_out, void *cuda_str
     g.out = d_out;
     cudaError_t e;
     const Plan pl = plan_for(h, d_out);
-    if (h->plan.mrg) {
+    if (pl.mrg) {
         if (pl.store != Store::ROW && pl.store != Store::ROW1K)
             return fail(PRNGD_EUNSUPPORTED, "MRG32k3a needs a 16-byte aligned output and even n_per_stream");
         e = prngd::launch_generate_mrg(g, (cudaStream_t)cuda_stream);
-    } else if (h->plan.jump) {
+    } else if (pl.jump) {
         const void *tables = nullptr;
         if ((e = prngd::jump_tables(prngd::kJumpDraws, &tables)) != cudaSuccess)
             return cuda_fail(e, "jump tables");

@@ -53,6 +53,7 @@ struct Plan {
     bool alg1;      // PRNGD_FLAG_ALG1
     bool jump;      // NEXT-3 intra-stream kernel (one warp per stream)
     bool mrg;       // NEXT-2 MRG32k3a base generator
+    bool store_auto;  // PRNGD_FLAG_STORE_AUTO: the library picks the store path / kernel
     Store store;
 };
 
@@ -65,6 +66,8 @@ constexpr uint64_t kSegOut = 128;
 constexpr uint64_t kSegDraws = 2 * kSegOut;
 // device byte tables [32][16][256] x uint4 of J_l = T^(lane_draws * l), cached per device
 cudaError_t jump_tables(uint64_t lane_draws, const void **out);
+// the same matrices as nibble tables [32][32][16] x uint4 (8 KiB per lane matrix)
+cudaError_t jump_tables_nibble(uint64_t lane_draws, const void **out);
 void jump_host(uint64_t n_draws, const uint32_t in[4], uint32_t out[4], int lane_table);
 
 // Launchers (prngd_kernels.cu).  They return cudaGetLastError() of the launch.

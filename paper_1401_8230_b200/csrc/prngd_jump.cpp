@@ -97,39 +97,71 @@ std::vector<uint32_t> build_tables(uint64_t lane_draws) {
     return tab;
 }
 
-std::mutex g_mu;
-std::map<std::pair<int, uint64_t>, void *> g_dev_tables;  // (device, lane_draws) -> tables
-std::map<uint64_t, std::vector<uint32_t>> g_host_tables;   // lane_draws -> host copy
+// Nibble tables of the same 32 lane matrices: [l][p][v] = J_l * (v << 4p), p < 32, v < 16 (8 KiB
+// per lane instead of 64 KiB: 32 loads per jump instead of 16, an 8x smaller cache footprint).
+std::vector<uint32_t> build_nibble_tables(uint64_t lane_draws) {
+    std::vector<uint32_t> tab((size_t)32 * 32 * 16 * 4, 0u);
+    const Mat128 step_lane = t_power(lane_draws);
+    Mat128 j = identity();
+    for (int l = 0; l < 32; ++l) {
+        for (int p = 0; p < 32; ++p)
+            for (int v = 0; v < 16; ++v) {
+                uint32_t *e = &tab[(((size_t)l * 32 + p) * 16 + v) * 4];
+                for (int t = 0; t < 4; ++t)
+                    if ((v >> t) & 1)
+                        for (int k = 0; k < 4; ++k) e[k] ^= j.col[4 * p + t].w[k];
+            }
+        j = mul(step_lane, j);
+    }
+    return tab;
+}
 
-const std::vector<uint32_t> &host_tables(uint64_t lane_draws) {  // call with g_mu held
-    auto it = g_host_tables.find(lane_draws);
+std::mutex g_mu;
+// key: lane_draws with bit 63 set for the nibble form
+std::map<std::pair<int, uint64_t>, void *> g_dev_tables;  // (device, key) -> tables
+std::map<uint64_t, std::vector<uint32_t>> g_host_tables;   // key -> host copy
+constexpr uint64_t kNibbleKey = 1ull << 63;
+
+const std::vector<uint32_t> &host_tables(uint64_t key) {  // call with g_mu held
+    auto it = g_host_tables.find(key);
     if (it == g_host_tables.end())
-        it = g_host_tables.emplace(lane_draws, build_tables(lane_draws)).first;
+        it = g_host_tables
+                 .emplace(key, (key & kNibbleKey) ? build_nibble_tables(key & ~kNibbleKey)
+                                                  : build_tables(key))
+                 .first;
     return it->second;
 }
 
-}  // namespace
-
-cudaError_t jump_tables(uint64_t lane_draws, const void **out) {
+cudaError_t device_tables(uint64_t key, const void **out) {
     int dev = -1;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lock(g_mu);
-    auto it = g_dev_tables.find({dev, lane_draws});
+    auto it = g_dev_tables.find({dev, key});
     if (it != g_dev_tables.end()) {
         *out = it->second;
         return cudaSuccess;
     }
-    const std::vector<uint32_t> &host = host_tables(lane_draws);
+    const std::vector<uint32_t> &host = host_tables(key);
     void *d = nullptr;
     if ((e = cudaMalloc(&d, host.size() * 4)) != cudaSuccess) return e;
     if ((e = cudaMemcpy(d, host.data(), host.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) {
         cudaFree(d);
         return e;
     }
-    g_dev_tables[{dev, lane_draws}] = d;
+    g_dev_tables[{dev, key}] = d;
     *out = d;
     return cudaSuccess;
+}
+
+}  // namespace
+
+cudaError_t jump_tables(uint64_t lane_draws, const void **out) {
+    return device_tables(lane_draws, out);
+}
+
+cudaError_t jump_tables_nibble(uint64_t lane_draws, const void **out) {
+    return device_tables(lane_draws | kNibbleKey, out);
 }
 
 void jump_host(uint64_t n_draws, const uint32_t in[4], uint32_t out[4], int lane_table) {

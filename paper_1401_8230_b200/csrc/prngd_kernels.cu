@@ -589,6 +589,22 @@ __device__ __forceinline__ Xs128 jump_state(const uint4 *__restrict__ tab, const
     return Xs128{r0, r1, r2, r3};
 }
 
+// The same jump through nibble tables: J * s = XOR over the 32 nibbles of s of tab[p][nibble].
+__device__ __forceinline__ Xs128 jump_state_nib(const uint4 *__restrict__ tab, const Xs128 &s) {
+    const uint32_t words[4] = {s.x, s.y, s.z, s.w};
+    uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+    for (int p = 0; p < 32; ++p) {
+        const uint32_t v = (words[p >> 3] >> (4 * (p & 7))) & 0xFu;
+        const uint4 t = __ldg(&tab[p * 16 + v]);
+        r0 ^= t.x;
+        r1 ^= t.y;
+        r2 ^= t.z;
+        r3 ^= t.w;
+    }
+    return Xs128{r0, r1, r2, r3};
+}
+
 // staging: row = lane (32 doubles = 16 chunks of 16 B), chunk c stored at c ^ (row & 15)
 __device__ __forceinline__ uint32_t jstage_off(uint32_t row, uint32_t j) {
     return row * 256u + ((((j >> 1) ^ (row & 15u))) << 4) + (j & 1u) * 8u;
@@ -680,7 +696,20 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
 // earlier lanes reject, but the output positions are not: the fast path assumes no rejection
 // (and no x1 = a - 1, the only row the R11 clamp can touch) and a warp vote at the end sends
 // the whole warp to seg_exact(), which rewrites every output of its rows exactly.
-constexpr int kSegHalf = 64;  // outputs per lane per flush (one 512-byte chunk)
+#ifndef PRNGD_SEG_HALF
+#define PRNGD_SEG_HALF 64
+#endif
+constexpr int kSegHalf = PRNGD_SEG_HALF;  // outputs per lane per flush (one 512-byte chunk)
+
+// How a lane reaches its segment start T^(256 j) s (A/B):
+//   0 byte tables, direct J_j (16 loads), next task's loads prefetched across a batch
+//   1 nibble tables, direct J_j (32 loads, 8 KiB per j)
+//   2 nibble tables, J_j as the product of J_(2^k) over the set bits k of j (<= log2 S stages)
+//   3 byte tables, direct J_j, no prefetch
+#ifndef PRNGD_SEG_JUMP
+#define PRNGD_SEG_JUMP 2  // cfg3 A/B: 0 -> 577, 1 -> 544, 2 -> 645, 3 -> 575 Gd/s
+#endif
+
 
 template <int MODE, bool IEEE>
 __device__ __forceinline__ void seg_exact(const GenArgs &g, Xs128 st, uint32_t j, uint32_t S,
@@ -731,64 +760,147 @@ __device__ __forceinline__ void seg_exact(const GenArgs &g, Xs128 st, uint32_t j
     }
 }
 
+// Lane j's segment start T^(256 j) s from its stream start s (PRNGD_SEG_JUMP selects how).
+__device__ __forceinline__ Xs128 seg_jump(const uint4 *__restrict__ tabs,
+                                          const uint4 *__restrict__ my_tab, uint32_t j,
+                                          uint32_t log2S, Xs128 s) {
+#if defined(PRNGD_SEG_NOJUMP_EXPERIMENT)
+    (void)tabs, (void)my_tab, (void)log2S;
+    s.x ^= j;  // A/B timing experiment only: wrong bits
+    return s;
+#elif PRNGD_SEG_JUMP == 0 || PRNGD_SEG_JUMP == 3
+    (void)tabs, (void)log2S;
+    return j ? jump_state(my_tab, s) : s;
+#elif PRNGD_SEG_JUMP == 1
+    (void)tabs, (void)log2S;
+    return j ? jump_state_nib(my_tab, s) : s;
+#else
+    (void)my_tab;
+    for (uint32_t k = 0; k < log2S; ++k)
+        if ((j >> k) & 1u) s = jump_state_nib(tabs + (size_t)(1u << k) * 32 * 16, s);
+    return s;
+#endif
+}
+
+// One batch of kCols outputs of the fast path into tile row `my`, 16-byte chunk c of the batch
+// at chunk (b * kCols / 2 + c) ^ lane of the row (conflict-free writes and flush reads).
 template <int MODE, bool IEEE>
-__global__ void __launch_bounds__(32)
-    gen_seg_kernel(const GenArgs g, const uint4 *__restrict__ tabs, uint32_t log2S) {
-    extern __shared__ uint8_t smem_raw[];
+__device__ __forceinline__ void seg_batch(Xs128 &st, bool &rej, uint32_t my, uint32_t b,
+                                          uint32_t lane, const GenArgs &g) {
     constexpr bool FULL32 = MODE == 2;
     constexpr bool EQ4 = MODE >= 1;
     const uint32_t sh1 = FULL32 ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
     const uint32_t w = FULL32 ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo;
     const uint32_t span_fast = FULL32 ? 0xFFFFFFFDu : g.span_fast;
+    double q[kCols];
+#pragma unroll
+    for (int i = 0; i < kCols; ++i) {
+        const uint32_t x1 = draw(st) >> sh1;
+        const uint32_t x2 = draw(st) >> sh2;
+        rej |= !accepted(x1, lo, span_fast);
+        q[i] = EQ4 ? eq4_pair<IEEE, false>(x1, x2, w, g.Cs, g.Ds, g.y)
+                   : map_pair<IEEE, false>(x1, x2, g.map);
+    }
+#pragma unroll
+    for (int c = 0; c < kCols / 2; ++c)
+        sts_v2(my + (((b * (kCols / 2) + c) ^ lane) << 4), q[2 * c], q[2 * c + 1]);
+}
+
+// One-warp CTAs (12 per SM, smem-bound), each running `tpc` consecutive warp tasks of 32
+// lane segments (a task = 32 / S rows = one contiguous 32 KiB block of the output), so the
+// hardware's in-order CTA dispatch keeps the blocks being written in one moving window (a
+// persistent grid striding over tasks measured 752 vs 912 Gd/s on the same stores).  The jump
+// of a lane's NEXT task is issued before the current task's first batch and folded in after
+// it, so its 16 table loads (L2 latency) overlap generation; only the CTA's first jump is
+// exposed.  The 64 registers the loads occupy are free at this occupancy.
+template <int MODE, bool IEEE>
+__global__ void __launch_bounds__(32, 12)
+    gen_seg_kernel(const GenArgs g, const uint4 *__restrict__ tabs, uint32_t log2S,
+                   uint64_t n_tasks, uint32_t tpc) {
+    const uint64_t t_end0 = ((uint64_t)blockIdx.x + 1) * tpc;
+    const uint64_t t_end = t_end0 < n_tasks ? t_end0 : n_tasks;
+    extern __shared__ uint8_t smem_raw[];
+    constexpr uint32_t kBatchesPerFlush = kSegHalf / kCols;
+    constexpr uint32_t kBatches = kSegOut / kCols;
     const uint32_t lane = threadIdx.x;
     const uint32_t S = 1u << log2S;            // lanes (segments) per row
     const uint32_t j = lane & (S - 1u);        // this lane's segment
+    const uint32_t rloc = lane >> log2S;       // this lane's row within the task
     const uint32_t rows_per_warp = 32u >> log2S;
-    const uint64_t row0 = (uint64_t)blockIdx.x * rows_per_warp;
-    const uint64_t row = row0 + (lane >> log2S);
-    const bool live = row < g.n_streams;
+#if PRNGD_SEG_JUMP == 1 || PRNGD_SEG_JUMP == 2
+    const uint4 *my_tab = tabs + (size_t)j * 32 * 16;   // nibble tables, 8 KiB per lane matrix
+#else
+    const uint4 *my_tab = tabs + (size_t)j * 16 * 256;  // byte tables, 64 KiB per lane matrix
+#endif
     const uint32_t tile = aligned_smem_base(smem_raw);
-    const uint32_t my = tile + lane * (kSegHalf * 8u);  // this lane's 512-byte tile row
-    Xs128 st = stream_start(g.seed, g.stream_begin + row);
-    if (j) st = jump_state(tabs + (size_t)j * 16 * 256, st);
-    const Xs128 seg0 = st;
-    bool rej = false;
+    const uint32_t my = tile + lane * (kSegHalf * 8u);  // this lane's tile row
+    uint64_t t = (uint64_t)blockIdx.x * tpc;
+    Xs128 st = stream_start(g.seed, g.stream_begin + t * rows_per_warp + rloc);
+    st = seg_jump(tabs, my_tab, j, log2S, st);
 #pragma unroll 1
-    for (uint32_t h = 0; h < kSegOut / kSegHalf; ++h) {
-#pragma unroll 1
-        for (uint32_t b = 0; b < kSegHalf / kCols; ++b) {
-            double q[kCols];
+    for (; t < t_end; ++t) {
+        const uint64_t row0 = t * rows_per_warp;
+        const uint64_t row = row0 + rloc;
+        const bool live = row < g.n_streams;
+        // tile rows that belong to existing rows: all 32 except in a ragged last task
+        const uint64_t rows_left = g.n_streams - row0;
+        const uint32_t nchunks = rows_left >= rows_per_warp ? 32u : (uint32_t)rows_left << log2S;
+        const Xs128 seg0 = st;
+        // next task's start state: S1 now, its jump loads in flight during the first batch
+        const uint64_t tn = t + 1;
+        Xs128 nxt = stream_start(g.seed, g.stream_begin + tn * rows_per_warp + rloc);
+        const bool jump_next = j != 0 && tn < t_end;
+        uint4 pf[16];
+#if !defined(PRNGD_SEG_NOJUMP_EXPERIMENT) && PRNGD_SEG_JUMP == 0
+        if (jump_next) {
+            const uint32_t words[4] = {nxt.x, nxt.y, nxt.z, nxt.w};
 #pragma unroll
-            for (int i = 0; i < kCols; ++i) {
-                const uint32_t x1 = draw(st) >> sh1;
-                const uint32_t x2 = draw(st) >> sh2;
-                rej |= !accepted(x1, lo, span_fast);
-                q[i] = EQ4 ? eq4_pair<IEEE, false>(x1, x2, w, g.Cs, g.Ds, g.y)
-                           : map_pair<IEEE, false>(x1, x2, g.map);
-            }
-            // 16-byte chunk c of tile row r at chunk c ^ r: conflict-free writes and reads
-#pragma unroll
-            for (int c = 0; c < kCols / 2; ++c)
-                sts_v2(my + (((b * (kCols / 2) + c) ^ lane) << 4), q[2 * c], q[2 * c + 1]);
+            for (int k = 0; k < 16; ++k)
+                pf[k] = __ldg(&my_tab[k * 256 + ((words[k >> 2] >> (8 * (k & 3))) & 0xFFu)]);
         }
-        __syncwarp();
-        // flush: tile row r -> 512 contiguous bytes of row(r), segment j(r), half h
+#endif
+        bool rej = false;
+        seg_batch<MODE, IEEE>(st, rej, my, 0, lane, g);
+#if !defined(PRNGD_SEG_NOJUMP_EXPERIMENT) && PRNGD_SEG_JUMP == 0
+        if (jump_next) {
+            uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                r0 ^= pf[k].x;
+                r1 ^= pf[k].y;
+                r2 ^= pf[k].z;
+                r3 ^= pf[k].w;
+            }
+            nxt = Xs128{r0, r1, r2, r3};
+        }
+#else
+        if (tn < t_end) nxt = seg_jump(tabs, my_tab, j, log2S, nxt);
+#endif
+#pragma unroll 1
+        for (uint32_t k = 1; k <= kBatches; ++k) {
+            if (k % kBatchesPerFlush == 0) {
+                // flush: tile row r -> 512 contiguous bytes at (row0 + r / S) * nps +
+                // (r % S) * 128 + h * 64 = row0 * nps + r * 128 + h * 64 (nps = 128 S): the
+                // task is one contiguous 32 KiB block, lane segments 1 KiB apart.
+                const uint32_t h = k / kBatchesPerFlush - 1;
+                __syncwarp();
+                double *base = g.out + row0 * g.nps + h * kSegHalf + 2 * lane;
 #pragma unroll 4
-        for (uint32_t r = 0; r < 32u; ++r) {
-            const uint64_t rr = row0 + (r >> log2S);
-            if (rr < g.n_streams) {
-                double a, b2;
-                lds_v2(tile + r * (kSegHalf * 8u) + ((lane ^ r) << 4), a, b2);
-                stg_v2_cs(g.out + rr * g.nps + (r & (S - 1u)) * kSegOut + h * kSegHalf + 2 * lane,
-                          a, b2);
+                for (uint32_t r = 0; r < nchunks; ++r) {
+                    double a, b2;
+                    lds_v2(tile + r * (kSegHalf * 8u) + ((lane ^ r) << 4), a, b2);
+                    stg_v2_cs(base + r * kSegOut, a, b2);
+                }
+                __syncwarp();
             }
+            if (k < kBatches) seg_batch<MODE, IEEE>(st, rej, my, k % kBatchesPerFlush, lane, g);
         }
-        __syncwarp();
-    }
-    if (__builtin_expect(__any_sync(0xFFFFFFFFu, rej), 0)) {
-        __syncwarp();  // the speculative stores above are ordered before the exact rewrite
-        seg_exact<MODE, IEEE>(g, seg0, j, S, row, live);
+        if (__builtin_expect(__any_sync(0xFFFFFFFFu, rej), 0)) {
+            __syncwarp();  // the speculative stores above are ordered before the exact rewrite
+            seg_exact<MODE, IEEE>(g, seg0, j, S, row, live);
+        }
+        st = nxt;
     }
 }
 
@@ -1071,16 +1183,23 @@ cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *ta
     uint32_t log2S = 0;
     while ((1ull << log2S) < S) ++log2S;
     const uint64_t rows_per_warp = 32u >> log2S;
-    const uint64_t grid = (g.n_streams + rows_per_warp - 1) / rows_per_warp;
-    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    const uint64_t n_tasks = (g.n_streams + rows_per_warp - 1) / rows_per_warp;
     const size_t smem = 1024 + (size_t)32 * kSegHalf * 8;
+    cudaError_t e;
+#if PRNGD_SEG_JUMP == 1 || PRNGD_SEG_JUMP == 2
+    (void)tables;
+    if ((e = jump_tables_nibble(kSegDraws, &tables)) != cudaSuccess) return e;
+#endif
     const uint4 *t = static_cast<const uint4 *>(tables);
     const int mode = kernel_mode(g);
-    cudaError_t e;
+    // consecutive tasks per CTA (hides all but the first jump); one when the grid is small
+    const uint32_t tpc = n_tasks >= 148ull * 12 * 16 ? 4u : 1u;
+    const uint64_t grid = (n_tasks + tpc - 1) / tpc;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
 #define PRNGD_SEG_LAUNCH(M, I)                                                                  \
     do {                                                                                        \
         if ((e = set_smem(gen_seg_kernel<M, I>, smem)) != cudaSuccess) return e;                \
-        gen_seg_kernel<M, I><<<(unsigned)grid, 32, smem, st>>>(g, t, log2S);                   \
+        gen_seg_kernel<M, I><<<(unsigned)grid, 32, smem, st>>>(g, t, log2S, n_tasks, tpc);     \
     } while (0)
     if (pl.ieee_div) {
         if (mode >= 1) PRNGD_SEG_LAUNCH(1, true);

@@ -186,3 +186,23 @@ def test_mrg_flag_rules(lib):
     h = P.prngd_create(**p, seed=1, n_streams=1, n_per_stream=2, flags=P.PRNGD_FLAG_MRG32K3A)
     assert P.prngd_get_info(h)["speculative"] == 0
     P.prngd_destroy(h)
+
+
+@pytest.mark.parametrize("name,flags,kernel,store", [
+    ("cfg1", 0, 1, 6),                          # AUTO, few streams, rare rejection: SEG
+    ("cfg2", 0, 2, 4),                          # AUTO, few streams, w = 8: NEXT-3 jump kernel
+    ("cfg3", 0, 0, 4),                          # AUTO, bulk: ROW
+    ("cfg4", 0, 0, 4),
+    ("cfg3", P.PRNGD_FLAG_STORE_SEG, 1, 6),     # explicit SEG
+    ("cfg2", P.PRNGD_FLAG_STORE_SEG, 0, 4),     # SEG ineligible (w = 8 is not speculative): ROW
+    ("cfg1", P.PRNGD_FLAG_STORE_ROW, 0, 4),     # an explicit store path is honoured
+    ("cfg1", P.PRNGD_FLAG_JUMP, 2, 4),
+])
+def test_kernel_selection(lib, name, flags, kernel, store):
+    """prngd_get_info reports the kernel and store path prngd_generate launches (host logic)."""
+    h = P.prngd_create(**{k: v for k, v in W.config(name, flags=flags).items() if k != "mrg"})
+    try:
+        info = P.prngd_get_info(h)
+        assert (info["kernel"], info["store"]) == (kernel, store)
+    finally:
+        P.prngd_destroy(h)

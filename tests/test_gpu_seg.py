@@ -43,6 +43,7 @@ def full(w):
 
 
 def run(p):
+    p["flags"] = p.get("flags", 0) | P.PRNGD_FLAG_STORE_SEG  # else AUTO may pick the jump kernel
     g = P.Generator(**p)
     assert g.info["kernel"] == SEG_KERNEL, g.info
     out = g.generate()
@@ -124,7 +125,8 @@ def test_seg_clamp_row_w27(orc):
 
 def test_seg_guard_bands(orc):
     GUARD = 4096
-    p = dict(full(17), seed=8, stream_begin=0, n_streams=203, n_per_stream=256)
+    p = dict(full(17), seed=8, stream_begin=0, n_streams=203, n_per_stream=256,
+             flags=P.PRNGD_FLAG_STORE_SEG)
     g = P.Generator(**p)
     assert g.info["kernel"] == SEG_KERNEL
     n = 203 * 256

@@ -165,3 +165,50 @@ extern "C" __attribute__((visibility("default"))) int wc_segments(double *p, uin
         p, rows, cols, S, chunk_bytes / 8, salt);
     return (int)cudaGetLastError();
 }
+
+// Rotated rows: the ROW kernel's pattern (one lane per row, 512-byte chunks) but lane r runs
+// its rows with a column phase: over M rows per lane (rows base + 32 m + r), at flush step t
+// lane r writes chunk (t + d_r) mod C of its current row, d_r = (r * skew) mod C, so one flush
+// touches many column offsets (address bits below the row size) instead of one.
+template <uint32_t C, uint32_t M>
+__global__ void __launch_bounds__(32) rot_rows(double *p, uint64_t rows, uint64_t cols,
+                                               uint32_t skew, uint64_t salt) {
+    extern __shared__ uint8_t pad[];
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t base = (uint64_t)blockIdx.x * 32u * M;
+    if (base >= rows) return;
+    if (salt == ~0ull) pad[threadIdx.x] = 0;
+    for (uint32_t t = 0; t < M * C; ++t) {
+#pragma unroll 4
+        for (uint32_t r = 0; r < 32; ++r) {
+            const uint32_t d = (r * skew) & (C - 1);
+            const uint32_t v = (t + d) & (M * C - 1);  // position in lane r's row sequence
+            const uint64_t row = base + 32u * (v / C) + r;
+            const uint64_t e = row * cols + (uint64_t)(v & (C - 1)) * 64 + 2 * lane;
+            if (row < rows)
+                asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p + e), "d"(hval(e, salt)),
+                             "d"(hval(e + 1, salt))
+                             : "memory");
+        }
+    }
+}
+
+extern "C" __attribute__((visibility("default"))) int wc_rot(double *p, uint64_t n, uint32_t M,
+                                                             uint32_t skew, uint32_t smem_pad,
+                                                             uint64_t salt, void *stream,
+                                                             uint64_t cols) {
+    const uint64_t rows = n / cols;
+    const uint64_t per = 32ull * M;
+    const unsigned grid = (unsigned)((rows + per - 1) / per);
+    cudaStream_t st = (cudaStream_t)stream;
+#define ROT(CC, MM)                                                                             \
+    if (cols / 64 == CC && M == MM) {                                                           \
+        cudaFuncSetAttribute(rot_rows<CC, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                             200 * 1024);                                                       \
+        rot_rows<CC, MM><<<grid, 32, smem_pad, st>>>(p, rows, cols, skew, salt);                \
+        return (int)cudaGetLastError();                                                         \
+    }
+    ROT(16, 1) ROT(16, 4) ROT(32, 1) ROT(32, 4) ROT(64, 1) ROT(64, 4)
+#undef ROT
+    return -1;
+}
