@@ -31,8 +31,9 @@ from paper_1401_8230_b200 import workloads as W  # noqa: E402
 
 METRIC = "Gdoubles/s generated (1/2/4/8 B200) and % of HBM-write roofline"
 FALLBACK_HBM = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
-KERNELS = {0: "gen_kernel", 1: "gen_seg_kernel", 2: "gen_jump_kernel", 3: "gen_mrg_kernel"}
-STORES = {0: "TMA", 1: "TILE", 2: "STG8", 3: "DIRECT", 4: "ROW", 5: "ROW1K", 6: "SEG"}
+KERNELS = {0: "gen_kernel", 1: "gen_seg_kernel", 2: "gen_jump_kernel", 3: "gen_mrg_kernel",
+           4: "gen_segc_kernel"}
+STORES = {0: "TMA", 1: "TILE", 2: "STG8", 3: "DIRECT", 4: "ROW", 5: "ROW1K", 6: "SEG", 7: "SEGC"}
 
 
 def parse():
@@ -52,7 +53,7 @@ def parse():
     ap.add_argument("--streams", type=int, default=0,
                     help="override streams per GPU (experiments; the config names it)")
     ap.add_argument("--store", default="auto",
-                    choices=["auto", "seg", "row", "row1k", "tma", "tile", "direct"],
+                    choices=["auto", "seg", "segc", "row", "row1k", "tma", "tile", "direct"],
                     help="store path A/B (include/prngd.h PRNGD_FLAG_STORE_*)")
     return ap.parse_args()
 

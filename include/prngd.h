@@ -61,6 +61,10 @@ typedef enum {
  *          its stream by GF(2) jump-ahead and owns that 1 KiB segment; each flush writes 512-byte
  *          chunks of every segment.  Needs rare rejection (prngd_info.speculative), pair-drop
  *          consumption and n_per_stream = 128 * 2^m <= 4096; otherwise ROW is used
+ *   SEGC   column blocks: a CTA of 8 warps owns 32 rows and warp j writes column block j
+ *          (n_per_stream / 8 outputs) of each, its lanes starting at pair j * n_per_stream / 8
+ *          by jump-ahead (shared-memory nibble tables); needs rare rejection, pair-drop and
+ *          n_per_stream % 512 == 0, otherwise ROW is used
  *   ROW    each warp stages 32 rows x 64 outputs in shared memory and writes every row
  *          as one 512-byte burst (32 lanes x 16-byte st.global) -- DRAM-friendly row bursts
  *   TMA    32 x 16-output warp tiles, one cp.async.bulk.tensor.2d store per 128-row CTA slab
@@ -74,6 +78,7 @@ typedef enum {
 #define PRNGD_FLAG_STORE_AUTO    (0u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_ROW     (5u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_SEG     (6u << PRNGD_STORE_SHIFT)
+#define PRNGD_FLAG_STORE_SEGC    (7u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_TMA     (1u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_TILE    (2u << PRNGD_STORE_SHIFT)
 #define PRNGD_FLAG_STORE_DIRECT  (3u << PRNGD_STORE_SHIFT)
@@ -128,9 +133,10 @@ typedef struct {
     uint64_t out_bytes;     /* 8 * n_outputs                                                 */
     uint32_t kernel;        /* kernel prngd_generate launches for a 256-byte aligned output:
                                0 gen_kernel (one lane per stream), 1 gen_seg_kernel (SEG),
-                               2 gen_jump_kernel (NEXT-3), 3 gen_mrg_kernel (NEXT-2)         */
+                               2 gen_jump_kernel (NEXT-3), 3 gen_mrg_kernel (NEXT-2),
+                               4 gen_segc_kernel (SEGC)                                        */
     uint32_t store;         /* its store path: 0 TMA, 1 TILE, 2 8-byte, 3 DIRECT, 4 ROW,
-                               5 ROW1K, 6 SEG                                                 */
+                               5 ROW1K, 6 SEG, 7 SEGC                                         */
 } prngd_info;
 
 /* Validate *p and build an immutable handle (host only: no CUDA call, no device memory).

@@ -129,7 +129,7 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     if (map_code > 2) return fail(PRNGD_EUNSUPPORTED, "unknown mapping code %u", map_code);
     if (map_code == 2 && !(p->a0 == 0 && p->b0 == 0 && p->a == (1ull << w) - 1 && p->b == p->a))
         return fail(PRNGD_EINVAL, "Eq.(6) needs the unit-interval range a0=b0=0, a=b=2^w-1");
-    if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 6)
+    if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 7)
         return fail(PRNGD_EUNSUPPORTED, "unknown store path %u",
                     (p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT);
 
@@ -243,6 +243,7 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         case PRNGD_FLAG_STORE_ROW1K: pl.store = Store::ROW1K; break;
         case PRNGD_FLAG_STORE_ROW: pl.store = Store::ROW; break;
         case PRNGD_FLAG_STORE_SEG: pl.store = Store::SEG; break;
+        case PRNGD_FLAG_STORE_SEGC: pl.store = Store::SEGC; break;
         default: pl.store = Store::ROW; break;  // AUTO: ROW; plan_for may pick SEG (below)
     }
     pl.store_auto = store_auto;
@@ -276,7 +277,8 @@ prngd_status prngd_get_info(const prngd_handle *h, prngd_info *info) {
     *info = h->info;
     const Plan pl = plan_for(h, reinterpret_cast<const void *>(uintptr_t{256}));
     info->store = (uint32_t)pl.store;
-    info->kernel = pl.mrg ? 3u : pl.jump ? 2u : pl.store == Store::SEG ? 1u : 0u;
+    info->kernel = pl.mrg ? 3u : pl.jump ? 2u : pl.store == Store::SEG ? 1u
+                                                : pl.store == Store::SEGC ? 4u : 0u;
     return PRNGD_OK;
 }
 
@@ -288,7 +290,8 @@ static Plan plan_for(const prngd_handle *h, const void *out, bool consume) {
     Plan pl = h->plan;
     // Fused consumer + outputs: the smem histogram leaves no room for row tiles at full
     // occupancy, so the default there is the register (DIRECT) store (measured best).
-    if (consume && (pl.store == Store::SEG || pl.store_auto)) pl.store = Store::DIRECT;
+    if (consume && (pl.store == Store::SEG || pl.store == Store::SEGC || pl.store_auto))
+        pl.store = Store::DIRECT;
     const uintptr_t a = (uintptr_t)out;
     const uint64_t nps = h->p.n_per_stream;
     const bool a32 = (a & 31u) == 0 && (nps & 3u) == 0;
@@ -302,6 +305,9 @@ static Plan plan_for(const prngd_handle *h, const void *out, bool consume) {
     const bool seg_ok = !pl.mrg && pl.spec && !pl.alg1 && a16 && nps % prngd::kSegOut == 0 &&
                         S >= 1 && S <= 32 && (S & (S - 1)) == 0;
     if (pl.store == Store::SEG && !seg_ok) pl.store = Store::ROW;
+    // SEGC: the same conditions with 8 column blocks of a multiple of 64 outputs each
+    const bool segc_ok = !pl.mrg && pl.spec && !pl.alg1 && a16 && nps % 512 == 0;
+    if (pl.store == Store::SEGC && !segc_ok) pl.store = Store::ROW;
     if (!consume && pl.store_auto && pl.jump && !(h->p.flags & PRNGD_FLAG_JUMP) && seg_ok) {
         pl.jump = false;
         pl.store = Store::SEG;
@@ -316,6 +322,7 @@ static Plan plan_for(const prngd_handle *h, const void *out, bool consume) {
 
 // Row-parallel generate kernels (one lane per stream, or per 1 KiB stream segment for SEG).
 static cudaError_t launch_rows(const GenArgs &g, const Plan &pl, cudaStream_t st, int sms) {
+    if (pl.store == Store::SEGC) return prngd::launch_generate_segc(g, pl, st);
     if (pl.store == Store::SEG) {
         const void *tables = nullptr;
         cudaError_t e = prngd::jump_tables(prngd::kSegDraws, &tables);

@@ -43,7 +43,10 @@ struct GenArgs {
 //   STG16:  32 x 16 smem tile + warp-coalesced 16-byte st.global;  STG8: 8-byte stores
 //   ROW1K:  as ROW with 128 outputs (1 KiB bursts) per row
 //   SEG:    nps/128 lanes per row (jump-ahead), each lane a 1 KiB segment; 512 B bursts
-enum class Store : int { TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3, ROW = 4, ROW1K = 5, SEG = 6 };
+//   SEGC:   a CTA of 8 warps owns 32 rows, warp j column block j (jump-ahead); 512 B bursts
+enum class Store : int {
+    TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3, ROW = 4, ROW1K = 5, SEG = 6, SEGC = 7
+};
 
 // Launch descriptors chosen by the host.
 struct Plan {
@@ -68,6 +71,8 @@ constexpr uint64_t kSegDraws = 2 * kSegOut;
 cudaError_t jump_tables(uint64_t lane_draws, const void **out);
 // the same matrices as nibble tables [32][32][16] x uint4 (8 KiB per lane matrix)
 cudaError_t jump_tables_nibble(uint64_t lane_draws, const void **out);
+// the byte tables with the lane index innermost, [16][256][32] x uint4
+cudaError_t jump_tables_interleaved(uint64_t lane_draws, const void **out);
 void jump_host(uint64_t n_draws, const uint32_t in[4], uint32_t out[4], int lane_table);
 
 // Launchers (prngd_kernels.cu).  They return cudaGetLastError() of the launch.
@@ -82,6 +87,7 @@ cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *t
                                  cudaStream_t st);
 cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *tables,
                                 cudaStream_t st);
+cudaError_t launch_generate_segc(const GenArgs &g, const Plan &pl, cudaStream_t st);
 cudaError_t launch_debug_raw(const GenArgs &g, uint32_t *d_raw, uint64_t draws, cudaStream_t st);
 cudaError_t launch_debug_pairs(const GenArgs &g, const Plan &pl, uint32_t *d_pidx,
                                uint64_t *d_consumed, cudaStream_t st);

@@ -706,8 +706,10 @@ constexpr int kSegHalf = PRNGD_SEG_HALF;  // outputs per lane per flush (one 512
 //   1 nibble tables, direct J_j (32 loads, 8 KiB per j)
 //   2 nibble tables, J_j as the product of J_(2^k) over the set bits k of j (<= log2 S stages)
 //   3 byte tables, direct J_j, no prefetch
+//   4 byte tables with the lane index innermost ([b][v][l]): the S lanes of a row jump the same
+//     state, so each load is one contiguous run per row; prefetched like 0
 #ifndef PRNGD_SEG_JUMP
-#define PRNGD_SEG_JUMP 2  // cfg3 A/B: 0 -> 577, 1 -> 544, 2 -> 645, 3 -> 575 Gd/s
+#define PRNGD_SEG_JUMP 4  // cfg3 A/B: 0 -> 577, 1 -> 544, 2 -> 645, 3 -> 575 Gd/s
 #endif
 
 
@@ -771,6 +773,21 @@ __device__ __forceinline__ Xs128 seg_jump(const uint4 *__restrict__ tabs,
 #elif PRNGD_SEG_JUMP == 0 || PRNGD_SEG_JUMP == 3
     (void)tabs, (void)log2S;
     return j ? jump_state(my_tab, s) : s;
+#elif PRNGD_SEG_JUMP == 4
+    (void)my_tab, (void)log2S;
+    if (!j) return s;
+    const uint32_t words[4] = {s.x, s.y, s.z, s.w};
+    uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint32_t v = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+        const uint4 t = __ldg(&tabs[((uint32_t)k * 256u + v) * 32u + j]);
+        r0 ^= t.x;
+        r1 ^= t.y;
+        r2 ^= t.z;
+        r3 ^= t.w;
+    }
+    return Xs128{r0, r1, r2, r3};
 #elif PRNGD_SEG_JUMP == 1
     (void)tabs, (void)log2S;
     return j ? jump_state_nib(my_tab, s) : s;
@@ -852,17 +869,20 @@ __global__ void __launch_bounds__(32, 12)
         Xs128 nxt = stream_start(g.seed, g.stream_begin + tn * rows_per_warp + rloc);
         const bool jump_next = j != 0 && tn < t_end;
         uint4 pf[16];
-#if !defined(PRNGD_SEG_NOJUMP_EXPERIMENT) && PRNGD_SEG_JUMP == 0
+#if !defined(PRNGD_SEG_NOJUMP_EXPERIMENT) && (PRNGD_SEG_JUMP == 0 || PRNGD_SEG_JUMP == 4)
         if (jump_next) {
             const uint32_t words[4] = {nxt.x, nxt.y, nxt.z, nxt.w};
 #pragma unroll
-            for (int k = 0; k < 16; ++k)
-                pf[k] = __ldg(&my_tab[k * 256 + ((words[k >> 2] >> (8 * (k & 3))) & 0xFFu)]);
+            for (int k = 0; k < 16; ++k) {
+                const uint32_t v = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+                pf[k] = PRNGD_SEG_JUMP == 4 ? __ldg(&tabs[((uint32_t)k * 256u + v) * 32u + j])
+                                            : __ldg(&my_tab[k * 256 + v]);
+            }
         }
 #endif
         bool rej = false;
         seg_batch<MODE, IEEE>(st, rej, my, 0, lane, g);
-#if !defined(PRNGD_SEG_NOJUMP_EXPERIMENT) && PRNGD_SEG_JUMP == 0
+#if !defined(PRNGD_SEG_NOJUMP_EXPERIMENT) && (PRNGD_SEG_JUMP == 0 || PRNGD_SEG_JUMP == 4)
         if (jump_next) {
             uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
 #pragma unroll
@@ -901,6 +921,151 @@ __global__ void __launch_bounds__(32, 12)
             seg_exact<MODE, IEEE>(g, seg0, j, S, row, live);
         }
         st = nxt;
+    }
+}
+
+// ------------------------------------------------------------------------------ SEGC store path
+// Column blocks: a CTA of kSegcWarps = 8 warps owns a task of 32 consecutive rows (one 256 KiB
+// block of the output for cfg3); lane r of every warp generates row row0 + r, and warp j owns
+// column block j (L = nps / 8 outputs) of all 32 rows.  Lane (j, r) starts at pair j * L of its
+// stream through J_j = T^(2 L j), applied with nibble tables held in shared memory (56 KiB,
+// loaded once per persistent CTA); because j is warp-uniform every lane of a warp reads the same
+// table.  Each warp flushes 512-byte row chunks exactly like the ROW kernel, but the CTA
+// completes its 32-row block in L / 64 flushes instead of nps / 64 (tools/rot_sweep.py
+// blockcol: 7.1 vs 6.7 TB/s for cfg3's rows, 6.6 vs 6.0 TB/s for cfg4's).
+// Rejection (and x1 = a - 1, the R11 clamp row) is speculated away; the warps flag their rows
+// in a per-task mask and, after the task's barrier, flagged rows are rewritten exactly: every
+// warp recounts its block's accepted pairs, a prefix over the 8 blocks (shared memory) places
+// each accepted output, and warp 7 continues the stream past pair nps for the missing tail.
+constexpr int kSegcWarps = 8;
+constexpr int kSegcTabBytes = (kSegcWarps - 1) * 32 * 16 * 16;  // J_1..J_7 nibble tables, 56 KiB
+
+__device__ __forceinline__ Xs128 jump_state_nib_smem(uint32_t tab, const Xs128 &s) {
+    const uint32_t words[4] = {s.x, s.y, s.z, s.w};
+    uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+    for (int p = 0; p < 32; ++p) {
+        const uint32_t v = (words[p >> 3] >> (4 * (p & 7))) & 0xFu;
+        uint32_t a, b, c, d;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                     : "r"(tab + (uint32_t)(p * 16 + v) * 16u));
+        r0 ^= a;
+        r1 ^= b;
+        r2 ^= c;
+        r3 ^= d;
+    }
+    return Xs128{r0, r1, r2, r3};
+}
+
+template <int MODE, bool IEEE>
+__device__ __noinline__ void segc_exact(const GenArgs &g, Xs128 st, uint32_t j, uint32_t lane,
+                                        uint64_t row, bool fix, uint32_t L, uint32_t *cnt) {
+    constexpr bool FULL32 = MODE == 2;
+    constexpr bool EQ4 = MODE >= 1;
+    const uint32_t sh1 = FULL32 ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
+    const uint32_t w = FULL32 ? 32u : g.w;
+    const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
+    const Xs128 seg0 = st;
+    if (fix) {  // pass 1: accepted pairs among this block's L pairs
+        uint32_t c = 0;
+        for (uint32_t i = 0; i < L; ++i) {
+            const uint32_t x1 = draw(st) >> sh1;
+            draw(st);
+            c += accepted(x1, lo, span) ? 1u : 0u;
+        }
+        cnt[j * 32 + lane] = c;
+    }
+    __syncthreads();
+    if (fix) {
+        uint32_t pos = 0, total = 0;
+        for (uint32_t i = 0; i < (uint32_t)kSegcWarps; ++i) {
+            const uint32_t c = cnt[i * 32 + lane];
+            pos += i < j ? c : 0u;
+            total += c;
+        }
+        // pass 2: every accepted pair at its sequential position (R11 clamp included)
+        st = seg0;
+        double *row_out = g.out + row * g.nps;
+        for (uint32_t i = 0; i < L; ++i) {
+            const uint32_t x1 = draw(st) >> sh1;
+            const uint32_t x2 = draw(st) >> sh2;
+            if (accepted(x1, lo, span)) {
+                row_out[pos++] = EQ4 ? eq4_pair<IEEE, true>(x1, x2, w, g.Cs, g.Ds, g.y)
+                                     : map_pair<IEEE, true>(x1, x2, g.map);
+            }
+        }
+        if (j == kSegcWarps - 1)  // the row's last block continues past pair nps
+            for (uint64_t p = total; p < g.nps; ++p)
+                row_out[p] = exact_output<EQ4, IEEE, false>(st, sh1, sh2, w, lo, span, g);
+    }
+    __syncthreads();  // cnt is reused by the next rewrite
+}
+
+template <int MODE, bool IEEE>
+__global__ void __launch_bounds__(kSegcWarps * 32, 1)
+    gen_segc_kernel(const GenArgs g, const uint4 *__restrict__ tabs, uint64_t n_tasks) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint32_t cnt[kSegcWarps * 32];
+    __shared__ uint32_t mask[3];
+    const uint32_t lane = threadIdx.x & 31u, j = threadIdx.x >> 5;
+    const uint32_t L = (uint32_t)(g.nps / kSegcWarps);  // outputs (pairs) per column block
+    const uint32_t base = aligned_smem_base(smem_raw);
+    const uint32_t tab_s = base;                                   // J_1..J_7, 8 KiB each
+    const uint32_t tile = base + kSegcTabBytes + j * (kSegHalf * 32u * 8u);
+    const uint32_t my = tile + lane * (kSegHalf * 8u);
+    {   // nibble tables of J_1..J_7 (lane matrices 1..7 of the global table) into smem
+        const uint4 *src = tabs + 32 * 16;
+        for (uint32_t i = threadIdx.x; i < (uint32_t)(kSegcTabBytes / 16); i += blockDim.x) {
+            const uint4 v = src[i];
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(tab_s + i * 16u), "r"(v.x),
+                         "r"(v.y), "r"(v.z), "r"(v.w)
+                         : "memory");
+        }
+        if (threadIdx.x < 3) mask[threadIdx.x] = 0u;
+    }
+    __syncthreads();
+    const uint32_t my_tab = tab_s + (j ? (j - 1u) : 0u) * (32u * 16u * 16u);
+    uint32_t it = 0;
+#pragma unroll 1
+    for (uint64_t t = blockIdx.x; t < n_tasks; t += gridDim.x, ++it) {
+        const uint64_t row0 = t * 32u;
+        const uint64_t row = row0 + lane;
+        const bool live = row < g.n_streams;
+        const uint64_t rows_left = g.n_streams - row0;
+        const uint32_t nrows = rows_left < 32u ? (uint32_t)rows_left : 32u;
+        Xs128 st = stream_start(g.seed, g.stream_begin + row);
+#ifndef PRNGD_SEG_NOJUMP_EXPERIMENT
+        if (j) st = jump_state_nib_smem(my_tab, st);
+#else
+        st.x ^= j;  // A/B timing experiment only: wrong bits
+#endif
+        const Xs128 seg0 = st;
+        bool rej = false;
+        double *blk = g.out + row0 * g.nps + (uint64_t)j * L + 2 * lane;
+#pragma unroll 1
+        for (uint32_t c0 = 0; c0 < L; c0 += kSegHalf) {
+#pragma unroll 1
+            for (uint32_t b = 0; b < (uint32_t)(kSegHalf / kCols); ++b)
+                seg_batch<MODE, IEEE>(st, rej, my, b, lane, g);
+            __syncwarp();
+            // one 512-byte chunk of row r per instruction (32 lanes x 16 B)
+            double *dst = blk + c0;
+#pragma unroll 4
+            for (uint32_t r = 0; r < nrows; ++r) {
+                double a, b2;
+                lds_v2(tile + r * (kSegHalf * 8u) + ((lane ^ r) << 4), a, b2);
+                stg_v2_cs(dst + (uint64_t)r * g.nps, a, b2);
+            }
+            __syncwarp();
+        }
+        const uint32_t flagged = __ballot_sync(0xFFFFFFFFu, rej && live);
+        if (lane == 0 && flagged) atomicOr(&mask[it % 3], flagged);
+        __syncthreads();  // also orders the speculative stores before any rewrite
+        const uint32_t m = mask[it % 3];
+        if (threadIdx.x == 0) mask[(it + 2) % 3] = 0u;  // read by everyone before barrier it
+        if (__builtin_expect(m != 0u, 0))
+            segc_exact<MODE, IEEE>(g, seg0, j, lane, row, live && ((m >> lane) & 1u), L, cnt);
     }
 }
 
@@ -1189,11 +1354,17 @@ cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *ta
 #if PRNGD_SEG_JUMP == 1 || PRNGD_SEG_JUMP == 2
     (void)tables;
     if ((e = jump_tables_nibble(kSegDraws, &tables)) != cudaSuccess) return e;
+#elif PRNGD_SEG_JUMP == 4
+    (void)tables;
+    if ((e = jump_tables_interleaved(kSegDraws, &tables)) != cudaSuccess) return e;
 #endif
     const uint4 *t = static_cast<const uint4 *>(tables);
     const int mode = kernel_mode(g);
     // consecutive tasks per CTA (hides all but the first jump); one when the grid is small
-    const uint32_t tpc = n_tasks >= 148ull * 12 * 16 ? 4u : 1u;
+#ifndef PRNGD_SEG_TPC
+#define PRNGD_SEG_TPC 4
+#endif
+    const uint32_t tpc = n_tasks >= 148ull * 12 * 16 ? PRNGD_SEG_TPC : 1u;
     const uint64_t grid = (n_tasks + tpc - 1) / tpc;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
 #define PRNGD_SEG_LAUNCH(M, I)                                                                  \
@@ -1212,6 +1383,39 @@ cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *ta
         PRNGD_SEG_LAUNCH(0, false);
     }
 #undef PRNGD_SEG_LAUNCH
+    return cudaGetLastError();
+}
+
+cudaError_t launch_generate_segc(const GenArgs &g, const Plan &pl, cudaStream_t st) {
+    // host checked: nps % (8 * 64) == 0, 16-byte aligned output, speculative, pair-drop
+    const uint64_t L = g.nps / kSegcWarps;
+    const void *tables = nullptr;
+    cudaError_t e = jump_tables_nibble(2 * L, &tables);
+    if (e != cudaSuccess) return e;
+    const uint4 *t = static_cast<const uint4 *>(tables);
+    const uint64_t n_tasks = (g.n_streams + 31) / 32;
+    const size_t smem = 1024 + (size_t)kSegcTabBytes + (size_t)kSegcWarps * 32 * kSegHalf * 8;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t grid = n_tasks < (uint64_t)sms ? n_tasks : (uint64_t)sms;  // one CTA per SM
+    const int mode = kernel_mode(g);
+#define PRNGD_SEGC_LAUNCH(M, I)                                                                 \
+    do {                                                                                        \
+        if ((e = set_smem(gen_segc_kernel<M, I>, smem)) != cudaSuccess) return e;               \
+        gen_segc_kernel<M, I><<<(unsigned)grid, kSegcWarps * 32, smem, st>>>(g, t, n_tasks);   \
+    } while (0)
+    if (pl.ieee_div) {
+        if (mode >= 1) PRNGD_SEGC_LAUNCH(1, true);
+        else PRNGD_SEGC_LAUNCH(0, true);
+    } else if (mode == 2) {
+        PRNGD_SEGC_LAUNCH(2, false);
+    } else if (mode == 1) {
+        PRNGD_SEGC_LAUNCH(1, false);
+    } else {
+        PRNGD_SEGC_LAUNCH(0, false);
+    }
+#undef PRNGD_SEGC_LAUNCH
     return cudaGetLastError();
 }
 

@@ -19,6 +19,7 @@ PRNGD_FLAG_ALG1 = 0x4
 PRNGD_FLAG_STORE_AUTO = 0 << 3
 PRNGD_FLAG_STORE_ROW = 5 << 3
 PRNGD_FLAG_STORE_SEG = 6 << 3
+PRNGD_FLAG_STORE_SEGC = 7 << 3
 PRNGD_FLAG_STORE_TMA = 1 << 3
 PRNGD_FLAG_STORE_TILE = 2 << 3
 PRNGD_FLAG_STORE_DIRECT = 3 << 3
@@ -32,6 +33,7 @@ PRNGD_FLAG_MRG32K3A = 0x800
 PRNGD_FLAG_NO_JUMP = 0x400
 MAP_FLAGS = {4: PRNGD_FLAG_MAP_EQ4, 5: PRNGD_FLAG_MAP_EQ5, 6: PRNGD_FLAG_MAP_EQ6}
 STORE_FLAGS = {"auto": PRNGD_FLAG_STORE_AUTO, "seg": PRNGD_FLAG_STORE_SEG,
+               "segc": PRNGD_FLAG_STORE_SEGC,
                "row": PRNGD_FLAG_STORE_ROW, "tma": PRNGD_FLAG_STORE_TMA,
                "tile": PRNGD_FLAG_STORE_TILE, "direct": PRNGD_FLAG_STORE_DIRECT,
                "row1k": PRNGD_FLAG_STORE_ROW1K}

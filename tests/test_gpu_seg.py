@@ -1,6 +1,10 @@
-"""GPU parity of the SEG store path (gen_seg_kernel): n_per_stream / 128 lanes share a row, lane
-j starts at pair 128 j of its stream by GF(2) jump-ahead, and a warp vote sends any warp that
-met a rejected x1 (or x1 = a - 1, the R11 clamp row) to the exact rewrite (seg_exact).
+"""GPU parity of the jump-ahead store paths:
+
+* SEG (gen_seg_kernel): n_per_stream / 128 lanes share a row, lane j starts at pair 128 j of its
+  stream by GF(2) jump-ahead, and a warp vote sends any warp that met a rejected x1 (or
+  x1 = a - 1, the R11 clamp row) to the exact rewrite (seg_exact);
+* SEGC (gen_segc_kernel): a CTA of 8 warps owns 32 rows, warp j column block j (pairs
+  j * nps / 8 ...), flagged rows rewritten exactly after the task barrier (segc_exact).
 
 The rejection cases use widths where rejection is rare enough for the speculative path
 (prngd_info.speculative) yet frequent at test sizes: w = 17 (p_rej = 2^-16 per pair) and
@@ -18,6 +22,7 @@ from paper_1401_8230_b200 import workloads as W  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 SEG_KERNEL = 1
+SEGC_KERNEL = 4
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -42,29 +47,41 @@ def full(w):
     return dict(w=w, a0=0, a=2**w - 1, b0=0, b=2**w - 1)
 
 
-def run(p):
-    p["flags"] = p.get("flags", 0) | P.PRNGD_FLAG_STORE_SEG  # else AUTO may pick the jump kernel
+def run(p, path="seg"):
+    flag = P.PRNGD_FLAG_STORE_SEG if path == "seg" else P.PRNGD_FLAG_STORE_SEGC
+    p["flags"] = p.get("flags", 0) | flag  # else AUTO may pick another kernel
     g = P.Generator(**p)
-    assert g.info["kernel"] == SEG_KERNEL, g.info
+    assert g.info["kernel"] == (SEG_KERNEL if path == "seg" else SEGC_KERNEL), g.info
     out = g.generate()
     torch.cuda.synchronize()
     return g, out
 
 
-@pytest.mark.parametrize("nps", [128, 256, 512, 1024, 2048, 4096])
+def eligible(path, nps):
+    return (nps % 128 == 0 and nps // 128 in (1, 2, 4, 8, 16, 32)) if path == "seg" \
+        else nps % 512 == 0
+
+
+@pytest.mark.parametrize("path", ["seg", "segc"])
+@pytest.mark.parametrize("nps", [128, 256, 512, 1024, 1536, 2048, 4096, 8192])
 @pytest.mark.parametrize("ns", [1, 37, 1000])
-def test_seg_full32_shapes(orc, nps, ns):
+def test_seg_full32_shapes(orc, nps, ns, path):
+    if not eligible(path, nps):
+        pytest.skip("shape not eligible for this path")
     p = dict(W.FULL32, seed=W.SEED, stream_begin=4242, n_streams=ns, n_per_stream=nps)
-    _, out = run(p)
+    _, out = run(p, path)
     assert_same(out, orc.generate(p)["out"])
 
 
+@pytest.mark.parametrize("path", ["seg", "segc"])
 @pytest.mark.parametrize("w", [17, 20])
 @pytest.mark.parametrize("nps", [128, 1024, 4096])
-def test_seg_rejections_exact_rewrite(orc, w, nps):
+def test_seg_rejections_exact_rewrite(orc, w, nps, path):
+    if not eligible(path, nps):
+        pytest.skip("shape not eligible for this path")
     ns = (1 << 22) // nps + 3      # ~4 M pairs: w = 17 -> ~128 rejections, w = 20 -> ~16
     p = dict(full(w), seed=W.SEED2, stream_begin=99, n_streams=ns, n_per_stream=nps)
-    g, out = run(p)
+    g, out = run(p, path)
     assert g.info["speculative"] == 1
     ref = orc.generate(p, want_consumed=True)
     extra = ref["consumed"].astype(np.int64) - nps
@@ -72,50 +89,55 @@ def test_seg_rejections_exact_rewrite(orc, w, nps):
     assert_same(out, ref["out"])
 
 
-def test_seg_rejection_in_last_segment(orc):
-    """Find rows (w = 17, nps = 512) whose rejections fall in the last segment (the tail draws
-    past pair n_per_stream come from the row's last lane) and check them bitwise."""
+@pytest.mark.parametrize("path", ["seg", "segc"])
+def test_seg_rejection_in_last_segment(orc, path):
+    """Find rows (w = 17, nps = 512) whose rejections fall in the last segment / block (the
+    tail draws past pair n_per_stream come from the row's last lane) and check them bitwise."""
     nps, ns = 512, 8192
     p = dict(full(17), seed=5, stream_begin=0, n_streams=ns, n_per_stream=nps)
-    g, out = run(p)
+    g, out = run(p, path)
     ref = orc.generate(p, want_pidx=True, want_consumed=True)
     pidx = ref["pidx"].reshape(ns, nps).astype(np.int64)
-    # a rejection at pair >= 384 (segment 3 of 4): output 383's pair index is 383
-    late = np.nonzero((pidx[:, 383] == 383) & (ref["consumed"] > nps))[0]
+    last = 384 if path == "seg" else 448   # first pair of the last segment (SEG) / block (SEGC)
+    late = np.nonzero((pidx[:, last - 1] == last - 1) & (ref["consumed"] > nps))[0]
     assert late.size > 0
     assert_same(out, ref["out"])
 
 
 @pytest.mark.parametrize("par", [W.ASYM, dict(w=32, a0=2**12, a=2**32 - 1, b0=0, b=2**32 - 1),
                                  dict(w=24, a0=0, a=2**24 - 1, b0=0, b=2**16 - 1)])
-def test_seg_general_ranges(orc, par):
+@pytest.mark.parametrize("path", ["seg", "segc"])
+def test_seg_general_ranges(orc, par, path):
     p = dict(par, seed=3, stream_begin=1 << 33, n_streams=3000, n_per_stream=2048)
-    _, out = run(p)
+    _, out = run(p, path)
     assert_same(out, orc.generate(p)["out"])
 
 
 @pytest.mark.parametrize("kind,open_", [(5, False), (6, False), (4, True), (6, True)])
-def test_seg_mappings(orc, kind, open_):
+@pytest.mark.parametrize("path", ["seg", "segc"])
+def test_seg_mappings(orc, kind, open_, path):
     flags = P.MAP_FLAGS[kind] | (P.PRNGD_FLAG_OPEN if open_ else 0)
     p = dict(full(20), seed=11, stream_begin=0, n_streams=2000, n_per_stream=1024, flags=flags)
-    _, out = run(p)
+    _, out = run(p, path)
     assert_same(out, orc.generate(p, kind=kind, open_interval=open_)["out"])
 
 
-def test_seg_ieee_division(orc):
+@pytest.mark.parametrize("path", ["seg", "segc"])
+def test_seg_ieee_division(orc, path):
     p = dict(full(20), seed=12, stream_begin=0, n_streams=2000, n_per_stream=1024,
              flags=P.PRNGD_FLAG_IEEE_DIV)
-    _, out = run(p)
+    _, out = run(p, path)
     assert_same(out, orc.generate(p)["out"])
 
 
-def test_seg_clamp_row_w27(orc):
+@pytest.mark.parametrize("path", ["seg", "segc"])
+def test_seg_clamp_row_w27(orc, path):
     """w = 27: x1 = a - 1 (the only row the R11 clamp can reach, routed to the exact rewrite)
     appears with probability 2^-27 per pair, rejection 2^-26.  Over these 2^28 pairs seed 2 has
     five x1 = a - 1 outputs (asserted through the oracle's own map).  Compared bitwise in full."""
     w = 27
     p = dict(full(w), seed=2, stream_begin=0, n_streams=1 << 18, n_per_stream=1024)
-    g, out = run(p)
+    g, out = run(p, path)
     assert g.info["clamp"] == 1
     ref = orc.generate(p)["out"]
     thr = orc.map_pairs(p, np.array([2**w - 2], dtype=np.uint32), np.array([0], dtype=np.uint32))
@@ -123,15 +145,16 @@ def test_seg_clamp_row_w27(orc):
     assert_same(out, ref)
 
 
-def test_seg_guard_bands(orc):
+@pytest.mark.parametrize("path,nps", [("seg", 256), ("segc", 512)])
+def test_seg_guard_bands(orc, path, nps):
     GUARD = 4096
-    p = dict(full(17), seed=8, stream_begin=0, n_streams=203, n_per_stream=256,
-             flags=P.PRNGD_FLAG_STORE_SEG)
+    flag = P.PRNGD_FLAG_STORE_SEG if path == "seg" else P.PRNGD_FLAG_STORE_SEGC
+    p = dict(full(17), seed=8, stream_begin=0, n_streams=203, n_per_stream=nps, flags=flag)
     g = P.Generator(**p)
-    assert g.info["kernel"] == SEG_KERNEL
-    n = 203 * 256
+    assert g.info["kernel"] == (SEG_KERNEL if path == "seg" else SEGC_KERNEL)
+    n = 203 * nps
     buf = torch.full((n + 2 * GUARD,), -3.25, dtype=torch.float64, device="cuda")
-    g.generate(buf[GUARD:GUARD + n].view(203, 256))
+    g.generate(buf[GUARD:GUARD + n].view(203, nps))
     torch.cuda.synchronize()
     assert bool((buf[:GUARD] == -3.25).all()) and bool((buf[GUARD + n:] == -3.25).all())
     assert_same(buf[GUARD:GUARD + n], orc.generate(p)["out"])
@@ -149,9 +172,10 @@ def test_seg_ineligible_shapes_fall_back(orc, nps, kernel):
     assert_same(out[rows], ref)
 
 
-def test_seg_generate_host_matches_device(orc):
+@pytest.mark.parametrize("path", ["seg", "segc"])
+def test_seg_generate_host_matches_device(orc, path):
     p = dict(full(17), seed=4, stream_begin=0, n_streams=70000, n_per_stream=1024)
-    g, out = run(p)
+    g, out = run(p, path)
     host = torch.empty(g.shape, dtype=torch.float64, pin_memory=True)
     P.prngd_generate_host(g.handle, host, torch.cuda.current_stream())
     assert_same(host, out)

@@ -13,6 +13,8 @@ from paper_1401_8230_b200 import build as B  # noqa: E402
 L = ctypes.CDLL(B.build_tools())
 L.wc_rot.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
                      ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint64]
+L.wc_blockcol.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                          ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32]
 L.wc_segments.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
                           ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint64]
 n = 1 << 30
@@ -37,7 +39,11 @@ for cols in [int(c) for c in sys.argv[1:]] or [1024]:
     pad = 16 * 1024
     res[f"c{cols}_seg_S1"] = timeit(lambda k: L.wc_segments(out.data_ptr(), n, 1, 512, pad, k, st.cuda_stream, cols))
     res[f"c{cols}_seg_1KiB"] = timeit(lambda k: L.wc_segments(out.data_ptr(), n, cols // 128, 512, pad, k, st.cuda_stream, cols))
-    for M in (1, 4):
+    for S, chunk, padk in ((8, 512, 150), (8, 512, 185), (8, 256, 88), (8, 256, 120), (8, 256, 60),
+                           (16, 256, 150), (16, 512, 210), (4, 512, 72)):
+        res[f"c{cols}_blockcol_S{S}_chunk{chunk}_pad{padk}k"] = timeit(
+            lambda k: L.wc_blockcol(out.data_ptr(), n, S, padk * 1024, k, st.cuda_stream, cols, chunk))
+    for M in ():
         for skew in (0, 1, 2, 3, 5, 7):
             res[f"c{cols}_rot_M{M}_skew{skew}"] = timeit(
                 lambda k: L.wc_rot(out.data_ptr(), n, M, skew, pad, k, st.cuda_stream, cols))

@@ -212,3 +212,39 @@ extern "C" __attribute__((visibility("default"))) int wc_rot(double *p, uint64_t
 #undef ROT
     return -1;
 }
+
+// Block columns: a CTA of S warps owns 32 rows; warp w writes column block w (cols / S doubles)
+// of every row, 512 bytes per row per flush (one row per instruction, like the ROW kernel), so
+// a warp's flush is strided by the row length but the CTA completes its 32-row block within
+// cols / S / 64 flushes.
+__global__ void blockcol_rows(double *p, uint64_t rows, uint64_t cols, uint32_t chunk,
+                              uint64_t salt) {
+    extern __shared__ uint8_t pad[];
+    const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5, S = blockDim.x >> 5;
+    const uint64_t row0 = (uint64_t)blockIdx.x * 32u;
+    if (row0 >= rows) return;
+    if (salt == ~0ull) pad[threadIdx.x] = 0;
+    const uint64_t seg = cols / S;
+    const uint32_t lpr = chunk / 16;  // lanes per row per instruction
+    for (uint64_t c0 = 0; c0 < seg; c0 += chunk / 8) {
+        for (uint32_t r = 0; r < 32; r += 32 / lpr) {
+            const uint64_t row = row0 + r + lane / lpr;
+            const uint64_t e = row * cols + w * seg + c0 + 2 * (lane % lpr);
+            if (row < rows)
+                asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p + e), "d"(hval(e, salt)),
+                             "d"(hval(e + 1, salt))
+                             : "memory");
+        }
+    }
+}
+
+extern "C" __attribute__((visibility("default"))) int wc_blockcol(double *p, uint64_t n,
+                                                                  uint32_t S, uint32_t smem_pad,
+                                                                  uint64_t salt, void *stream,
+                                                                  uint64_t cols, uint32_t chunk) {
+    const uint64_t rows = n / cols;
+    cudaFuncSetAttribute(blockcol_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    blockcol_rows<<<(unsigned)((rows + 31) / 32), 32 * S, smem_pad, (cudaStream_t)stream>>>(
+        p, rows, cols, chunk, salt);
+    return (int)cudaGetLastError();
+}
