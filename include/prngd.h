@@ -104,6 +104,13 @@ typedef enum {
  * outputs #3s..#3s+2.  prngd_generate only (pair-drop, ROW store: 16-byte aligned output and
  * even n_per_stream); EUNSUPPORTED elsewhere. */
 #define PRNGD_FLAG_MRG32K3A      0x800u
+/* prngd_generate_consume counts into per-SM 16-bit packed shared-memory counters.  By default the
+ * adds are optimistic (no return value, no carry tracking): each CTA checks afterwards that its
+ * counters sum to the outputs it counted, and on a mismatch (a counter wrapped) an exact pass
+ * with carry tracking recomputes the histogram in the same call (3 launches per call: consume,
+ * exact pass -- which returns at once when nothing wrapped -- and finalize).  This flag uses the
+ * carry-tracking adds from the start (2 launches). */
+#define PRNGD_FLAG_EXACT_HIST    0x1000u
 #define PRNGD_FLAG_JUMP          0x200u
 #define PRNGD_FLAG_NO_JUMP       0x400u
 #define PRNGD_FLAG_ALG1       0x4u  /* NEXT-2 reading of Alg. 1: a rejected x1 is

@@ -116,7 +116,7 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         return fail(PRNGD_EINVAL, "stream_begin + n_streams overflows 64 bits");
     const uint32_t known = PRNGD_FLAG_IEEE_DIV | PRNGD_FLAG_ALG1 | PRNGD_STORE_MASK |
                            PRNGD_MAP_MASK | PRNGD_FLAG_OPEN | PRNGD_FLAG_JUMP | PRNGD_FLAG_NO_JUMP |
-                           PRNGD_FLAG_MRG32K3A;
+                           PRNGD_FLAG_MRG32K3A | PRNGD_FLAG_EXACT_HIST;
     const bool mrg = (p->flags & PRNGD_FLAG_MRG32K3A) != 0;
     if (mrg && (bit_length(p->a) > 31 || bit_length(p->b) > 31))
         return fail(PRNGD_EINVAL, "MRG32k3a draws are at most 31 bits wide (bitlen(a), bitlen(b) <= 31)");
@@ -247,6 +247,7 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         default: pl.store = Store::ROW; break;  // AUTO: ROW; plan_for may pick SEG (below)
     }
     pl.store_auto = store_auto;
+    pl.exact_hist = (p->flags & PRNGD_FLAG_EXACT_HIST) != 0;
     *out = h;
     return PRNGD_OK;
 }
@@ -288,10 +289,10 @@ uint32_t prngd_last_launches(const prngd_handle *h) { return h ? h->last_launche
 // the next one that is legal (same bits whichever path writes them).
 static Plan plan_for(const prngd_handle *h, const void *out, bool consume) {
     Plan pl = h->plan;
-    // Fused consumer + outputs: the smem histogram leaves no room for row tiles at full
-    // occupancy, so the default there is the register (DIRECT) store (measured best).
+    // Fused consumer + outputs: 12 warps with 8 KiB row tiles (256-byte row bursts) next to the
+    // 128 KiB histogram (cfg5: 539 Gd/s vs 473 for the register DIRECT store).
     if (consume && (pl.store == Store::SEG || pl.store == Store::SEGC || pl.store_auto))
-        pl.store = Store::DIRECT;
+        pl.store = Store::ROW;
     const uintptr_t a = (uintptr_t)out;
     const uint64_t nps = h->p.n_per_stream;
     const bool a32 = (a & 31u) == 0 && (nps & 3u) == 0;

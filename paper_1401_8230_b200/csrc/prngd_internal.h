@@ -34,6 +34,7 @@ struct GenArgs {
     uint32_t *hist_slab;    // [gridDim.x][32768] packed u16 pairs (consume kernels only)
     int64_t *hist_spill;    // [65536] int64 carries of the packed counters
     double *pow_slab;       // [gridDim.x][4]
+    uint32_t *overflow;     // set by an optimistic (RED) consume kernel whose 16-bit fields wrapped
 };
 
 // How a warp's outputs reach HBM (include/prngd.h PRNGD_FLAG_STORE_*):
@@ -57,6 +58,7 @@ struct Plan {
     bool jump;      // NEXT-3 intra-stream kernel (one warp per stream)
     bool mrg;       // NEXT-2 MRG32k3a base generator
     bool store_auto;  // PRNGD_FLAG_STORE_AUTO: the library picks the store path / kernel
+    bool exact_hist;  // PRNGD_FLAG_EXACT_HIST: carry-tracking histogram adds from the start
     Store store;
 };
 

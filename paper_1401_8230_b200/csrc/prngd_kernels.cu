@@ -53,8 +53,12 @@ constexpr size_t gen_smem() {
 constexpr int kConsWarpsTiles = 12;         // warps per CTA, consume kernel staging tiles in smem
 constexpr int kConsWarpsRegs = 24;          // warps per CTA, consume kernel without tiles (<= 85 regs)
 
-constexpr int kConsWarpsRow = 12;           // consume + ROW store: 12 x 8 KiB tiles + histogram
-constexpr int kConsRowCols = 32;            // consume + ROW store: 256-byte row bursts
+#ifndef PRNGD_CONS_ROW_WARPS
+#define PRNGD_CONS_ROW_WARPS 12
+#define PRNGD_CONS_ROW_COLS 32
+#endif
+constexpr int kConsWarpsRow = PRNGD_CONS_ROW_WARPS;  // consume + ROW store: 12 x 8 KiB tiles
+constexpr int kConsRowCols = PRNGD_CONS_ROW_COLS;    // + histogram; 256-byte row bursts
 template <Store ST, bool WRITE>
 constexpr int cons_warps() {
     return (WRITE && ST == Store::ROW) ? kConsWarpsRow
@@ -110,7 +114,8 @@ __device__ __forceinline__ uint32_t tile_off(uint32_t row, uint32_t chunk) {
 }
 
 // ------------------------------------------------------------------------------ consumer (S7)
-struct Consumer {
+template <bool RED>
+struct ConsumerT {
     double s1, s2, s3, s4;
     uint32_t *hist;   // shared: 32768 words, counter of bin b in half (b & 1) of word b >> 1
     int64_t *spill;   // global: carries of the packed counters, [65536]
@@ -134,8 +139,15 @@ struct Consumer {
         const uint32_t bin = bin16(q);
         const uint32_t sh = (bin & 1u) << 4;
         const uint32_t inc = 1u << sh;
-        const uint32_t nw = atomicAdd(&hist[bin >> 1], inc) + inc;
-        if (__builtin_expect(((nw >> sh) & 0xFFFFu) == 0u, 0)) carry(bin, nw);
+        if (RED) {
+            // optimistic: no return value, no carry check; a wrapped field is detected after
+            // the kernel (field sum != outputs counted) and the exact pass redoes the histogram
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(&hist[bin >> 1])), "r"(inc)
+                         : "memory");
+        } else {
+            const uint32_t nw = atomicAdd(&hist[bin >> 1], inc) + inc;
+            if (__builtin_expect(((nw >> sh) & 0xFFFFu) == 0u, 0)) carry(bin, nw);
+        }
     }
     __device__ __noinline__ void carry(uint32_t bin, uint32_t nw) {
         unsigned long long *sp = reinterpret_cast<unsigned long long *>(spill);
@@ -146,6 +158,8 @@ struct Consumer {
         }
     }
 };
+
+using Consumer = ConsumerT<false>;
 
 struct NoConsumer {
     __device__ __forceinline__ void init(uint32_t *, int64_t *) {}
@@ -369,7 +383,27 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
             }
         }
         __syncwarp();
-        if constexpr (CPR >= 32) {
+        if (nrows == 32u && col0 + RC <= g.nps) {
+            // full tile: unconditional stores, pointer stepped by rows (the common case)
+            constexpr uint32_t RPI = CPR >= 32 ? 1u : 32u / CPR;   // rows per instruction
+            constexpr uint32_t LPR = CPR >= 32 ? 32u : CPR;        // lanes per row
+            const uint32_t c = lane % LPR, rsub = lane / LPR;
+#pragma unroll
+            for (uint32_t h = 0; h < (CPR >= 32 ? CPR / 32 : 1u); ++h) {
+                const uint32_t ch = h * 32u + c;  // this lane's 16-byte chunk of the row segment
+                double *dst = g.out + (row0 + rsub) * g.nps + col0 + 2 * ch;
+                const uint64_t step = (uint64_t)RPI * g.nps;
+                uint32_t a = tile + rsub * (RC * 8u);
+#pragma unroll 8
+                for (uint32_t r = rsub; r < 32u; r += RPI) {
+                    double v0, v1;
+                    lds_v2(a + ((ch ^ (r & (CPR - 1))) << 4), v0, v1);
+                    stg_v2_cs(dst, v0, v1);
+                    dst += step;
+                    a += RPI * (RC * 8u);
+                }
+            }
+        } else if constexpr (CPR >= 32) {
             // one row per instruction: 32 lanes x 16 B = 512 B of the same row
 #pragma unroll
             for (uint32_t h = 0; h < CPR / 32; ++h) {
@@ -461,9 +495,15 @@ __global__ void __launch_bounds__(gen_warps<ST>() * 32)
 
 // S1-S7, persistent: one CTA per SM owning a 128 KiB packed histogram; warps take 32-stream
 // tasks round-robin.  Writes per-CTA slabs that finalize_kernel reduces.
-template <int MODE, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE>
+// RED: optimistic no-return shared-memory adds; the CTA then checks that its 16-bit fields sum
+// to the number of outputs it counted (any wrapped field makes the sum short) and raises
+// g.overflow.  EXACT_GUARD: the exact (carry-tracking) kernel of the fallback pass, which
+// returns at once unless that flag is set and then rewrites every slab.
+template <int MODE, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE, bool RED = false,
+          bool EXACT_GUARD = false>
 __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     consume_kernel(const __grid_constant__ CUtensorMap tmap, const GenArgs g) {
+    if (EXACT_GUARD && *(volatile const uint32_t *)g.overflow == 0u) return;
     constexpr int kWarps = cons_warps<ST, WRITE>();
     constexpr int NB = ring<ST, WRITE>();
     extern __shared__ uint8_t smem_raw[];
@@ -474,7 +514,7 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     const uint32_t tiles = base + kHistWords * 4u + warp * (NB * kTileBytes);
     for (uint32_t i = threadIdx.x; i < kHistWords; i += blockDim.x) hist[i] = 0u;
     __syncthreads();
-    Consumer cons;
+    ConsumerT<RED> cons;
     cons.init(hist, g.hist_spill);
     uint32_t it = 0;
     const uint64_t n_tasks = (g.n_streams + 31u) / 32u;
@@ -509,14 +549,47 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     }
     uint4 *dst = reinterpret_cast<uint4 *>(g.hist_slab + (size_t)blockIdx.x * kHistWords);
     const uint4 *src = reinterpret_cast<const uint4 *>(hist);
-    for (uint32_t i = threadIdx.x; i < kHistWords / 4; i += blockDim.x) dst[i] = src[i];
+    unsigned long long fsum = 0;  // sum of this thread's 16-bit fields (RED check)
+    for (uint32_t i = threadIdx.x; i < kHistWords / 4; i += blockDim.x) {
+        const uint4 v = src[i];
+        dst[i] = v;
+        if (RED)
+            fsum += (v.x & 0xFFFFu) + (v.x >> 16) + (v.y & 0xFFFFu) + (v.y >> 16) +
+                    (v.z & 0xFFFFu) + (v.z >> 16) + (v.w & 0xFFFFu) + (v.w >> 16);
+    }
+    if (RED) {
+        // outputs this CTA counted: live rows of its tasks x nps
+        unsigned long long expect = 0;
+        if (lane == 0)
+            for (uint64_t t = (uint64_t)blockIdx.x * kWarps + warp; t < n_tasks;
+                 t += (uint64_t)gridDim.x * kWarps) {
+                const uint64_t left = g.n_streams - t * 32u;
+                expect += (left < 32u ? left : 32u) * g.nps;
+            }
+        for (int o = 16; o > 0; o >>= 1) fsum += __shfl_xor_sync(~0u, fsum, o);
+        __shared__ unsigned long long part[2][kWarps];
+        if (lane == 0) {
+            part[0][warp] = fsum;
+            part[1][warp] = expect;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long a = 0, b = 0;
+            for (int wi = 0; wi < kWarps; ++wi) {
+                a += part[0][wi];
+                b += part[1][wi];
+            }
+            if (a != b) atomicOr(g.overflow, 1u);
+        }
+    }
 }
 
 // Reduce the per-CTA slabs into the caller's accumulators; resets the spill array to zero.
 __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int n_slabs,
                                                        int64_t *spill, const double *pow_slab,
                                                        int64_t *d_hist, double *d_pow,
-                                                       int64_t *d_count) {
+                                                       int64_t *d_count, uint32_t *overflow) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *overflow = 0u;  // read by the exact pass before
     __shared__ long long part[8];
     long long local = 0;
     for (uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x; wi < kHistWords;
@@ -1231,14 +1304,15 @@ cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, i
 }
 
 size_t consume_scratch_bytes(int num_sms) {
-    return (size_t)num_sms * kHistWords * 4u + 65536u * 8u + (size_t)num_sms * 4u * 8u;
+    return (size_t)num_sms * kHistWords * 4u + 65536u * 8u + (size_t)num_sms * 4u * 8u + 16u;
 }
 
-template <int MODE, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE>
+template <int MODE, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE, bool RED = false,
+          bool EXACT_GUARD = false>
 static cudaError_t cons_launch(const CUtensorMap &m, const GenArgs &g, int grid,
                                cudaStream_t st) {
     constexpr int kWarps = cons_warps<ST, WRITE>();
-    auto k = consume_kernel<MODE, SPEC, IEEE, ALG1, ST, WRITE>;
+    auto k = consume_kernel<MODE, SPEC, IEEE, ALG1, ST, WRITE, RED, EXACT_GUARD>;
     const size_t smem = 1024 + (size_t)kHistWords * 4u +
                         (WRITE && ST == Store::ROW ? (size_t)kWarps * 32 * kConsRowCols * 8
                                                    : (size_t)kWarps * ring<ST, WRITE>() * kTileBytes);
@@ -1248,21 +1322,21 @@ static cudaError_t cons_launch(const CUtensorMap &m, const GenArgs &g, int grid,
     return cudaGetLastError();
 }
 
-template <Store ST, bool WRITE>
+template <Store ST, bool WRITE, bool RED = false, bool EG = false>
 static cudaError_t cons_dispatch(const CUtensorMap &m, const GenArgs &g, const Plan &pl,
                                  int mode, int grid, cudaStream_t st) {
     if (pl.spec && !pl.ieee_div && !pl.alg1) {
-        if (mode == 2) return cons_launch<2, true, false, false, ST, WRITE>(m, g, grid, st);
-        if (mode == 1) return cons_launch<1, true, false, false, ST, WRITE>(m, g, grid, st);
+        if (mode == 2) return cons_launch<2, true, false, false, ST, WRITE, RED, EG>(m, g, grid, st);
+        if (mode == 1) return cons_launch<1, true, false, false, ST, WRITE, RED, EG>(m, g, grid, st);
     }
     if (pl.alg1)
-        return pl.ieee_div ? cons_launch<0, false, true, true, ST, WRITE>(m, g, grid, st)
-                           : cons_launch<0, false, false, true, ST, WRITE>(m, g, grid, st);
+        return pl.ieee_div ? cons_launch<0, false, true, true, ST, WRITE, RED, EG>(m, g, grid, st)
+                           : cons_launch<0, false, false, true, ST, WRITE, RED, EG>(m, g, grid, st);
     if (pl.spec)
-        return pl.ieee_div ? cons_launch<0, true, true, false, ST, WRITE>(m, g, grid, st)
-                           : cons_launch<0, true, false, false, ST, WRITE>(m, g, grid, st);
-    return pl.ieee_div ? cons_launch<0, false, true, false, ST, WRITE>(m, g, grid, st)
-                       : cons_launch<0, false, false, false, ST, WRITE>(m, g, grid, st);
+        return pl.ieee_div ? cons_launch<0, true, true, false, ST, WRITE, RED, EG>(m, g, grid, st)
+                           : cons_launch<0, true, false, false, ST, WRITE, RED, EG>(m, g, grid, st);
+    return pl.ieee_div ? cons_launch<0, false, true, false, ST, WRITE, RED, EG>(m, g, grid, st)
+                       : cons_launch<0, false, false, false, ST, WRITE, RED, EG>(m, g, grid, st);
 }
 
 cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d_out,
@@ -1277,6 +1351,8 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
     g.hist_slab = reinterpret_cast<uint32_t *>(sp);
     g.hist_spill = reinterpret_cast<int64_t *>(sp + (size_t)num_sms * kHistWords * 4u);
     g.pow_slab = reinterpret_cast<double *>(sp + (size_t)num_sms * kHistWords * 4u + 65536u * 8u);
+    g.overflow = reinterpret_cast<uint32_t *>(sp + (size_t)num_sms * kHistWords * 4u +
+                                              65536u * 8u + (size_t)num_sms * 4u * 8u);
     const uint64_t tasks = (g.n_streams + 31u) / 32u;
     const int kw = kConsWarpsRow;  // grid sizing: the smallest CTA bounds the task count
     int grid = num_sms;
@@ -1286,27 +1362,41 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
     std::memset(&m, 0, sizeof(m));
     const int f32 = kernel_mode(g);
     cudaError_t e;
+    // Histogram adds are optimistic (RED, no carry tracking) unless the caller asked for the
+    // exact carry path; an overflow found by the RED kernel triggers the exact pass (launched
+    // always, returning at once when the flag is clear), which redoes every slab.
+    const bool red = !pl.exact_hist;
     if (!d_out) {
-        e = cons_dispatch<Store::STG8, false>(m, g, pl, f32, grid, st);
+        e = red ? cons_dispatch<Store::STG8, false, true>(m, g, pl, f32, grid, st)
+                : cons_dispatch<Store::STG8, false>(m, g, pl, f32, grid, st);
     } else {
         Store s = pl.store;
         if (s == Store::TMA && make_tmap(&m, d_out, g.n_streams, g.nps, 32u) != cudaSuccess)
             s = Store::STG16;
+#define PRNGD_CONS_W(S)                                                                         \
+    (red ? cons_dispatch<S, true, true>(m, g, pl, f32, grid, st)                                 \
+         : cons_dispatch<S, true>(m, g, pl, f32, grid, st))
         switch (s) {
             case Store::ROW:
-            case Store::ROW1K: e = cons_dispatch<Store::ROW, true>(m, g, pl, f32, grid, st); break;
-            case Store::DIRECT: e = cons_dispatch<Store::DIRECT, true>(m, g, pl, f32, grid, st); break;
-            case Store::TMA: e = cons_dispatch<Store::TMA, true>(m, g, pl, f32, grid, st); break;
-            case Store::STG16: e = cons_dispatch<Store::STG16, true>(m, g, pl, f32, grid, st); break;
-            default: e = cons_dispatch<Store::STG8, true>(m, g, pl, f32, grid, st); break;
+            case Store::ROW1K: e = PRNGD_CONS_W(Store::ROW); break;
+            case Store::DIRECT: e = PRNGD_CONS_W(Store::DIRECT); break;
+            case Store::TMA: e = PRNGD_CONS_W(Store::TMA); break;
+            case Store::STG16: e = PRNGD_CONS_W(Store::STG16); break;
+            default: e = PRNGD_CONS_W(Store::STG8); break;
         }
+#undef PRNGD_CONS_W
     }
     if (e != cudaSuccess) return e;
     *launches = 1;
+    if (red) {  // exact fallback pass: consume-only (the outputs are already written)
+        e = cons_dispatch<Store::STG8, false, false, true>(m, g, pl, f32, grid, st);
+        if (e != cudaSuccess) return e;
+        *launches = 2;
+    }
     finalize_kernel<<<32, 256, 0, st>>>(g.hist_slab, grid, g.hist_spill, g.pow_slab, d_hist,
-                                         d_pow, d_count);
+                                         d_pow, d_count, g.overflow);
     e = cudaGetLastError();
-    if (e == cudaSuccess) *launches = 2;
+    if (e == cudaSuccess) *launches += 1;
     return e;
 }
 

@@ -30,6 +30,7 @@ PRNGD_FLAG_MAP_EQ6 = 2 << 6
 PRNGD_FLAG_OPEN = 0x100
 PRNGD_FLAG_JUMP = 0x200
 PRNGD_FLAG_MRG32K3A = 0x800
+PRNGD_FLAG_EXACT_HIST = 0x1000
 PRNGD_FLAG_NO_JUMP = 0x400
 MAP_FLAGS = {4: PRNGD_FLAG_MAP_EQ4, 5: PRNGD_FLAG_MAP_EQ5, 6: PRNGD_FLAG_MAP_EQ6}
 STORE_FLAGS = {"auto": PRNGD_FLAG_STORE_AUTO, "seg": PRNGD_FLAG_STORE_SEG,

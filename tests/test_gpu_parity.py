@@ -246,7 +246,7 @@ def test_consume_matches_oracle(orc, name, write, flags):
     out = torch.empty(g.shape, dtype=torch.float64, device="cuda") if write else None
     _, hist, pw, cnt = g.generate_consume(out)
     torch.cuda.synchronize()
-    assert g.last_launches == 2
+    assert g.last_launches == 3  # optimistic consume, exact pass (idle here), finalize
     r = orc.generate(p, want_out=write, want_stats=True)
     assert np.array_equal(hist.cpu().numpy(), r["hist"])
     assert cnt.item() == r["count"] == p["n_streams"] * p["n_per_stream"]
@@ -268,11 +268,15 @@ def test_consume_accumulates_across_shards(orc):
     assert np.allclose(pw.cpu().numpy(), ref["pow"], rtol=1e-12, atol=0)
 
 
-def test_consume_packed_counter_carries():
+@pytest.mark.parametrize("exact", [False, True])
+def test_consume_packed_counter_carries(exact):
     """w=1, [0;2] x [0;1]: every output is 1/3 or 2/3, so two bins (one low, one high field of a
     packed word) receive ~2^27 counts -- thousands of 16-bit carries per CTA.  The histogram must
-    equal the counts of the written outputs (torch bincount, independent of the consumer)."""
-    p = dict(w=1, a0=0, a=2, b0=0, b=1, seed=5, n_streams=4096, n_per_stream=65536)
+    equal the counts of the written outputs (torch bincount, independent of the consumer).
+    Default flags: the optimistic adds wrap, the CTA check raises the overflow flag and the exact
+    pass recomputes the histogram; EXACT_HIST: carry tracking from the start."""
+    p = dict(w=1, a0=0, a=2, b0=0, b=1, seed=5, n_streams=4096, n_per_stream=65536,
+             flags=P.PRNGD_FLAG_EXACT_HIST if exact else 0)
     g = P.Generator(**p)
     out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
     _, hist, pw, cnt = g.generate_consume(out)
@@ -284,6 +288,24 @@ def test_consume_packed_counter_carries():
     nz = torch.nonzero(ref).view(-1).tolist()
     assert nz == [21845, 43690]
     assert ref.max().item() > 2 * 148 * 65536  # carries certainly happened
+    assert g.last_launches == (2 if exact else 3)
+    # a second call on the same handle: the overflow flag was reset by the first call's finalize
+    _, hist2, _, _ = g.generate_consume(out)
+    torch.cuda.synchronize()
+    assert torch.equal(hist2, ref)
+
+
+def test_consume_exact_hist_flag_matches_oracle(orc):
+    p = W.config("cfg2", flags=P.PRNGD_FLAG_EXACT_HIST)
+    g = P.Generator(**p)
+    out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+    _, hist, pw, cnt = g.generate_consume(out)
+    torch.cuda.synchronize()
+    assert g.last_launches == 2
+    r = orc.generate(p, want_stats=True)
+    assert np.array_equal(hist.cpu().numpy(), r["hist"]) and cnt.item() == r["count"]
+    assert np.allclose(pw.cpu().numpy(), r["pow"], rtol=1e-12, atol=0)
+    assert_same(out, r["out"])
 
 
 def test_cfg4_histogram_full_size_consistent():
