@@ -53,12 +53,15 @@ constexpr size_t gen_smem() {
 constexpr int kConsWarpsTiles = 12;         // warps per CTA, consume kernel staging tiles in smem
 constexpr int kConsWarpsRegs = 24;          // warps per CTA, consume kernel without tiles (<= 85 regs)
 
+// consume + ROW store: 16 warps x 4 KiB tiles (128-byte row bursts) + the 128 KiB histogram.
+// A/B on cfg5 (write + histogram + moments): 6 x 16 KiB -> 415, 8 x 8 KiB -> 526,
+// 12 x 8 KiB -> 544, 16 x 4 KiB -> 561-566, 20 x 4 KiB -> 538, 24 x 4 KiB -> 525 Gd/s.
 #ifndef PRNGD_CONS_ROW_WARPS
-#define PRNGD_CONS_ROW_WARPS 12
-#define PRNGD_CONS_ROW_COLS 32
+#define PRNGD_CONS_ROW_WARPS 16
+#define PRNGD_CONS_ROW_COLS 16
 #endif
-constexpr int kConsWarpsRow = PRNGD_CONS_ROW_WARPS;  // consume + ROW store: 12 x 8 KiB tiles
-constexpr int kConsRowCols = PRNGD_CONS_ROW_COLS;    // + histogram; 256-byte row bursts
+constexpr int kConsWarpsRow = PRNGD_CONS_ROW_WARPS;
+constexpr int kConsRowCols = PRNGD_CONS_ROW_COLS;
 template <Store ST, bool WRITE>
 constexpr int cons_warps() {
     return (WRITE && ST == Store::ROW) ? kConsWarpsRow
