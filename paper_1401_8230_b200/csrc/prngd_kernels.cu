@@ -36,8 +36,10 @@ constexpr int ring() {
                : (ST == Store::TMA ? kNBufTma : 1);
 }
 constexpr int kGenWarps = 4;                // warps per CTA, generate kernel (tile paths)
-constexpr int kRowCols = 64;                // ROW path: outputs per row per burst (512 B)
-constexpr int kRowTileBytes = 32 * kRowCols * 8;  // 16 KiB per warp
+#ifndef PRNGD_ROW_COLS
+#define PRNGD_ROW_COLS 64
+#endif
+constexpr int kRowCols = PRNGD_ROW_COLS;    // ROW path: outputs per row per burst (512 B)
 
 template <Store ST>
 constexpr bool is_row() { return ST == Store::ROW || ST == Store::ROW1K; }
@@ -47,7 +49,7 @@ template <Store ST>
 constexpr int gen_warps() { return is_row<ST>() ? 1 : kGenWarps; }
 template <Store ST>
 constexpr size_t gen_smem() {
-    return is_row<ST>() ? 1024 + (size_t)32 * row_cols<ST>() * 8
+    return is_row<ST>() ? 1024 + (size_t)32 * (row_cols<ST>() * 8 + 16)
                         : 1024 + (size_t)kGenWarps * (ST == Store::TMA ? 2 : 1) * kTileBytes;
 }
 constexpr int kConsWarpsTiles = 12;         // warps per CTA, consume kernel staging tiles in smem
@@ -361,7 +363,11 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
     constexpr uint32_t CPR = RC / 2;  // 16-byte chunks per row segment
     const bool live = (row0 + lane) < g.n_streams;
     const uint32_t nrows = (g.n_streams - row0) < 32u ? (uint32_t)(g.n_streams - row0) : 32u;
-    const uint32_t my_row = tile + lane * (RC * 8u);
+    // tile row stride RC * 8 + 16 bytes: the 16-byte pad staggers the rows over the banks, so
+    // both the per-lane row writes and the per-row flush reads are conflict-free with plain
+    // (immediate-offset) addresses
+    constexpr uint32_t RS = RC * 8u + 16u;
+    const uint32_t my_row = tile + lane * RS;
 #pragma unroll 1
     for (uint64_t col0 = 0; col0 < g.nps; col0 += RC) {
 #pragma unroll 1
@@ -382,7 +388,7 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
 #pragma unroll
             for (int c = 0; c < kCols / 2; ++c) {
                 const uint32_t chunk = b * (kCols / 2) + c;  // logical 16-byte chunk of the row
-                sts_v2(my_row + ((chunk ^ (lane & (CPR - 1))) << 4), q[2 * c], q[2 * c + 1]);
+                sts_v2(my_row + (chunk << 4), q[2 * c], q[2 * c + 1]);
             }
         }
         __syncwarp();
@@ -396,14 +402,14 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
                 const uint32_t ch = h * 32u + c;  // this lane's 16-byte chunk of the row segment
                 double *dst = g.out + (row0 + rsub) * g.nps + col0 + 2 * ch;
                 const uint64_t step = (uint64_t)RPI * g.nps;
-                uint32_t a = tile + rsub * (RC * 8u);
+                uint32_t a = tile + rsub * RS + (ch << 4);
 #pragma unroll 8
                 for (uint32_t r = rsub; r < 32u; r += RPI) {
                     double v0, v1;
-                    lds_v2(a + ((ch ^ (r & (CPR - 1))) << 4), v0, v1);
+                    lds_v2(a, v0, v1);
                     stg_v2_cs(dst, v0, v1);
                     dst += step;
-                    a += RPI * (RC * 8u);
+                    a += RPI * RS;
                 }
             }
         } else if constexpr (CPR >= 32) {
@@ -416,7 +422,7 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
 #pragma unroll 4
                     for (uint32_t r = 0; r < nrows; ++r) {
                         double a, b2;
-                        lds_v2(tile + r * (RC * 8u) + (((h * 32u + lane) ^ r) << 4), a, b2);
+                        lds_v2(tile + r * RS + ((h * 32u + lane) << 4), a, b2);
                         stg_v2_cs(dst + (uint64_t)r * g.nps, a, b2);
                     }
                 }
@@ -430,7 +436,7 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
                 const uint32_t r = r0 + rsub;
                 if (r < nrows && col < g.nps) {
                     double a, b2;
-                    lds_v2(tile + r * (RC * 8u) + ((c ^ (r & (CPR - 1))) << 4), a, b2);
+                    lds_v2(tile + r * RS + (c << 4), a, b2);
                     stg_v2_cs(g.out + (row0 + r) * g.nps + col, a, b2);
                 }
             }
@@ -527,7 +533,7 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
         if constexpr (WRITE && ST == Store::ROW) {
             XsProducer<MODE, SPEC, IEEE, ALG1> prod(g, g.stream_begin + t * 32u + lane);
             run_rows_burst<true, kConsRowCols>(
-                g, base + kHistWords * 4u + warp * (32u * kConsRowCols * 8u), lane, t * 32u, prod,
+                g, base + kHistWords * 4u + warp * (32u * (kConsRowCols * 8u + 16u)), lane, t * 32u, prod,
                 cons);
         }
         else
@@ -776,6 +782,7 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
 #define PRNGD_SEG_HALF 64
 #endif
 constexpr int kSegHalf = PRNGD_SEG_HALF;  // outputs per lane per flush (one 512-byte chunk)
+constexpr uint32_t kSegRS = kSegHalf * 8u + 16u;  // padded tile row stride (bytes)
 
 // How a lane reaches its segment start T^(256 j) s (A/B):
 //   0 byte tables, direct J_j (16 loads), next task's loads prefetched across a batch
@@ -875,8 +882,8 @@ __device__ __forceinline__ Xs128 seg_jump(const uint4 *__restrict__ tabs,
 #endif
 }
 
-// One batch of kCols outputs of the fast path into tile row `my`, 16-byte chunk c of the batch
-// at chunk (b * kCols / 2 + c) ^ lane of the row (conflict-free writes and flush reads).
+// One batch of kCols outputs of the fast path into tile row `my` (row stride kSegRS: padded by
+// 16 bytes, so lane writes and per-row flush reads are conflict-free).
 template <int MODE, bool IEEE>
 __device__ __forceinline__ void seg_batch(Xs128 &st, bool &rej, uint32_t my, uint32_t b,
                                           uint32_t lane, const GenArgs &g) {
@@ -897,7 +904,7 @@ __device__ __forceinline__ void seg_batch(Xs128 &st, bool &rej, uint32_t my, uin
     }
 #pragma unroll
     for (int c = 0; c < kCols / 2; ++c)
-        sts_v2(my + (((b * (kCols / 2) + c) ^ lane) << 4), q[2 * c], q[2 * c + 1]);
+        sts_v2(my + ((b * (kCols / 2) + c) << 4), q[2 * c], q[2 * c + 1]);
 }
 
 // One-warp CTAs (12 per SM, smem-bound), each running `tpc` consecutive warp tasks of 32
@@ -927,7 +934,7 @@ __global__ void __launch_bounds__(32, 12)
     const uint4 *my_tab = tabs + (size_t)j * 16 * 256;  // byte tables, 64 KiB per lane matrix
 #endif
     const uint32_t tile = aligned_smem_base(smem_raw);
-    const uint32_t my = tile + lane * (kSegHalf * 8u);  // this lane's tile row
+    const uint32_t my = tile + lane * kSegRS;  // this lane's tile row
     uint64_t t = (uint64_t)blockIdx.x * tpc;
     Xs128 st = stream_start(g.seed, g.stream_begin + t * rows_per_warp + rloc);
     st = seg_jump(tabs, my_tab, j, log2S, st);
@@ -985,7 +992,7 @@ __global__ void __launch_bounds__(32, 12)
 #pragma unroll 4
                 for (uint32_t r = 0; r < nchunks; ++r) {
                     double a, b2;
-                    lds_v2(tile + r * (kSegHalf * 8u) + ((lane ^ r) << 4), a, b2);
+                    lds_v2(tile + r * kSegRS + (lane << 4), a, b2);
                     stg_v2_cs(base + r * kSegOut, a, b2);
                 }
                 __syncwarp();
@@ -1088,8 +1095,8 @@ __global__ void __launch_bounds__(kSegcWarps * 32, 1)
     const uint32_t L = (uint32_t)(g.nps / kSegcWarps);  // outputs (pairs) per column block
     const uint32_t base = aligned_smem_base(smem_raw);
     const uint32_t tab_s = base;                                   // J_1..J_7, 8 KiB each
-    const uint32_t tile = base + kSegcTabBytes + j * (kSegHalf * 32u * 8u);
-    const uint32_t my = tile + lane * (kSegHalf * 8u);
+    const uint32_t tile = base + kSegcTabBytes + j * (32u * kSegRS);
+    const uint32_t my = tile + lane * kSegRS;
     {   // nibble tables of J_1..J_7 (lane matrices 1..7 of the global table) into smem
         const uint4 *src = tabs + 32 * 16;
         for (uint32_t i = threadIdx.x; i < (uint32_t)(kSegcTabBytes / 16); i += blockDim.x) {
@@ -1130,7 +1137,7 @@ __global__ void __launch_bounds__(kSegcWarps * 32, 1)
 #pragma unroll 4
             for (uint32_t r = 0; r < nrows; ++r) {
                 double a, b2;
-                lds_v2(tile + r * (kSegHalf * 8u) + ((lane ^ r) << 4), a, b2);
+                lds_v2(tile + r * kSegRS + (lane << 4), a, b2);
                 stg_v2_cs(dst + (uint64_t)r * g.nps, a, b2);
             }
             __syncwarp();
@@ -1317,7 +1324,7 @@ static cudaError_t cons_launch(const CUtensorMap &m, const GenArgs &g, int grid,
     constexpr int kWarps = cons_warps<ST, WRITE>();
     auto k = consume_kernel<MODE, SPEC, IEEE, ALG1, ST, WRITE, RED, EXACT_GUARD>;
     const size_t smem = 1024 + (size_t)kHistWords * 4u +
-                        (WRITE && ST == Store::ROW ? (size_t)kWarps * 32 * kConsRowCols * 8
+                        (WRITE && ST == Store::ROW ? (size_t)kWarps * 32 * (kConsRowCols * 8 + 16)
                                                    : (size_t)kWarps * ring<ST, WRITE>() * kTileBytes);
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
@@ -1404,7 +1411,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
 }
 
 cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st) {
-    const size_t smem = 1024 + (size_t)32 * kMrgCols * 8;
+    const size_t smem = 1024 + (size_t)32 * (kMrgCols * 8 + 16);
     const uint64_t grid = (g.n_streams + 31) / 32;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     cudaError_t e = set_smem(gen_mrg_kernel, smem);
@@ -1442,7 +1449,7 @@ cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *ta
     while ((1ull << log2S) < S) ++log2S;
     const uint64_t rows_per_warp = 32u >> log2S;
     const uint64_t n_tasks = (g.n_streams + rows_per_warp - 1) / rows_per_warp;
-    const size_t smem = 1024 + (size_t)32 * kSegHalf * 8;
+    const size_t smem = 1024 + (size_t)32 * kSegRS;
     cudaError_t e;
 #if PRNGD_SEG_JUMP == 1 || PRNGD_SEG_JUMP == 2
     (void)tables;
@@ -1487,7 +1494,7 @@ cudaError_t launch_generate_segc(const GenArgs &g, const Plan &pl, cudaStream_t 
     if (e != cudaSuccess) return e;
     const uint4 *t = static_cast<const uint4 *>(tables);
     const uint64_t n_tasks = (g.n_streams + 31) / 32;
-    const size_t smem = 1024 + (size_t)kSegcTabBytes + (size_t)kSegcWarps * 32 * kSegHalf * 8;
+    const size_t smem = 1024 + (size_t)kSegcTabBytes + (size_t)kSegcWarps * 32 * kSegRS;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
