@@ -194,13 +194,14 @@ __device__ __forceinline__ double exact_output(Xs128 &st, uint32_t sh1, uint32_t
 // kCols consecutive outputs of this lane's stream, into registers q[0..kCols).
 template <int MODE, bool SPEC, bool IEEE, bool ALG1>
 __device__ __forceinline__ void produce_batch(Xs128 &st, double (&q)[kCols], const GenArgs &g) {
-    // MODE 2: w = 32 full range, Eq.(4) closed (every constant compiled in); MODE 1: Eq.(4)
-    // closed with runtime ranges; MODE 0: any mapping (runtime-uniform selection).
+    // MODE 2: w = 32 full range, Eq.(4) closed (every constant compiled in); MODE 3: Eq.(4),
+    // w = 32 and 32-bit x1 draws (v = x1:x2 is a register pair), runtime x2 width and accept
+    // band (cfg4); MODE 1: Eq.(4) with runtime ranges; MODE 0: any mapping (runtime-uniform).
     constexpr bool FULL32 = MODE == 2;
     constexpr bool EQ4 = MODE >= 1;
-    const uint32_t sh1 = FULL32 ? 0u : g.sh1;
+    const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1;
     const uint32_t sh2 = FULL32 ? 0u : g.sh2;
-    const uint32_t w = FULL32 ? 32u : g.w;
+    const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo;
     const uint32_t span = FULL32 ? 0xFFFFFFFEu : g.span;
     if (SPEC) {
@@ -700,8 +701,8 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
     const uint64_t row = (uint64_t)blockIdx.x * kJumpWarps + warp;
     if (row >= g.n_streams) return;
     constexpr bool FULL32 = MODE == 2;
-    const uint32_t sh1 = FULL32 ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
-    const uint32_t w = FULL32 ? 32u : g.w;
+    const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
+    const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
     const uint32_t stage = aligned_smem_base(smem_raw) + warp * (32u * kJumpPairs * 8u);
     const uint4 *my_tab = tabs + (size_t)lane * 16 * 256;
@@ -801,8 +802,8 @@ __device__ __forceinline__ void seg_exact(const GenArgs &g, Xs128 st, uint32_t j
                                           uint64_t row, bool live) {
     constexpr bool FULL32 = MODE == 2;
     constexpr bool EQ4 = MODE >= 1;
-    const uint32_t sh1 = FULL32 ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
-    const uint32_t w = FULL32 ? 32u : g.w;
+    const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
+    const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
     const Xs128 seg0 = st;
     // pass 1: accepted pairs among this lane's kSegOut pairs
@@ -889,8 +890,8 @@ __device__ __forceinline__ void seg_batch(Xs128 &st, bool &rej, uint32_t my, uin
                                           uint32_t lane, const GenArgs &g) {
     constexpr bool FULL32 = MODE == 2;
     constexpr bool EQ4 = MODE >= 1;
-    const uint32_t sh1 = FULL32 ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
-    const uint32_t w = FULL32 ? 32u : g.w;
+    const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
+    const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo;
     const uint32_t span_fast = FULL32 ? 0xFFFFFFFDu : g.span_fast;
     double q[kCols];
@@ -1046,8 +1047,8 @@ __device__ __noinline__ void segc_exact(const GenArgs &g, Xs128 st, uint32_t j, 
                                         uint64_t row, bool fix, uint32_t L, uint32_t *cnt) {
     constexpr bool FULL32 = MODE == 2;
     constexpr bool EQ4 = MODE >= 1;
-    const uint32_t sh1 = FULL32 ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
-    const uint32_t w = FULL32 ? 32u : g.w;
+    const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
+    const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
     const Xs128 seg0 = st;
     if (fix) {  // pass 1: accepted pairs among this block's L pairs
@@ -1276,6 +1277,7 @@ static cudaError_t gen_dispatch_store(const CUtensorMap &m, const GenArgs &g, co
                                       int mode, cudaStream_t st) {
     if (pl.spec && !pl.ieee_div && !pl.alg1) {
         if (mode == 2) return gen_launch<2, true, false, false, ST>(m, g, st);
+        if (mode == 3) return gen_launch<3, true, false, false, ST>(m, g, st);
         if (mode == 1) return gen_launch<1, true, false, false, ST>(m, g, st);
     }
     if (pl.alg1)
@@ -1293,7 +1295,13 @@ static int kernel_mode(const GenArgs &g) {
     const bool eq4 = g.map.kind == 4 && g.map.open == 0;
     const bool full32 = eq4 && g.w == 32 && g.sh1 == 0 && g.sh2 == 0 && g.lo == 1u &&
                         g.span == 0xFFFFFFFEu && g.span_fast == 0xFFFFFFFDu;
-    return full32 ? 2 : (eq4 ? 1 : 0);
+    const bool w32 = eq4 && g.w == 32 && g.sh1 == 0;
+    return full32 ? 2 : (w32 ? 3 : (eq4 ? 1 : 0));
+}
+// the jump / SEG / SEGC kernels are instantiated for modes 0-2 only (3 is a case of 1)
+static int kernel_mode_012(const GenArgs &g) {
+    const int m = kernel_mode(g);
+    return m == 3 ? 1 : m;
 }
 
 cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, int) {
@@ -1337,6 +1345,7 @@ static cudaError_t cons_dispatch(const CUtensorMap &m, const GenArgs &g, const P
                                  int mode, int grid, cudaStream_t st) {
     if (pl.spec && !pl.ieee_div && !pl.alg1) {
         if (mode == 2) return cons_launch<2, true, false, false, ST, WRITE, RED, EG>(m, g, grid, st);
+        if (mode == 3) return cons_launch<3, true, false, false, ST, WRITE, RED, EG>(m, g, grid, st);
         if (mode == 1) return cons_launch<1, true, false, false, ST, WRITE, RED, EG>(m, g, grid, st);
     }
     if (pl.alg1)
@@ -1427,7 +1436,7 @@ cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *t
     const uint64_t grid = (g.n_streams + kJumpWarps - 1) / kJumpWarps;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     const uint4 *t = static_cast<const uint4 *>(tables);
-    const int mode = kernel_mode(g);
+    const int mode = kernel_mode_012(g);
     cudaError_t e;
     if (mode == 2) {
         if ((e = set_smem(gen_jump_kernel<2>, smem)) != cudaSuccess) return e;
@@ -1459,7 +1468,7 @@ cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *ta
     if ((e = jump_tables_interleaved(kSegDraws, &tables)) != cudaSuccess) return e;
 #endif
     const uint4 *t = static_cast<const uint4 *>(tables);
-    const int mode = kernel_mode(g);
+    const int mode = kernel_mode_012(g);
     // consecutive tasks per CTA (hides all but the first jump); one when the grid is small
 #ifndef PRNGD_SEG_TPC
 #define PRNGD_SEG_TPC 4
@@ -1499,7 +1508,7 @@ cudaError_t launch_generate_segc(const GenArgs &g, const Plan &pl, cudaStream_t 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t grid = n_tasks < (uint64_t)sms ? n_tasks : (uint64_t)sms;  // one CTA per SM
-    const int mode = kernel_mode(g);
+    const int mode = kernel_mode_012(g);
 #define PRNGD_SEGC_LAUNCH(M, I)                                                                 \
     do {                                                                                        \
         if ((e = set_smem(gen_segc_kernel<M, I>, smem)) != cudaSuccess) return e;               \

@@ -496,3 +496,23 @@ def test_guard_bands_mrg(orc):
     torch.cuda.synchronize()
     assert _guards_intact(buf, 45 * 70)
     assert_same(out, orc.generate(p)["out"])
+
+
+@pytest.mark.parametrize("par", [dict(w=32, a0=2**12, a=2**32 - 1, b0=0, b=2**20 - 1),
+                                 dict(w=32, a0=0, a=2**32 - 1, b0=0, b=2**31 - 1),
+                                 dict(w=32, a0=5, a=2**32 - 3, b0=0, b=2**32 - 1)])
+def test_w32_runtime_band_kernel(orc, par):
+    """Kernel MODE 3 (w = 32, 32-bit x1 draws, runtime x2 width and accept band: cfg4's family)
+    through the ROW generator and the fused consumer, with rare rejections (p ~ 1e-6) included."""
+    p = dict(par, seed=21, stream_begin=5, n_streams=4096, n_per_stream=1024,
+             flags=P.PRNGD_FLAG_STORE_ROW)
+    _, out = gen(p)
+    r = orc.generate(p, want_stats=True, want_consumed=True)
+    assert_same(out, r["out"])
+    g = P.Generator(**p)
+    out2 = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+    _, hist, pw, cnt = g.generate_consume(out2)
+    torch.cuda.synchronize()
+    assert_same(out2, r["out"])
+    assert np.array_equal(hist.cpu().numpy(), r["hist"]) and cnt.item() == r["count"]
+    assert np.allclose(pw.cpu().numpy(), r["pow"], rtol=1e-12, atol=0)
