@@ -99,7 +99,7 @@ class ClockSampler:
     }
 
     def __init__(self, index: int):
-        self.samples, self.reasons, self.ok = [], 0, False
+        self.samples, self.power, self.reasons, self.ok = [], [], 0, False
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -116,6 +116,7 @@ class ClockSampler:
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
                 self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
             except Exception:
                 pass
             time.sleep(0.005)
@@ -145,8 +146,12 @@ class ClockSampler:
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["nvml unavailable"]}
         rs = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max,
-                "reasons": rs, "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max,
+               "reasons": rs, "samples": len(self.samples)}
+        if self.power:
+            out["power_w_median"] = statistics.median(self.power)
+            out["power_w_max"] = max(self.power)
+        return out
 
 
 def cpu_baseline(p: dict, target_s: float = 12.0) -> dict:

@@ -119,7 +119,9 @@ __device__ __forceinline__ uint32_t tile_off(uint32_t row, uint32_t chunk) {
 }
 
 // ------------------------------------------------------------------------------ consumer (S7)
-template <bool RED>
+// RED: optimistic no-return adds (see consume_kernel); BELOW1: the mapping never returns 1.0
+// (Eq.(4) closed with the R11 clamp), so the R18 top-bin guard is not needed.
+template <bool RED, bool BELOW1 = false>
 struct ConsumerT {
     double s1, s2, s3, s4;
     uint32_t *hist;   // shared: 32768 words, counter of bin b in half (b & 1) of word b >> 1
@@ -141,9 +143,10 @@ struct ConsumerT {
         s2 = __dadd_rn(s2, z2);
         s3 = __fma_rn(z2, q, s3);
         s4 = __fma_rn(z2, z2, s4);
-        const uint32_t bin = bin16(q);
+        const uint32_t bin = BELOW1 ? (uint32_t)__double2uint_rz(__dmul_rn(q, 65536.0)) : bin16(q);
+        // 1 << (16 * (bin & 1)) as a rotate of 1 by bin * 16 (the amount is taken mod 32)
         const uint32_t sh = (bin & 1u) << 4;
-        const uint32_t inc = 1u << sh;
+        const uint32_t inc = __funnelshift_l(1u, 1u, bin << 4);
         if (RED) {
             // optimistic: no return value, no carry check; a wrapped field is detected after
             // the kernel (field sum != outputs counted) and the exact pass redoes the histogram
@@ -164,7 +167,7 @@ struct ConsumerT {
     }
 };
 
-using Consumer = ConsumerT<false>;
+using Consumer = ConsumerT<false, false>;
 
 struct NoConsumer {
     __device__ __forceinline__ void init(uint32_t *, int64_t *) {}
@@ -524,7 +527,7 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     const uint32_t tiles = base + kHistWords * 4u + warp * (NB * kTileBytes);
     for (uint32_t i = threadIdx.x; i < kHistWords; i += blockDim.x) hist[i] = 0u;
     __syncthreads();
-    ConsumerT<RED> cons;
+    ConsumerT<RED, (MODE >= 1)> cons;
     cons.init(hist, g.hist_spill);
     uint32_t it = 0;
     const uint64_t n_tasks = (g.n_streams + 31u) / 32u;

@@ -7,6 +7,6 @@ for c in "$@"; do
 import sys,json
 s=sys.stdin.read()
 try:
-    d=json.loads(s); print('$c', '${TAG:-}', round(d['value'],1), d['roofline'].get('kernel'), d['clocks']['sm_mhz'], d['clocks']['reasons'])
+    d=json.loads(s); print('$c', '${TAG:-}', round(d['value'],1), d['roofline'].get('kernel'), d['clocks']['sm_mhz'], d['clocks'].get('power_w_median'), d['clocks']['reasons'])
 except Exception: print('$c', '${TAG:-}', 'FAILED:', s[-300:])"
 done
