@@ -248,3 +248,39 @@ extern "C" __attribute__((visibility("default"))) int wc_blockcol(double *p, uin
         p, rows, cols, chunk, salt);
     return (int)cudaGetLastError();
 }
+
+// Shared-memory histogram increment ceiling: every thread issues `iters` adds of 1 << 16*(b&1)
+// into a 32768-word (128 KiB) packed histogram at pseudo-random bins b (xorshift32 per thread),
+// RED (no return) when red != 0, else atomicAdd with its return value consumed.  One CTA of
+// `warps` warps per SM (the fused consumer's shape).  Returns via *ops the total adds.
+__global__ void smem_hist_rate(uint32_t iters, int red, unsigned long long *sink) {
+    extern __shared__ uint32_t h[];
+    for (uint32_t i = threadIdx.x; i < 32768; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    uint32_t x = 0x9E3779B9u * (blockIdx.x * blockDim.x + threadIdx.x + 1), acc = 0;
+    for (uint32_t k = 0; k < iters; ++k) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            x ^= x << 13; x ^= x >> 17; x ^= x << 5;
+            const uint32_t b = x >> 16;
+            const uint32_t inc = __funnelshift_l(1u, 1u, b << 4);
+            if (red)
+                asm volatile("red.shared.add.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&h[b >> 1])), "r"(inc) : "memory");
+            else
+                acc += atomicAdd(&h[b >> 1], inc);
+        }
+    }
+    if (acc == 0xFFFFFFFFu) sink[0] = acc;
+}
+
+extern "C" __attribute__((visibility("default"))) int wc_smem_hist(uint32_t iters, int red,
+                                                                   int warps, void *stream,
+                                                                   void *sink) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(smem_hist_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+    smem_hist_rate<<<sms, warps * 32, 131072, (cudaStream_t)stream>>>(
+        iters, red, (unsigned long long *)sink);
+    return (int)cudaGetLastError();
+}
