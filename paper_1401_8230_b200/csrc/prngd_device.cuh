@@ -52,27 +52,40 @@ struct Mrg32k3a {
 //   m1 (c = 209):   one fold leaves r < 2^32 + 2^28.8 < 2 m1
 //   m2 (c = 22853): two folds leave r < 2^32 + 2^17.8 < 2 m2
 // and the final r - m, when r >= m, is the 32-bit sum lo(r) + c (wrapping when hi(r) = 0).
-__device__ __forceinline__ uint32_t mrg_next(Mrg32k3a &m) {
-    // component 1: fold in 32-bit halves (hi * 209 < 2^32, so the sum carries at most once)
-    const uint64_t t1 = 1403580ull * m.s1 + 810728ull * (kM1 - m.s0);
+// component 1: x_n = (1403580 x_{n-2} - 810728 x_{n-3}) mod m1 from (x_{n-2}, x_{n-3});
+// fold in 32-bit halves (hi * 209 < 2^32, so the sum carries at most once)
+__device__ __forceinline__ uint32_t mrg_c1(uint32_t xm2, uint32_t xm3) {
+    const uint64_t t1 = 1403580ull * xm2 + 810728ull * (kM1 - xm3);
     const uint32_t h1 = (uint32_t)(t1 >> 32), l1 = (uint32_t)t1;
     const uint32_t f1 = l1 + h1 * 209u;
-    const uint32_t p1 = (f1 < l1 || f1 >= kM1) ? f1 + 209u : f1;
-    m.s0 = m.s1;
-    m.s1 = m.s2;
-    m.s2 = p1;
-    // component 2: first fold kept as (hi, lo) 32-bit words, second fold as above
-    const uint64_t t2 = 527612ull * m.t2 + 1370589ull * (kM2 - m.t0);
+    return (f1 < l1 || f1 >= kM1) ? f1 + 209u : f1;
+}
+// component 2: y_n = (527612 y_{n-1} - 1370589 y_{n-3}) mod m2 from (y_{n-1}, y_{n-3});
+// first fold kept as (hi, lo) 32-bit words, second fold as above
+__device__ __forceinline__ uint32_t mrg_c2(uint32_t ym1, uint32_t ym3) {
+    const uint64_t t2 = 527612ull * ym1 + 1370589ull * (kM2 - ym3);
     const uint32_t h2 = (uint32_t)(t2 >> 32), l2 = (uint32_t)t2;
     const uint32_t g_lo = l2 + h2 * 22853u;
     const uint32_t g_hi = __umulhi(h2, 22853u) + (g_lo < l2 ? 1u : 0u);
     const uint32_t f2 = g_lo + g_hi * 22853u;
-    const uint32_t p2 = (f2 < g_lo || f2 >= kM2) ? f2 + 22853u : f2;
+    return (f2 < g_lo || f2 >= kM2) ? f2 + 22853u : f2;
+}
+// u = (x_n - y_n) mod m1 with 0 reported as m1
+__device__ __forceinline__ uint32_t mrg_combine(uint32_t p1, uint32_t p2) {
+    const uint32_t z = p1 - p2;  // wraps when p1 <= p2: then p1 - p2 + m1 = z - 209 (mod 2^32)
+    return p1 > p2 ? z : z - 209u;
+}
+
+__device__ __forceinline__ uint32_t mrg_next(Mrg32k3a &m) {
+    const uint32_t p1 = mrg_c1(m.s1, m.s0);
+    m.s0 = m.s1;
+    m.s1 = m.s2;
+    m.s2 = p1;
+    const uint32_t p2 = mrg_c2(m.t2, m.t0);
     m.t0 = m.t1;
     m.t1 = m.t2;
     m.t2 = p2;
-    const uint32_t z = p1 - p2;  // wraps when p1 <= p2: then p1 - p2 + m1 = z - 209 (mod 2^32)
-    return p1 > p2 ? z : z - 209u;
+    return mrg_combine(p1, p2);
 }
 
 // R23: uniform width-bit value: discard u with u - 1 >= T = floor(m1 / 2^width) * 2^width.

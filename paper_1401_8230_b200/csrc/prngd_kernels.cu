@@ -344,20 +344,70 @@ struct XsProducer {  // xorshift128 base generator (S1-S5)
     }
 };
 
-struct MrgProducer {  // NEXT-2: MRG32k3a base generator, reduced draws (R21-R23), pair-drop
-    Mrg32k3a st;
-    __device__ __forceinline__ MrgProducer(const GenArgs &g, uint64_t s)
-        : st(mrg_stream_start(g.seed, s)) {}
+// MRG32k3a without divergent draw loops.  A lane turns every draw into the R23 / pair-drop
+// state machine with predicated logic (draw for x1 or x2 by the lane's own phase, reduce-to-width
+// test, band test when a pair completes) and appends each accepted pair to a per-lane ring of
+// kMrgRing pairs in shared memory.  The warp draws 3 values per lane per step (the unroll by the
+// MRG's period-3 register rotation, so the state needs no moves) until every lane holds a
+// batch; lanes ahead keep drawing into their ring while it has room, which evens out the
+// per-lane acceptance luck across batches.  The consumption order of every stream is exactly the
+// sequential one (NEXT-2).
+constexpr uint32_t kMrgRing = 64;  // pairs per lane (power of two)
+
+template <bool EQ4>
+struct MrgProducer2 {
+    uint32_t A, B, C, D, E, F;  // component 1 (oldest..newest) and component 2 state
+    uint32_t rd, wr;            // ring counters (free-running)
+    uint32_t x1;                // pending x1 (when have1)
+    bool have1;
+    uint32_t ring;              // this lane's ring (shared address), entries of 8 bytes
+    __device__ __forceinline__ MrgProducer2(const GenArgs &g, uint64_t s, uint32_t ring_base) {
+        const Mrg32k3a m = mrg_stream_start(g.seed, s);
+        A = m.s0, B = m.s1, C = m.s2, D = m.t0, E = m.t1, F = m.t2;
+        rd = wr = 0u;
+        x1 = 0u;
+        have1 = false;
+        ring = ring_base;
+    }
+    __device__ __forceinline__ void take(uint32_t u, const GenArgs &g) {
+        const uint32_t x = u - 1u;
+        const bool v = x < (have1 ? g.mrg_t2 : g.mrg_t1);       // R23 reduce-to-width
+        const bool push = v && have1 && accepted(x1, g.lo, g.span);  // pair complete
+        if (push) {
+            const uint32_t a = ring + ((wr & (kMrgRing - 1)) << 3);
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x1),
+                         "r"(x & g.mrg_mask2)
+                         : "memory");
+        }
+        wr += push ? 1u : 0u;
+        x1 = (v && !have1) ? (x & g.mrg_mask1) : x1;
+        have1 = v ? !have1 : have1;
+    }
     __device__ __forceinline__ void operator()(double (&q)[kCols], const GenArgs &g) {
+#pragma unroll 1
+        while (__any_sync(0xFFFFFFFFu, wr - rd < (uint32_t)kCols)) {
+            if (wr - rd <= kMrgRing - 2u) {  // 3 draws complete at most 2 pairs
+                uint32_t p1 = mrg_c1(B, A), p2 = mrg_c2(F, D);
+                A = p1, D = p2;
+                take(mrg_combine(p1, p2), g);
+                p1 = mrg_c1(C, B), p2 = mrg_c2(D, E);
+                B = p1, E = p2;
+                take(mrg_combine(p1, p2), g);
+                p1 = mrg_c1(A, C), p2 = mrg_c2(E, F);
+                C = p1, F = p2;
+                take(mrg_combine(p1, p2), g);
+            }
+        }
 #pragma unroll
         for (int i = 0; i < kCols; ++i) {
-            uint32_t x1, x2;
-            do {
-                x1 = mrg_reduced(st, g.mrg_t1, g.mrg_mask1);
-                x2 = mrg_reduced(st, g.mrg_t2, g.mrg_mask2);
-            } while (!accepted(x1, g.lo, g.span));
-            q[i] = map_pair<false, true>(x1, x2, g.map);
+            uint32_t a1, a2;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                         : "=r"(a1), "=r"(a2)
+                         : "r"(ring + (((rd + i) & (kMrgRing - 1)) << 3)));
+            q[i] = EQ4 ? eq4_pair<false, true>(a1, a2, g.w, g.Cs, g.Ds, g.y)
+                       : map_pair<false, true>(a1, a2, g.map);
         }
+        rd += kCols;
     }
 };
 
@@ -640,16 +690,21 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
 // Same ROW burst store, MRG32k3a base draws (ALU/latency-bound: ~2 x 25 integer ops per draw),
 // so shorter bursts (smaller tiles) buy occupancy.
 #ifndef PRNGD_MRG_RC
-#define PRNGD_MRG_RC 16  // A/B on cfg3 shape: 16 -> 136, 32 -> 129, 64 -> 119 Gd/s
+#define PRNGD_MRG_RC 16  // A/B on cfg3 shape (per-draw loops): 16 -> 136, 32 -> 129, 64 -> 119
 #endif
 constexpr int kMrgCols = PRNGD_MRG_RC;
+constexpr size_t kMrgTileBytes = (size_t)32 * (kMrgCols * 8 + 16);
+template <bool EQ4>
 __global__ void __launch_bounds__(32) gen_mrg_kernel(const GenArgs g) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t row0 = (uint64_t)blockIdx.x * 32u;
     NoConsumer nc;
-    MrgProducer prod(g, g.stream_begin + row0 + lane);
-    run_rows_burst<false, kMrgCols>(g, aligned_smem_base(smem_raw), lane, row0, prod, nc);
+    const uint32_t base = aligned_smem_base(smem_raw);
+    // ring rows padded by 8 bytes: lanes at equal ring positions land on different banks
+    MrgProducer2<EQ4> prod(g, g.stream_begin + row0 + lane,
+                           base + (uint32_t)kMrgTileBytes + lane * (kMrgRing * 8u + 8u));
+    run_rows_burst<false, kMrgCols>(g, base, lane, row0, prod, nc);
 }
 
 // ------------------------------------------------------------------------------ NEXT-3 jump kernel
@@ -1423,12 +1478,14 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
 }
 
 cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st) {
-    const size_t smem = 1024 + (size_t)32 * (kMrgCols * 8 + 16);
+    const size_t smem = 1024 + kMrgTileBytes + (size_t)32 * (kMrgRing * 8 + 8);
     const uint64_t grid = (g.n_streams + 31) / 32;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    cudaError_t e = set_smem(gen_mrg_kernel, smem);
+    const bool eq4 = g.map.kind == 4 && g.map.open == 0;
+    auto k = eq4 ? gen_mrg_kernel<true> : gen_mrg_kernel<false>;
+    cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
-    gen_mrg_kernel<<<(unsigned)grid, 32, smem, st>>>(g);
+    k<<<(unsigned)grid, 32, smem, st>>>(g);
     return cudaGetLastError();
 }
 
