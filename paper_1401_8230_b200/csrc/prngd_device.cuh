@@ -88,6 +88,37 @@ __device__ __forceinline__ uint32_t mrg_next(Mrg32k3a &m) {
     return mrg_combine(p1, p2);
 }
 
+// The same recurrences in binary64: every product and sum below is an integer < 2^53, so each
+// operation is exact and the state values are bit-for-bit the integer ones.  k = nearest
+// integer to p / m (p * (1/m) rounded by the 2^52 + 2^51 shift), r = p - k m in [-m/2, m/2],
+// + m when negative.  FP64-pipe work instead of ~20 INT32 instructions per component.
+constexpr double kRoundShift = 6755399441055744.0;  // 2^52 + 2^51
+__device__ __forceinline__ double mrg_modd(double p, double m, double inv_m) {
+    const double k = __dsub_rn(__fma_rn(p, inv_m, kRoundShift), kRoundShift);
+    double r = __fma_rn(-k, m, p);
+    // r += m when r < 0, as one predicated add (a select would cost two FSELs)
+    asm("{\n\t.reg .pred p;\n\tsetp.lt.f64 p, %0, 0d0000000000000000;\n\t@p add.rn.f64 %0, %0, %1;\n\t}"
+        : "+d"(r)
+        : "d"(m));
+    return r;
+}
+__device__ __forceinline__ double mrg_c1d(double xm2, double xm3) {
+    return mrg_modd(__fma_rn(1403580.0, xm2, -__dmul_rn(810728.0, xm3)), 4294967087.0,
+                    1.0 / 4294967087.0);
+}
+__device__ __forceinline__ double mrg_c2d(double ym1, double ym3) {
+    return mrg_modd(__fma_rn(527612.0, ym1, -__dmul_rn(1370589.0, ym3)), 4294944443.0,
+                    1.0 / 4294944443.0);
+}
+// u = (x_n - y_n) mod m1 in [1, m1] as an integer
+__device__ __forceinline__ uint32_t mrg_combined(double p1, double p2) {
+    double d = __dsub_rn(p1, p2);
+    asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %0, 0d0000000000000000;\n\t@p add.rn.f64 %0, %0, %1;\n\t}"
+        : "+d"(d)
+        : "d"(4294967087.0));
+    return (uint32_t)__double2uint_rz(d);
+}
+
 // R23: uniform width-bit value: discard u with u - 1 >= T = floor(m1 / 2^width) * 2^width.
 __device__ __forceinline__ uint32_t mrg_reduced(Mrg32k3a &m, uint32_t T, uint32_t mask) {
     uint32_t u;

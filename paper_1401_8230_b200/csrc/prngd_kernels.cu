@@ -352,22 +352,48 @@ struct XsProducer {  // xorshift128 base generator (S1-S5)
 // batch; lanes ahead keep drawing into their ring while it has room, which evens out the
 // per-lane acceptance luck across batches.  The consumption order of every stream is exactly the
 // sequential one (NEXT-2).
-constexpr uint32_t kMrgRing = 64;  // pairs per lane (power of two)
+#ifndef PRNGD_MRG_RING
+#define PRNGD_MRG_RING 32
+#endif
+constexpr uint32_t kMrgRing = PRNGD_MRG_RING;  // pairs per lane (power of two, >= 2 kCols)
 
+// MRG_FP64: 0 = both components in 32-bit integer arithmetic, 1 = component 1 in binary64,
+// 2 = both in binary64 (exact either way; A/B of INT32 vs FP64 pipe load)
+#ifndef PRNGD_MRG_FP64
+#define PRNGD_MRG_FP64 2
+#endif
+template <int FP> struct MrgWord { using T = uint32_t; };
+template <> struct MrgWord<1> { using T = double; };
 template <bool EQ4>
 struct MrgProducer2 {
-    uint32_t A, B, C, D, E, F;  // component 1 (oldest..newest) and component 2 state
+    using T1 = typename MrgWord<PRNGD_MRG_FP64 >= 1 ? 1 : 0>::T;  // component 1 word
+    using T2 = typename MrgWord<PRNGD_MRG_FP64 >= 2 ? 1 : 0>::T;  // component 2 word
+    T1 A, B, C;                 // component 1, oldest..newest (rotating roles)
+    T2 D, E, F;                 // component 2
     uint32_t rd, wr;            // ring counters (free-running)
     uint32_t x1;                // pending x1 (when have1)
     bool have1;
     uint32_t ring;              // this lane's ring (shared address), entries of 8 bytes
     __device__ __forceinline__ MrgProducer2(const GenArgs &g, uint64_t s, uint32_t ring_base) {
         const Mrg32k3a m = mrg_stream_start(g.seed, s);
-        A = m.s0, B = m.s1, C = m.s2, D = m.t0, E = m.t1, F = m.t2;
+        A = (T1)m.s0, B = (T1)m.s1, C = (T1)m.s2, D = (T2)m.t0, E = (T2)m.t1, F = (T2)m.t2;
         rd = wr = 0u;
         x1 = 0u;
         have1 = false;
         ring = ring_base;
+    }
+    static __device__ __forceinline__ uint32_t c1(uint32_t a, uint32_t b) { return mrg_c1(a, b); }
+    static __device__ __forceinline__ double c1(double a, double b) { return mrg_c1d(a, b); }
+    static __device__ __forceinline__ uint32_t c2(uint32_t a, uint32_t b) { return mrg_c2(a, b); }
+    static __device__ __forceinline__ double c2(double a, double b) { return mrg_c2d(a, b); }
+    static __device__ __forceinline__ uint32_t combine(uint32_t p1, uint32_t p2) {
+        return mrg_combine(p1, p2);
+    }
+    static __device__ __forceinline__ uint32_t combine(double p1, double p2) {
+        return mrg_combined(p1, p2);
+    }
+    static __device__ __forceinline__ uint32_t combine(double p1, uint32_t p2) {
+        return mrg_combine((uint32_t)__double2uint_rz(p1), p2);
     }
     __device__ __forceinline__ void take(uint32_t u, const GenArgs &g) {
         const uint32_t x = u - 1u;
@@ -387,15 +413,12 @@ struct MrgProducer2 {
 #pragma unroll 1
         while (__any_sync(0xFFFFFFFFu, wr - rd < (uint32_t)kCols)) {
             if (wr - rd <= kMrgRing - 2u) {  // 3 draws complete at most 2 pairs
-                uint32_t p1 = mrg_c1(B, A), p2 = mrg_c2(F, D);
-                A = p1, D = p2;
-                take(mrg_combine(p1, p2), g);
-                p1 = mrg_c1(C, B), p2 = mrg_c2(D, E);
-                B = p1, E = p2;
-                take(mrg_combine(p1, p2), g);
-                p1 = mrg_c1(A, C), p2 = mrg_c2(E, F);
-                C = p1, F = p2;
-                take(mrg_combine(p1, p2), g);
+                A = c1(B, A), D = c2(F, D);
+                take(combine(A, D), g);
+                B = c1(C, B), E = c2(D, E);
+                take(combine(B, E), g);
+                C = c1(A, C), F = c2(E, F);
+                take(combine(C, F), g);
             }
         }
 #pragma unroll
