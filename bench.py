@@ -350,15 +350,19 @@ def main():
                 "peak_source": src, "algorithmic_adds_per_launch": nout, "kernel_ms": kern_ms,
                 "note": "issue-bound below this peak (DESIGN.md section 8)"}
     elif p.get("mrg"):
-        # MRG32k3a: integer arithmetic bound.  Algorithmic INT32 ops per output = 56 (DESIGN.md
-        # section 8: 24 per MRG32k3a output + 3 for reduce-to-width, 2 draws, + 2 accept).
-        ops = 56
+        # MRG32k3a (NEXT-2) runs its recurrences in exact binary64: FP64-pipe bound.
+        # Algorithmic FP64 operations per output: 17 per MRG32k3a draw
+        # (two components x 7: product, fused product-difference, rounding shift pair, remainder,
+        # compare, predicated add; combination 3), 2 draws per output plus the 1/64 of 26-bit
+        # draws reduce-to-width rejects, plus 4 for Eq.(4): 17 x 2.03 + 4 = 38.5.
+        ops = 38.5
         ach = ops * nout / (kern_ms * 1e-3) / 1e9
-        pk = 128.0 * sms * clk_ghz  # ALU (64) + FMA/IMAD (64) INT32 lanes per clk per SM
-        roof = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "Gop/s", "frac": ach / pk,
+        pk = 64.0 * sms * clk_ghz  # FP64 lanes per clk per SM (ncu pipe-utilisation calibrated)
+        roof = {"bound": "fp64", "achieved": ach, "peak": pk, "unit": "Gop/s", "frac": ach / pk,
                 "traffic": None, "kernel": "gen_mrg_kernel",
-                "peak_source": "derived: 128 INT32 lanes/clk/SM x SMs x max SM clock",
-                "algorithmic_int_ops_per_output": ops, "kernel_ms": kern_ms,
+                "peak_source": "derived: 64 FP64 lanes/clk/SM x SMs x max SM clock (ncu: "
+                               "pipe_fp64 42% at 26.7 lanes/clk/SM measured)",
+                "algorithmic_fp64_ops_per_output": ops, "kernel_ms": kern_ms,
                 "hbm_write_gbs": achieved}
 
     # -------------------------------------------------- pure-store ceiling on the same buffer
