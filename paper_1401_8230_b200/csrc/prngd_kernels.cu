@@ -736,6 +736,7 @@ __global__ void __launch_bounds__(32) gen_mrg_kernel(const GenArgs g) {
 // the per-lane accepted counts places every accepted output (pair-drop, R2), so the layout is
 // exactly the sequential one.  Lane 31's final state starts the next round.
 constexpr int kJumpPairs = (int)(kJumpDraws / 2);
+constexpr uint64_t kJumpTail = 24;  // remainders up to this many outputs finish on one lane
 constexpr int kJumpWarps = 4;
 
 __device__ __forceinline__ Xs128 jump_state(const uint4 *__restrict__ tab, const Xs128 &s) {
@@ -848,6 +849,18 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
         S.z = __shfl_sync(0xFFFFFFFFu, st.z, 31);
         S.w = __shfl_sync(0xFFFFFFFFu, st.w, 31);
         base += total;
+        // A short remainder (rejections made the last round fall a few outputs short, e.g.
+        // ~8 of 1024 at w = 8) is cheaper as a sequential tail on one lane than as a full round.
+        const uint64_t rem = g.nps - base;
+        if (rem > 0 && rem <= kJumpTail) {
+            if (lane == 0) {
+                Xs128 t = S;
+                for (uint64_t i = 0; i < rem; ++i)
+                    row_out[base + i] =
+                        exact_output<(MODE >= 1), false, false>(t, sh1, sh2, w, lo, span, g);
+            }
+            break;
+        }
     }
 }
 
