@@ -16,6 +16,8 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <set>
+#include <utility>
 
 #include "prngd_device.cuh"
 #include "prngd_internal.h"
@@ -1348,9 +1350,22 @@ static cudaError_t make_tmap(CUtensorMap *m, double *out, uint64_t n_streams, ui
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// The dynamic shared-memory opt-in of a kernel, set once per (kernel, device): every kernel
+// instantiation always launches with the same size, and the attribute call costs host time on
+// the launch path of the small configurations.
 template <class K>
 static cudaError_t set_smem(K kernel, size_t bytes) {
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const std::pair<const void *, int> key{reinterpret_cast<const void *>(kernel), dev};
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(key)) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done.insert(key);
+    return e;
 }
 
 template <int MODE, bool SPEC, bool IEEE, bool ALG1, Store ST>
