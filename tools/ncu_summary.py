@@ -21,6 +21,11 @@ KEYS = [
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
     "sm__cycles_elapsed.avg.per_second",
+    # store coalescing: sectors per L1 store request (16 = one 512-byte row burst per
+    # instruction) and per L2 write request (4 = full 128-byte lines)
+    "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum",
+    "lts__t_requests_srcunit_tex_op_write.sum", "lts__t_sectors_srcunit_tex_op_write.sum",
+    "lts__t_sectors_srcunit_tex_op_write.sum.pct_of_peak_sustained_elapsed",
 ]
 STALLS = "smsp__pcsamp_warps_issue_stalled_"
 # workload -> (bench store label, algorithmic bytes per launch)
