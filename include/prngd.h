@@ -93,7 +93,7 @@ typedef enum {
 #define PRNGD_FLAG_MAP_EQ6       (2u << PRNGD_MAP_SHIFT)
 #define PRNGD_FLAG_OPEN          0x100u  /* return 1 - z': never 0; the histogram puts
                                             1.0 in bin 65535 (R18) */
-/* NEXT-3 intra-stream parallelism: one warp per stream, lanes start at draws 0, 64, 128, ... of
+/* NEXT-3 intra-stream parallelism: one warp per stream, lanes start at draws 0, 32, 64, ... of
  * the stream via GF(2) jump-ahead of xorshift128 and a warp scan of accepted counts places every
  * output exactly where the sequential order puts it.  Chosen automatically by prngd_generate
  * when there are too few streams to fill the GPU (AUTO store path, n_streams < 16384 and n_per_stream >= 512,
@@ -203,7 +203,7 @@ PRNGD_API prngd_status prngd_debug_map(const prngd_handle *h, const uint32_t *d_
 
 /* Host-only check of the jump-ahead: out = T^n_draws * in for the xorshift128 state
  * (x, y, z, w) = in[0..3].  lane_table >= 0 applies instead the byte table the GPU uses for lane
- * `lane_table` (= T^(d * lane_table)) with per-lane distance d = n_draws, or d = 64 (the NEXT-3
+ * `lane_table` (= T^(d * lane_table)) with per-lane distance d = n_draws, or d = 32 (the NEXT-3
  * jump kernel's tables) when n_draws is 0; the SEG store path uses d = 256.  No CUDA call. */
 PRNGD_API prngd_status prngd_debug_jump(uint64_t n_draws, const uint32_t *in, uint32_t *out,
                                         int lane_table);

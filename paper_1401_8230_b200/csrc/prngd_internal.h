@@ -63,8 +63,8 @@ struct Plan {
 };
 
 // NEXT-3 jump-ahead (prngd_jump.cpp): lane l of a warp starts a round at draw l*kJumpDraws of
-// its stream (kJumpDraws / 2 pairs per lane per round, 32 lanes per stream).
-constexpr uint64_t kJumpDraws = 64;
+// its stream (kJumpDraws / 2 = 16 pairs per lane per round, 32 lanes per stream).
+constexpr uint64_t kJumpDraws = 32;
 // SEG store path: a lane owns a 1 KiB segment (kSegOut outputs = pairs) of its stream's row and
 // starts at draw j * kSegDraws (segment j) via the same byte tables built for that distance.
 constexpr uint64_t kSegOut = 128;

@@ -733,13 +733,19 @@ __global__ void __launch_bounds__(32) gen_mrg_kernel(const GenArgs g) {
 }
 
 // ------------------------------------------------------------------------------ NEXT-3 jump kernel
-// One warp per stream.  Each round, lane l jumps the stream state by l * kJumpDraws draws
-// (J_l = T^(64 l), byte tables) and produces kJumpPairs = 32 consecutive pairs; a warp scan of
-// the per-lane accepted counts places every accepted output (pair-drop, R2), so the layout is
-// exactly the sequential one.  Lane 31's final state starts the next round.
+// One warp per stream, kJumpWarps streams per CTA (a 4096-stream config is a single wave).  Each round, lane
+// l jumps the round-start state by l * kJumpDraws draws (J_l = T^(32 l), byte tables) and draws
+// kJumpPairs = 16 consecutive pairs, keeping the outputs in registers; a warp scan of the
+// per-lane accepted counts gives every accepted output its sequential position (pair-drop, R2),
+// the lanes scatter them into a compact shared-memory run, and the warp writes the run with
+// coalesced stores.  Lane 31's final state starts the next round; a short remainder is finished
+// by one lane sequentially.
 constexpr int kJumpPairs = (int)(kJumpDraws / 2);
 constexpr uint64_t kJumpTail = 24;  // remainders up to this many outputs finish on one lane
-constexpr int kJumpWarps = 4;
+#ifndef PRNGD_JUMP_WARPS
+#define PRNGD_JUMP_WARPS 4
+#endif
+constexpr int kJumpWarps = PRNGD_JUMP_WARPS;  // warps (streams) per CTA
 
 __device__ __forceinline__ Xs128 jump_state(const uint4 *__restrict__ tab, const Xs128 &s) {
     const uint32_t words[4] = {s.x, s.y, s.z, s.w};
@@ -772,23 +778,19 @@ __device__ __forceinline__ Xs128 jump_state_nib(const uint4 *__restrict__ tab, c
     return Xs128{r0, r1, r2, r3};
 }
 
-// staging: row = lane (32 doubles = 16 chunks of 16 B), chunk c stored at c ^ (row & 15)
-__device__ __forceinline__ uint32_t jstage_off(uint32_t row, uint32_t j) {
-    return row * 256u + ((((j >> 1) ^ (row & 15u))) << 4) + (j & 1u) * 8u;
-}
-
 template <int MODE>
 __global__ void __launch_bounds__(kJumpWarps * 32)
     gen_jump_kernel(const GenArgs g, const uint4 *__restrict__ tabs) {
     extern __shared__ uint8_t smem_raw[];
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t row = (uint64_t)blockIdx.x * kJumpWarps + warp;
     if (row >= g.n_streams) return;
     constexpr bool FULL32 = MODE == 2;
+    constexpr bool EQ4 = MODE >= 1;
     const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
     const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
-    const uint32_t stage = aligned_smem_base(smem_raw) + warp * (32u * kJumpPairs * 8u);
+    const uint32_t comp = aligned_smem_base(smem_raw) + warp * (32u * kJumpPairs * 8u);
     const uint4 *my_tab = tabs + (size_t)lane * 16 * 256;
     double *row_out = g.out + row * g.nps;
     Xs128 S = stream_start(g.seed, g.stream_begin + row);
@@ -796,21 +798,15 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
 #pragma unroll 1
     while (base < g.nps) {
         Xs128 st = lane ? jump_state(my_tab, S) : S;
+        double q[kJumpPairs];
         uint32_t mask = 0;
 #pragma unroll
-        for (int half = 0; half < kJumpPairs / kCols; ++half) {
-            double q[kCols];
-#pragma unroll
-            for (int i = 0; i < kCols; ++i) {
-                const uint32_t x1 = draw(st) >> sh1;
-                const uint32_t x2 = draw(st) >> sh2;
-                mask |= (accepted(x1, lo, span) ? 1u : 0u) << (half * kCols + i);
-                q[i] = MODE >= 1 ? eq4_pair<false, true>(x1, x2, w, g.Cs, g.Ds, g.y)
-                                 : map_pair<false, true>(x1, x2, g.map);
-            }
-#pragma unroll
-            for (int c = 0; c < kCols / 2; ++c)
-                sts_v2(stage + jstage_off(lane, half * kCols + 2 * c), q[2 * c], q[2 * c + 1]);
+        for (int i = 0; i < kJumpPairs; ++i) {
+            const uint32_t x1 = draw(st) >> sh1;
+            const uint32_t x2 = draw(st) >> sh2;
+            mask |= (accepted(x1, lo, span) ? 1u : 0u) << i;
+            q[i] = EQ4 ? eq4_pair<false, true>(x1, x2, w, g.Cs, g.Ds, g.y)
+                       : map_pair<false, true>(x1, x2, g.map);
         }
         const uint32_t cnt = __popc(mask);
         uint32_t incl = cnt;
@@ -820,30 +816,21 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
             if (lane >= (uint32_t)o) incl += t;
         }
         const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        // compact: accepted output k of this lane at position incl - cnt + k of the round
+        uint32_t pos = incl - cnt;
+#pragma unroll
+        for (int i = 0; i < kJumpPairs; ++i) {
+            if ((mask >> i) & 1u) {
+                sts_f64(comp + pos * 8u, q[i]);
+                ++pos;
+            }
+        }
         __syncwarp();
-        if (total == 32u * kJumpPairs) {
-            // no rejection this round: the staging tile is already in output order
-#pragma unroll 4
-            for (uint32_t k = 0; k < (uint32_t)kJumpPairs; ++k) {
-                const uint64_t pos = base + k * 32u + lane;
-                if (pos < g.nps) {
-                    double v;
-                    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(stage + jstage_off(k, lane)));
-                    row_out[pos] = v;
-                }
-            }
-        } else {
-            uint64_t pos = base + incl - cnt;
-            for (uint32_t j = 0; j < (uint32_t)kJumpPairs; ++j) {
-                if ((mask >> j) & 1u) {
-                    if (pos < g.nps) {
-                        double v;
-                        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(stage + jstage_off(lane, j)));
-                        row_out[pos] = v;
-                    }
-                    ++pos;
-                }
-            }
+        const uint64_t n = (g.nps - base) < (uint64_t)total ? (g.nps - base) : (uint64_t)total;
+        for (uint32_t j = lane; j < (uint32_t)n; j += 32u) {
+            double v;
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(comp + j * 8u));
+            row_out[base + j] = v;
         }
         __syncwarp();
         S.x = __shfl_sync(0xFFFFFFFFu, st.x, 31);
@@ -853,13 +840,12 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
         base += total;
         // A short remainder (rejections made the last round fall a few outputs short, e.g.
         // ~8 of 1024 at w = 8) is cheaper as a sequential tail on one lane than as a full round.
-        const uint64_t rem = g.nps - base;
+        const uint64_t rem = g.nps > base ? g.nps - base : 0;
         if (rem > 0 && rem <= kJumpTail) {
             if (lane == 0) {
                 Xs128 t = S;
                 for (uint64_t i = 0; i < rem; ++i)
-                    row_out[base + i] =
-                        exact_output<(MODE >= 1), false, false>(t, sh1, sh2, w, lo, span, g);
+                    row_out[base + i] = exact_output<EQ4, false, false>(t, sh1, sh2, w, lo, span, g);
             }
             break;
         }
