@@ -294,7 +294,10 @@ def main():
     # workloads write a 256 MiB scratch buffer between timed steps (an L2 flush) and are timed
     # by per-step events around the step alone.
     l2_flush = 8 * nout < (256 << 20)
+    # (written, then a second buffer read, so the flush's own dirty lines are written back
+    # before the timed step rather than during it)
     scratch = torch.empty(32 << 20, dtype=torch.float64, device="cuda") if l2_flush else None
+    scratch_rd = torch.zeros(32 << 20, dtype=torch.float64, device="cuda") if l2_flush else None
     use_graph = args.graph == "on" or (args.graph == "auto" and world == 1 and not l2_flush and
                                         wa.elapsed_time(wb) / 3 < 0.2)
     graph = None
@@ -326,6 +329,7 @@ def main():
         elif l2_flush:
             for k in range(args.steps):
                 scratch.fill_(float(k))
+                scratch_rd.sum()
                 ev[k][0].record(stream)
                 step()
                 ev[k][1].record(stream)
@@ -455,8 +459,9 @@ def main():
             "config": {"workload": f"{args.workload}: {desc}",
                        "streams_per_gpu": p["n_streams"], "n_per_stream": p["n_per_stream"],
                        "seed": p["seed"], "bytes_written_per_step_per_gpu": 8 * nout,
-                       "l2": ("outputs fit in the 126 MB L2: a 256 MiB buffer is written "
-                              "between timed steps (L2 flush); per-step events time the step"
+                       "l2": ("outputs fit in the 126 MB L2: a 256 MiB buffer is written and "
+                              "another read between timed steps (L2 flush, write-back drained); "
+                              "per-step events time the step"
                               if l2_flush else
                               "inputs none; 8 B/output written, >126 MB L2 per step (no flush)"),
                        "parallelism": f"stream-range shards x{world}",
