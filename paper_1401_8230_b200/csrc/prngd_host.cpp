@@ -205,6 +205,7 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     g.lo = (uint32_t)(p->a0 + 1);
     g.span = (uint32_t)(p->a - p->a0 - 1);
     g.span_fast = g.span - I.clamp;
+    g.pow2w = w < 32 ? (1u << w) : 0u;
     g.map.Cs = Cs;
     g.map.Ds = Ds;
     g.map.y = y;

@@ -27,6 +27,7 @@ struct GenArgs {
     uint32_t sh1, sh2;      // draw widths, x = u >> sh (R4)
     uint32_t lo, span;      // accept iff (x1 - lo) < span  <=>  a0 < x1 < a   (R3)
     uint32_t span_fast;     // span - clamp: speculative band excluding x1 = a - 1 when R11 applies
+    uint32_t pow2w;         // 2^w for w <= 31 (v = x1 * 2^w + x2 in one wide multiply-add), else 0
     MapArgs map;            // mapping of the generic kernels (Eq.(4)/(5)/(6), open interval)
     uint32_t mrg_t1, mrg_t2;        // NEXT-2: reduce-to-width thresholds for bitlen(a), bitlen(b)
     uint32_t mrg_mask1, mrg_mask2;  //         and the width masks

@@ -176,6 +176,15 @@ struct NoConsumer {
     __device__ __forceinline__ void add(double) {}
 };
 
+// Eq.(4) of one pair on the specialised paths: MODE 2/3 compose v = x1:x2 as a register pair
+// (w = 32), MODE 1 as one wide multiply-add x1 * 2^w + x2 (w <= 31).
+template <int MODE, bool IEEE>
+__device__ __forceinline__ double eq4_mode(uint32_t x1, uint32_t x2, const GenArgs &g) {
+    const uint64_t v = (MODE == 2 || MODE == 3) ? (((uint64_t)x1 << 32) | (uint64_t)x2)
+                                                : (uint64_t)x1 * g.pow2w + (uint64_t)x2;
+    return eq4_scaled<IEEE, false>(v, g.Cs, g.Ds, g.y);
+}
+
 // ------------------------------------------------------------------------------ one batch
 // One pair of the exact path: draw until accepted, then Eq.(1)+(4) with the clamp.
 template <bool EQ4, bool IEEE, bool ALG1>
@@ -222,8 +231,7 @@ __device__ __forceinline__ void produce_batch(Xs128 &st, double (&q)[kCols], con
             const uint32_t x1 = draw(st) >> sh1;
             const uint32_t x2 = draw(st) >> sh2;
             rej |= !accepted(x1, lo, span_fast);
-            q[i] = EQ4 ? eq4_pair<IEEE, false>(x1, x2, w, g.Cs, g.Ds, g.y)
-                       : map_pair<IEEE, false>(x1, x2, g.map);
+            q[i] = EQ4 ? eq4_mode<MODE, IEEE>(x1, x2, g) : map_pair<IEEE, false>(x1, x2, g.map);
         }
         if (__builtin_expect(!__any_sync(0xFFFFFFFFu, rej), 1)) return;
         st = saved;
@@ -429,8 +437,11 @@ struct MrgProducer2 {
             asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
                          : "=r"(a1), "=r"(a2)
                          : "r"(ring + (((rd + i) & (kMrgRing - 1)) << 3)));
-            q[i] = EQ4 ? eq4_pair<false, true>(a1, a2, g.w, g.Cs, g.Ds, g.y)
-                       : map_pair<false, true>(a1, a2, g.map);
+            q[i] = EQ4 ? eq4_mode<1, false>(a1, a2, g) : map_pair<false, true>(a1, a2, g.map);
+        }
+        if (EQ4 && g.span != g.span_fast) {  // R11 clamp only where the host found it needed
+#pragma unroll
+            for (int i = 0; i < kCols; ++i) q[i] = fmin(q[i], kBelowOne);
         }
         rd += kCols;
     }
@@ -805,8 +816,11 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
             const uint32_t x1 = draw(st) >> sh1;
             const uint32_t x2 = draw(st) >> sh2;
             mask |= (accepted(x1, lo, span) ? 1u : 0u) << i;
-            q[i] = EQ4 ? eq4_pair<false, true>(x1, x2, w, g.Cs, g.Ds, g.y)
-                       : map_pair<false, true>(x1, x2, g.map);
+            q[i] = EQ4 ? eq4_mode<MODE, false>(x1, x2, g) : map_pair<false, true>(x1, x2, g.map);
+        }
+        if (EQ4 && g.span != g.span_fast) {  // R11 clamp only where the host found it needed
+#pragma unroll
+            for (int i = 0; i < kJumpPairs; ++i) q[i] = fmin(q[i], kBelowOne);
         }
         const uint32_t cnt = __popc(mask);
         uint32_t incl = cnt;
@@ -973,7 +987,6 @@ __device__ __forceinline__ void seg_batch(Xs128 &st, bool &rej, uint32_t my, uin
     constexpr bool FULL32 = MODE == 2;
     constexpr bool EQ4 = MODE >= 1;
     const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
-    const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo;
     const uint32_t span_fast = FULL32 ? 0xFFFFFFFDu : g.span_fast;
     double q[kCols];
@@ -982,8 +995,7 @@ __device__ __forceinline__ void seg_batch(Xs128 &st, bool &rej, uint32_t my, uin
         const uint32_t x1 = draw(st) >> sh1;
         const uint32_t x2 = draw(st) >> sh2;
         rej |= !accepted(x1, lo, span_fast);
-        q[i] = EQ4 ? eq4_pair<IEEE, false>(x1, x2, w, g.Cs, g.Ds, g.y)
-                   : map_pair<IEEE, false>(x1, x2, g.map);
+        q[i] = EQ4 ? eq4_mode<MODE, IEEE>(x1, x2, g) : map_pair<IEEE, false>(x1, x2, g.map);
     }
 #pragma unroll
     for (int c = 0; c < kCols / 2; ++c)
@@ -1391,12 +1403,9 @@ static int kernel_mode(const GenArgs &g) {
     const bool full32 = eq4 && g.w == 32 && g.sh1 == 0 && g.sh2 == 0 && g.lo == 1u &&
                         g.span == 0xFFFFFFFEu && g.span_fast == 0xFFFFFFFDu;
     const bool w32 = eq4 && g.w == 32 && g.sh1 == 0;
-    return full32 ? 2 : (w32 ? 3 : (eq4 ? 1 : 0));
-}
-// the jump / SEG / SEGC kernels are instantiated for modes 0-2 only (3 is a case of 1)
-static int kernel_mode_012(const GenArgs &g) {
-    const int m = kernel_mode(g);
-    return m == 3 ? 1 : m;
+    // MODE 1 composes v with one wide multiply-add and needs w <= 31; w = 32 with a narrower
+    // x1 (rare) takes the generic kernel
+    return full32 ? 2 : (w32 ? 3 : ((eq4 && g.w <= 31) ? 1 : 0));
 }
 
 cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, int) {
@@ -1518,7 +1527,7 @@ cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st) {
     const size_t smem = 1024 + kMrgTileBytes + (size_t)32 * (kMrgRing * 8 + 8);
     const uint64_t grid = (g.n_streams + 31) / 32;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    const bool eq4 = g.map.kind == 4 && g.map.open == 0;
+    const bool eq4 = g.map.kind == 4 && g.map.open == 0 && g.w <= 31;
     auto k = eq4 ? gen_mrg_kernel<true> : gen_mrg_kernel<false>;
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
@@ -1533,18 +1542,20 @@ cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *t
     const uint64_t grid = (g.n_streams + kJumpWarps - 1) / kJumpWarps;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     const uint4 *t = static_cast<const uint4 *>(tables);
-    const int mode = kernel_mode_012(g);
+    const int mode = kernel_mode(g);
     cudaError_t e;
-    if (mode == 2) {
-        if ((e = set_smem(gen_jump_kernel<2>, smem)) != cudaSuccess) return e;
-        gen_jump_kernel<2><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);
-    } else if (mode == 1) {
-        if ((e = set_smem(gen_jump_kernel<1>, smem)) != cudaSuccess) return e;
-        gen_jump_kernel<1><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);
-    } else {
-        if ((e = set_smem(gen_jump_kernel<0>, smem)) != cudaSuccess) return e;
-        gen_jump_kernel<0><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);
+#define PRNGD_JUMP_LAUNCH(M)                                                                    \
+    do {                                                                                        \
+        if ((e = set_smem(gen_jump_kernel<M>, smem)) != cudaSuccess) return e;                  \
+        gen_jump_kernel<M><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);               \
+    } while (0)
+    switch (mode) {
+        case 3: PRNGD_JUMP_LAUNCH(3); break;
+        case 2: PRNGD_JUMP_LAUNCH(2); break;
+        case 1: PRNGD_JUMP_LAUNCH(1); break;
+        default: PRNGD_JUMP_LAUNCH(0); break;
     }
+#undef PRNGD_JUMP_LAUNCH
     return cudaGetLastError();
 }
 
@@ -1565,7 +1576,7 @@ cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *ta
     if ((e = jump_tables_interleaved(kSegDraws, &tables)) != cudaSuccess) return e;
 #endif
     const uint4 *t = static_cast<const uint4 *>(tables);
-    const int mode = kernel_mode_012(g);
+    const int mode = kernel_mode(g);
     // consecutive tasks per CTA (hides all but the first jump); one when the grid is small
 #ifndef PRNGD_SEG_TPC
 #define PRNGD_SEG_TPC 4
@@ -1579,14 +1590,18 @@ cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *ta
         gen_seg_kernel<M, I><<<(unsigned)grid, 32, smem, st>>>(g, t, log2S, n_tasks, tpc);     \
     } while (0)
     if (pl.ieee_div) {
-        if (mode >= 1) PRNGD_SEG_LAUNCH(1, true);
-        else PRNGD_SEG_LAUNCH(0, true);
-    } else if (mode == 2) {
-        PRNGD_SEG_LAUNCH(2, false);
-    } else if (mode == 1) {
-        PRNGD_SEG_LAUNCH(1, false);
+        switch (mode) {
+            case 3: case 2: PRNGD_SEG_LAUNCH(3, true); break;
+            case 1: PRNGD_SEG_LAUNCH(1, true); break;
+            default: PRNGD_SEG_LAUNCH(0, true); break;
+        }
     } else {
-        PRNGD_SEG_LAUNCH(0, false);
+        switch (mode) {
+            case 3: PRNGD_SEG_LAUNCH(3, false); break;
+            case 2: PRNGD_SEG_LAUNCH(2, false); break;
+            case 1: PRNGD_SEG_LAUNCH(1, false); break;
+            default: PRNGD_SEG_LAUNCH(0, false); break;
+        }
     }
 #undef PRNGD_SEG_LAUNCH
     return cudaGetLastError();
@@ -1605,21 +1620,25 @@ cudaError_t launch_generate_segc(const GenArgs &g, const Plan &pl, cudaStream_t 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t grid = n_tasks < (uint64_t)sms ? n_tasks : (uint64_t)sms;  // one CTA per SM
-    const int mode = kernel_mode_012(g);
+    const int mode = kernel_mode(g);
 #define PRNGD_SEGC_LAUNCH(M, I)                                                                 \
     do {                                                                                        \
         if ((e = set_smem(gen_segc_kernel<M, I>, smem)) != cudaSuccess) return e;               \
         gen_segc_kernel<M, I><<<(unsigned)grid, kSegcWarps * 32, smem, st>>>(g, t, n_tasks);   \
     } while (0)
     if (pl.ieee_div) {
-        if (mode >= 1) PRNGD_SEGC_LAUNCH(1, true);
-        else PRNGD_SEGC_LAUNCH(0, true);
-    } else if (mode == 2) {
-        PRNGD_SEGC_LAUNCH(2, false);
-    } else if (mode == 1) {
-        PRNGD_SEGC_LAUNCH(1, false);
+        switch (mode) {
+            case 3: case 2: PRNGD_SEGC_LAUNCH(3, true); break;
+            case 1: PRNGD_SEGC_LAUNCH(1, true); break;
+            default: PRNGD_SEGC_LAUNCH(0, true); break;
+        }
     } else {
-        PRNGD_SEGC_LAUNCH(0, false);
+        switch (mode) {
+            case 3: PRNGD_SEGC_LAUNCH(3, false); break;
+            case 2: PRNGD_SEGC_LAUNCH(2, false); break;
+            case 1: PRNGD_SEGC_LAUNCH(1, false); break;
+            default: PRNGD_SEGC_LAUNCH(0, false); break;
+        }
     }
 #undef PRNGD_SEGC_LAUNCH
     return cudaGetLastError();
