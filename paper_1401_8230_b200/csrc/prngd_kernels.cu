@@ -374,8 +374,8 @@ constexpr uint32_t kMrgRing = PRNGD_MRG_RING;  // pairs per lane (power of two, 
 #endif
 template <int FP> struct MrgWord { using T = uint32_t; };
 template <> struct MrgWord<1> { using T = double; };
-template <bool EQ4>
-struct MrgProducer2 {
+template <bool EQ4, bool SAMEW>
+struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold and mask)
     using T1 = typename MrgWord<PRNGD_MRG_FP64 >= 1 ? 1 : 0>::T;  // component 1 word
     using T2 = typename MrgWord<PRNGD_MRG_FP64 >= 2 ? 1 : 0>::T;  // component 2 word
     T1 A, B, C;                 // component 1, oldest..newest (rotating roles)
@@ -407,12 +407,12 @@ struct MrgProducer2 {
     }
     __device__ __forceinline__ void take(uint32_t u, const GenArgs &g) {
         const uint32_t x = u - 1u;
-        const bool v = x < (have1 ? g.mrg_t2 : g.mrg_t1);       // R23 reduce-to-width
+        const bool v = x < (SAMEW ? g.mrg_t1 : (have1 ? g.mrg_t2 : g.mrg_t1));  // R23
         const bool push = v && have1 && accepted(x1, g.lo, g.span);  // pair complete
         if (push) {
             const uint32_t a = ring + ((wr & (kMrgRing - 1)) << 3);
             asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x1),
-                         "r"(x & g.mrg_mask2)
+                         "r"(x & (SAMEW ? g.mrg_mask1 : g.mrg_mask2))
                          : "memory");
         }
         wr += push ? 1u : 0u;
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
 #endif
 constexpr int kMrgCols = PRNGD_MRG_RC;
 constexpr size_t kMrgTileBytes = (size_t)32 * (kMrgCols * 8 + 16);
-template <bool EQ4>
+template <bool EQ4, bool SAMEW>
 __global__ void __launch_bounds__(32) gen_mrg_kernel(const GenArgs g) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t lane = threadIdx.x & 31u;
@@ -738,7 +738,7 @@ __global__ void __launch_bounds__(32) gen_mrg_kernel(const GenArgs g) {
     NoConsumer nc;
     const uint32_t base = aligned_smem_base(smem_raw);
     // ring rows padded by 8 bytes: lanes at equal ring positions land on different banks
-    MrgProducer2<EQ4> prod(g, g.stream_begin + row0 + lane,
+    MrgProducer2<EQ4, SAMEW> prod(g, g.stream_begin + row0 + lane,
                            base + (uint32_t)kMrgTileBytes + lane * (kMrgRing * 8u + 8u));
     run_rows_burst<false, kMrgCols>(g, base, lane, row0, prod, nc);
 }
@@ -1528,7 +1528,9 @@ cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st) {
     const uint64_t grid = (g.n_streams + 31) / 32;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     const bool eq4 = g.map.kind == 4 && g.map.open == 0 && g.w <= 31;
-    auto k = eq4 ? gen_mrg_kernel<true> : gen_mrg_kernel<false>;
+    const bool samew = g.mrg_t1 == g.mrg_t2 && g.mrg_mask1 == g.mrg_mask2;
+    auto k = eq4 ? (samew ? gen_mrg_kernel<true, true> : gen_mrg_kernel<true, false>)
+                 : (samew ? gen_mrg_kernel<false, true> : gen_mrg_kernel<false, false>);
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
     k<<<(unsigned)grid, 32, smem, st>>>(g);
