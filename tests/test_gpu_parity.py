@@ -421,7 +421,8 @@ def test_jump_general_ranges(orc):
 
 @pytest.mark.parametrize("par", [dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1),
                                  dict(w=31, a0=0, a=2**31 - 1, b0=0, b=2**31 - 1),
-                                 dict(w=16, a0=3, a=40000, b0=0, b=2**12 - 1)])
+                                 dict(w=16, a0=3, a=40000, b0=0, b=2**12 - 1),
+                                 dict(w=32, a0=0, a=2**31 - 1, b0=0, b=2**31 - 1)])
 @pytest.mark.parametrize("kind", [4, 5])
 def test_mrg32k3a_bitwise(orc, par, kind):
     p = dict(par, seed=11, n_streams=300, n_per_stream=130,
