@@ -179,7 +179,8 @@ def cpu_baseline(p: dict, target_s: float = 12.0) -> dict:
     try:
         import threading
         cores = max(1, len(os.sched_getaffinity(0)))
-        per = max(256, ns // 4 // 256 * 256)   # ~a quarter of the 1-core sample per thread
+        # half the 1-core sample in total (bounded host memory), split over the cores
+        per = max(256, ns // (2 * cores) // 256 * 256)
         per = min(per, max(1, p["n_streams"] // cores))
         outs = [None] * cores
 
