@@ -50,6 +50,8 @@ def parse():
                     help="consume workloads: fused histogram/moments only, outputs not stored")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flags", type=int, default=0, help="extra prngd flags")
+    ap.add_argument("--reduce", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1 statistics exchange: peer-memory atomics in the kernel, or NCCL")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay each step from a CUDA graph (auto: steps under 0.2 ms, N=1)")
     ap.add_argument("--streams", type=int, default=0,
@@ -274,9 +276,18 @@ def main():
     if not torch.cuda.is_available():
         print(json.dumps({"error": "no CUDA device"}))
         return 1
+    # Test hooks for exercising the N > 1 code path on a one-GPU box (timings meaningless):
+    # PRNGD_BENCH_SAME_GPU=1 puts every rank on cuda:0, PRNGD_BENCH_BACKEND=gloo avoids NCCL's
+    # one-rank-per-GPU rule.  The driver's multi-GPU runs use neither.
+    if os.environ.get("PRNGD_BENCH_SAME_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("PRNGD_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     p = workload_params(args.workload, rank, world)
     if args.streams:
@@ -294,9 +305,29 @@ def main():
         hist = torch.zeros(65536, dtype=torch.int64, device="cuda")
         pw = torch.zeros(4, dtype=torch.float64, device="cuda")
         cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    # The statistics exchange (N > 1): by default rank 0's accumulator is mapped into every rank
+    # (CUDA IPC, peer memory over NVLink) and each rank's finalize kernel adds into it with device
+    # atomics -- fused into the library's own launches; NCCL all-reduce is the fallback.
+    peer, reduce_mode = None, None
+    if consume and world > 1:
+        reduce_mode = "nccl"
+        if args.reduce == "p2p":
+            try:
+                peer = D.PeerStats()
+                peer.zero(stream)
+                torch.cuda.synchronize()
+                reduce_mode = "p2p"
+            except Exception as e:  # every rank sees the same broadcast error
+                reduce_mode = f"nccl (peer memory unavailable: {e})"
+                peer = None
+            dist.barrier()
 
     def step(st=stream):
-        if consume:
+        if consume and peer is not None:
+            # accumulates over steps into rank 0's peer-mapped buffer (no per-step collective)
+            P.prngd_generate_consume(g.handle, None if args.no_write else out, peer.hist,
+                                     peer.pow, peer.count, st)
+        elif consume:
             hist.zero_(), pw.zero_(), cnt.zero_()
             P.prngd_generate_consume(g.handle, None if args.no_write else out, hist, pw, cnt, st)
             if world > 1:  # the path's only exchange: NCCL all-reduce of the statistics
@@ -497,6 +528,7 @@ def main():
                        "parallelism": f"stream-range shards x{world}",
                        "flags": p["flags"], "store": args.store,
                        "cuda_graph": graph is not None,
+                       "stats_reduce": reduce_mode,
                        "write_outputs": not (consume and args.no_write)},
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -507,6 +539,13 @@ def main():
             "pct_hbm_write_roofline": 100.0 * achieved / peak if roof["bound"] == "hbm" else None,
         }
         print(json.dumps(line), flush=True)
+    if peer is not None:  # the owner frees only after every other rank unmapped
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank != 0:
+            peer.close()
+        dist.barrier()
+        peer.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -166,8 +166,12 @@ PRNGD_API prngd_status prngd_generate(const prngd_handle *h, double *d_out, void
  *   d_hist[bin] += #{outputs with (uint32)(z' * 65536.0) == bin}    (65536 int64, R16)
  *   d_pow[p-1] += sum z'^p, p = 1..4                                  (4 doubles)
  *   d_count[0] += number of outputs                                  (1 int64)
- * All three accumulate, so shards may add into one buffer.  d_hist, d_pow, d_count: device,
- * 8-byte aligned, required.  Two kernel launches (generate+bin, then slab reduction). */
+ * All three accumulate with device atomics, so shards -- including other processes on other
+ * GPUs that mapped the same buffer with prngd_ipc_open (peer memory over NVLink) -- may add
+ * into one buffer concurrently: the statistics reduction then happens inside this call's own
+ * kernels.  d_hist, d_pow, d_count: device (local or peer-mapped), 8-byte aligned, required.
+ * Three kernel launches (generate + bin, the exact pass that returns at once unless a 16-bit
+ * counter wrapped, slab reduction); two with PRNGD_FLAG_EXACT_HIST. */
 PRNGD_API prngd_status prngd_generate_consume(const prngd_handle *h, double *d_out, int64_t *d_hist,
                                     double *d_pow, int64_t *d_count, void *cuda_stream);
 
@@ -213,6 +217,23 @@ PRNGD_API prngd_status prngd_debug_jump(uint64_t n_draws, const uint32_t *in, ui
  * (x1, x2) from a counter-based hash of (seed, i), i < n.  Validation of R10 on the GPU. */
 PRNGD_API prngd_status prngd_debug_div_check(const prngd_handle *h, uint64_t n, uint64_t seed,
                                    unsigned long long *d_mismatch, void *cuda_stream);
+
+/* ---- Peer-memory plumbing for the multi-GPU statistics reduction (SURVEY 8(e), NEXT-4 over
+ * NVLink peer memory instead of multicast).  One process allocates the accumulator
+ * (prngd_peer_alloc: zeroed device memory of this process's current device), exports it
+ * (prngd_ipc_export: PRNGD_IPC_HANDLE_BYTES opaque bytes, to be sent to the other processes of
+ * the node by any means), and every other process maps it (prngd_ipc_open) and passes the
+ * mapped pointers to prngd_generate_consume.  prngd_copy / prngd_zero are stream-ordered
+ * device copies / zero-fills of such raw allocations.  All return PRNGD_ECUDA with the CUDA
+ * error in prngd_last_error() when the runtime refuses (e.g. no peer access). */
+#define PRNGD_IPC_HANDLE_BYTES 64
+PRNGD_API prngd_status prngd_peer_alloc(uint64_t bytes, void **d_ptr);
+PRNGD_API prngd_status prngd_peer_free(void *d_ptr);
+PRNGD_API prngd_status prngd_ipc_export(void *d_ptr, void *handle_out);
+PRNGD_API prngd_status prngd_ipc_open(const void *handle, void **d_ptr);
+PRNGD_API prngd_status prngd_ipc_close(void *d_ptr);
+PRNGD_API prngd_status prngd_copy(void *dst, const void *src, uint64_t bytes, void *cuda_stream);
+PRNGD_API prngd_status prngd_zero(void *d_ptr, uint64_t bytes, void *cuda_stream);
 
 #ifdef __cplusplus
 }

@@ -542,4 +542,60 @@ prngd_status prngd_debug_div_check(const prngd_handle *h, uint64_t n, uint64_t s
     return PRNGD_OK;
 }
 
+prngd_status prngd_peer_alloc(uint64_t bytes, void **d_ptr) {
+    if (!d_ptr || bytes == 0) return fail(PRNGD_EINVAL, "null pointer or zero size");
+    *d_ptr = nullptr;
+    cudaError_t e = cudaMalloc(d_ptr, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(PRNGD_ENOMEM, "peer accumulator (%llu bytes): %s", (unsigned long long)bytes,
+                    cudaGetErrorString(e));
+    }
+    if ((e = cudaMemset(*d_ptr, 0, bytes)) != cudaSuccess) return cuda_fail(e, "cudaMemset");
+    return PRNGD_OK;
+}
+
+prngd_status prngd_peer_free(void *d_ptr) {
+    if (!d_ptr) return PRNGD_OK;
+    cudaError_t e = cudaFree(d_ptr);
+    return e == cudaSuccess ? PRNGD_OK : cuda_fail(e, "cudaFree");
+}
+
+prngd_status prngd_ipc_export(void *d_ptr, void *handle_out) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == PRNGD_IPC_HANDLE_BYTES, "IPC handle size");
+    if (!d_ptr || !handle_out) return fail(PRNGD_EINVAL, "null argument");
+    cudaIpcMemHandle_t hnd;
+    cudaError_t e = cudaIpcGetMemHandle(&hnd, d_ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    std::memcpy(handle_out, &hnd, sizeof(hnd));
+    return PRNGD_OK;
+}
+
+prngd_status prngd_ipc_open(const void *handle, void **d_ptr) {
+    if (!handle || !d_ptr) return fail(PRNGD_EINVAL, "null argument");
+    cudaIpcMemHandle_t hnd;
+    std::memcpy(&hnd, handle, sizeof(hnd));
+    *d_ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(d_ptr, hnd, cudaIpcMemLazyEnablePeerAccess);
+    return e == cudaSuccess ? PRNGD_OK : cuda_fail(e, "cudaIpcOpenMemHandle");
+}
+
+prngd_status prngd_ipc_close(void *d_ptr) {
+    if (!d_ptr) return PRNGD_OK;
+    cudaError_t e = cudaIpcCloseMemHandle(d_ptr);
+    return e == cudaSuccess ? PRNGD_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
+prngd_status prngd_copy(void *dst, const void *src, uint64_t bytes, void *cuda_stream) {
+    if ((!dst || !src) && bytes) return fail(PRNGD_EINVAL, "null pointer");
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)cuda_stream);
+    return e == cudaSuccess ? PRNGD_OK : cuda_fail(e, "cudaMemcpyAsync");
+}
+
+prngd_status prngd_zero(void *d_ptr, uint64_t bytes, void *cuda_stream) {
+    if (!d_ptr && bytes) return fail(PRNGD_EINVAL, "null pointer");
+    cudaError_t e = cudaMemsetAsync(d_ptr, 0, bytes, (cudaStream_t)cuda_stream);
+    return e == cudaSuccess ? PRNGD_OK : cuda_fail(e, "cudaMemsetAsync");
+}
+
 }  // extern "C"

@@ -703,8 +703,11 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
         hi += spill[2 * wi + 1];
         spill[2 * wi] = 0;
         spill[2 * wi + 1] = 0;
-        d_hist[2 * wi] += lo;
-        d_hist[2 * wi + 1] += hi;
+        // device atomics: the accumulators may be shared by several shards, also by processes
+        // on other GPUs through peer memory (prngd_ipc_open) -- the statistics reduction
+        unsigned long long *h = reinterpret_cast<unsigned long long *>(d_hist);
+        if (lo) atomicAdd(&h[2 * wi], (unsigned long long)lo);
+        if (hi) atomicAdd(&h[2 * wi + 1], (unsigned long long)hi);
         local += lo + hi;
     }
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(~0u, local, o);
@@ -718,7 +721,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
     if (blockIdx.x == 0 && threadIdx.x < 4) {
         double acc = 0.0;
         for (int s = 0; s < n_slabs; ++s) acc = __dadd_rn(acc, pow_slab[s * 4 + threadIdx.x]);
-        d_pow[threadIdx.x] = __dadd_rn(d_pow[threadIdx.x], acc);
+        atomicAdd(&d_pow[threadIdx.x], acc);
     }
 }
 

@@ -5,7 +5,15 @@ stream-id ranges with NO communication on the generation path: rank r of R gener
 streams [stream_begin_r, stream_begin_r + n_r) into its own HBM; its outputs are the contiguous
 slice [stream_begin_r * n_per_stream, ...) of the logical global array.  The only exchange is
 the all-reduce of the fused consumer's statistics (65536-bin int64 histogram, 4 FP64 power sums,
-int64 count), done with torch.distributed (NCCL over NVLink on B200, gloo in the CPU tests).
+int64 count).  Two ways:
+
+* PeerStats (default for the fused consumer): rank 0's accumulator is mapped into every rank with
+  CUDA IPC (peer memory over NVLink); each rank's prngd_generate_consume adds its partial sums into
+  it with device atomics inside its own finalize kernel -- the collective is fused into the
+  library's kernels, no separate launch (NEXT-4 over peer memory; NVLS multicast is unavailable
+  in this environment).
+* allreduce_stats: torch.distributed all-reduce after the kernel (NCCL over NVLink on B200, gloo
+  in the CPU tests) -- the baseline and the fallback.
 """
 from __future__ import annotations
 
@@ -60,6 +68,70 @@ def allreduce_stats(hist, pw, count, group=None, deterministic: bool = False):
     else:
         dist.all_reduce(pw, group=group)
     return hist, pw, count
+
+
+class PeerStats:
+    """Rank `owner`'s statistics accumulator (65536 int64 bins, 1 int64 count, 4 FP64 power
+    sums) mapped into every rank of `group` through CUDA IPC, so prngd_generate_consume on any
+    rank adds into it directly (device atomics in the library's finalize kernel).
+
+    Usage: ps = PeerStats(group); ps.zero(); barrier; every rank:
+    P.prngd_generate_consume(h, out, ps.hist, ps.pow, ps.count, stream); cuda sync; barrier;
+    on the owner ps.read().  Needs peer access between the ranks' GPUs (NVLink / NVSwitch) or
+    ranks on one GPU; raises otherwise (callers fall back to allreduce_stats)."""
+
+    NBINS = 65536
+    NBYTES = (65536 + 1 + 4) * 8
+
+    def __init__(self, group=None, owner: int = 0):
+        import torch.distributed as dist
+        from . import prngd as P
+        self.P = P
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.owner = owner
+        self.base = None
+        err = None
+        handle = None
+        if self.rank == owner:
+            try:
+                self.base = P.prngd_peer_alloc(self.NBYTES)
+                handle = P.prngd_ipc_export(self.base)
+            except Exception as e:  # reported to every rank below
+                err = str(e)
+        objs = [(handle, err)]
+        if dist.is_initialized():
+            dist.broadcast_object_list(objs, src=owner, group=group)
+        handle, err = objs[0]
+        if err is not None:
+            raise RuntimeError(f"peer accumulator unavailable: {err}")
+        if self.rank != owner:
+            self.base = P.prngd_ipc_open(handle)
+        self.hist = self.base
+        self.count = self.base + self.NBINS * 8
+        self.pow = self.base + (self.NBINS + 1) * 8
+
+    def zero(self, stream=None):
+        """Owner only: zero the accumulator (stream-ordered)."""
+        if self.rank == self.owner:
+            self.P.prngd_zero(self.base, self.NBYTES, stream)
+
+    def read(self):
+        """Owner only: (hist int64[65536], pow float64[4], count int64[1]) torch copies."""
+        import torch
+        buf = torch.empty(self.NBYTES // 8, dtype=torch.int64, device="cuda")
+        self.P.prngd_copy(buf, self.base, self.NBYTES, None)
+        torch.cuda.current_stream().synchronize()
+        return buf[:self.NBINS], buf[self.NBINS + 1:].view(torch.float64), buf[self.NBINS:self.NBINS + 1]
+
+    def close(self):
+        if self.base is None:
+            return
+        if self.rank == self.owner:
+            self.P.prngd_peer_free(self.base)
+        else:
+            self.P.prngd_ipc_close(self.base)
+        self.base = None
 
 
 def generate_sharded(p: dict, mode: str = STRONG, consume: bool = False, write: bool = True,

@@ -44,6 +44,8 @@ EXPORTS = (
     "prngd_generate_host", "prngd_last_launches", "prngd_status_string", "prngd_last_error",
     "prngd_abi_version", "prngd_debug_raw", "prngd_debug_pairs", "prngd_debug_map",
     "prngd_debug_div_check", "prngd_debug_jump",
+    "prngd_peer_alloc", "prngd_peer_free", "prngd_ipc_export", "prngd_ipc_open",
+    "prngd_ipc_close", "prngd_copy", "prngd_zero",
 )
 
 
@@ -95,6 +97,13 @@ def lib():
             "prngd_debug_map": (st, [vp, vp, vp, vp, u64, vp]),
             "prngd_debug_div_check": (st, [vp, u64, u64, vp, vp]),
             "prngd_debug_jump": (st, [u64, vp, vp, C.c_int]),
+            "prngd_peer_alloc": (st, [u64, C.POINTER(vp)]),
+            "prngd_peer_free": (st, [vp]),
+            "prngd_ipc_export": (st, [vp, vp]),
+            "prngd_ipc_open": (st, [vp, C.POINTER(vp)]),
+            "prngd_ipc_close": (st, [vp]),
+            "prngd_copy": (st, [vp, vp, u64, vp]),
+            "prngd_zero": (st, [vp, u64, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -111,9 +120,11 @@ def _check(status: int, what: str):
 
 
 def _ptr(t):
-    """Device/host pointer of a torch tensor or numpy array (None -> NULL)."""
+    """Device/host pointer of a torch tensor or numpy array (None -> NULL, int -> itself)."""
     if t is None:
         return None
+    if isinstance(t, int):
+        return t
     if hasattr(t, "data_ptr"):
         return t.data_ptr()
     return t.ctypes.data
@@ -184,6 +195,45 @@ def prngd_debug_map(h: int, x1, x2, z, stream=None):
 def prngd_debug_div_check(h: int, n: int, seed: int, mismatch, stream=None):
     _check(lib().prngd_debug_div_check(h, n, seed, _ptr(mismatch), _stream_ptr(stream)),
            "prngd_debug_div_check")
+
+
+IPC_HANDLE_BYTES = 64
+
+
+def prngd_peer_alloc(nbytes: int) -> int:
+    """Zeroed device allocation of the current device (raw pointer) for peer sharing."""
+    p = C.c_void_p()
+    _check(lib().prngd_peer_alloc(nbytes, C.byref(p)), "prngd_peer_alloc")
+    return p.value
+
+
+def prngd_peer_free(ptr: int):
+    _check(lib().prngd_peer_free(ptr), "prngd_peer_free")
+
+
+def prngd_ipc_export(ptr: int) -> bytes:
+    buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+    _check(lib().prngd_ipc_export(ptr, buf), "prngd_ipc_export")
+    return buf.raw
+
+
+def prngd_ipc_open(handle: bytes) -> int:
+    buf = C.create_string_buffer(bytes(handle), IPC_HANDLE_BYTES)
+    p = C.c_void_p()
+    _check(lib().prngd_ipc_open(buf, C.byref(p)), "prngd_ipc_open")
+    return p.value
+
+
+def prngd_ipc_close(ptr: int):
+    _check(lib().prngd_ipc_close(ptr), "prngd_ipc_close")
+
+
+def prngd_copy(dst, src, nbytes: int, stream=None):
+    _check(lib().prngd_copy(_ptr(dst), _ptr(src), nbytes, _stream_ptr(stream)), "prngd_copy")
+
+
+def prngd_zero(ptr, nbytes: int, stream=None):
+    _check(lib().prngd_zero(_ptr(ptr), nbytes, _stream_ptr(stream)), "prngd_zero")
 
 
 def prngd_debug_jump(n_draws: int, state, lane_table: int = -1):

@@ -1,0 +1,82 @@
+"""Multi-process statistics reduction through peer memory (dist.PeerStats): rank 0's accumulator
+is mapped into the other ranks with CUDA IPC and every rank's prngd_generate_consume adds its
+shard's histogram / power sums / count into it with device atomics (the collective fused into the
+library's finalize kernel).  Run here as 2-3 processes on ONE GPU (IPC works between processes on
+one device); the kernels never wait on one another -- the ranks synchronise on the host (gloo
+barriers) -- so sharing the GPU is safe.  Compared with the oracle over the whole stream range."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, p, calls, queue):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1401_8230_b200 import dist as D
+        from paper_1401_8230_b200 import prngd as P
+        q = D.shard_params(p, rank, world, D.STRONG)
+        g = P.Generator(**q)
+        ps = D.PeerStats()
+        ps.zero()
+        torch.cuda.synchronize()
+        dist.barrier()
+        out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+        for _ in range(calls):  # the accumulator sums over calls as well as ranks
+            P.prngd_generate_consume(g.handle, out, ps.hist, ps.pow, ps.count,
+                                     torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:
+            hist, pw, cnt = ps.read()
+            queue.put((hist.cpu().numpy(), pw.cpu().numpy(), int(cnt.item()),
+                       out[:2].cpu().numpy()))
+        dist.barrier()
+        if rank != 0:
+            ps.close()
+        dist.barrier()
+        if rank == 0:
+            ps.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,calls,name", [(2, 1, "cfg1"), (3, 2, "cfg2")])
+def test_peer_memory_statistics_reduction(orc, world, calls, name):
+    import torch.multiprocessing as mp
+    from paper_1401_8230_b200 import workloads as W
+    p = W.config(name, n_streams=3000, n_per_stream=520)
+    ctx = mp.get_context("spawn")
+    queue = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, p, calls, queue))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = queue.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=300)
+        assert pr.exitcode == 0
+    hist, pw, cnt, head = res
+    ref = orc.generate(p, want_stats=True)
+    assert cnt == calls * ref["count"]
+    assert np.array_equal(hist, calls * ref["hist"])
+    assert np.allclose(pw, calls * ref["pow"], rtol=1e-12, atol=0)
+    assert np.array_equal(head.view(np.int64), ref["out"][:2].view(np.int64))  # rank 0's rows
