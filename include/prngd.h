@@ -24,7 +24,10 @@
  *     the host buffer is complete.  Kernel faults surface at the caller's next synchronisation.
  *   - No call throws or aborts; errors are returned as prngd_status, with a detail string in
  *     prngd_last_error() (thread-local).  A handle is immutable after prngd_create, so several
- *     threads may use one handle concurrently on different streams / buffers.
+ *     threads may use one handle concurrently on different streams / buffers -- with one
+ *     exception: prngd_generate_consume reduces through per-handle device scratch (per-SM
+ *     histogram slabs, carry array, overflow flag), so its calls on ONE handle must be ordered
+ *     on one stream; concurrent consumers use separate handles.
  */
 #ifndef PRNGD_H
 #define PRNGD_H
