@@ -618,7 +618,10 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     uint32_t it = 0;
     const uint64_t n_tasks = (g.n_streams + 31u) / 32u;
 #pragma unroll 1
-    for (uint64_t t = (uint64_t)blockIdx.x * kWarps + warp; t < n_tasks;
+    // task t = blockIdx.x + gridDim.x * (warp + kWarps * k): the tasks in flight at any time
+    // are one contiguous block (as with CTA-major order), and a small config's few tasks land
+    // on different SMs instead of filling the first CTA's warps
+    for (uint64_t t = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * warp; t < n_tasks;
          t += (uint64_t)gridDim.x * kWarps) {
         if constexpr (WRITE && ST == Store::ROW) {
             XsProducer<MODE, SPEC, IEEE, ALG1> prod(g, g.stream_begin + t * 32u + lane);
@@ -660,7 +663,7 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
         // outputs this CTA counted: live rows of its tasks x nps
         unsigned long long expect = 0;
         if (lane == 0)
-            for (uint64_t t = (uint64_t)blockIdx.x * kWarps + warp; t < n_tasks;
+            for (uint64_t t = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * warp; t < n_tasks;
                  t += (uint64_t)gridDim.x * kWarps) {
                 const uint64_t left = g.n_streams - t * 32u;
                 expect += (left < 32u ? left : 32u) * g.nps;
@@ -1480,9 +1483,8 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
     g.overflow = reinterpret_cast<uint32_t *>(sp + (size_t)num_sms * kHistWords * 4u +
                                               65536u * 8u + (size_t)num_sms * 4u * 8u);
     const uint64_t tasks = (g.n_streams + 31u) / 32u;
-    const int kw = kConsWarpsRow;  // grid sizing: the smallest CTA bounds the task count
-    int grid = num_sms;
-    if ((uint64_t)grid * kw > tasks) grid = (int)((tasks + kw - 1) / kw);
+    int grid = num_sms;  // persistent, one CTA per SM; every CTA gets a task when tasks >= grid
+    if ((uint64_t)grid > tasks) grid = (int)tasks;
     if (grid < 1) grid = 1;
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
