@@ -1,7 +1,10 @@
 """Instruction mix per output from an ncu SASS source export: python tools/sass_mix.py file outputs"""
 import collections
 import csv
+import signal
 import sys
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)  # quiet when piped into head
 
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[1]
