@@ -486,23 +486,61 @@ def main():
     # -------------------------------------------------- end to end through the C ABI, host buffer
     e2e = None
     if args.e2e_steps > 0 and not consume:
-        host = torch.empty((p["n_streams"], p["n_per_stream"]), dtype=torch.float64,
-                           pin_memory=True)
-        P.prngd_generate_host(g.handle, host, stream)  # warm-up (allocates staging)
+        # prngd_generate_host into pinned host memory.  The sample is bounded at 2^17 streams
+        # (1 GiB at cfg3's row length) per rank so N ranks do not pin N x 8 GiB of host memory;
+        # the call is PCIe-bound, so the rate does not depend on the sample size.
+        ns_e = min(p["n_streams"], 1 << 17)
+        ge = P.Generator(**dict(p, n_streams=ns_e))
+        ne = ns_e * p["n_per_stream"]
+        host = torch.empty((ns_e, p["n_per_stream"]), dtype=torch.float64, pin_memory=True)
+        P.prngd_generate_host(ge.handle, host, stream)  # warm-up (allocates staging)
         if world > 1:
             dist.barrier()
         te = time.perf_counter()
         for _ in range(args.e2e_steps):
-            P.prngd_generate_host(g.handle, host, stream)
+            P.prngd_generate_host(ge.handle, host, stream)
         torch.cuda.synchronize()
         de = torch.tensor([time.perf_counter() - te], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(de, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * nout * args.e2e_steps / de.item() / 1e9, "unit": "Gdoubles/s",
-               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * nout,
-               "note": "prngd_generate_host: chunked generate + pinned D2H, overlapped; inputs "
-                       "are the parameter struct only"}
+        e2e = {"value": world * ne * args.e2e_steps / de.item() / 1e9, "unit": "Gdoubles/s",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * ne,
+               "note": f"prngd_generate_host: chunked generate + pinned D2H, overlapped; inputs "
+                       f"are the parameter struct only; {ns_e} streams x {p['n_per_stream']} "
+                       f"per rank per step"}
         del host
+        ge.close()
+    elif args.e2e_steps > 0 and consume:
+        # The consumer's result is its statistics: every step generates (and writes, unless
+        # --no-write) on the device, reduces, and reads the histogram + power sums + count back
+        # into pinned host memory (the step's "metric").
+        hh = torch.empty(65536, dtype=torch.int64, pin_memory=True)
+        hp = torch.empty(4, dtype=torch.float64, pin_memory=True)
+        hc = torch.empty(1, dtype=torch.int64, pin_memory=True)
+        step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        te = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            step()
+            if peer is not None:
+                if rank == 0:
+                    P.prngd_copy(hh, peer.hist, 65536 * 8, stream)
+                    P.prngd_copy(hp, peer.pow, 32, stream)
+                    P.prngd_copy(hc, peer.count, 8, stream)
+            else:
+                hh.copy_(hist, non_blocking=True)
+                hp.copy_(pw, non_blocking=True)
+                hc.copy_(cnt, non_blocking=True)
+            torch.cuda.synchronize()
+        de = torch.tensor([time.perf_counter() - te], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(de, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * nout * args.e2e_steps / de.item() / 1e9, "unit": "Gdoubles/s",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 65536 * 8 + 32 + 8,
+               "note": "prngd_generate_consume per step + D2H of the statistics (histogram, power "
+                       "sums, count) into pinned host memory, synchronised every step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
