@@ -179,3 +179,15 @@ def test_seg_generate_host_matches_device(orc, path):
     host = torch.empty(g.shape, dtype=torch.float64, pin_memory=True)
     P.prngd_generate_host(g.handle, host, torch.cuda.current_stream())
     assert_same(host, out)
+
+
+def test_seg_multi_task_ctas_with_prefetched_jumps(orc):
+    """Bulk SEG launches give each one-warp CTA 4 consecutive tasks and prefetch the next task's
+    jump during the current one (n_tasks >= 148 * 12 * 16).  nps = 256 (S = 2, 16 rows per task),
+    w = 20 (rejections -> exact rewrites inside multi-task CTAs), ragged last CTA; bitwise."""
+    ns = 148 * 12 * 16 * 16 + 37
+    p = dict(full(20), seed=13, stream_begin=5, n_streams=ns, n_per_stream=256)
+    _, out = run(p)
+    ref = orc.generate(p, want_consumed=True)
+    assert (ref["consumed"] > 256).sum() > 50
+    assert_same(out, ref["out"])
