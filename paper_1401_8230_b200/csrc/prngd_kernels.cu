@@ -24,7 +24,12 @@
 
 namespace prngd {
 
-constexpr int kCols = 16;                   // outputs per lane per batch (128 B of its row)
+#ifndef PRNGD_KCOLS
+#define PRNGD_KCOLS 16
+#endif
+// outputs per lane per batch (128 B of its row); must divide every row-tile width (the fused
+// consumer's is 16).  A/B on cfg3 (ROW, 200 steps): 8 -> 780-782, 16 -> 787, 32 -> 777-779.
+constexpr int kCols = PRNGD_KCOLS;
 constexpr int kTileBytes = 32 * kCols * 8;  // 4 KiB per warp tile
 constexpr int kNBufTma = 2;                 // tiles per warp when the TMA stores them (async)
 
