@@ -763,7 +763,10 @@ __global__ void __launch_bounds__(32) gen_mrg_kernel(const GenArgs g) {
 // coalesced stores.  Lane 31's final state starts the next round; a short remainder is finished
 // by one lane sequentially.
 constexpr int kJumpPairs = (int)(kJumpDraws / 2);
-constexpr uint64_t kJumpTail = 24;  // remainders up to this many outputs finish on one lane
+#ifndef PRNGD_JUMP_TAIL
+#define PRNGD_JUMP_TAIL 24
+#endif
+constexpr uint64_t kJumpTail = PRNGD_JUMP_TAIL;  // remainders up to this many finish on one lane
 #ifndef PRNGD_JUMP_WARPS
 #define PRNGD_JUMP_WARPS 4
 #endif
@@ -813,13 +816,33 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
     const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
     const uint32_t comp = aligned_smem_base(smem_raw) + warp * (32u * kJumpPairs * 8u);
-    const uint4 *my_tab = tabs + (size_t)lane * 16 * 256;
     double *row_out = g.out + row * g.nps;
     Xs128 S = stream_start(g.seed, g.stream_begin + row);
     uint64_t base = 0;
 #pragma unroll 1
     while (base < g.nps) {
-        Xs128 st = lane ? jump_state(my_tab, S) : S;
+#ifndef PRNGD_JUMP_NOJUMP_EXPERIMENT
+        // every lane jumps the same round-start state: with the lane index innermost in the
+        // byte tables ([b][v][lane]) each of the 16 loads reads one contiguous 512-byte run
+        Xs128 st = S;
+        if (lane) {
+            const uint32_t words[4] = {S.x, S.y, S.z, S.w};
+            uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const uint32_t v = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+                const uint4 t = __ldg(&tabs[((uint32_t)k * 256u + v) * 32u + lane]);
+                r0 ^= t.x;
+                r1 ^= t.y;
+                r2 ^= t.z;
+                r3 ^= t.w;
+            }
+            st = Xs128{r0, r1, r2, r3};
+        }
+#else
+        Xs128 st = S;
+        st.x ^= lane;  // A/B timing experiment only: wrong bits
+#endif
         double q[kJumpPairs];
         uint32_t mask = 0;
 #pragma unroll
@@ -1550,6 +1573,9 @@ cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st) {
 cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *tables,
                                  cudaStream_t st) {
     (void)pl;
+    (void)tables;  // the kernel reads the lane-interleaved layout of the same matrices
+    cudaError_t e0 = jump_tables_interleaved(kJumpDraws, &tables);
+    if (e0 != cudaSuccess) return e0;
     const size_t smem = 1024 + (size_t)kJumpWarps * 32 * kJumpPairs * 8;
     const uint64_t grid = (g.n_streams + kJumpWarps - 1) / kJumpWarps;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
