@@ -284,3 +284,59 @@ extern "C" __attribute__((visibility("default"))) int wc_smem_hist(uint32_t iter
         iters, red, (unsigned long long *)sink);
     return (int)cudaGetLastError();
 }
+
+// Distributed-shared-memory histogram adds: a cluster of C CTAs (one per SM) splits the 65536
+// packed bins, CTA c owning bins [c*65536/C, (c+1)*65536/C) in (65536/C)/2 words; every thread
+// adds to random bins wherever they live (red.shared::cluster into the owner's shared memory).
+// Measures whether a cluster-split histogram can free shared memory at the consumer's rate.
+__global__ void dsmem_hist_rate(uint32_t iters, unsigned long long *sink) {
+    extern __shared__ uint32_t h[];
+    uint32_t csize, crank;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    const uint32_t words = 32768u / csize;
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) h[i] = 0;
+    asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    uint32_t x = 0x9E3779B9u * (blockIdx.x * blockDim.x + threadIdx.x + 1);
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(h);
+    for (uint32_t k = 0; k < iters; ++k) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            x ^= x << 13; x ^= x >> 17; x ^= x << 5;
+            const uint32_t b = x >> 16;
+            const uint32_t inc = __funnelshift_l(1u, 1u, b << 4);
+            const uint32_t w = b >> 1;
+            const uint32_t owner = w / words, off = (w - owner * words) * 4u;
+            uint32_t ra;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base + off), "r"(owner));
+            asm volatile("red.shared::cluster.add.u32 [%0], %1;" ::"r"(ra), "r"(inc) : "memory");
+        }
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (x == 0xFFFFFFFFu) sink[0] = x;
+}
+
+extern "C" __attribute__((visibility("default"))) int wc_dsmem_hist(uint32_t iters, int csize,
+                                                                    int warps, void *stream,
+                                                                    void *sink) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = 131072 / csize;
+    cudaFuncSetAttribute(dsmem_hist_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(dsmem_hist_rate, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(sms / csize * csize));
+    cfg.blockDim = dim3(warps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, dsmem_hist_rate, iters, (unsigned long long *)sink);
+    return (int)cudaGetLastError();
+}
