@@ -205,6 +205,22 @@ def cpu_baseline(p: dict, target_s: float = 12.0) -> dict:
     return res
 
 
+def device_facts(torch) -> dict:
+    """SURVEY Appendix B facts confirmed on the box the bench ran on."""
+    try:
+        pr = torch.cuda.get_device_properties(torch.cuda.current_device())
+        d = {"name": pr.name, "sm_count": pr.multi_processor_count,
+             "cc": f"{pr.major}.{pr.minor}", "hbm_gib": round(pr.total_memory / 2**30, 1)}
+        for k in ("L2_cache_size", "shared_memory_per_multiprocessor",
+                  "shared_memory_per_block_optin", "regs_per_multiprocessor",
+                  "max_threads_per_multi_processor"):
+            if hasattr(pr, k):
+                d[k] = getattr(pr, k)
+        return d
+    except Exception as e:  # informational only
+        return {"error": str(e)}
+
+
 def write_ceiling(out, stream, torch) -> dict:
     import ctypes
     try:
@@ -572,6 +588,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
+            "device": device_facts(torch),
             "gpu_launches": launches_per_step * args.steps,
             "per_step": step_stats,
             "pct_hbm_write_roofline": 100.0 * achieved / peak if roof["bound"] == "hbm" else None,
