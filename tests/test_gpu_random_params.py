@@ -67,3 +67,31 @@ def test_random_parameter_sets_bitwise(orc, i):
         assert np.array_equal(hist.cpu().numpy(), ref["hist"]), f"case {i}: histogram"
         assert cnt.item() == ref["count"]
         assert np.allclose(pw.cpu().numpy(), ref["pow"], rtol=1e-12, atol=0)
+
+
+def _mrg_case(i):
+    rng = np.random.default_rng(5000 + i)
+    w = int(rng.integers(1, 33))
+    wb = int(rng.integers(1, min(w, 31) + 1))
+    b = (1 << wb) - 1
+    wa = int(rng.integers(2, 32))
+    a = int(rng.integers(max(2, 1 << (wa - 1)), (1 << wa)))
+    lo = max(0, a - 1 - int(rng.integers(max(2, (1 << wa) // 64), (1 << wa) + 1)))
+    a0 = int(rng.integers(lo, a - 1)) if a - 1 > lo else max(0, a - 2)
+    kind = 5 if rng.random() < 0.3 else 4
+    p = dict(w=w, a0=a0, a=a, b0=0, b=b, seed=int(rng.integers(0, 2**63)), stream_begin=int(i * 977),
+             n_streams=int(rng.integers(1, 200)), n_per_stream=2 * int(rng.integers(1, 300)),
+             mrg=True)
+    return p, P.PRNGD_FLAG_MRG32K3A | P.MAP_FLAGS[kind], kind
+
+
+@pytest.mark.parametrize("i", range(16))
+def test_random_parameter_sets_mrg32k3a_bitwise(orc, i):
+    p, flags, kind = _mrg_case(i)
+    g = P.Generator(**dict(p, flags=flags))
+    out = g.generate()
+    torch.cuda.synchronize()
+    ref = orc.generate(p, kind=kind)["out"]
+    got = out.cpu().numpy().view(np.int64).ravel()
+    bad = np.nonzero(got != ref.view(np.int64).ravel())[0]
+    assert bad.size == 0, f"case {i} {p}: {bad.size} mismatches, first {bad[:5]}"
