@@ -328,14 +328,32 @@ def main():
     if consume and world > 1:
         reduce_mode = "nccl"
         if args.reduce == "p2p":
+            err = None
             try:
                 peer = D.PeerStats()
                 peer.zero(stream)
                 torch.cuda.synchronize()
+                if os.environ.get("PRNGD_BENCH_FAIL_PEER_RANK") == str(rank):  # test hook
+                    raise RuntimeError("simulated peer-mapping failure")
+            except Exception as e:  # e.g. no peer access to rank 0's GPU
+                err, peer = str(e), None
+            # every rank must take the same path: p2p only if it worked everywhere
+            ok = torch.tensor([0 if err else 1], dtype=torch.int32, device="cuda")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() == 1:
                 reduce_mode = "p2p"
-            except Exception as e:  # every rank sees the same broadcast error
-                reduce_mode = f"nccl (peer memory unavailable: {e})"
-                peer = None
+            else:
+                if peer is not None:
+                    torch.cuda.synchronize()
+                    if rank != 0:
+                        peer.close()
+                    dist.barrier()
+                    if rank == 0:
+                        peer.close()
+                    peer = None
+                else:
+                    dist.barrier()
+                reduce_mode = "nccl (peer memory unavailable" + (f": {err})" if err else " on a rank)")
             dist.barrier()
 
     def step(st=stream):
