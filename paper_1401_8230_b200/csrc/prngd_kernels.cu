@@ -1,15 +1,20 @@
 // prngd_kernels.cu -- sm_100a kernels of the PRNGD hot path.
 //
-// Work decomposition: one warp owns 32 consecutive streams (rows of the [n_streams][nps]
-// output), one stream per lane; the xorshift128 state lives in 4 registers for the whole
-// stream.  A lane produces its stream's outputs in batches of kCols = 16 doubles (128 bytes,
-// one full cache line of its row).  The warp stages a 32 x 16 double tile in shared memory
-// (128B-swizzled so the per-lane 16-byte writes are bank-conflict-free) and writes it out
-// either with one TMA tensor store (cp.async.bulk.tensor.2d; the hardware clips the ragged
-// row/column tails) or with warp-coalesced 16-byte st.global (8 lanes per 128-byte row).
-// Rejection is handled per lane; with rare rejection (w = 32) the batch is computed
-// speculatively and recomputed exactly if any lane of the warp drew a rejected x1, so the
-// common path has no per-output branch.
+// Kernels (all bit-identical to the oracle; which one a call launches: prngd_get_info):
+//   gen_kernel        S1-S6, one lane per stream (the xorshift128 state in 4 registers for the
+//                     whole stream), batches of kCols = 16 outputs computed speculatively (a warp
+//                     vote replays a batch exactly when a lane drew a rejected x1 or the R11
+//                     clamp row); store paths: ROW (default: 32 x 64-output tiles in padded shared
+//                     memory, each row written as one 512-byte burst), and the A/B paths TMA, TILE,
+//                     DIRECT, ROW1K
+//   gen_seg_kernel    SEG: several lanes per stream via GF(2) jump-ahead, 1 KiB row segments
+//   gen_segc_kernel   SEGC: column-block CTAs via jump-ahead (A/B)
+//   gen_jump_kernel   NEXT-3: one warp per stream for few-stream configs
+//   gen_mrg_kernel    NEXT-2: MRG32k3a base generator in exact binary64
+//   consume_kernel    S1-S7: the fused 2^16-bin histogram + power sums (optimistic packed
+//                     shared-memory counters) with optional ROW stores; + its exact fallback pass
+//   finalize_kernel   slab reduction into the caller's (local or peer-mapped) accumulators
+//   debug_*           validation hooks of include/prngd.h
 #include <cuda.h>
 #include <cuda_runtime.h>
 
