@@ -161,8 +161,9 @@ PRNGD_API prngd_status prngd_destroy(prngd_handle *h);
 PRNGD_API prngd_status prngd_get_info(const prngd_handle *h, prngd_info *info);
 
 /* S1-S6: d_out[i * n_per_stream + j] = output j of global stream stream_begin + i.
- * d_out: device, >= n_streams * n_per_stream doubles, 8-byte aligned (16-byte aligned and an
- * even n_per_stream enable the TMA tensor-store path).  One kernel launch. */
+ * d_out: device, >= n_streams * n_per_stream doubles, 8-byte aligned (a 16-byte aligned output
+ * and an even n_per_stream enable the row-burst store paths; see the store flags above).  One
+ * kernel launch; prngd_get_info reports which kernel and store path. */
 PRNGD_API prngd_status prngd_generate(const prngd_handle *h, double *d_out, void *cuda_stream);
 
 /* S1-S7: as prngd_generate (outputs written only if d_out != NULL), plus the fused consumer:
