@@ -457,7 +457,18 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
     }
 };
 
-template <bool CONSUME, int RC, class Prod, class Cons>
+// BULK (A/B): full tiles leave through the copy engine instead of LDS + STG: every lane issues
+// one cp.async.bulk of its own 512-byte row segment (shared -> global) and waits for the copy's
+// shared-memory reads before it overwrites the row.
+#ifndef PRNGD_ROW_BULK
+#define PRNGD_ROW_BULK 0
+#endif
+__device__ __forceinline__ void bulk_s2g(double *dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(src), "r"(bytes)
+                 : "memory");
+}
+template <bool CONSUME, int RC, class Prod, class Cons, bool BULK = false>
 __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, uint32_t lane,
                                                uint64_t row0, Prod &prod, Cons &cons) {
     constexpr uint32_t CPR = RC / 2;  // 16-byte chunks per row segment
@@ -474,6 +485,7 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
         for (uint32_t b = 0; b < RC / kCols; ++b) {
             double q[kCols];
             prod(q, g);
+            if (BULK && b == 0) bulk_wait_read<0>();  // the previous tile's copy read the row
             if (CONSUME && live) {
                 const uint64_t base = col0 + b * kCols;
                 if (base + kCols <= g.nps) {
@@ -491,7 +503,15 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
                 sts_v2(my_row + (chunk << 4), q[2 * c], q[2 * c + 1]);
             }
         }
+        if (BULK && col0 + RC <= g.nps) {
+            // each lane: its own row segment, written by itself, to its own row of the output
+            fence_proxy_async_smem();
+            if (live) bulk_s2g(g.out + (row0 + lane) * g.nps + col0, my_row, RC * 8u);
+            bulk_commit();
+            continue;
+        }
         __syncwarp();
+        if (BULK) bulk_wait_read<0>();
         if (nrows == 32u && col0 + RC <= g.nps) {
             // full tile: unconditional stores, pointer stepped by rows (the common case)
             constexpr uint32_t RPI = CPR >= 32 ? 1u : 32u / CPR;   // rows per instruction
@@ -543,6 +563,7 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
         }
         __syncwarp();
     }
+    if (BULK) bulk_wait_all();
 }
 
 __device__ __forceinline__ uint32_t aligned_smem_base(uint8_t *raw) {
@@ -560,8 +581,9 @@ __global__ void __launch_bounds__(gen_warps<ST>() * 32)
     if constexpr (is_row<ST>()) {
         NoConsumer nc;
         XsProducer<MODE, SPEC, IEEE, ALG1> prod(g, g.stream_begin + row0 + lane);
-        run_rows_burst<false, row_cols<ST>()>(g, aligned_smem_base(smem_raw), lane, row0, prod,
-                                              nc);
+        run_rows_burst<false, row_cols<ST>(), decltype(prod), NoConsumer,
+                       (PRNGD_ROW_BULK != 0 && ST == Store::ROW)>(g, aligned_smem_base(smem_raw),
+                                                                  lane, row0, prod, nc);
     } else if constexpr (ST == Store::TMA) {
         // CTA-level staging: the 4 warps fill one 128-row x 16-column slab (16 KiB, two slots)
         // and thread 0 writes it with ONE tensor store per batch.  Warps past n_streams keep
