@@ -50,6 +50,9 @@ def parse():
                     help="consume workloads: fused histogram/moments only, outputs not stored")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flags", type=int, default=0, help="extra prngd flags")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank its own per-GPU shard (default); strong: one global "
+                         "stream space split over the ranks")
     ap.add_argument("--reduce", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1 statistics exchange: peer-memory atomics in the kernel, or NCCL")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
@@ -67,8 +70,15 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def workload_params(name: str, rank: int, world: int) -> dict:
+def workload_params(name: str, rank: int, world: int, scaling: str = "weak") -> dict:
     from paper_1401_8230_b200 import dist as D
+    if scaling == "strong":
+        # a fixed global stream space split over the ranks (cfg5's 2^23 global
+        # streams; at N = 1 that is 2^34 outputs, so use it with --no-write)
+        p = W.config(name)
+        if name == "cfg5":
+            p["n_streams"] = 1 << 23
+        return D.shard_params(p, rank, world, D.STRONG)
     # per-GPU shard of the global stream space: rank r owns [r*n, (r+1)*n) (weak scaling)
     return D.shard_params(W.config(name), rank, world, D.WEAK)
 
@@ -305,7 +315,7 @@ def main():
         else:
             dist.init_process_group(backend)
 
-    p = workload_params(args.workload, rank, world)
+    p = workload_params(args.workload, rank, world, args.scaling)
     if args.streams:
         p["stream_begin"] = rank * args.streams
         p["n_streams"] = args.streams
@@ -439,7 +449,8 @@ def main():
            else [a.elapsed_time(b) for a, b in ev])
     step_stats = {"step_ms_median": statistics.median(per), "step_ms_best": min(per),
                   "value_at_median": world * nout / (statistics.median(per) * 1e-3) / 1e9,
-                  "value_at_best": world * nout / (min(per) * 1e-3) / 1e9}
+                  "value_at_best": world * nout / (min(per) * 1e-3) / 1e9,
+                  "note": "this rank's per-step events (x N ranks)"}
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -451,7 +462,12 @@ def main():
             tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms = tt.item()
-    value = world * nout / (ms * 1e-3) / 1e9
+    total_out = world * nout
+    if world > 1:  # strong sharding gives ranks slightly different counts
+        tt = torch.tensor([nout], dtype=torch.int64, device="cuda")
+        dist.all_reduce(tt)
+        total_out = int(tt.item())
+    value = total_out / (ms * 1e-3) / 1e9
 
     # -------------------------------------------------- roofline of the dominant kernel
     # For write workloads the step is exactly one generate launch; its average duration is
@@ -587,7 +603,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "Gdoubles/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"{args.workload}: {desc}",
                        "streams_per_gpu": p["n_streams"], "n_per_stream": p["n_per_stream"],
