@@ -303,9 +303,21 @@ static Plan plan_for(const prngd_handle *h, const void *out, bool consume) {
     // kernel for few-stream generate calls (cfg1: 76 vs 64 Gd/s); for bulk shapes ROW stays
     // ahead (cfg3: 790 vs 645 Gd/s: the per-segment jump costs more than the store pattern
     // gains).
-    const uint64_t S = nps / prngd::kSegOut;
-    const bool seg_ok = !pl.mrg && pl.spec && !pl.alg1 && a16 && nps % prngd::kSegOut == 0 &&
-                        S >= 1 && S <= 32 && (S & (S - 1)) == 0;
+    // segment length: 128 outputs (1 KiB, the measured best store pattern) unless the grid
+    // would not fill one wave of resident warps (148 SMs x 12), then the shortest of 64 / 32
+    // that the row length allows (more lanes per row, a shorter serial chain per lane)
+    auto seg_fits = [&](uint64_t so) {
+        const uint64_t S = nps / so;
+        return nps % so == 0 && S >= 1 && S <= 32 && (S & (S - 1)) == 0;
+    };
+    pl.seg_out = 0;
+    for (uint64_t so : {128ull, 64ull, 32ull}) {
+        if (!seg_fits(so)) continue;
+        pl.seg_out = (uint32_t)so;
+        const uint64_t warps = h->p.n_streams * (nps / so) / 32u;
+        if (warps >= 148ull * 12) break;
+    }
+    const bool seg_ok = !pl.mrg && pl.spec && !pl.alg1 && a16 && pl.seg_out != 0;
     if (pl.store == Store::SEG && !seg_ok) pl.store = Store::ROW;
     // SEGC: the same conditions with 8 column blocks of a multiple of 64 outputs each
     const bool segc_ok = !pl.mrg && pl.spec && !pl.alg1 && a16 && nps % 512 == 0;

@@ -60,6 +60,7 @@ struct Plan {
     bool mrg;       // NEXT-2 MRG32k3a base generator
     bool store_auto;  // PRNGD_FLAG_STORE_AUTO: the library picks the store path / kernel
     bool exact_hist;  // PRNGD_FLAG_EXACT_HIST: carry-tracking histogram adds from the start
+    uint32_t seg_out; // SEG: outputs per lane segment (128, or 64 / 32 for few-stream shapes)
     Store store;
 };
 

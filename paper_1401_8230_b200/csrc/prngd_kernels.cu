@@ -954,7 +954,7 @@ constexpr uint32_t kSegRS = kSegHalf * 8u + 16u;  // padded tile row stride (byt
 #endif
 
 
-template <int MODE, bool IEEE>
+template <int MODE, bool IEEE, int SO>
 __device__ __forceinline__ void seg_exact(const GenArgs &g, Xs128 st, uint32_t j, uint32_t S,
                                           uint64_t row, bool live) {
     constexpr bool FULL32 = MODE == 2;
@@ -966,7 +966,7 @@ __device__ __forceinline__ void seg_exact(const GenArgs &g, Xs128 st, uint32_t j
     // pass 1: accepted pairs among this lane's kSegOut pairs
     uint32_t cnt = 0;
 #pragma unroll 1
-    for (uint32_t i = 0; i < kSegOut; ++i) {
+    for (uint32_t i = 0; i < (uint32_t)SO; ++i) {
         const uint32_t x1 = draw(st) >> sh1;
         draw(st);
         cnt += accepted(x1, lo, span) ? 1u : 0u;
@@ -983,7 +983,7 @@ __device__ __forceinline__ void seg_exact(const GenArgs &g, Xs128 st, uint32_t j
     uint32_t pos = incl - cnt;
     double *row_out = g.out + row * g.nps;
 #pragma unroll 1
-    for (uint32_t i = 0; i < kSegOut; ++i) {
+    for (uint32_t i = 0; i < (uint32_t)SO; ++i) {
         const uint32_t x1 = draw(st) >> sh1;
         const uint32_t x2 = draw(st) >> sh2;
         if (accepted(x1, lo, span)) {
@@ -1070,15 +1070,19 @@ __device__ __forceinline__ void seg_batch(Xs128 &st, bool &rej, uint32_t my, uin
 // of a lane's NEXT task is issued before the current task's first batch and folded in after
 // it, so its 16 table loads (L2 latency) overlap generation; only the CTA's first jump is
 // exposed.  The 64 registers the loads occupy are free at this occupancy.
-template <int MODE, bool IEEE>
+// SO = outputs per lane segment (128 = 1 KiB; 64 / 32 for few-stream shapes, which gives more
+// lanes per row and a shorter serial chain per lane).  F = outputs per flush.
+template <int MODE, bool IEEE, int SO>
 __global__ void __launch_bounds__(32, 12)
     gen_seg_kernel(const GenArgs g, const uint4 *__restrict__ tabs, uint32_t log2S,
                    uint64_t n_tasks, uint32_t tpc) {
     const uint64_t t_end0 = ((uint64_t)blockIdx.x + 1) * tpc;
     const uint64_t t_end = t_end0 < n_tasks ? t_end0 : n_tasks;
     extern __shared__ uint8_t smem_raw[];
-    constexpr uint32_t kBatchesPerFlush = kSegHalf / kCols;
-    constexpr uint32_t kBatches = kSegOut / kCols;
+    constexpr uint32_t F = SO < kSegHalf ? SO : kSegHalf;
+    constexpr uint32_t RS = F * 8u + 16u;  // padded tile row stride
+    constexpr uint32_t kBatchesPerFlush = F / kCols;
+    constexpr uint32_t kBatches = SO / kCols;
     const uint32_t lane = threadIdx.x;
     const uint32_t S = 1u << log2S;            // lanes (segments) per row
     const uint32_t j = lane & (S - 1u);        // this lane's segment
@@ -1090,7 +1094,7 @@ __global__ void __launch_bounds__(32, 12)
     const uint4 *my_tab = tabs + (size_t)j * 16 * 256;  // byte tables, 64 KiB per lane matrix
 #endif
     const uint32_t tile = aligned_smem_base(smem_raw);
-    const uint32_t my = tile + lane * kSegRS;  // this lane's tile row
+    const uint32_t my = tile + lane * RS;  // this lane's tile row
     uint64_t t = (uint64_t)blockIdx.x * tpc;
     Xs128 st = stream_start(g.seed, g.stream_begin + t * rows_per_warp + rloc);
     st = seg_jump(tabs, my_tab, j, log2S, st);
@@ -1139,17 +1143,21 @@ __global__ void __launch_bounds__(32, 12)
 #pragma unroll 1
         for (uint32_t k = 1; k <= kBatches; ++k) {
             if (k % kBatchesPerFlush == 0) {
-                // flush: tile row r -> 512 contiguous bytes at (row0 + r / S) * nps +
-                // (r % S) * 128 + h * 64 = row0 * nps + r * 128 + h * 64 (nps = 128 S): the
-                // task is one contiguous 32 KiB block, lane segments 1 KiB apart.
+                // flush: tile row r (segment r of the task) -> F outputs at (row0 + r / S) * nps
+                // + (r % S) * SO + h * F = row0 * nps + r * SO + h * F (nps = SO * S): the task
+                // is one contiguous block, lane segments SO outputs apart.  One instruction
+                // writes 64 outputs (512 B): 64 / F tile rows, lane l at element 2 l of them.
                 const uint32_t h = k / kBatchesPerFlush - 1;
                 __syncwarp();
-                double *base = g.out + row0 * g.nps + h * kSegHalf + 2 * lane;
+                double *base = g.out + row0 * g.nps + h * F;
+                const uint32_t ninstr = nchunks * F / 64u;
 #pragma unroll 4
-                for (uint32_t r = 0; r < nchunks; ++r) {
+                for (uint32_t i = 0; i < ninstr; ++i) {
+                    const uint32_t e = i * 64u + 2u * lane;  // element of the flushed block
+                    const uint32_t r = e / F, c = (e % F) / 2u;
                     double a, b2;
-                    lds_v2(tile + r * kSegRS + (lane << 4), a, b2);
-                    stg_v2_cs(base + r * kSegOut, a, b2);
+                    lds_v2(tile + r * RS + (c << 4), a, b2);
+                    stg_v2_cs(base + (uint64_t)r * SO + (e % F), a, b2);
                 }
                 __syncwarp();
             }
@@ -1157,7 +1165,7 @@ __global__ void __launch_bounds__(32, 12)
         }
         if (__builtin_expect(__any_sync(0xFFFFFFFFu, rej), 0)) {
             __syncwarp();  // the speculative stores above are ordered before the exact rewrite
-            seg_exact<MODE, IEEE>(g, seg0, j, S, row, live);
+            seg_exact<MODE, IEEE, SO>(g, seg0, j, S, row, live);
         }
         st = nxt;
     }
@@ -1626,19 +1634,22 @@ cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *t
 
 cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *tables,
                                 cudaStream_t st) {
-    const uint64_t S = g.nps / kSegOut;  // host checked: nps = 128 * S, S a power of two <= 32
+    const uint32_t SO = pl.seg_out ? pl.seg_out : (uint32_t)kSegOut;
+    const uint64_t S = g.nps / SO;  // host checked: nps = SO * S, S a power of two <= 32
     uint32_t log2S = 0;
     while ((1ull << log2S) < S) ++log2S;
     const uint64_t rows_per_warp = 32u >> log2S;
     const uint64_t n_tasks = (g.n_streams + rows_per_warp - 1) / rows_per_warp;
-    const size_t smem = 1024 + (size_t)32 * kSegRS;
+    const uint32_t F = SO < (uint32_t)kSegHalf ? SO : (uint32_t)kSegHalf;
+    const size_t smem = 1024 + (size_t)32 * (F * 8 + 16);
     cudaError_t e;
+    (void)tables;
 #if PRNGD_SEG_JUMP == 1 || PRNGD_SEG_JUMP == 2
-    (void)tables;
-    if ((e = jump_tables_nibble(kSegDraws, &tables)) != cudaSuccess) return e;
+    if ((e = jump_tables_nibble(2 * SO, &tables)) != cudaSuccess) return e;
 #elif PRNGD_SEG_JUMP == 4
-    (void)tables;
-    if ((e = jump_tables_interleaved(kSegDraws, &tables)) != cudaSuccess) return e;
+    if ((e = jump_tables_interleaved(2 * SO, &tables)) != cudaSuccess) return e;
+#else
+    if ((e = jump_tables(2 * SO, &tables)) != cudaSuccess) return e;
 #endif
     const uint4 *t = static_cast<const uint4 *>(tables);
     const int mode = kernel_mode(g);
@@ -1649,10 +1660,16 @@ cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *ta
     const uint32_t tpc = n_tasks >= 148ull * 12 * 16 ? PRNGD_SEG_TPC : 1u;
     const uint64_t grid = (n_tasks + tpc - 1) / tpc;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+#define PRNGD_SEG_LAUNCH3(M, I, SOV)                                                            \
+    do {                                                                                        \
+        if ((e = set_smem(gen_seg_kernel<M, I, SOV>, smem)) != cudaSuccess) return e;           \
+        gen_seg_kernel<M, I, SOV><<<(unsigned)grid, 32, smem, st>>>(g, t, log2S, n_tasks, tpc); \
+    } while (0)
 #define PRNGD_SEG_LAUNCH(M, I)                                                                  \
     do {                                                                                        \
-        if ((e = set_smem(gen_seg_kernel<M, I>, smem)) != cudaSuccess) return e;                \
-        gen_seg_kernel<M, I><<<(unsigned)grid, 32, smem, st>>>(g, t, log2S, n_tasks, tpc);     \
+        if (SO == 32) PRNGD_SEG_LAUNCH3(M, I, 32);                                              \
+        else if (SO == 64) PRNGD_SEG_LAUNCH3(M, I, 64);                                         \
+        else PRNGD_SEG_LAUNCH3(M, I, 128);                                                      \
     } while (0)
     if (pl.ieee_div) {
         switch (mode) {
@@ -1669,6 +1686,7 @@ cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *ta
         }
     }
 #undef PRNGD_SEG_LAUNCH
+#undef PRNGD_SEG_LAUNCH3
     return cudaGetLastError();
 }
 
