@@ -319,7 +319,7 @@ def main():
     if args.streams:
         p["stream_begin"] = rank * args.streams
         p["n_streams"] = args.streams
-    p["flags"] = args.flags | P.STORE_FLAGS[args.store]
+    p["flags"] = args.flags | P.STORE_FLAGS[args.store] | p.get("map_flags", 0)
     if p.get("mrg"):
         p["flags"] |= P.PRNGD_FLAG_MRG32K3A
     consume = args.workload == "cfg5" or args.consume

@@ -195,6 +195,37 @@ __device__ __forceinline__ double eq4_mode(uint32_t x1, uint32_t x2, const GenAr
     return eq4_scaled<IEEE, false>(v, g.Cs, g.Ds, g.y);
 }
 
+// Kernel MODE >= 16: the mapping fixed at compile time (NEXT-1 on the bulk path): MODE = 16 +
+// 4 K + 2 OPEN + W32, K = 0 Eq.(4) (with the open interval; the closed form is MODE 1-3),
+// 1 Eq.(5), 2 Eq.(6).  The same operations, in the same order, as map_pair's runtime choice.
+constexpr int kModeStatic = 16;
+template <int MODE>
+constexpr bool mode_static() { return MODE >= kModeStatic; }
+template <int MODE, bool IEEE, bool CLAMP>
+__device__ __forceinline__ double map_static(uint32_t x1, uint32_t x2, const GenArgs &g) {
+    constexpr int K = (MODE - kModeStatic) >> 2;
+    constexpr bool OPEN = ((MODE - kModeStatic) >> 1) & 1;
+    constexpr bool W32 = (MODE - kModeStatic) & 1;
+    const MapArgs &m = g.map;
+    const uint32_t xs = x1 - m.sub;
+    const uint64_t v = W32 ? (((uint64_t)xs << 32) | (uint64_t)x2)
+                           : (uint64_t)xs * g.pow2w + (uint64_t)x2;
+    double n = __dsub_rn(__ull2double_rn(v), m.Cs);
+    if (K == 2) n = __dmul_rn(n, m.scale);
+    double q;
+    if (IEEE) {
+        q = __ddiv_rn(n, m.Ds);
+    } else {
+        const double q0 = __dmul_rn(n, m.y);
+        const double r = __fma_rn(-q0, m.Ds, n);
+        q = __fma_rn(r, m.y, q0);
+    }
+    if (K == 1) q = __dmul_rn(q, m.scale);
+    if (CLAMP) q = fmin(q, kBelowOne);
+    if (OPEN) q = __dsub_rn(1.0, q);
+    return q;
+}
+
 // ------------------------------------------------------------------------------ one batch
 // One pair of the exact path: draw until accepted, then Eq.(1)+(4) with the clamp.
 template <bool EQ4, bool IEEE, bool ALG1>
@@ -222,7 +253,7 @@ __device__ __forceinline__ void produce_batch(Xs128 &st, double (&q)[kCols], con
     // w = 32 and 32-bit x1 draws (v = x1:x2 is a register pair), runtime x2 width and accept
     // band (cfg4); MODE 1: Eq.(4) with runtime ranges; MODE 0: any mapping (runtime-uniform).
     constexpr bool FULL32 = MODE == 2;
-    constexpr bool EQ4 = MODE >= 1;
+    constexpr bool EQ4 = MODE >= 1 && MODE <= 3;
     const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1;
     const uint32_t sh2 = FULL32 ? 0u : g.sh2;
     const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
@@ -241,7 +272,9 @@ __device__ __forceinline__ void produce_batch(Xs128 &st, double (&q)[kCols], con
             const uint32_t x1 = draw(st) >> sh1;
             const uint32_t x2 = draw(st) >> sh2;
             rej |= !accepted(x1, lo, span_fast);
-            q[i] = EQ4 ? eq4_mode<MODE, IEEE>(x1, x2, g) : map_pair<IEEE, false>(x1, x2, g.map);
+            q[i] = EQ4 ? eq4_mode<MODE, IEEE>(x1, x2, g)
+                       : mode_static<MODE>() ? map_static<MODE, IEEE, false>(x1, x2, g)
+                                             : map_pair<IEEE, false>(x1, x2, g.map);
         }
         if (__builtin_expect(!__any_sync(0xFFFFFFFFu, rej), 1)) return;
         st = saved;
@@ -645,7 +678,7 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     const uint32_t tiles = base + kHistWords * 4u + warp * (NB * kTileBytes);
     for (uint32_t i = threadIdx.x; i < kHistWords; i += blockDim.x) hist[i] = 0u;
     __syncthreads();
-    ConsumerT<RED, (MODE >= 1)> cons;
+    ConsumerT<RED, (MODE >= 1 && MODE <= 3)> cons;
     cons.init(hist, g.hist_spill);
     uint32_t it = 0;
     const uint64_t n_tasks = (g.n_streams + 31u) / 32u;
@@ -1449,8 +1482,24 @@ static cudaError_t gen_launch(const CUtensorMap &m, const GenArgs &g, cudaStream
 }
 
 template <Store ST>
+static cudaError_t gen_dispatch_static(const CUtensorMap &m, const GenArgs &g, int mode,
+                                       cudaStream_t st) {
+    switch (mode - kModeStatic) {
+#define PRNGD_STATIC(C) case C: return gen_launch<kModeStatic + C, true, false, false, ST>(m, g, st);
+        PRNGD_STATIC(2) PRNGD_STATIC(3) PRNGD_STATIC(4) PRNGD_STATIC(5) PRNGD_STATIC(6)
+        PRNGD_STATIC(7) PRNGD_STATIC(8) PRNGD_STATIC(9) PRNGD_STATIC(10) PRNGD_STATIC(11)
+#undef PRNGD_STATIC
+        default: return gen_launch<0, true, false, false, ST>(m, g, st);
+    }
+}
+
+template <Store ST>
 static cudaError_t gen_dispatch_store(const CUtensorMap &m, const GenArgs &g, const Plan &pl,
                                       int mode, cudaStream_t st) {
+    if constexpr (ST == Store::ROW) {
+        if (mode >= kModeStatic && pl.spec && !pl.ieee_div && !pl.alg1)
+            return gen_dispatch_static<ST>(m, g, mode, st);
+    }
     if (pl.spec && !pl.ieee_div && !pl.alg1) {
         if (mode == 2) return gen_launch<2, true, false, false, ST>(m, g, st);
         if (mode == 3) return gen_launch<3, true, false, false, ST>(m, g, st);
@@ -1474,7 +1523,14 @@ static int kernel_mode(const GenArgs &g) {
     const bool w32 = eq4 && g.w == 32 && g.sh1 == 0;
     // MODE 1 composes v with one wide multiply-add and needs w <= 31; w = 32 with a narrower
     // x1 (rare) takes the generic kernel
-    return full32 ? 2 : (w32 ? 3 : ((eq4 && g.w <= 31) ? 1 : 0));
+    if (full32) return 2;
+    if (w32) return 3;
+    if (eq4) return g.w <= 31 ? 1 : 0;
+    // the other mappings: compile-time mapping on the bulk ROW path (w = 32 needs sh1 = 0 for
+    // the register-pair composition of x1 - sub)
+    const int k = g.map.kind == 5 ? 1 : (g.map.kind == 6 ? 2 : 0);
+    if (g.w == 32 && g.sh1 != 0) return 0;
+    return kModeStatic + 4 * k + 2 * (g.map.open ? 1 : 0) + (g.w == 32 ? 1 : 0);
 }
 
 cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, int) {

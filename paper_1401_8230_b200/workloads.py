@@ -24,6 +24,14 @@ CONFIGS = {
     "cfg4": dict(ASYM, seed=SEED, stream_begin=0, n_streams=2**20, n_per_stream=4096),
     "cfg5": dict(FULL32, seed=SEED, stream_begin=0, n_streams=2**20, n_per_stream=2048),
     # NEXT-2 (not a BASELINE config): cfg3's shape on the MRG32k3a base generator, 26-bit draws
+    # NEXT-1 (not BASELINE configs): cfg3's shape with the other mappings.  `map` / `open` are
+    # the oracle's parameters, `map_flags` the same choice as include/prngd.h flag bits.
+    "eq5": dict(FULL32, seed=SEED, stream_begin=0, n_streams=2**20, n_per_stream=1024, map=5,
+                map_flags=1 << 6),
+    "eq6": dict(FULL32, seed=SEED, stream_begin=0, n_streams=2**20, n_per_stream=1024, map=6,
+                map_flags=2 << 6),
+    "open4": dict(FULL32, seed=SEED, stream_begin=0, n_streams=2**20, n_per_stream=1024,
+                  open=True, map_flags=0x100),
     "mrg26": dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1, seed=SEED, stream_begin=0,
                   n_streams=2**20, n_per_stream=1024, mrg=True),
 }
@@ -35,6 +43,9 @@ DESCRIPTIONS = {
     "cfg4": "x1 in [1,2^32-1], x2 in [0,2^31-1], k=2^-32, 2^20 x 4096, write + histogram",
     "cfg5": "w=32 full range, 2^23 global streams, 2^20 x 2048 per GPU, write + hist + moments",
     "mrg26": "NEXT-2: MRG32k3a base generator, w=26 full range, 2^20 streams x 1024",
+    "eq5": "NEXT-1: Eq.(5) discrete-grid normalisation, cfg3 shape",
+    "eq6": "NEXT-1: Eq.(6) unit-interval form, cfg3 shape",
+    "open4": "NEXT-1: open interval 1 - z' of Eq.(4), cfg3 shape",
 }
 
 

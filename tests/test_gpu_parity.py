@@ -347,6 +347,23 @@ def test_mappings_bitwise(orc, name, kind, open_):
         assert bool((out >= 0).all()) and bool((out < 1).all())
 
 
+@pytest.mark.parametrize("kind,open_", [v for v in VARIANTS if v != (4, False)])
+@pytest.mark.parametrize("name,ns,nps", [("cfg3", 300, 517), ("cfg2", 97, 1030), ("w27", 64, 640)])
+def test_mappings_static_row_kernel(orc, name, ns, nps, kind, open_):
+    """Compile-time mapping kernels (MODE >= 16) of the bulk ROW path: Eq.(5)/(6)
+    and the open interval, several tiles and a ragged tail, bitwise."""
+    flags = P.MAP_FLAGS[kind] | (P.PRNGD_FLAG_OPEN if open_ else 0) | P.STORE_FLAGS["row"]
+    if name == "w27":  # w >= 27: the R11 clamp is live; narrower accept band
+        if kind == 6:
+            pytest.skip("Eq.(6) needs the full range (P:150-153)")
+        p = dict(w=27, a0=5, a=2**27 - 3, b0=0, b=2**27 - 1, seed=77, stream_begin=2**40 + 3,
+                 n_streams=ns, n_per_stream=nps)
+    else:
+        p = W.config(name, n_streams=ns, n_per_stream=nps, stream_begin=2**40 + 3)
+    _, out = gen(p, flags=flags)
+    assert_same(out, orc.generate(p, kind=kind, open_interval=open_)["out"])
+
+
 @pytest.mark.parametrize("kind,open_", VARIANTS)
 def test_mappings_exhaustive_w8(orc, kind, open_):
     flags = P.MAP_FLAGS[kind] | (P.PRNGD_FLAG_OPEN if open_ else 0)

@@ -12,6 +12,9 @@ run --workload cfg4 --steps 50 --consume
 run --workload cfg5 --steps 50
 run --workload cfg5 --steps 50 --no-write
 run --workload mrg26 --steps 50
+run --workload eq5 --steps 100
+run --workload eq6 --steps 100
+run --workload open4 --steps 100
 python bench.py > gpurun_out/bench_default.log 2>&1; tail -1 gpurun_out/bench_default.log >> $out
 python bench.py --impl reference --steps 3 --warmup 1 2>/dev/null | tail -1 >> $out
 echo done
