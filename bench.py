@@ -511,19 +511,22 @@ def main():
                 "peak_source": src, "algorithmic_adds_per_launch": nout, "kernel_ms": kern_ms,
                 "note": "issue-bound below this peak (DESIGN.md section 8)"}
     elif p.get("mrg"):
-        # MRG32k3a (NEXT-2) runs its recurrences in exact binary64: FP64-pipe bound.
-        # Algorithmic FP64 operations per output: 17 per MRG32k3a draw
-        # (two components x 7: product, fused product-difference, rounding shift pair, remainder,
-        # compare, predicated add; combination 3), 2 draws per output plus the 1/64 of 26-bit
-        # draws reduce-to-width rejects, plus 4 for Eq.(4): 17 x 2.03 + 4 = 38.5.
-        ops = 38.5
+        # MRG32k3a (NEXT-2): instruction-issue bound.  Algorithmic
+        # instructions per output: per MRG32k3a draw 27 (two binary64 components x 5: product,
+        # fused product-difference, rounding-shift pair, remainder; combination 9: two exact
+        # conversions, two canonical-representative fixes of 2, subtract-and-wrap 3; R23 test +
+        # mask 2; band test 2; ring append 4), 2.03 draws per output (26-bit reduce-to-width
+        # rejects 1/64), plus 9 per output (Eq.(4) 6, ring read 2, store 1): 27 x 2.03 + 9 = 64.
+        # Peak: 4 schedulers x 32 lanes per clock per SM x SMs x max SM clock.
+        ops = 64.0
         ach = ops * nout / (kern_ms * 1e-3) / 1e9
-        pk = 64.0 * sms * clk_ghz  # FP64 lanes per clk per SM (ncu pipe-utilisation calibrated)
-        roof = {"bound": "fp64", "achieved": ach, "peak": pk, "unit": "Gop/s", "frac": ach / pk,
+        pk = 4 * 32.0 * sms * clk_ghz
+        roof = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "Ginstr/s", "frac": ach / pk,
                 "traffic": None, "kernel": "gen_mrg_kernel",
-                "peak_source": "derived: 64 FP64 lanes/clk/SM x SMs x max SM clock (ncu: "
-                               "pipe_fp64 42% at 26.7 lanes/clk/SM measured)",
-                "algorithmic_fp64_ops_per_output": ops, "kernel_ms": kern_ms,
+                "peak_source": "derived: 4 warp-instructions/clk/SM (one per scheduler) x 32 "
+                               "lanes x SMs x max SM clock",
+                "algorithmic_instructions_per_output": ops,
+                "fp64_ops_per_output": 24.3, "kernel_ms": kern_ms,
                 "hbm_write_gbs": achieved}
 
     # -------------------------------------------------- pure-store ceiling on the same buffer

@@ -88,35 +88,37 @@ __device__ __forceinline__ uint32_t mrg_next(Mrg32k3a &m) {
     return mrg_combine(p1, p2);
 }
 
-// The same recurrences in binary64: every product and sum below is an integer < 2^53, so each
-// operation is exact and the state values are bit-for-bit the integer ones.  k = nearest
-// integer to p / m (p * (1/m) rounded by the 2^52 + 2^51 shift), r = p - k m in [-m/2, m/2],
-// + m when negative.  FP64-pipe work instead of ~20 INT32 instructions per component.
+// The same recurrences in binary64, on balanced representatives: every product and sum below
+// is an integer < 2^53, so each operation is exact.  k = p * (1/m) rounded to an integer by the
+// 2^52 + 2^51 shift (nearest, up to the rounding of p * (1/m), which only moves r by one m
+// near a half-integer quotient), r = p - k m.  r is congruent to the integer recurrence's value
+// and |r| <= m/2 + 2 < 2^31, so no correction is needed between draws: with |x| < 2^31 (or a
+// canonical x < 2^32 in one operand, the stream start) |1403580 x - 810728 x'| and
+// |527612 y - 1370589 y'| stay below 8e15 < 2^53.  The canonical values are taken only when a
+// draw is combined (mrg_combined_b, integer).  m and 1/m come from the kernel parameters, so
+// the FMAs read them from the constant bank.
 constexpr double kRoundShift = 6755399441055744.0;  // 2^52 + 2^51
-__device__ __forceinline__ double mrg_modd(double p, double m, double inv_m) {
+__device__ __forceinline__ double mrg_modb(double p, double m, double inv_m) {
     const double k = __dsub_rn(__fma_rn(p, inv_m, kRoundShift), kRoundShift);
-    double r = __fma_rn(-k, m, p);
-    // r += m when r < 0, as one predicated add (a select would cost two FSELs)
-    asm("{\n\t.reg .pred p;\n\tsetp.lt.f64 p, %0, 0d0000000000000000;\n\t@p add.rn.f64 %0, %0, %1;\n\t}"
-        : "+d"(r)
-        : "d"(m));
-    return r;
+    return __fma_rn(-k, m, p);
 }
-__device__ __forceinline__ double mrg_c1d(double xm2, double xm3) {
-    return mrg_modd(__fma_rn(1403580.0, xm2, -__dmul_rn(810728.0, xm3)), 4294967087.0,
-                    1.0 / 4294967087.0);
+__device__ __forceinline__ double mrg_c1d(double xm2, double xm3, double m1, double inv_m1) {
+    return mrg_modb(__fma_rn(1403580.0, xm2, -__dmul_rn(810728.0, xm3)), m1, inv_m1);
 }
-__device__ __forceinline__ double mrg_c2d(double ym1, double ym3) {
-    return mrg_modd(__fma_rn(527612.0, ym1, -__dmul_rn(1370589.0, ym3)), 4294944443.0,
-                    1.0 / 4294944443.0);
+__device__ __forceinline__ double mrg_c2d(double ym1, double ym3, double m2, double inv_m2) {
+    return mrg_modb(__fma_rn(527612.0, ym1, -__dmul_rn(1370589.0, ym3)), m2, inv_m2);
 }
-// u = (x_n - y_n) mod m1 in [1, m1] as an integer
-__device__ __forceinline__ uint32_t mrg_combined(double p1, double p2) {
-    double d = __dsub_rn(p1, p2);
-    asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %0, 0d0000000000000000;\n\t@p add.rn.f64 %0, %0, %1;\n\t}"
-        : "+d"(d)
-        : "d"(4294967087.0));
-    return (uint32_t)__double2uint_rz(d);
+// u - 1 for u = (x_n - y_n) mod m1 in [1, m1] (mrg_combine), as one three-input add
+__device__ __forceinline__ uint32_t mrg_combine_m1(uint32_t p1, uint32_t p2) {
+    const uint32_t z = p1 - p2 - 1u;
+    return p1 > p2 ? z : z - 209u;
+}
+// u - 1 from balanced p1 = x_n (mod m1), p2 = y_n (mod m2)
+__device__ __forceinline__ uint32_t mrg_combined_b_m1(double p1, double p2) {
+    const int32_t i1 = __double2int_rz(p1), i2 = __double2int_rz(p2);  // exact: integers
+    const uint32_t c1 = i1 < 0 ? (uint32_t)i1 + kM1 : (uint32_t)i1;
+    const uint32_t c2 = i2 < 0 ? (uint32_t)i2 + kM2 : (uint32_t)i2;
+    return mrg_combine_m1(c1, c2);
 }
 
 // R23: uniform width-bit value: discard u with u - 1 >= T = floor(m1 / 2^width) * 2^width.

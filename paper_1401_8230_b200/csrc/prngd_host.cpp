@@ -228,6 +228,10 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         g.mrg_t2 = (uint32_t)(m1 / s2 * s2);
         g.mrg_mask1 = (uint32_t)(s1 - 1);
         g.mrg_mask2 = (uint32_t)(s2 - 1);
+        g.mrg_m1 = 4294967087.0;
+        g.mrg_inv1 = 1.0 / 4294967087.0;
+        g.mrg_m2 = 4294944443.0;
+        g.mrg_inv2 = 1.0 / 4294944443.0;
         I.speculative = 0;
         pl.spec = false;
     }

@@ -31,6 +31,7 @@ struct GenArgs {
     MapArgs map;            // mapping of the generic kernels (Eq.(4)/(5)/(6), open interval)
     uint32_t mrg_t1, mrg_t2;        // NEXT-2: reduce-to-width thresholds for bitlen(a), bitlen(b)
     uint32_t mrg_mask1, mrg_mask2;  //         and the width masks
+    double mrg_m1, mrg_inv1, mrg_m2, mrg_inv2;  // MRG32k3a moduli and RN(1/m) (binary64 form)
     // consumer (S7)
     uint32_t *hist_slab;    // [gridDim.x][32768] packed u16 pairs (consume kernels only)
     int64_t *hist_spill;    // [65536] int64 carries of the packed counters

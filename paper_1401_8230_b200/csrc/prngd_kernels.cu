@@ -397,18 +397,23 @@ struct XsProducer {  // xorshift128 base generator (S1-S5)
     }
 };
 
-// MRG32k3a without divergent draw loops.  A lane turns every draw into the R23 / pair-drop
-// state machine with predicated logic (draw for x1 or x2 by the lane's own phase, reduce-to-width
-// test, band test when a pair completes) and appends each accepted pair to a per-lane ring of
-// kMrgRing pairs in shared memory.  The warp draws 3 values per lane per step (the unroll by the
-// MRG's period-3 register rotation, so the state needs no moves) until every lane holds a
-// batch; lanes ahead keep drawing into their ring while it has room, which evens out the
-// per-lane acceptance luck across batches.  The consumption order of every stream is exactly the
-// sequential one (NEXT-2).
+// MRG32k3a without divergent draw loops.  A lane turns every draw into predicated logic: the
+// R23 reduce-to-width test, then the value is appended to a per-lane ring of valid draws in
+// shared memory (x1 at even, x2 at odd positions of the valid sequence); a valid x2 whose x1
+// lies outside the band retracts the pair (pair-drop), so the ring only ever holds
+// accepted pairs plus at most one pending x1.  The warp draws 3 values per lane per step (the
+// unroll by the MRG's period-3 register rotation, so the state needs no moves) until every lane
+// holds a batch; lanes ahead keep drawing while their ring has room, which evens out the
+// per-lane acceptance luck across batches.  The consumption order of every stream is exactly
+// the sequential one (NEXT-2).
 #ifndef PRNGD_MRG_RING
 #define PRNGD_MRG_RING 32
 #endif
-constexpr uint32_t kMrgRing = PRNGD_MRG_RING;  // pairs per lane (power of two, >= 2 kCols)
+constexpr uint32_t kMrgRing = PRNGD_MRG_RING;      // pairs per lane (power of two, >= kCols)
+constexpr uint32_t kMrgRingBytes = kMrgRing * 8u;  // per lane: 2 kMrgRing 4-byte draws
+// a lane one draw short of a batch must still have room for a 3-draw step (else the fill loop
+// never ends)
+static_assert(kMrgRingBytes >= 8u * kCols + 12u, "MRG ring smaller than a batch + one step");
 
 // MRG_FP64: 0 = both components in 32-bit integer arithmetic, 1 = component 1 in binary64,
 // 2 = both in binary64 (exact either way; A/B of INT32 vs FP64 pipe load)
@@ -421,51 +426,63 @@ template <bool EQ4, bool SAMEW>
 struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold and mask)
     using T1 = typename MrgWord<PRNGD_MRG_FP64 >= 1 ? 1 : 0>::T;  // component 1 word
     using T2 = typename MrgWord<PRNGD_MRG_FP64 >= 2 ? 1 : 0>::T;  // component 2 word
+    const GenArgs &k;  // moduli and reciprocals (constant bank)
     T1 A, B, C;                 // component 1, oldest..newest (rotating roles)
     T2 D, E, F;                 // component 2
-    uint32_t rd, wr;            // ring counters (free-running)
-    uint32_t x1;                // pending x1 (when have1)
-    bool have1;
-    uint32_t ring;              // this lane's ring (shared address), entries of 8 bytes
-    __device__ __forceinline__ MrgProducer2(const GenArgs &g, uint64_t s, uint32_t ring_base) {
+    // ring byte counters (free-running, 4 per draw).  Both start at 8 * lane: lane l's entries
+    // are rotated by 2 l so lanes at equal counts use different banks (the ring is 256-byte
+    // aligned, so an entry's address is ring | (counter & (kMrgRingBytes - 4)))
+    uint32_t wr, rd;
+    uint32_t bad1;              // 4: the pending x1 lies outside the band, else 0
+    uint32_t ring;              // this lane's ring (shared address), kMrgRingBytes aligned
+    __device__ __forceinline__ MrgProducer2(const GenArgs &g, uint64_t s, uint32_t ring_base,
+                                            uint32_t lane)
+        : k(g) {
         const Mrg32k3a m = mrg_stream_start(g.seed, s);
         A = (T1)m.s0, B = (T1)m.s1, C = (T1)m.s2, D = (T2)m.t0, E = (T2)m.t1, F = (T2)m.t2;
-        rd = wr = 0u;
-        x1 = 0u;
-        have1 = false;
+        rd = wr = 8u * lane;
+        bad1 = 0u;
         ring = ring_base;
     }
     static __device__ __forceinline__ uint32_t c1(uint32_t a, uint32_t b) { return mrg_c1(a, b); }
-    static __device__ __forceinline__ double c1(double a, double b) { return mrg_c1d(a, b); }
+    __device__ __forceinline__ double c1(double a, double b) const {
+        return mrg_c1d(a, b, k.mrg_m1, k.mrg_inv1);
+    }
     static __device__ __forceinline__ uint32_t c2(uint32_t a, uint32_t b) { return mrg_c2(a, b); }
-    static __device__ __forceinline__ double c2(double a, double b) { return mrg_c2d(a, b); }
+    __device__ __forceinline__ double c2(double a, double b) const {
+        return mrg_c2d(a, b, k.mrg_m2, k.mrg_inv2);
+    }
+    // u - 1 of the combined draw (R21), the value R23 tests
     static __device__ __forceinline__ uint32_t combine(uint32_t p1, uint32_t p2) {
-        return mrg_combine(p1, p2);
+        return mrg_combine_m1(p1, p2);
     }
     static __device__ __forceinline__ uint32_t combine(double p1, double p2) {
-        return mrg_combined(p1, p2);
+        return mrg_combined_b_m1(p1, p2);
     }
     static __device__ __forceinline__ uint32_t combine(double p1, uint32_t p2) {
-        return mrg_combine((uint32_t)__double2uint_rz(p1), p2);
+        const int32_t i1 = __double2int_rz(p1);
+        return mrg_combine_m1(i1 < 0 ? (uint32_t)i1 + kM1 : (uint32_t)i1, p2);
     }
-    __device__ __forceinline__ void take(uint32_t u, const GenArgs &g) {
-        const uint32_t x = u - 1u;
-        const bool v = x < (SAMEW ? g.mrg_t1 : (have1 ? g.mrg_t2 : g.mrg_t1));  // R23
-        const bool push = v && have1 && accepted(x1, g.lo, g.span);  // pair complete
-        if (push) {
-            const uint32_t a = ring + ((wr & (kMrgRing - 1)) << 3);
-            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x1),
-                         "r"(x & (SAMEW ? g.mrg_mask1 : g.mrg_mask2))
-                         : "memory");
-        }
-        wr += push ? 1u : 0u;
-        x1 = (v && !have1) ? (x & g.mrg_mask1) : x1;
-        have1 = v ? !have1 : have1;
+    __device__ __forceinline__ void take(uint32_t x, const GenArgs &g) {  // x = u - 1
+        const uint32_t odd = wr & 4u;  // 4: this draw would be an x2
+        const bool v = x < (SAMEW ? g.mrg_t1 : (odd ? g.mrg_t2 : g.mrg_t1));  // R23
+        const uint32_t xm = x & (SAMEW ? g.mrg_mask1 : (odd ? g.mrg_mask2 : g.mrg_mask1));
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+                     "@p st.shared.u32 [%0], %1;\n\t}" ::"r"(ring | (wr & (kMrgRingBytes - 4u))),
+                     "r"(xm), "r"((uint32_t)v)
+                     : "memory");
+        // a valid x2 completes the pair: kept (+4) or dropped with its x1 (-4).  bad1
+        // (4 = the pending x1 is outside the band) is rewritten by every valid draw; only an
+        // x1's value is ever read (at the next valid draw, which is then an x2)
+        const uint32_t bad = accepted(xm, g.lo, g.span) ? 0u : 4u;
+        const uint32_t d = 4u - ((odd & bad1) << 1);
+        wr = v ? wr + d : wr;
+        bad1 = v ? bad : bad1;
     }
     __device__ __forceinline__ void operator()(double (&q)[kCols], const GenArgs &g) {
 #pragma unroll 1
-        while (__any_sync(0xFFFFFFFFu, wr - rd < (uint32_t)kCols)) {
-            if (wr - rd <= kMrgRing - 2u) {  // 3 draws complete at most 2 pairs
+        while (__any_sync(0xFFFFFFFFu, wr - rd < 8u * (uint32_t)kCols)) {
+            if (wr - rd <= kMrgRingBytes - 12u) {  // room for 3 more draws
                 A = c1(B, A), D = c2(F, D);
                 take(combine(A, D), g);
                 B = c1(C, B), E = c2(D, E);
@@ -479,14 +496,14 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
             uint32_t a1, a2;
             asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
                          : "=r"(a1), "=r"(a2)
-                         : "r"(ring + (((rd + i) & (kMrgRing - 1)) << 3)));
+                         : "r"(ring | ((rd + 8u * i) & (kMrgRingBytes - 8u))));
             q[i] = EQ4 ? eq4_mode<1, false>(a1, a2, g) : map_pair<false, true>(a1, a2, g.map);
         }
         if (EQ4 && g.span != g.span_fast) {  // R11 clamp only where the host found it needed
 #pragma unroll
             for (int i = 0; i < kCols; ++i) q[i] = fmin(q[i], kBelowOne);
         }
-        rd += kCols;
+        rd += 8u * kCols;
     }
 };
 
@@ -802,15 +819,16 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
 constexpr int kMrgCols = PRNGD_MRG_RC;
 constexpr size_t kMrgTileBytes = (size_t)32 * (kMrgCols * 8 + 16);
 template <bool EQ4, bool SAMEW>
-__global__ void __launch_bounds__(32) gen_mrg_kernel(const GenArgs g) {
+__global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ GenArgs g) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t row0 = (uint64_t)blockIdx.x * 32u;
     NoConsumer nc;
-    const uint32_t base = aligned_smem_base(smem_raw);
-    // ring rows padded by 8 bytes: lanes at equal ring positions land on different banks
+    // 256-byte alignment is all the rings need (no TMA here): a smaller footprint, more warps
+    const uint32_t base = (smem_u32(smem_raw) + (kMrgRingBytes - 1)) & ~(kMrgRingBytes - 1);
+    static_assert(kMrgTileBytes % kMrgRingBytes == 0, "rings must stay kMrgRingBytes aligned");
     MrgProducer2<EQ4, SAMEW> prod(g, g.stream_begin + row0 + lane,
-                           base + (uint32_t)kMrgTileBytes + lane * (kMrgRing * 8u + 8u));
+                                  base + (uint32_t)kMrgTileBytes + lane * kMrgRingBytes, lane);
     run_rows_burst<false, kMrgCols>(g, base, lane, row0, prod, nc);
 }
 
@@ -1648,7 +1666,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
 }
 
 cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st) {
-    const size_t smem = 1024 + kMrgTileBytes + (size_t)32 * (kMrgRing * 8 + 8);
+    const size_t smem = kMrgRingBytes + kMrgTileBytes + (size_t)32 * kMrgRingBytes;
     const uint64_t grid = (g.n_streams + 31) / 32;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     const bool eq4 = g.map.kind == 4 && g.map.open == 0 && g.w <= 31;

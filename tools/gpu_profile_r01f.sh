@@ -1,0 +1,15 @@
+#!/bin/bash
+# Round-1 final evidence after the compile-time mapping kernels and the MRG32k3a rewrite:
+# the whole GPU test suite, ncu captures of the changed kernels, the default bench line's launch
+# list, and the benchmark sweep.
+mkdir -p gpurun_out
+python -m paper_1401_8230_b200.build > gpurun_out/build.log 2>&1
+timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/gputests_full.log 2>&1; echo "tests rc=$?"
+bash tools/prof_one.sh r01f_cfg3_row gen_kernel --workload cfg3
+bash tools/prof_one.sh r01f_mrg26 gen_mrg --workload mrg26
+bash tools/prof_one.sh r01f_eq5_row gen_kernel --workload eq5
+python bench.py > gpurun_out/r01f_default_plain.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+      --log-file gpurun_out/r01f_default_launches.csv python bench.py > /dev/null 2>&1
+bash tools/bench_all.sh
+echo profiled

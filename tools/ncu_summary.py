@@ -68,6 +68,13 @@ def main():
                                       f"--clock-control none, one launch)"})
     with open(f"profiles/{tag}_summary.txt", "w") as f:
         f.write("\n".join(out) + "\n")
+    try:  # merge: a capture updates its workloads' entries and keeps the others
+        with open("profiles/traffic.json") as f:
+            prev = json.load(f).get("entries", [])
+    except (OSError, ValueError):
+        prev = []
+    fresh = {e["workload"]: e for e in traffic}
+    traffic = [fresh.pop(e["workload"], e) for e in prev] + list(fresh.values())
     with open("profiles/traffic.json", "w") as f:
         json.dump({"entries": traffic,
                    "note": "write bytes sit slightly below the algorithmic bytes: dirty lines "
