@@ -136,7 +136,7 @@ __device__ __forceinline__ uint32_t tile_off(uint32_t row, uint32_t chunk) {
 template <bool RED, bool BELOW1 = false>
 struct ConsumerT {
     double s1, s2, s3, s4;
-    uint32_t *hist;   // shared: 32768 words, counter of bin b in half (b & 1) of word b >> 1
+    uint32_t *hist;   // shared: 32768 words; word j holds bin j (low half), bin j + 32768 (high)
     int64_t *spill;   // global: carries of the packed counters, [65536]
     __device__ __forceinline__ void init(uint32_t *h, int64_t *sp) {
         s1 = s2 = s3 = s4 = 0.0;
@@ -155,26 +155,31 @@ struct ConsumerT {
         s2 = __dadd_rn(s2, z2);
         s3 = __fma_rn(z2, q, s3);
         s4 = __fma_rn(z2, z2, s4);
-        const uint32_t bin = BELOW1 ? (uint32_t)__double2uint_rz(__dmul_rn(q, 65536.0)) : bin16(q);
-        // 1 << (16 * (bin & 1)) as a rotate of 1 by bin * 16 (the amount is taken mod 32)
-        const uint32_t sh = (bin & 1u) << 4;
-        const uint32_t inc = __funnelshift_l(1u, 1u, bin << 4);
+        // t = floor(q * 2^18) = 4 bin + 2 fraction bits (the scaling is exact, so t >> 2 is R16's
+        // floor(q * 2^16)): the word's byte offset is t & 0x1FFFC and the half is bit 17, with
+        // no shifts (bins b and b + 32768 share word b)
+        const uint32_t t0 = (uint32_t)__double2uint_rz(__dmul_rn(q, 262144.0));
+        const uint32_t t = BELOW1 ? t0 : min(t0, 262143u);  // R18: q = 1 -> top bin
+        const uint32_t off = t & 0x1FFFCu;
+        const bool high = t >= 0x20000u;
+        const uint32_t inc = high ? 0x10000u : 1u;
         if (RED) {
             // optimistic: no return value, no carry check; a wrapped field is detected after
             // the kernel (field sum != outputs counted) and the exact pass redoes the histogram
-            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(&hist[bin >> 1])), "r"(inc)
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(hist) + off), "r"(inc)
                          : "memory");
         } else {
-            const uint32_t nw = atomicAdd(&hist[bin >> 1], inc) + inc;
-            if (__builtin_expect(((nw >> sh) & 0xFFFFu) == 0u, 0)) carry(bin, nw);
+            const uint32_t nw = atomicAdd(&hist[off >> 2], inc) + inc;
+            if (__builtin_expect(((high ? nw >> 16 : nw) & 0xFFFFu) == 0u, 0))
+                carry(off >> 2, high, nw);
         }
     }
-    __device__ __noinline__ void carry(uint32_t bin, uint32_t nw) {
+    __device__ __noinline__ void carry(uint32_t word, bool high, uint32_t nw) {
         unsigned long long *sp = reinterpret_cast<unsigned long long *>(spill);
-        atomicAdd(&sp[bin], 65536ull);
-        if ((bin & 1u) == 0u) {
-            atomicAdd(&sp[bin | 1u], 0xFFFFFFFFFFFFFFFFull);  // -1: the carry went into H
-            if (nw == 0u) atomicAdd(&sp[bin | 1u], 65536ull);  // ... and wrapped the word
+        atomicAdd(&sp[word + (high ? 32768u : 0u)], 65536ull);
+        if (!high) {
+            atomicAdd(&sp[word + 32768u], 0xFFFFFFFFFFFFFFFFull);  // -1: the carry went into H
+            if (nw == 0u) atomicAdd(&sp[word + 32768u], 65536ull);  // ... and wrapped the word
         }
     }
 };
@@ -784,15 +789,15 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
             lo += v & 0xFFFFu;
             hi += v >> 16;
         }
-        lo += spill[2 * wi];
-        hi += spill[2 * wi + 1];
-        spill[2 * wi] = 0;
-        spill[2 * wi + 1] = 0;
+        lo += spill[wi];  // word wi: bin wi (low half) and bin wi + 32768 (high half)
+        hi += spill[wi + 32768u];
+        spill[wi] = 0;
+        spill[wi + 32768u] = 0;
         // device atomics: the accumulators may be shared by several shards, also by processes
         // on other GPUs through peer memory (prngd_ipc_open) -- the statistics reduction
         unsigned long long *h = reinterpret_cast<unsigned long long *>(d_hist);
-        if (lo) atomicAdd(&h[2 * wi], (unsigned long long)lo);
-        if (hi) atomicAdd(&h[2 * wi + 1], (unsigned long long)hi);
+        if (lo) atomicAdd(&h[wi], (unsigned long long)lo);
+        if (hi) atomicAdd(&h[wi + 32768u], (unsigned long long)hi);
         local += lo + hi;
     }
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(~0u, local, o);
@@ -818,6 +823,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
 #endif
 constexpr int kMrgCols = PRNGD_MRG_RC;
 constexpr size_t kMrgTileBytes = (size_t)32 * (kMrgCols * 8 + 16);
+#ifndef PRNGD_MRG_DIRECT
+#define PRNGD_MRG_DIRECT 0  // A/B: 1 = register stores, no shared-memory tile (more warps per SM)
+#endif
+constexpr size_t kMrgStageBytes = PRNGD_MRG_DIRECT ? 0 : kMrgTileBytes;
 template <bool EQ4, bool SAMEW>
 __global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ GenArgs g) {
     extern __shared__ uint8_t smem_raw[];
@@ -828,8 +837,30 @@ __global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ Gen
     const uint32_t base = (smem_u32(smem_raw) + (kMrgRingBytes - 1)) & ~(kMrgRingBytes - 1);
     static_assert(kMrgTileBytes % kMrgRingBytes == 0, "rings must stay kMrgRingBytes aligned");
     MrgProducer2<EQ4, SAMEW> prod(g, g.stream_begin + row0 + lane,
-                                  base + (uint32_t)kMrgTileBytes + lane * kMrgRingBytes, lane);
-    run_rows_burst<false, kMrgCols>(g, base, lane, row0, prod, nc);
+                                  base + (uint32_t)kMrgStageBytes + lane * kMrgRingBytes, lane);
+    if constexpr (PRNGD_MRG_DIRECT != 0) {
+        // each lane writes its own row straight from registers (16-byte stores); the L2 merges
+        // the row's 128-byte lines before they reach HBM
+        const bool live = row0 + lane < g.n_streams;
+        double *dst = g.out + (row0 + lane) * g.nps;
+        const bool vec = (g.nps % 2u) == 0u && (reinterpret_cast<uintptr_t>(g.out) & 15u) == 0u;
+#pragma unroll 1
+        for (uint64_t col0 = 0; col0 < g.nps; col0 += kCols) {
+            double q[kCols];
+            prod(q, g);
+            if (!live) continue;
+            if (vec && col0 + kCols <= g.nps) {
+#pragma unroll
+                for (int c = 0; c < kCols / 2; ++c) stg_v2_cs(dst + col0 + 2 * c, q[2 * c], q[2 * c + 1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < kCols; ++i)
+                    if (col0 + i < g.nps) dst[col0 + i] = q[i];
+            }
+        }
+    } else {
+        run_rows_burst<false, kMrgCols>(g, base, lane, row0, prod, nc);
+    }
 }
 
 // ------------------------------------------------------------------------------ NEXT-3 jump kernel
@@ -1666,7 +1697,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
 }
 
 cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st) {
-    const size_t smem = kMrgRingBytes + kMrgTileBytes + (size_t)32 * kMrgRingBytes;
+    const size_t smem = kMrgRingBytes + kMrgStageBytes + (size_t)32 * kMrgRingBytes;
     const uint64_t grid = (g.n_streams + 31) / 32;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     const bool eq4 = g.map.kind == 4 && g.map.open == 0 && g.w <= 31;

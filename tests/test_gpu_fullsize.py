@@ -1,8 +1,9 @@
 """Full-size parity at BASELINE.json's sizes, in the launch configuration bench.py times.
 
-Every output of cfg3 (2^30) and cfg4 (2^32), and the cfg5 per-GPU histogram / count (2^31
+Every output of cfg3 (2^30) and cfg4 (2^32), the cfg5 per-GPU histogram / count (2^31
 outputs), against the CPU oracle run in parallel worker processes over stream ranges (the oracle
-itself is unchanged and single-threaded; the pool only splits the streams)."""
+itself is unchanged and single-threaded; the pool only splits the streams), and sampled rows of
+the NEXT-1 / NEXT-2 bench workloads (eq5, eq6, open4, mrg26) at their full size."""
 import multiprocessing as mp
 import os
 
@@ -73,5 +74,29 @@ def test_cfg5_shard_statistics(orc):
             c += cc
     assert np.array_equal(hist.cpu().numpy(), h) and cnt.item() == c == 2**31
     assert np.allclose(pw.cpu().numpy(), s, rtol=1e-12, atol=0)
+    del out
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["eq5", "eq6", "open4", "mrg26"])
+def test_next_workloads_sampled_rows(orc, name):
+    """The NEXT-1 / NEXT-2 bench workloads at full size (2^30 outputs, the flags bench.py sets):
+    the first and last 64 rows and 4096 seeded random rows, each against the oracle."""
+    p = dict(W.CONFIGS[name])
+    flags = p.get("map_flags", 0) | (P.PRNGD_FLAG_MRG32K3A if p.get("mrg") else 0)
+    g = P.Generator(**dict(p, flags=flags))
+    out = g.generate()
+    torch.cuda.synchronize()
+    assert g.last_launches == 1
+    ns = p["n_streams"]
+    rng = np.random.default_rng(2024)
+    rows = np.unique(np.concatenate([np.arange(64), np.arange(ns - 64, ns),
+                                     rng.integers(0, ns, 4096)]))
+    got = out[torch.from_numpy(rows).cuda()].cpu().numpy()
+    bad = 0
+    for i, r in enumerate(rows):
+        ref = orc.generate(p, stream_begin=p["stream_begin"] + int(r), n_streams=1)["out"]
+        bad += int(np.count_nonzero(got[i].view(np.int64) != ref.view(np.int64)))
+    assert bad == 0
     del out
     torch.cuda.empty_cache()
