@@ -425,9 +425,15 @@ struct XsProducer {  // xorshift128 base generator (S1-S5)
 #endif
 constexpr uint32_t kMrgRing = PRNGD_MRG_RING;      // pairs per lane (power of two, >= kCols)
 constexpr uint32_t kMrgRingBytes = kMrgRing * 8u;  // per lane: 2 kMrgRing 4-byte draws
-// a lane one draw short of a batch must still have room for a 3-draw step (else the fill loop
+#ifndef PRNGD_MRG_STEP
+#define PRNGD_MRG_STEP 9  // draws per lane per fill-loop step (a multiple of the period 3);
+                          // A/B on mrg26: 3 -> 304, 6 -> 326, 9 -> 330, 12-18 -> 328-331, 24 -> 313
+#endif
+constexpr uint32_t kMrgStep = PRNGD_MRG_STEP;
+static_assert(kMrgStep % 3 == 0, "the register rotation has period 3");
+// a lane one draw short of a batch must still have room for a whole step (else the fill loop
 // never ends)
-static_assert(kMrgRingBytes >= 8u * kCols + 12u, "MRG ring smaller than a batch + one step");
+static_assert(kMrgRingBytes >= 8u * kCols + 4u * kMrgStep, "MRG ring smaller than batch + step");
 
 // MRG_FP64: 0 = both components in 32-bit integer arithmetic, 1 = component 1 in binary64,
 // 2 = both in binary64 (exact either way; A/B of INT32 vs FP64 pipe load)
@@ -496,13 +502,16 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
     __device__ __forceinline__ void operator()(double (&q)[kCols], const GenArgs &g) {
 #pragma unroll 1
         while (__any_sync(0xFFFFFFFFu, wr - rd < 8u * (uint32_t)kCols)) {
-            if (wr - rd <= kMrgRingBytes - 12u) {  // room for 3 more draws
-                A = c1(B, A), D = c2(F, D);
-                take(combine(A, D), g);
-                B = c1(C, B), E = c2(D, E);
-                take(combine(B, E), g);
-                C = c1(A, C), F = c2(E, F);
-                take(combine(C, F), g);
+            if (wr - rd <= kMrgRingBytes - 4u * kMrgStep) {  // room for kMrgStep more draws
+#pragma unroll
+                for (int r = 0; r < kMrgStep / 3; ++r) {
+                    A = c1(B, A), D = c2(F, D);
+                    take(combine(A, D), g);
+                    B = c1(C, B), E = c2(D, E);
+                    take(combine(B, E), g);
+                    C = c1(A, C), F = c2(E, F);
+                    take(combine(C, F), g);
+                }
             }
         }
 #pragma unroll
