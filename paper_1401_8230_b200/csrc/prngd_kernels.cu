@@ -425,6 +425,12 @@ struct XsProducer {  // xorshift128 base generator (S1-S5)
 #endif
 constexpr uint32_t kMrgRing = PRNGD_MRG_RING;      // pairs per lane (power of two, >= kCols)
 constexpr uint32_t kMrgRingBytes = kMrgRing * 8u;  // per lane: 2 kMrgRing 4-byte draws
+// Output staging of the MRG kernel: 0 = a ROW tile beside the rings; 1 = register stores, no
+// tile (A/B: 283 vs 304 Gd/s); 2 = staged in the ring bytes the batch just consumed (no tile,
+// 25 instead of 17 warps per SM; bit-exact, A/B: 324.5 vs 330.5 Gd/s -- not occupancy-bound)
+#ifndef PRNGD_MRG_STAGE
+#define PRNGD_MRG_STAGE 0
+#endif
 #ifndef PRNGD_MRG_STEP
 #define PRNGD_MRG_STEP 9  // draws per lane per fill-loop step (a multiple of the period 3);
                           // A/B on mrg26: 3 -> 304, 6 -> 326, 9 -> 330, 12-18 -> 328-331, 24 -> 313
@@ -460,7 +466,7 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
         : k(g) {
         const Mrg32k3a m = mrg_stream_start(g.seed, s);
         A = (T1)m.s0, B = (T1)m.s1, C = (T1)m.s2, D = (T2)m.t0, E = (T2)m.t1, F = (T2)m.t2;
-        rd = wr = 8u * lane;
+        rd = wr = (PRNGD_MRG_STAGE == 2 ? 16u : 8u) * lane;
         bad1 = 0u;
         ring = ring_base;
     }
@@ -841,10 +847,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
 #endif
 constexpr int kMrgCols = PRNGD_MRG_RC;
 constexpr size_t kMrgTileBytes = (size_t)32 * (kMrgCols * 8 + 16);
-#ifndef PRNGD_MRG_DIRECT
-#define PRNGD_MRG_DIRECT 0  // A/B: 1 = register stores, no shared-memory tile (more warps per SM)
-#endif
-constexpr size_t kMrgStageBytes = PRNGD_MRG_DIRECT ? 0 : kMrgTileBytes;
+constexpr size_t kMrgStageBytes = PRNGD_MRG_STAGE == 0 ? kMrgTileBytes : 0;
 template <bool EQ4, bool SAMEW>
 __global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ GenArgs g) {
     extern __shared__ uint8_t smem_raw[];
@@ -856,7 +859,45 @@ __global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ Gen
     static_assert(kMrgTileBytes % kMrgRingBytes == 0, "rings must stay kMrgRingBytes aligned");
     MrgProducer2<EQ4, SAMEW> prod(g, g.stream_begin + row0 + lane,
                                   base + (uint32_t)kMrgStageBytes + lane * kMrgRingBytes, lane);
-    if constexpr (PRNGD_MRG_DIRECT != 0) {
+    if constexpr (PRNGD_MRG_STAGE == 2) {
+        // Every lane consumes exactly 128 bytes of its ring per batch, and its read counter
+        // started at 16 * lane, so the bytes batch b consumed sit at (16 l + 128 b) mod 256 of
+        // lane l's ring for every l: free until the next fill, they hold the lane's 16 outputs
+        // while the warp writes the 32 x 128-byte tile row by row (16-byte chunks, 4 rows per
+        // instruction).
+        const uint32_t rings = base;
+        const bool live = row0 + lane < g.n_streams;
+        const bool full_rows = row0 + 32u <= g.n_streams;
+        const bool vec = (g.nps % 2u) == 0u && (reinterpret_cast<uintptr_t>(g.out) & 15u) == 0u;
+        const uint32_t c = lane & 7u, rsub = lane >> 3;
+        double *dst = g.out + (row0 + lane) * g.nps;
+        uint32_t boff = 0u;
+#pragma unroll 1
+        for (uint64_t col0 = 0; col0 < g.nps; col0 += kCols, boff ^= 128u) {
+            double q[kCols];
+            prod(q, g);
+            if (vec && full_rows && col0 + kCols <= g.nps) {
+                const uint32_t my = rings + lane * kMrgRingBytes, o0 = 16u * lane + boff;
+#pragma unroll
+                for (int k = 0; k < kCols / 2; ++k)
+                    sts_v2(my | ((o0 + 16u * k) & 0xF0u), q[2 * k], q[2 * k + 1]);
+                __syncwarp();
+                double *d = g.out + (row0 + rsub) * g.nps + col0 + 2 * c;
+#pragma unroll
+                for (uint32_t r = rsub; r < 32u; r += 4u) {
+                    double a, b;
+                    lds_v2(rings + r * kMrgRingBytes + ((16u * r + boff + 16u * c) & 0xF0u), a, b);
+                    stg_v2_cs(d, a, b);
+                    d += 4u * g.nps;
+                }
+                __syncwarp();
+            } else if (live) {
+#pragma unroll
+                for (int i = 0; i < kCols; ++i)
+                    if (col0 + i < g.nps) dst[col0 + i] = q[i];
+            }
+        }
+    } else if constexpr (PRNGD_MRG_STAGE == 1) {
         // each lane writes its own row straight from registers (16-byte stores); the L2 merges
         // the row's 128-byte lines before they reach HBM
         const bool live = row0 + lane < g.n_streams;
