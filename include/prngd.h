@@ -104,7 +104,7 @@ typedef enum {
 /* NEXT-2: MRG32k3a base generator (L'Ecuyer 1999; P:165 names it) instead of xorshift128.
  * x1 and x2 are uniform bitlen(a)- and bitlen(b)-bit values obtained from MRG32k3a outputs by
  * reduce-to-width rejection (both widths <= 31); each stream's state comes from SplitMix64
- * outputs #3s..#3s+2.  prngd_generate only (pair-drop, ROW store: 16-byte aligned output and
+ * outputs #3s..#3s+2.  prngd_generate and prngd_generate_host only (pair-drop, ROW store: 16-byte aligned output and
  * even n_per_stream); EUNSUPPORTED elsewhere. */
 #define PRNGD_FLAG_MRG32K3A      0x800u
 /* prngd_generate_consume counts into per-SM 16-bit packed shared-memory counters.  By default the

@@ -427,7 +427,6 @@ prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64
 
 prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stream) {
     if (!h || !h_out) return fail(PRNGD_EINVAL, "null handle or host pointer");
-    if (h->plan.mrg) return fail(PRNGD_EUNSUPPORTED, "generate_host runs on xorshift128 only");
     int sms = 0;
     prngd_status s = device_ready(&sms);
     if (s != PRNGD_OK) return s;
@@ -478,8 +477,9 @@ prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stre
         g.stream_begin = h->p.stream_begin + r0;
         g.n_streams = nr;
         g.out = h->stage[b];
-        if ((e = launch_rows(g, plan_for(h, h->stage[b]), gs, sms)) != cudaSuccess)
-            return cuda_fail(e, "generate kernel launch");
+        e = h->plan.mrg ? prngd::launch_generate_mrg(g, gs)
+                        : launch_rows(g, plan_for(h, h->stage[b]), gs, sms);
+        if (e != cudaSuccess) return cuda_fail(e, "generate kernel launch");
         ++launches;
         if ((e = cudaEventRecord(h->ev_gen[b], gs)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
         if ((e = cudaStreamWaitEvent(h->copy_stream, h->ev_gen[b], 0)) != cudaSuccess)

@@ -448,6 +448,21 @@ def test_mrg32k3a_bitwise(orc, par, kind):
     assert_same(out, orc.generate(p, kind=kind)["out"])
 
 
+def test_mrg32k3a_generate_host(orc):
+    """prngd_generate_host on the MRG32k3a kernel: several staging chunks (streams of 96 KiB)."""
+    p = dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1, seed=5, n_streams=5000,
+             n_per_stream=12288, flags=P.PRNGD_FLAG_MRG32K3A, mrg=True)
+    g = P.Generator(**p)
+    host = g.generate_host().numpy()
+    dev = g.generate()
+    torch.cuda.synchronize()
+    assert np.array_equal(host.view(np.int64), dev.cpu().numpy().view(np.int64))
+    rows = [0, 1, 2751, 2752, 4999]  # 256 MiB chunks: 2752 rows (whole warp tasks)
+    for r in rows:
+        ref = orc.generate(p, stream_begin=r, n_streams=1)["out"]
+        assert np.array_equal(host[r].view(np.int64), ref.ravel().view(np.int64))
+
+
 def test_mrg32k3a_unsupported_calls():
     p = dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1, seed=1, n_streams=32, n_per_stream=64,
              flags=P.PRNGD_FLAG_MRG32K3A)
