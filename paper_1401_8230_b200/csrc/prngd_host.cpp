@@ -387,11 +387,39 @@ static prngd_status ensure_device_scratch(prngd_handle *h) {
     return PRNGD_OK;
 }
 
+// Two device staging buffers of whole warp tasks, about 256 MiB each (generate_host; the
+// MRG32k3a consume-only path uses the first).  *rows = streams per buffer.
+static prngd_status ensure_stage(prngd_handle *h, uint64_t *rows_out) {
+    const uint64_t row_bytes = h->p.n_per_stream * 8u;
+    const uint64_t target = 256ull << 20;  // 256 MiB per chunk, two chunks in flight
+    uint64_t rows = target / row_bytes;
+    if (rows < 1) rows = 1;
+    rows = (rows + 31) / 32 * 32;          // whole warp tasks
+    if (rows > h->p.n_streams) rows = h->p.n_streams;
+    if (h->stage_rows < rows) {
+        for (int i = 0; i < 2; ++i) {
+            if (h->stage[i]) cudaFree(h->stage[i]);
+            h->stage[i] = nullptr;
+        }
+        h->stage_rows = 0;
+        for (int i = 0; i < 2; ++i) {
+            const cudaError_t e = cudaMalloc(&h->stage[i], rows * row_bytes);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return fail(PRNGD_ENOMEM, "staging buffer (%llu bytes): %s",
+                            (unsigned long long)(rows * row_bytes), cudaGetErrorString(e));
+            }
+        }
+        h->stage_rows = rows;
+    }
+    *rows_out = rows;
+    return PRNGD_OK;
+}
+
 prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64_t *d_hist,
                                     double *d_pow, int64_t *d_count, void *cuda_stream) {
     if (!hc || !d_hist || !d_pow || !d_count)
         return fail(PRNGD_EINVAL, "null handle or accumulator pointer");
-    if (hc->plan.mrg) return fail(PRNGD_EUNSUPPORTED, "the fused consumer runs on xorshift128 only");
     if (((uintptr_t)d_hist | (uintptr_t)d_pow | (uintptr_t)d_count) & 7u)
         return fail(PRNGD_EINVAL, "accumulators must be 8-byte aligned");
     if (d_out && ((uintptr_t)d_out & 7u)) return fail(PRNGD_EINVAL, "d_out must be 8-byte aligned");
@@ -416,6 +444,34 @@ prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64
         h->cons_bytes = need;
     }
     int launches = 0;
+    if (h->plan.mrg) {
+        // MRG32k3a: the generator kernel writes the values (d_out, or staged chunks when d_out
+        // is null), then S7 runs over them in memory (launch_consume_memory)
+        cudaStream_t st = (cudaStream_t)cuda_stream;
+        const uint64_t nps = h->p.n_per_stream;
+        uint64_t rows = h->p.n_streams;
+        if (!d_out && (s = ensure_stage(h, &rows)) != PRNGD_OK) return s;
+        for (uint64_t r0 = 0; r0 < h->p.n_streams; r0 += rows) {
+            const uint64_t nr = (h->p.n_streams - r0) < rows ? (h->p.n_streams - r0) : rows;
+            GenArgs g = h->args;
+            g.stream_begin = h->p.stream_begin + r0;
+            g.n_streams = nr;
+            g.out = d_out ? d_out : h->stage[0];
+            const Plan pl = plan_for(h, g.out);
+            if (pl.store != Store::ROW && pl.store != Store::ROW1K)
+                return fail(PRNGD_EUNSUPPORTED,
+                            "MRG32k3a needs a 16-byte aligned output and even n_per_stream");
+            cudaError_t e = prngd::launch_generate_mrg(g, st);
+            if (e != cudaSuccess) return cuda_fail(e, "generate kernel launch");
+            int l = 0;
+            e = prngd::launch_consume_memory(h->args, g.out, nr * nps, d_hist, d_pow, d_count,
+                                             h->cons_scratch, h->cons_bytes, st, sms, &l);
+            if (e != cudaSuccess) return cuda_fail(e, "consume launch");
+            launches += 1 + l;
+        }
+        h->last_launches.store((uint32_t)launches);
+        return PRNGD_OK;
+    }
     cudaError_t e = prngd::launch_generate_consume(h->args, plan_for(h, d_out, true), d_out, d_hist,
                                                    d_pow, d_count, h->cons_scratch,
                                                    h->cons_bytes, (cudaStream_t)cuda_stream, sms,
@@ -434,28 +490,9 @@ prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stre
     if ((s = ensure_device_scratch(h)) != PRNGD_OK) return s;
     const uint64_t nps = h->p.n_per_stream;
     const uint64_t row_bytes = nps * 8u;
-    const uint64_t target = 256ull << 20;  // 256 MiB per chunk, two chunks in flight
-    uint64_t rows = target / row_bytes;
-    if (rows < 1) rows = 1;
-    rows = (rows + 31) / 32 * 32;          // whole warp tasks
-    if (rows > h->p.n_streams) rows = h->p.n_streams;
+    uint64_t rows = 0;
+    if ((s = ensure_stage(h, &rows)) != PRNGD_OK) return s;
     cudaError_t e;
-    if (h->stage_rows < rows) {
-        for (int i = 0; i < 2; ++i) {
-            if (h->stage[i]) cudaFree(h->stage[i]);
-            h->stage[i] = nullptr;
-        }
-        h->stage_rows = 0;
-        for (int i = 0; i < 2; ++i) {
-            e = cudaMalloc(&h->stage[i], rows * row_bytes);
-            if (e != cudaSuccess) {
-                cudaGetLastError();
-                return fail(PRNGD_ENOMEM, "staging buffer (%llu bytes): %s",
-                            (unsigned long long)(rows * row_bytes), cudaGetErrorString(e));
-            }
-        }
-        h->stage_rows = rows;
-    }
     if (!h->copy_stream) {
         if ((e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
             return cuda_fail(e, "cudaStreamCreate");
@@ -477,8 +514,10 @@ prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stre
         g.stream_begin = h->p.stream_begin + r0;
         g.n_streams = nr;
         g.out = h->stage[b];
-        e = h->plan.mrg ? prngd::launch_generate_mrg(g, gs)
-                        : launch_rows(g, plan_for(h, h->stage[b]), gs, sms);
+        const Plan pl = plan_for(h, h->stage[b]);
+        if (pl.mrg && pl.store != Store::ROW && pl.store != Store::ROW1K)
+            return fail(PRNGD_EUNSUPPORTED, "MRG32k3a needs an even n_per_stream");
+        e = pl.mrg ? prngd::launch_generate_mrg(g, gs) : launch_rows(g, pl, gs, sms);
         if (e != cudaSuccess) return cuda_fail(e, "generate kernel launch");
         ++launches;
         if ((e = cudaEventRecord(h->ev_gen[b], gs)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");

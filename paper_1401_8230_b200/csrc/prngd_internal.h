@@ -87,6 +87,11 @@ cudaError_t launch_generate_consume(const GenArgs &g, const Plan &pl, double *d_
                                     void *scratch, size_t scratch_bytes, cudaStream_t st,
                                     int num_sms, int *launches);
 size_t consume_scratch_bytes(int num_sms);
+// S7 over n values already in device memory (src): histogram kernel, exact pass, finalize
+cudaError_t launch_consume_memory(const GenArgs &g, const double *src, uint64_t n, int64_t *d_hist,
+                                  double *d_pow, int64_t *d_count, void *scratch,
+                                  size_t scratch_bytes, cudaStream_t st, int num_sms,
+                                  int *launches);
 cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st);
 cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *tables,
                                  cudaStream_t st);

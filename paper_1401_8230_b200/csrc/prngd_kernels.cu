@@ -703,6 +703,94 @@ __global__ void __launch_bounds__(gen_warps<ST>() * 32)
     }
 }
 
+// End of a consumer CTA: moments reduced (warp tree, then per-CTA in warp order: deterministic
+// for a fixed grid) into g.pow_slab, the packed histogram copied to this CTA's slab, and for the
+// optimistic (RED) adds the field-sum check against the outputs counted (`expect`: this
+// thread's share), which raises g.overflow when a 16-bit field wrapped.
+template <bool RED, int kWarps, class Cons>
+__device__ __forceinline__ void consume_epilogue(const Cons &cons, const uint32_t *hist,
+                                                 const GenArgs &g, unsigned long long expect) {
+    __shared__ double red[kWarps][4];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    double s[4] = {cons.s1, cons.s2, cons.s3, cons.s4};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        for (int o = 16; o > 0; o >>= 1) s[k] = __dadd_rn(s[k], __shfl_xor_sync(~0u, s[k], o));
+    if (lane == 0)
+        for (int k = 0; k < 4; ++k) red[warp][k] = s[k];
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double acc = 0.0;
+        for (int wi = 0; wi < kWarps; ++wi) acc = __dadd_rn(acc, red[wi][threadIdx.x]);
+        g.pow_slab[blockIdx.x * 4 + threadIdx.x] = acc;
+    }
+    uint4 *dst = reinterpret_cast<uint4 *>(g.hist_slab + (size_t)blockIdx.x * kHistWords);
+    const uint4 *src = reinterpret_cast<const uint4 *>(hist);
+    unsigned long long fsum = 0;  // sum of this thread's 16-bit fields (RED check)
+    for (uint32_t i = threadIdx.x; i < kHistWords / 4; i += blockDim.x) {
+        const uint4 v = src[i];
+        dst[i] = v;
+        if (RED)
+            fsum += (v.x & 0xFFFFu) + (v.x >> 16) + (v.y & 0xFFFFu) + (v.y >> 16) +
+                    (v.z & 0xFFFFu) + (v.z >> 16) + (v.w & 0xFFFFu) + (v.w >> 16);
+    }
+    if (RED) {
+        for (int o = 16; o > 0; o >>= 1) {
+            fsum += __shfl_xor_sync(~0u, fsum, o);
+            expect += __shfl_xor_sync(~0u, expect, o);
+        }
+        __shared__ unsigned long long part[2][kWarps];
+        if (lane == 0) {
+            part[0][warp] = fsum;
+            part[1][warp] = expect;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long a = 0, b = 0;
+            for (int wi = 0; wi < kWarps; ++wi) {
+                a += part[0][wi];
+                b += part[1][wi];
+            }
+            if (a != b && !PRNGD_HIST8_SIM) atomicOr(g.overflow, 1u);
+        }
+    }
+}
+
+// S7 over values already in device memory (the MRG32k3a path: generate, then this kernel on
+// the written outputs).  Persistent, one CTA per SM, grid-stride coalesced loads; the same
+// packed histogram, optimistic adds, exact pass and slabs as consume_kernel.
+constexpr int kHistMemWarps = 16;
+template <bool RED, bool EXACT_GUARD>
+__global__ void __launch_bounds__(kHistMemWarps * 32, 1)
+    hist_mem_kernel(const double *__restrict__ src, uint64_t n, const __grid_constant__ GenArgs g) {
+    if (EXACT_GUARD && *(volatile const uint32_t *)g.overflow == 0u) return;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base = aligned_smem_base(smem_raw);
+    uint32_t *hist = reinterpret_cast<uint32_t *>(smem_raw + (base - smem_u32(smem_raw)));
+    for (uint32_t i = threadIdx.x; i < kHistWords; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    ConsumerT<RED, false> cons;
+    cons.init(hist, g.hist_spill);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long counted = 0;
+#pragma unroll 1
+    for (; i + 3 * stride < n; i += 4 * stride) {
+        double q[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q[k] = __ldcs(src + i + k * stride);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cons.add(q[k]);
+        counted += 4;
+    }
+#pragma unroll 1
+    for (; i < n; i += stride) {
+        cons.add(__ldcs(src + i));
+        ++counted;
+    }
+    consume_epilogue<RED, kHistMemWarps>(cons, hist, g, counted);
+}
+
 // S1-S7, persistent: one CTA per SM owning a 128 KiB packed histogram; warps take 32-stream
 // tasks round-robin.  Writes per-CTA slabs that finalize_kernel reduces.
 // RED: optimistic no-return shared-memory adds; the CTA then checks that its 16-bit fields sum
@@ -717,7 +805,6 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     constexpr int kWarps = cons_warps<ST, WRITE>();
     constexpr int NB = ring<ST, WRITE>();
     extern __shared__ uint8_t smem_raw[];
-    __shared__ double red[kWarps][4];
     const uint32_t base = aligned_smem_base(smem_raw);
     uint32_t *hist = reinterpret_cast<uint32_t *>(smem_raw + (base - smem_u32(smem_raw)));
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
@@ -747,54 +834,15 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     if constexpr (WRITE && ST == Store::TMA) {
         if (lane == 0) bulk_wait_all();
     }
-    // moments: warp tree, then per-CTA in warp order (deterministic for a fixed grid)
-    double s[4] = {cons.s1, cons.s2, cons.s3, cons.s4};
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-        for (int o = 16; o > 0; o >>= 1) s[k] = __dadd_rn(s[k], __shfl_xor_sync(~0u, s[k], o));
-    if (lane == 0)
-        for (int k = 0; k < 4; ++k) red[warp][k] = s[k];
-    __syncthreads();
-    if (threadIdx.x < 4) {
-        double acc = 0.0;
-        for (int wi = 0; wi < kWarps; ++wi) acc = __dadd_rn(acc, red[wi][threadIdx.x]);
-        g.pow_slab[blockIdx.x * 4 + threadIdx.x] = acc;
-    }
-    uint4 *dst = reinterpret_cast<uint4 *>(g.hist_slab + (size_t)blockIdx.x * kHistWords);
-    const uint4 *src = reinterpret_cast<const uint4 *>(hist);
-    unsigned long long fsum = 0;  // sum of this thread's 16-bit fields (RED check)
-    for (uint32_t i = threadIdx.x; i < kHistWords / 4; i += blockDim.x) {
-        const uint4 v = src[i];
-        dst[i] = v;
-        if (RED)
-            fsum += (v.x & 0xFFFFu) + (v.x >> 16) + (v.y & 0xFFFFu) + (v.y >> 16) +
-                    (v.z & 0xFFFFu) + (v.z >> 16) + (v.w & 0xFFFFu) + (v.w >> 16);
-    }
-    if (RED) {
-        // outputs this CTA counted: live rows of its tasks x nps
-        unsigned long long expect = 0;
-        if (lane == 0)
-            for (uint64_t t = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * warp; t < n_tasks;
-                 t += (uint64_t)gridDim.x * kWarps) {
-                const uint64_t left = g.n_streams - t * 32u;
-                expect += (left < 32u ? left : 32u) * g.nps;
-            }
-        for (int o = 16; o > 0; o >>= 1) fsum += __shfl_xor_sync(~0u, fsum, o);
-        __shared__ unsigned long long part[2][kWarps];
-        if (lane == 0) {
-            part[0][warp] = fsum;
-            part[1][warp] = expect;
+    // outputs this CTA counted (RED check): live rows of its tasks x nps, summed on lane 0
+    unsigned long long expect = 0;
+    if (RED && lane == 0)
+        for (uint64_t t = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * warp; t < n_tasks;
+             t += (uint64_t)gridDim.x * kWarps) {
+            const uint64_t left = g.n_streams - t * 32u;
+            expect += (left < 32u ? left : 32u) * g.nps;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long a = 0, b = 0;
-            for (int wi = 0; wi < kWarps; ++wi) {
-                a += part[0][wi];
-                b += part[1][wi];
-            }
-            if (a != b && !PRNGD_HIST8_SIM) atomicOr(g.overflow, 1u);
-        }
-    }
+    consume_epilogue<RED, kWarps>(cons, hist, g, expect);
 }
 
 // Reduce the per-CTA slabs into the caller's accumulators; resets the spill array to zero.
@@ -1753,6 +1801,35 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
     e = cudaGetLastError();
     if (e == cudaSuccess) *launches += 1;
     return e;
+}
+
+cudaError_t launch_consume_memory(const GenArgs &g0, const double *src, uint64_t n,
+                                  int64_t *d_hist, double *d_pow, int64_t *d_count, void *scratch,
+                                  size_t scratch_bytes, cudaStream_t st, int num_sms,
+                                  int *launches) {
+    *launches = 0;
+    if (scratch_bytes < consume_scratch_bytes(num_sms)) return cudaErrorInvalidValue;
+    GenArgs g = g0;
+    uint8_t *sp = static_cast<uint8_t *>(scratch);
+    g.hist_slab = reinterpret_cast<uint32_t *>(sp);
+    g.hist_spill = reinterpret_cast<int64_t *>(sp + (size_t)num_sms * kHistWords * 4u);
+    g.pow_slab = reinterpret_cast<double *>(sp + (size_t)num_sms * kHistWords * 4u + 65536u * 8u);
+    g.overflow = reinterpret_cast<uint32_t *>(sp + (size_t)num_sms * kHistWords * 4u +
+                                              65536u * 8u + (size_t)num_sms * 4u * 8u);
+    const int grid = num_sms;  // every CTA writes its slab (empty ones too): finalize reads all
+    const size_t smem = 1024 + (size_t)kHistWords * 4u;
+    cudaError_t e;
+    if ((e = set_smem(hist_mem_kernel<true, false>, smem)) != cudaSuccess) return e;
+    hist_mem_kernel<true, false><<<grid, kHistMemWarps * 32, smem, st>>>(src, n, g);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = set_smem(hist_mem_kernel<false, true>, smem)) != cudaSuccess) return e;
+    hist_mem_kernel<false, true><<<grid, kHistMemWarps * 32, smem, st>>>(src, n, g);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    finalize_kernel<<<32, 256, 0, st>>>(g.hist_slab, grid, g.hist_spill, g.pow_slab, d_hist,
+                                         d_pow, d_count, g.overflow);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    *launches = 3;
+    return cudaSuccess;
 }
 
 cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st) {

@@ -463,12 +463,64 @@ def test_mrg32k3a_generate_host(orc):
         assert np.array_equal(host[r].view(np.int64), ref.ravel().view(np.int64))
 
 
+def _mrg_stats_match(g, p, out=None):
+    """Histogram and count against the oracle's; the power sums (R16, relative 1e-12) against
+    pairwise (numpy) sums of the oracle's outputs: at 10^7-10^8 outputs the oracle's own
+    sequential sums drift by ~1e-12 relative themselves."""
+    _, hist, pw, cnt = g.generate_consume(out)
+    torch.cuda.synchronize()
+    ref = orc_mod().generate(p, want_out=True, want_stats=True)
+    assert np.array_equal(hist.cpu().numpy(), ref["hist"])
+    assert cnt.item() == ref["count"] == p["n_streams"] * p["n_per_stream"]
+    z = ref["out"].ravel()
+    z2 = z * z
+    exact = np.array([z.sum(), z2.sum(), (z2 * z).sum(), (z2 * z2).sum()])
+    assert np.allclose(pw.cpu().numpy(), exact, rtol=1e-12, atol=0)
+    return ref
+
+
+def orc_mod():
+    import oracle
+    return oracle
+
+
+@pytest.mark.parametrize("kind", [4, 5])
+def test_mrg32k3a_generate_consume(kind):
+    """S7 on the MRG32k3a path (generate, then the histogram kernel over the written values)."""
+    p = dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1, seed=9, n_streams=700, n_per_stream=1030,
+             flags=P.PRNGD_FLAG_MRG32K3A | P.MAP_FLAGS[kind], mrg=True, map=kind)
+    g = P.Generator(**p)
+    out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+    ref = _mrg_stats_match(g, p, out)
+    assert np.array_equal(out.cpu().numpy().view(np.int64), ref["out"].view(np.int64))
+    assert g.last_launches == 4
+
+
+def test_mrg32k3a_consume_only_chunks():
+    """Consume-only (no output buffer): staged 256 MiB chunks, the statistics accumulate."""
+    p = dict(w=26, a0=5, a=2**26 - 3, b0=0, b=2**20 - 1, seed=3, n_streams=3000,
+             n_per_stream=12288, flags=P.PRNGD_FLAG_MRG32K3A, mrg=True)
+    g = P.Generator(**p)
+    _mrg_stats_match(g, p)
+    assert g.last_launches == 8  # two chunks x (generate, histogram, exact pass, finalize)
+
+
+def test_mrg32k3a_consume_counter_wrap():
+    """8 distinct values over 2^26.3 outputs: every CTA's 16-bit fields wrap, the exact pass
+    must take over (memory histogram kernel)."""
+    p = dict(w=2, a0=0, a=3, b0=0, b=3, seed=4, n_streams=8192, n_per_stream=10240,
+             flags=P.PRNGD_FLAG_MRG32K3A, mrg=True)
+    g = P.Generator(**p)
+    out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+    _mrg_stats_match(g, p, out)
+    del out
+    torch.cuda.empty_cache()
+
+
 def test_mrg32k3a_unsupported_calls():
     p = dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1, seed=1, n_streams=32, n_per_stream=64,
              flags=P.PRNGD_FLAG_MRG32K3A)
     g = P.Generator(**p)
-    with pytest.raises(P.PrngdError):
-        g.generate_consume()
     with pytest.raises(P.PrngdError):
         g.raw(4)
 

@@ -12,6 +12,7 @@ run --workload cfg4 --steps 50 --consume
 run --workload cfg5 --steps 50
 run --workload cfg5 --steps 50 --no-write
 run --workload mrg26 --steps 50
+run --workload mrg26 --steps 20 --consume
 run --workload eq5 --steps 100
 run --workload eq6 --steps 100
 run --workload open4 --steps 100
