@@ -107,7 +107,7 @@ typedef enum {
  * outputs #3s..#3s+2.  Pair-drop only; needs a 16-byte aligned output and even n_per_stream.
  * prngd_generate, prngd_generate_host, and prngd_generate_consume, which on this generator is
  * not fused: the generator kernel writes the values (to d_out, or to the handle's 256 MiB
- * staging chunks when d_out is NULL) and a histogram kernel reads them back (4 launches per
+ * staging chunks of about 1 GiB when d_out is NULL) and a histogram kernel reads them back (4 launches per
  * chunk: generate, histogram, exact pass, slab reduction).  EUNSUPPORTED for the debug hooks
  * and with PRNGD_FLAG_ALG1 / PRNGD_FLAG_JUMP. */
 #define PRNGD_FLAG_MRG32K3A      0x800u

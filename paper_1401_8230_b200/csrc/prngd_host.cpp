@@ -28,7 +28,7 @@ struct prngd_handle {
     void *cons_scratch = nullptr;
     size_t cons_bytes = 0;
     double *stage[2] = {nullptr, nullptr};
-    size_t stage_rows = 0;
+    size_t stage_rows[2] = {0, 0};
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_gen[2] = {nullptr, nullptr};
     cudaEvent_t ev_copy[2] = {nullptr, nullptr};
@@ -387,30 +387,27 @@ static prngd_status ensure_device_scratch(prngd_handle *h) {
     return PRNGD_OK;
 }
 
-// Two device staging buffers of whole warp tasks, about 256 MiB each (generate_host; the
-// MRG32k3a consume-only path uses the first).  *rows = streams per buffer.
-static prngd_status ensure_stage(prngd_handle *h, uint64_t *rows_out) {
+// Device staging buffers of whole warp tasks: generate_host keeps two of about 256 MiB in
+// flight; the MRG32k3a consume-only path uses one of about 1 GiB (a 256 MiB chunk of a 1024-output
+// shape is only 1024 one-warp CTAs, 40% of one wave).  *rows = streams per buffer.
+static prngd_status ensure_stage(prngd_handle *h, uint64_t target, int nbuf, uint64_t *rows_out) {
     const uint64_t row_bytes = h->p.n_per_stream * 8u;
-    const uint64_t target = 256ull << 20;  // 256 MiB per chunk, two chunks in flight
     uint64_t rows = target / row_bytes;
     if (rows < 1) rows = 1;
     rows = (rows + 31) / 32 * 32;          // whole warp tasks
     if (rows > h->p.n_streams) rows = h->p.n_streams;
-    if (h->stage_rows < rows) {
-        for (int i = 0; i < 2; ++i) {
-            if (h->stage[i]) cudaFree(h->stage[i]);
-            h->stage[i] = nullptr;
+    for (int i = 0; i < nbuf; ++i) {
+        if (h->stage_rows[i] >= rows) continue;
+        if (h->stage[i]) cudaFree(h->stage[i]);
+        h->stage[i] = nullptr;
+        h->stage_rows[i] = 0;
+        const cudaError_t e = cudaMalloc(&h->stage[i], rows * row_bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(PRNGD_ENOMEM, "staging buffer (%llu bytes): %s",
+                        (unsigned long long)(rows * row_bytes), cudaGetErrorString(e));
         }
-        h->stage_rows = 0;
-        for (int i = 0; i < 2; ++i) {
-            const cudaError_t e = cudaMalloc(&h->stage[i], rows * row_bytes);
-            if (e != cudaSuccess) {
-                cudaGetLastError();
-                return fail(PRNGD_ENOMEM, "staging buffer (%llu bytes): %s",
-                            (unsigned long long)(rows * row_bytes), cudaGetErrorString(e));
-            }
-        }
-        h->stage_rows = rows;
+        h->stage_rows[i] = rows;
     }
     *rows_out = rows;
     return PRNGD_OK;
@@ -450,7 +447,7 @@ prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64
         cudaStream_t st = (cudaStream_t)cuda_stream;
         const uint64_t nps = h->p.n_per_stream;
         uint64_t rows = h->p.n_streams;
-        if (!d_out && (s = ensure_stage(h, &rows)) != PRNGD_OK) return s;
+        if (!d_out && (s = ensure_stage(h, 1ull << 30, 1, &rows)) != PRNGD_OK) return s;
         for (uint64_t r0 = 0; r0 < h->p.n_streams; r0 += rows) {
             const uint64_t nr = (h->p.n_streams - r0) < rows ? (h->p.n_streams - r0) : rows;
             GenArgs g = h->args;
@@ -491,7 +488,7 @@ prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stre
     const uint64_t nps = h->p.n_per_stream;
     const uint64_t row_bytes = nps * 8u;
     uint64_t rows = 0;
-    if ((s = ensure_stage(h, &rows)) != PRNGD_OK) return s;
+    if ((s = ensure_stage(h, 256ull << 20, 2, &rows)) != PRNGD_OK) return s;
     cudaError_t e;
     if (!h->copy_stream) {
         if ((e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)

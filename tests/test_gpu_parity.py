@@ -465,18 +465,28 @@ def test_mrg32k3a_generate_host(orc):
 
 def _mrg_stats_match(g, p, out=None):
     """Histogram and count against the oracle's; the power sums (R16, relative 1e-12) against
-    pairwise (numpy) sums of the oracle's outputs: at 10^7-10^8 outputs the oracle's own
-    sequential sums drift by ~1e-12 relative themselves."""
+    pairwise (numpy) sums of the oracle's outputs, taken over 2048-stream pieces: at 10^7-10^8
+    outputs the oracle's own sequential sums drift by ~1e-12 relative themselves."""
     _, hist, pw, cnt = g.generate_consume(out)
     torch.cuda.synchronize()
-    ref = orc_mod().generate(p, want_out=True, want_stats=True)
-    assert np.array_equal(hist.cpu().numpy(), ref["hist"])
-    assert cnt.item() == ref["count"] == p["n_streams"] * p["n_per_stream"]
-    z = ref["out"].ravel()
-    z2 = z * z
-    exact = np.array([z.sum(), z2.sum(), (z2 * z).sum(), (z2 * z2).sum()])
-    assert np.allclose(pw.cpu().numpy(), exact, rtol=1e-12, atol=0)
-    return ref
+    h = np.zeros(65536, dtype=np.int64)
+    c = 0
+    parts = []
+    for s0 in range(0, p["n_streams"], 2048):
+        ns = min(2048, p["n_streams"] - s0)
+        r = orc_mod().generate(p, stream_begin=p.get("stream_begin", 0) + s0, n_streams=ns,
+                               want_out=True, want_stats=True)
+        h += r["hist"]
+        c += r["count"]
+        z = r["out"].ravel()
+        z2 = z * z
+        parts.append([z.sum(), z2.sum(), (z2 * z).sum(), (z2 * z2).sum()])
+        if out is not None:
+            got = out[s0:s0 + ns].cpu().numpy()
+            assert np.array_equal(got.view(np.int64), r["out"].view(np.int64))
+    assert np.array_equal(hist.cpu().numpy(), h)
+    assert cnt.item() == c == p["n_streams"] * p["n_per_stream"]
+    assert np.allclose(pw.cpu().numpy(), np.array(parts).sum(axis=0), rtol=1e-12, atol=0)
 
 
 def orc_mod():
@@ -491,14 +501,14 @@ def test_mrg32k3a_generate_consume(kind):
              flags=P.PRNGD_FLAG_MRG32K3A | P.MAP_FLAGS[kind], mrg=True, map=kind)
     g = P.Generator(**p)
     out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
-    ref = _mrg_stats_match(g, p, out)
-    assert np.array_equal(out.cpu().numpy().view(np.int64), ref["out"].view(np.int64))
+    _mrg_stats_match(g, p, out)
     assert g.last_launches == 4
 
 
 def test_mrg32k3a_consume_only_chunks():
-    """Consume-only (no output buffer): staged 256 MiB chunks, the statistics accumulate."""
-    p = dict(w=26, a0=5, a=2**26 - 3, b0=0, b=2**20 - 1, seed=3, n_streams=3000,
+    """Consume-only (no output buffer): staged 1 GiB chunks (10944 streams of 96 KiB here),
+    the statistics accumulate over the chunks."""
+    p = dict(w=26, a0=5, a=2**26 - 3, b0=0, b=2**20 - 1, seed=3, n_streams=11500,
              n_per_stream=12288, flags=P.PRNGD_FLAG_MRG32K3A, mrg=True)
     g = P.Generator(**p)
     _mrg_stats_match(g, p)
