@@ -198,7 +198,7 @@ int oracle_generate_gen(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64
                         int64_t *hist, double *pw, int64_t *count)
 {
     if (!valid(w, a0, a, b0, b)) return 1;
-    if (mrg && (alg1 || bitlen(a) > 31 || bitlen(b) > 31)) return 1;
+    if (mrg && (bitlen(a) > 31 || bitlen(b) > 31)) return 1;
     if (kind != 4 && kind != 5 && kind != 6) return 1;
     if (kind == 6 && !(a0 == 0 && b0 == 0 && a == (1ull << w) - 1 && b == a)) return 1;
     int sh1 = 32 - bitlen(a); /* R4: x = top bits of the 32-bit draw */
@@ -212,7 +212,16 @@ int oracle_generate_gen(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64
         uint64_t p = 0; /* pairs (R2) or draws (Alg. 1) consumed so far */
         for (uint64_t j = 0; j < n_per_stream; j++) {
             uint32_t x1, x2;
-            if (mrg) {
+            if (mrg && alg1) {
+                /* Alg. 1 over reduced MRG32k3a values (R23): redraw R1 alone until
+                   accepted, then draw R2 */
+                do {
+                    x1 = oracle_mrg_reduced(ms, bitlen(a), &mdraws);
+                    p++;
+                } while (!oracle_accept(a0, a, x1));
+                x2 = oracle_mrg_reduced(ms, bitlen(b), &mdraws);
+                p++;
+            } else if (mrg) {
                 /* pair-drop (R2) over pairs of reduced MRG32k3a values (R23) */
                 do {
                     x1 = oracle_mrg_reduced(ms, bitlen(a), &mdraws);

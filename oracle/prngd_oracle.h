@@ -90,8 +90,8 @@ uint32_t oracle_mrg_next(int64_t s[6]);
 void oracle_mrg_stream_state(uint64_t seed, uint64_t s, int64_t st[6]);
 uint32_t oracle_mrg_reduced(int64_t st[6], int width, uint64_t *draws);
 /* oracle_generate_ex with a base-generator switch: mrg != 0 draws x1, x2 as reduced MRG32k3a
- * values of bitlen(a), bitlen(b) bits (both <= 31; pair-drop only); consumed[] then counts MRG
- * outputs. */
+ * values of bitlen(a), bitlen(b) bits (both <= 31; pair-drop, or Alg. 1 with alg1 != 0);
+ * consumed[] then counts MRG outputs. */
 int oracle_generate_gen(uint32_t w, uint64_t a0, uint64_t a, uint64_t b0, uint64_t b,
                         uint64_t seed, uint64_t stream_begin, uint64_t n_streams,
                         uint64_t n_per_stream, int kind, int alg1, int open_interval, int mrg,

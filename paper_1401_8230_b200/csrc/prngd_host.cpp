@@ -120,8 +120,8 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     const bool mrg = (p->flags & PRNGD_FLAG_MRG32K3A) != 0;
     if (mrg && (bit_length(p->a) > 31 || bit_length(p->b) > 31))
         return fail(PRNGD_EINVAL, "MRG32k3a draws are at most 31 bits wide (bitlen(a), bitlen(b) <= 31)");
-    if (mrg && (p->flags & (PRNGD_FLAG_ALG1 | PRNGD_FLAG_JUMP)))
-        return fail(PRNGD_EUNSUPPORTED, "MRG32k3a supports pair-drop consumption without jump-ahead");
+    if (mrg && (p->flags & PRNGD_FLAG_JUMP))
+        return fail(PRNGD_EUNSUPPORTED, "MRG32k3a has no jump-ahead path");
     if ((p->flags & PRNGD_FLAG_JUMP) && (p->flags & (PRNGD_FLAG_NO_JUMP | PRNGD_FLAG_ALG1)))
         return fail(PRNGD_EUNSUPPORTED, "jump-ahead needs pair-drop consumption and no NO_JUMP");
     if (p->flags & ~known) return fail(PRNGD_EUNSUPPORTED, "unknown flag bits 0x%x", p->flags & ~known);
@@ -363,7 +363,7 @@ prngd_status prngd_generate(const prngd_handle *h, double *d_out, void *cuda_str
     if (pl.mrg) {
         if (pl.store != Store::ROW && pl.store != Store::ROW1K)
             return fail(PRNGD_EUNSUPPORTED, "MRG32k3a needs a 16-byte aligned output and even n_per_stream");
-        e = prngd::launch_generate_mrg(g, (cudaStream_t)cuda_stream);
+        e = prngd::launch_generate_mrg(g, pl.alg1, (cudaStream_t)cuda_stream);
     } else if (pl.jump) {
         const void *tables = nullptr;
         if ((e = prngd::jump_tables(prngd::kJumpDraws, &tables)) != cudaSuccess)
@@ -458,7 +458,7 @@ prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64
             if (pl.store != Store::ROW && pl.store != Store::ROW1K)
                 return fail(PRNGD_EUNSUPPORTED,
                             "MRG32k3a needs a 16-byte aligned output and even n_per_stream");
-            cudaError_t e = prngd::launch_generate_mrg(g, st);
+            cudaError_t e = prngd::launch_generate_mrg(g, pl.alg1, st);
             if (e != cudaSuccess) return cuda_fail(e, "generate kernel launch");
             int l = 0;
             e = prngd::launch_consume_memory(h->args, g.out, nr * nps, d_hist, d_pow, d_count,
@@ -514,7 +514,7 @@ prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stre
         const Plan pl = plan_for(h, h->stage[b]);
         if (pl.mrg && pl.store != Store::ROW && pl.store != Store::ROW1K)
             return fail(PRNGD_EUNSUPPORTED, "MRG32k3a needs an even n_per_stream");
-        e = pl.mrg ? prngd::launch_generate_mrg(g, gs) : launch_rows(g, pl, gs, sms);
+        e = pl.mrg ? prngd::launch_generate_mrg(g, pl.alg1, gs) : launch_rows(g, pl, gs, sms);
         if (e != cudaSuccess) return cuda_fail(e, "generate kernel launch");
         ++launches;
         if ((e = cudaEventRecord(h->ev_gen[b], gs)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");

@@ -92,7 +92,7 @@ cudaError_t launch_consume_memory(const GenArgs &g, const double *src, uint64_t 
                                   double *d_pow, int64_t *d_count, void *scratch,
                                   size_t scratch_bytes, cudaStream_t st, int num_sms,
                                   int *launches);
-cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st);
+cudaError_t launch_generate_mrg(const GenArgs &g, bool alg1, cudaStream_t st);
 cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *tables,
                                  cudaStream_t st);
 cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *tables,

@@ -448,7 +448,7 @@ static_assert(kMrgRingBytes >= 8u * kCols + 4u * kMrgStep, "MRG ring smaller tha
 #endif
 template <int FP> struct MrgWord { using T = uint32_t; };
 template <> struct MrgWord<1> { using T = double; };
-template <bool EQ4, bool SAMEW>
+template <bool EQ4, bool SAMEW, bool ALG1 = false>
 struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold and mask)
     using T1 = typename MrgWord<PRNGD_MRG_FP64 >= 1 ? 1 : 0>::T;  // component 1 word
     using T2 = typename MrgWord<PRNGD_MRG_FP64 >= 2 ? 1 : 0>::T;  // component 2 word
@@ -501,9 +501,16 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
         // (4 = the pending x1 is outside the band) is rewritten by every valid draw; only an
         // x1's value is ever read (at the next valid draw, which is then an x2)
         const uint32_t bad = accepted(xm, g.lo, g.span) ? 0u : 4u;
-        const uint32_t d = 4u - ((odd & bad1) << 1);
-        wr = v ? wr + d : wr;
-        bad1 = v ? bad : bad1;
+        if (ALG1) {
+            // Alg. 1: an x1 outside the band is redrawn alone (not kept), x2 is
+            // never tested
+            const bool keep = odd != 0u || bad == 0u;
+            wr = (v && keep) ? wr + 4u : wr;
+        } else {
+            const uint32_t d = 4u - ((odd & bad1) << 1);
+            wr = v ? wr + d : wr;
+            bad1 = v ? bad : bad1;
+        }
     }
     __device__ __forceinline__ void operator()(double (&q)[kCols], const GenArgs &g) {
 #pragma unroll 1
@@ -896,7 +903,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
 constexpr int kMrgCols = PRNGD_MRG_RC;
 constexpr size_t kMrgTileBytes = (size_t)32 * (kMrgCols * 8 + 16);
 constexpr size_t kMrgStageBytes = PRNGD_MRG_STAGE == 0 ? kMrgTileBytes : 0;
-template <bool EQ4, bool SAMEW>
+template <bool EQ4, bool SAMEW, bool ALG1>
 __global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ GenArgs g) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t lane = threadIdx.x & 31u;
@@ -905,7 +912,7 @@ __global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ Gen
     // 256-byte alignment is all the rings need (no TMA here): a smaller footprint, more warps
     const uint32_t base = (smem_u32(smem_raw) + (kMrgRingBytes - 1)) & ~(kMrgRingBytes - 1);
     static_assert(kMrgTileBytes % kMrgRingBytes == 0, "rings must stay kMrgRingBytes aligned");
-    MrgProducer2<EQ4, SAMEW> prod(g, g.stream_begin + row0 + lane,
+    MrgProducer2<EQ4, SAMEW, ALG1> prod(g, g.stream_begin + row0 + lane,
                                   base + (uint32_t)kMrgStageBytes + lane * kMrgRingBytes, lane);
     if constexpr (PRNGD_MRG_STAGE == 2) {
         // Every lane consumes exactly 128 bytes of its ring per batch, and its read counter
@@ -1832,14 +1839,16 @@ cudaError_t launch_consume_memory(const GenArgs &g0, const double *src, uint64_t
     return cudaSuccess;
 }
 
-cudaError_t launch_generate_mrg(const GenArgs &g, cudaStream_t st) {
+cudaError_t launch_generate_mrg(const GenArgs &g, bool alg1, cudaStream_t st) {
     const size_t smem = kMrgRingBytes + kMrgStageBytes + (size_t)32 * kMrgRingBytes;
     const uint64_t grid = (g.n_streams + 31) / 32;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     const bool eq4 = g.map.kind == 4 && g.map.open == 0 && g.w <= 31;
     const bool samew = g.mrg_t1 == g.mrg_t2 && g.mrg_mask1 == g.mrg_mask2;
-    auto k = eq4 ? (samew ? gen_mrg_kernel<true, true> : gen_mrg_kernel<true, false>)
-                 : (samew ? gen_mrg_kernel<false, true> : gen_mrg_kernel<false, false>);
+    auto k = alg1 ? (eq4 ? gen_mrg_kernel<true, false, true> : gen_mrg_kernel<false, false, true>)
+                  : eq4 ? (samew ? gen_mrg_kernel<true, true, false> : gen_mrg_kernel<true, false, false>)
+                        : (samew ? gen_mrg_kernel<false, true, false>
+                                 : gen_mrg_kernel<false, false, false>);
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
     k<<<(unsigned)grid, 32, smem, st>>>(g);

@@ -180,9 +180,12 @@ def test_mrg_flag_rules(lib):
         P.prngd_create(**W.FULL32, seed=1, n_streams=1, n_per_stream=2, flags=P.PRNGD_FLAG_MRG32K3A)
     assert e.value.status == P.PRNGD_EINVAL
     p = dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1)
-    with pytest.raises(P.PrngdError):
+    with pytest.raises(P.PrngdError):   # no jump-ahead for MRG32k3a
         P.prngd_create(**p, seed=1, n_streams=1, n_per_stream=2,
-                       flags=P.PRNGD_FLAG_MRG32K3A | P.PRNGD_FLAG_ALG1)
+                       flags=P.PRNGD_FLAG_MRG32K3A | P.PRNGD_FLAG_JUMP)
+    h = P.prngd_create(**p, seed=1, n_streams=1, n_per_stream=2,
+                       flags=P.PRNGD_FLAG_MRG32K3A | P.PRNGD_FLAG_ALG1)   # Alg. 1 on MRG32k3a
+    P.prngd_destroy(h)
     h = P.prngd_create(**p, seed=1, n_streams=1, n_per_stream=2, flags=P.PRNGD_FLAG_MRG32K3A)
     assert P.prngd_get_info(h)["speculative"] == 0
     P.prngd_destroy(h)

@@ -494,6 +494,18 @@ def orc_mod():
     return oracle
 
 
+def test_mrg32k3a_alg1_bitwise(orc):
+    """Alg. 1 consumption on MRG32k3a: a narrow band (most x1 redrawn) and a wide one."""
+    for par in (dict(w=16, a0=3000, a=3400, b0=0, b=2**16 - 1),
+                dict(w=26, a0=5, a=2**26 - 3, b0=0, b=2**20 - 1)):
+        p = dict(par, seed=13, n_streams=333, n_per_stream=258, alg1=True, mrg=True,
+                 flags=P.PRNGD_FLAG_MRG32K3A | P.PRNGD_FLAG_ALG1)
+        _, out = gen(p)
+        assert_same(out, orc.generate(p)["out"])
+        g = P.Generator(**p)
+        _mrg_stats_match(g, p)
+
+
 @pytest.mark.parametrize("kind", [4, 5])
 def test_mrg32k3a_generate_consume(kind):
     """S7 on the MRG32k3a path (generate, then the histogram kernel over the written values)."""

@@ -82,10 +82,12 @@ def _mrg_case(i):
     p = dict(w=w, a0=a0, a=a, b0=0, b=b, seed=int(rng.integers(0, 2**63)), stream_begin=int(i * 977),
              n_streams=int(rng.integers(1, 200)), n_per_stream=2 * int(rng.integers(1, 300)),
              mrg=True)
-    return p, P.PRNGD_FLAG_MRG32K3A | P.MAP_FLAGS[kind], kind
+    alg1 = bool(rng.random() < 0.35)  # Alg. 1 consumption on MRG32k3a
+    p["alg1"] = alg1
+    return p, P.PRNGD_FLAG_MRG32K3A | P.MAP_FLAGS[kind] | (P.PRNGD_FLAG_ALG1 if alg1 else 0), kind
 
 
-@pytest.mark.parametrize("i", range(16))
+@pytest.mark.parametrize("i", range(24))
 def test_random_parameter_sets_mrg32k3a_bitwise(orc, i):
     p, flags, kind = _mrg_case(i)
     g = P.Generator(**dict(p, flags=flags))

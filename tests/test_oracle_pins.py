@@ -451,6 +451,37 @@ def test_mrg32k3a_definition_first_outputs(orc):
         assert u == (z if z else M1) and 1 <= u <= M1
 
 
+def test_mrg_alg1_consumption(orc):
+    """Alg. 1 on reduced MRG32k3a values (R23).  Pins: (a) with a band that rejects
+    nothing in these streams, Alg. 1 and pair-drop consume the same values in the same order, so
+    the outputs coincide; (b) with a narrow band, the Alg. 1 stream is the reduced-value sequence
+    cut as 'first in-band value, then the next value', read off the pair-drop-free raw sequence."""
+    full = dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1, seed=21, n_streams=16,
+                n_per_stream=300, mrg=True)
+    pd = orc.generate(full, want_pidx=True)
+    assert np.array_equal(pd["pidx"], np.tile(np.arange(300, dtype=np.uint32), (16, 1)))
+    a1 = orc.generate(full, alg1=True)
+    assert np.array_equal(a1["out"].view(np.int64), pd["out"].view(np.int64))
+    # (b): w = 8 draws (x = top... reduced to 8 bits), band a0 < x1 < a with a - a0 = 40
+    p = dict(w=8, a0=100, a=140, b0=0, b=255, seed=22, n_streams=1, n_per_stream=200, mrg=True)
+    r = orc.generate(p, alg1=True, want_consumed=True)
+    st = list(orc.mrg_stream_state(p["seed"], 0))
+    m1 = 2**32 - 209
+    T = (m1 // 256) * 256
+    raw = [u - 1 for u in orc.mrg_sequence(st, int(r["consumed"][0]))]
+    vals = [x & 255 for x in raw if x < T]            # R23: reduce to 8 bits by rejection
+    x1s, x2s, k = [], [], 0
+    while len(x1s) < 200:
+        while not (100 < vals[k] < 140):              # Alg. 1: redraw R1 alone
+            k += 1
+        x1s.append(vals[k])
+        x2s.append(vals[k + 1])
+        k += 2
+    assert k == len(vals)                             # every consumed value was used
+    z = orc.map_kind(p, 4, np.array(x1s, np.uint32), np.array(x2s, np.uint32))
+    assert np.array_equal(np.asarray(z).view(np.int64), r["out"].ravel().view(np.int64))
+
+
 def test_mrg_stream_states_in_range(orc):
     for s in range(300):
         st = orc.mrg_stream_state(1, s)
