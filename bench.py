@@ -494,6 +494,19 @@ def main():
             "frac_of_8TBs_nominal": achieved / 8000.0}
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     clk_ghz = (ClockSampler.max_mhz_static() or 1965) / 1e3
+    if consume and not args.no_write and not p.get("mrg"):
+        # The fused write + statistics kernel is not HBM-bound (S7): its
+        # instruction-issue share, from the algorithmic count per output -- generator 18
+        # (2 xorshift128 draws x 6, band test 1, Eq.(4) 5), statistics 11 (power sums 5; bin and
+        # packed add 6), store 1.5 (STS, LDS, STG per 2 outputs): 30.5 -- against 4 schedulers x
+        # 32 lanes x SMs x max SM clock.
+        ins = 30.5
+        roof["issue"] = {"algorithmic_instructions_per_output": ins,
+                         "achieved": ins * nout / (kern_ms * 1e-3) / 1e9,
+                         "peak": 4 * 32.0 * sms * clk_ghz, "unit": "Ginstr/s",
+                         "frac": ins * nout / (kern_ms * 1e-3) / 1e9 / (4 * 32.0 * sms * clk_ghz),
+                         "note": "issue/latency-bound with 16 warps per SM: 35.6 issued per "
+                                 "output at 64% issue (profiles/r01g_summary.txt)"}
     if consume and args.no_write:
         # Nothing is written: one shared-memory histogram add per output.  Peak = the measured
         # rate of the same packed adds (no return value) at the kernel's 24 warps per SM
