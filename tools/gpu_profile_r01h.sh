@@ -1,0 +1,16 @@
+#!/bin/bash
+# Round-1 final evidence (MRG32k3a consume + Alg. 1, generate_host on MRG, bench roofline.issue):
+# the whole GPU test suite, ncu captures of those kernels, the default bench line's launch list,
+# the benchmark sweep.
+mkdir -p gpurun_out
+python -m paper_1401_8230_b200.build > gpurun_out/build.log 2>&1
+timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/gputests_full.log 2>&1; echo "tests rc=$?"
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+bash tools/prof_one.sh r01h_mrg26 gen_mrg --workload mrg26
+bash tools/prof_one.sh r01h_cfg3_row gen_kernel --workload cfg3
+bash tools/prof_one.sh r01h_cfg5_consume consume_kernel --workload cfg5
+python bench.py > gpurun_out/r01h_default_plain.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+      --log-file gpurun_out/r01h_default_launches.csv python bench.py > /dev/null 2>&1
+bash tools/bench_all.sh
+echo profiled
