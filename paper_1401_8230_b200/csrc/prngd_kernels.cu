@@ -994,6 +994,12 @@ constexpr uint64_t kJumpTail = PRNGD_JUMP_TAIL;  // remainders up to this many f
 #define PRNGD_JUMP_WARPS 4
 #endif
 constexpr int kJumpWarps = PRNGD_JUMP_WARPS;  // warps (streams) per CTA
+// Compaction run of one round: output p at byte 8 (p + p / 16).  Lane l writes its i-th
+// accepted output near p = 16 l + i, so without the pad every lane of a store hits the same
+// bank (a 128-byte stride); with it they spread over the banks.  Reads of consecutive p stay
+// contiguous within each run of 16.
+constexpr uint32_t kJumpCompBytes = 32u * kJumpPairs * 8u + (32u * kJumpPairs / 16u + 2u) * 8u;
+__device__ __forceinline__ uint32_t jump_comp_off(uint32_t p) { return (p + (p >> 4)) << 3; }
 
 __device__ __forceinline__ Xs128 jump_state(const uint4 *__restrict__ tab, const Xs128 &s) {
     const uint32_t words[4] = {s.x, s.y, s.z, s.w};
@@ -1038,7 +1044,7 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
     const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
     const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
-    const uint32_t comp = aligned_smem_base(smem_raw) + warp * (32u * kJumpPairs * 8u);
+    const uint32_t comp = aligned_smem_base(smem_raw) + warp * kJumpCompBytes;
     double *row_out = g.out + row * g.nps;
     Xs128 S = stream_start(g.seed, g.stream_begin + row);
     uint64_t base = 0;
@@ -1092,7 +1098,7 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
 #pragma unroll
         for (int i = 0; i < kJumpPairs; ++i) {
             if ((mask >> i) & 1u) {
-                sts_f64(comp + pos * 8u, q[i]);
+                sts_f64(comp + jump_comp_off(pos), q[i]);
                 ++pos;
             }
         }
@@ -1100,7 +1106,7 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
         const uint64_t n = (g.nps - base) < (uint64_t)total ? (g.nps - base) : (uint64_t)total;
         for (uint32_t j = lane; j < (uint32_t)n; j += 32u) {
             double v;
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(comp + j * 8u));
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(comp + jump_comp_off(j)));
             row_out[base + j] = v;
         }
         __syncwarp();
@@ -1861,7 +1867,7 @@ cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *t
     (void)tables;  // the kernel reads the lane-interleaved layout of the same matrices
     cudaError_t e0 = jump_tables_interleaved(kJumpDraws, &tables);
     if (e0 != cudaSuccess) return e0;
-    const size_t smem = 1024 + (size_t)kJumpWarps * 32 * kJumpPairs * 8;
+    const size_t smem = 1024 + (size_t)kJumpWarps * kJumpCompBytes;
     const uint64_t grid = (g.n_streams + kJumpWarps - 1) / kJumpWarps;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     const uint4 *t = static_cast<const uint4 *>(tables);
