@@ -216,7 +216,7 @@ PRNGD_API prngd_status prngd_debug_map(const prngd_handle *h, const uint32_t *d_
 
 /* Host-only check of the jump-ahead: out = T^n_draws * in for the xorshift128 state
  * (x, y, z, w) = in[0..3].  lane_table >= 0 applies instead the byte table the GPU uses for lane
- * `lane_table` (= T^(d * lane_table)) with per-lane distance d = n_draws, or d = 32 (the NEXT-3
+ * `lane_table` (= T^(d * lane_table)) with per-lane distance d = n_draws, or d = 34 (the NEXT-3
  * jump kernel's tables) when n_draws is 0; the SEG store path uses d = 256.  No CUDA call. */
 PRNGD_API prngd_status prngd_debug_jump(uint64_t n_draws, const uint32_t *in, uint32_t *out,
                                         int lane_table);

@@ -46,7 +46,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
         else:
-            cmd = [NVCC, *FLAGS, "-Wno-deprecated-gpu-targets", "-x", "c++", "-c", src, "-o", obj]
+            cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-Wno-deprecated-gpu-targets",
+                   "-x", "c++", "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode:
             sys.stderr.write(r.stdout + r.stderr)

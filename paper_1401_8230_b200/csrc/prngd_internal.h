@@ -66,8 +66,12 @@ struct Plan {
 };
 
 // NEXT-3 jump-ahead (prngd_jump.cpp): lane l of a warp starts a round at draw l*kJumpDraws of
-// its stream (kJumpDraws / 2 = 16 pairs per lane per round, 32 lanes per stream).
-constexpr uint64_t kJumpDraws = 32;
+// its stream (kJumpDraws / 2 = 17 pairs per lane per round, 32 lanes per stream: two rounds
+// cover a 1024-output row with up to 5.9% rejection, so no sequential tail is needed).
+#ifndef PRNGD_JUMP_PAIRS
+#define PRNGD_JUMP_PAIRS 17  // cfg2 A/B: 16 -> 224, 17 -> 249-251, 18 -> 232, 24 -> 224 Gd/s
+#endif
+constexpr uint64_t kJumpDraws = 2 * PRNGD_JUMP_PAIRS;
 // SEG store path: a lane owns a 1 KiB segment (kSegOut outputs = pairs) of its stream's row and
 // starts at draw j * kSegDraws (segment j) via the same byte tables built for that distance.
 constexpr uint64_t kSegOut = 128;

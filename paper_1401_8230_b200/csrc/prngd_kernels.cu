@@ -979,7 +979,7 @@ __global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ Gen
 
 // ------------------------------------------------------------------------------ NEXT-3 jump kernel
 // One warp per stream, kJumpWarps streams per CTA (a 4096-stream config is a single wave).  Each round, lane
-// l jumps the round-start state by l * kJumpDraws draws (J_l = T^(32 l), byte tables) and draws
+// l jumps the round-start state by l * kJumpDraws draws (J_l = T^(34 l), byte tables) and draws
 // kJumpPairs = 16 consecutive pairs, keeping the outputs in registers; a warp scan of the
 // per-lane accepted counts gives every accepted output its sequential position (pair-drop, R2),
 // the lanes scatter them into a compact shared-memory run, and the warp writes the run with
@@ -998,8 +998,12 @@ constexpr int kJumpWarps = PRNGD_JUMP_WARPS;  // warps (streams) per CTA
 // accepted output near p = 16 l + i, so without the pad every lane of a store hits the same
 // bank (a 128-byte stride); with it they spread over the banks.  Reads of consecutive p stay
 // contiguous within each run of 16.
+// (An odd kJumpPairs spreads the lanes by itself: no pad.)
+constexpr uint32_t kJumpPad = (kJumpPairs % 2 == 0) ? 1u : 0u;
 constexpr uint32_t kJumpCompBytes = 32u * kJumpPairs * 8u + (32u * kJumpPairs / 16u + 2u) * 8u;
-__device__ __forceinline__ uint32_t jump_comp_off(uint32_t p) { return (p + (p >> 4)) << 3; }
+__device__ __forceinline__ uint32_t jump_comp_off(uint32_t p) {
+    return (p + kJumpPad * (p >> 4)) << 3;
+}
 
 __device__ __forceinline__ Xs128 jump_state(const uint4 *__restrict__ tab, const Xs128 &s) {
     const uint32_t words[4] = {s.x, s.y, s.z, s.w};

@@ -160,9 +160,12 @@ def test_jump_ahead_matches_sequential_draws(lib, orc):
             got = P.prngd_debug_jump(n, st)
             # the state after n draws holds the last four outputs (x, y, z, w)
             assert got == tuple(seq[n - 4:n]) if n >= 4 else got[3] == seq[n - 1]
+        # NEXT-3 jump kernel tables: lane l of a round starts at draw 34 l (17 pairs per lane)
         for lane in (0, 1, 2, 17, 31):
-            assert P.prngd_debug_jump(0, st, lane) == P.prngd_debug_jump(32 * lane, st) if lane \
-                else P.prngd_debug_jump(0, st, 0) == st
+            if lane:
+                assert P.prngd_debug_jump(0, st, lane) == tuple(seq[34 * lane - 4:34 * lane])
+            else:
+                assert P.prngd_debug_jump(0, st, 0) == st
         # SEG store path tables: lane j of a row starts at draw 256 j (pair 128 j)
         seq = orc.xs128_sequence(st, 256 * 31)
         for lane in (1, 2, 7, 15, 31):
