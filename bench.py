@@ -525,13 +525,14 @@ def main():
                 "note": "issue-bound below this peak (DESIGN.md section 8)"}
     elif p.get("mrg"):
         # MRG32k3a (NEXT-2): instruction-issue bound.  Algorithmic
-        # instructions per output: per MRG32k3a draw 27 (two binary64 components x 5: product,
-        # fused product-difference, rounding-shift pair, remainder; combination 9: two exact
-        # conversions, two canonical-representative fixes of 2, subtract-and-wrap 3; R23 test +
-        # mask 2; band test 2; ring append 4), 2.03 draws per output (26-bit reduce-to-width
-        # rejects 1/64), plus 9 per output (Eq.(4) 6, ring read 2, store 1): 27 x 2.03 + 9 = 64.
+        # instructions per output (mrg26 runs the per-batch band test): per MRG32k3a draw 24
+        # (two binary64 components x 5: product, fused product-difference, rounding-shift pair,
+        # remainder; combination 9: two exact conversions, two canonical-representative fixes
+        # of 2, subtract-and-wrap 3; R23 test + mask 2; ring append 3: address, predicated store,
+        # counter), 2.03 draws per output (26-bit reduce-to-width rejects 1/64), plus 11 per
+        # output (Eq.(4) 6, ring read 2, band test 2, store 1): 24 x 2.03 + 11 = 60.
         # Peak: 4 schedulers x 32 lanes per clock per SM x SMs x max SM clock.
-        ops = 64.0
+        ops = 60.0
         ach = ops * nout / (kern_ms * 1e-3) / 1e9
         pk = 4 * 32.0 * sms * clk_ghz
         roof = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "Ginstr/s", "frac": ach / pk,

@@ -448,7 +448,42 @@ static_assert(kMrgRingBytes >= 8u * kCols + 4u * kMrgStep, "MRG ring smaller tha
 #endif
 template <int FP> struct MrgWord { using T = uint32_t; };
 template <> struct MrgWord<1> { using T = double; };
-template <bool EQ4, bool SAMEW, bool ALG1 = false>
+// SPECB slow path: rewrite a lane's buffered draws [rd, wr) of its ring (kMrgRingBytes at
+// `ring`) without the out-of-band x1 (and, pair-drop, its x2), in order; a trailing pending x1
+// stays pending (pair-drop drops its pair once the x2 is drawn).  Returns the new write counter.
+template <bool ALG1>
+__device__ __noinline__ uint32_t mrg_drop_out_of_band(uint32_t ring, uint32_t rd, uint32_t wr,
+                                                      uint32_t lo, uint32_t span) {
+    uint32_t src = rd, dst = rd;
+    bool expect_x1 = true;
+    while (src != wr) {
+        uint32_t x;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(ring | (src & (kMrgRingBytes - 4u))));
+        bool keep = true;
+        if (expect_x1 && !accepted(x, lo, span)) {
+            if (ALG1) {
+                keep = false;             // Alg. 1: redraw x1 alone
+            } else if (src + 4u != wr) {
+                keep = false;             // pair-drop: the x2 goes with it
+                src += 4u;
+            }                             // else pending: kept, dropped once its pair completes
+        }
+        if (keep) {
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(ring | (dst & (kMrgRingBytes - 4u))), "r"(x)
+                         : "memory");
+            dst += 4u;
+            expect_x1 = !expect_x1;
+        }
+        src += 4u;
+    }
+    return dst;
+}
+
+// SPECB: the band test is taken out of the per-draw path (the host chose it because fewer than
+// 1 in 4096 x1 fall outside the band): every valid draw is appended, a batch checks its 16 x1
+// when it is read, and a warp with an out-of-band x1 compacts those lanes' rings (dropping the
+// pair, or the x1 alone for Alg. 1), refills and reads again.
+template <bool EQ4, bool SAMEW, bool ALG1 = false, bool SPECB = false>
 struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold and mask)
     using T1 = typename MrgWord<PRNGD_MRG_FP64 >= 1 ? 1 : 0>::T;  // component 1 word
     using T2 = typename MrgWord<PRNGD_MRG_FP64 >= 2 ? 1 : 0>::T;  // component 2 word
@@ -500,6 +535,10 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
         // a valid x2 completes the pair: kept (+4) or dropped with its x1 (-4).  bad1
         // (4 = the pending x1 is outside the band) is rewritten by every valid draw; only an
         // x1's value is ever read (at the next valid draw, which is then an x2)
+        if (SPECB) {  // band checked when the batch is read
+            wr = v ? wr + 4u : wr;
+            return;
+        }
         const uint32_t bad = accepted(xm, g.lo, g.span) ? 0u : 4u;
         if (ALG1) {
             // Alg. 1: an x1 outside the band is redrawn alone (not kept), x2 is
@@ -512,7 +551,7 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
             bad1 = v ? bad : bad1;
         }
     }
-    __device__ __forceinline__ void operator()(double (&q)[kCols], const GenArgs &g) {
+    __device__ __forceinline__ void fill(const GenArgs &g) {
 #pragma unroll 1
         while (__any_sync(0xFFFFFFFFu, wr - rd < 8u * (uint32_t)kCols)) {
             if (wr - rd <= kMrgRingBytes - 4u * kMrgStep) {  // room for kMrgStep more draws
@@ -527,14 +566,27 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
                 }
             }
         }
+    }
+    __device__ __forceinline__ void operator()(double (&q)[kCols], const GenArgs &g) {
+        uint32_t a1[kCols], a2[kCols];
+#pragma unroll 1
+        while (true) {
+            fill(g);
 #pragma unroll
-        for (int i = 0; i < kCols; ++i) {
-            uint32_t a1, a2;
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
-                         : "=r"(a1), "=r"(a2)
-                         : "r"(ring | ((rd + 8u * i) & (kMrgRingBytes - 8u))));
-            q[i] = EQ4 ? eq4_mode<1, false>(a1, a2, g) : map_pair<false, true>(a1, a2, g.map);
+            for (int i = 0; i < kCols; ++i)
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                             : "=r"(a1[i]), "=r"(a2[i])
+                             : "r"(ring | ((rd + 8u * i) & (kMrgRingBytes - 8u))));
+            if (!SPECB) break;
+            bool bad = false;
+#pragma unroll
+            for (int i = 0; i < kCols; ++i) bad |= !accepted(a1[i], g.lo, g.span);
+            if (__builtin_expect(!__any_sync(0xFFFFFFFFu, bad), 1)) break;
+            if (bad) wr = mrg_drop_out_of_band<ALG1>(ring, rd, wr, g.lo, g.span);
         }
+#pragma unroll
+        for (int i = 0; i < kCols; ++i)
+            q[i] = EQ4 ? eq4_mode<1, false>(a1[i], a2[i], g) : map_pair<false, true>(a1[i], a2[i], g.map);
         if (EQ4 && g.span != g.span_fast) {  // R11 clamp only where the host found it needed
 #pragma unroll
             for (int i = 0; i < kCols; ++i) q[i] = fmin(q[i], kBelowOne);
@@ -903,7 +955,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
 constexpr int kMrgCols = PRNGD_MRG_RC;
 constexpr size_t kMrgTileBytes = (size_t)32 * (kMrgCols * 8 + 16);
 constexpr size_t kMrgStageBytes = PRNGD_MRG_STAGE == 0 ? kMrgTileBytes : 0;
-template <bool EQ4, bool SAMEW, bool ALG1>
+template <bool EQ4, bool SAMEW, bool ALG1, bool SPECB = false>
 __global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ GenArgs g) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t lane = threadIdx.x & 31u;
@@ -912,7 +964,7 @@ __global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ Gen
     // 256-byte alignment is all the rings need (no TMA here): a smaller footprint, more warps
     const uint32_t base = (smem_u32(smem_raw) + (kMrgRingBytes - 1)) & ~(kMrgRingBytes - 1);
     static_assert(kMrgTileBytes % kMrgRingBytes == 0, "rings must stay kMrgRingBytes aligned");
-    MrgProducer2<EQ4, SAMEW, ALG1> prod(g, g.stream_begin + row0 + lane,
+    MrgProducer2<EQ4, SAMEW, ALG1, SPECB> prod(g, g.stream_begin + row0 + lane,
                                   base + (uint32_t)kMrgStageBytes + lane * kMrgRingBytes, lane);
     if constexpr (PRNGD_MRG_STAGE == 2) {
         // Every lane consumes exactly 128 bytes of its ring per batch, and its read counter
@@ -1855,10 +1907,21 @@ cudaError_t launch_generate_mrg(const GenArgs &g, bool alg1, cudaStream_t st) {
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     const bool eq4 = g.map.kind == 4 && g.map.open == 0 && g.w <= 31;
     const bool samew = g.mrg_t1 == g.mrg_t2 && g.mrg_mask1 == g.mrg_mask2;
-    auto k = alg1 ? (eq4 ? gen_mrg_kernel<true, false, true> : gen_mrg_kernel<false, false, true>)
-                  : eq4 ? (samew ? gen_mrg_kernel<true, true, false> : gen_mrg_kernel<true, false, false>)
-                        : (samew ? gen_mrg_kernel<false, true, false>
-                                 : gen_mrg_kernel<false, false, false>);
+    // band test per batch instead of per draw when fewer than 1 in 4096 x1 are out of band.
+    // Alg. 1 drops a single draw, which shifts the x1/x2 roles of the later ones: only when
+    // both have the same width (threshold and mask) is that harmless.
+    const uint64_t range1 = (uint64_t)g.mrg_mask1 + 1u;
+    const bool specb = (range1 - g.span) * 4096u < range1 && (!alg1 || samew);
+    auto k = alg1 ? (specb ? (eq4 ? gen_mrg_kernel<true, true, true, true>
+                                  : gen_mrg_kernel<false, true, true, true>)
+                           : (eq4 ? gen_mrg_kernel<true, false, true> : gen_mrg_kernel<false, false, true>))
+             : specb ? (eq4 ? (samew ? gen_mrg_kernel<true, true, false, true>
+                                     : gen_mrg_kernel<true, false, false, true>)
+                            : (samew ? gen_mrg_kernel<false, true, false, true>
+                                     : gen_mrg_kernel<false, false, false, true>))
+                     : eq4 ? (samew ? gen_mrg_kernel<true, true, false> : gen_mrg_kernel<true, false, false>)
+                           : (samew ? gen_mrg_kernel<false, true, false>
+                                    : gen_mrg_kernel<false, false, false>);
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
     k<<<(unsigned)grid, 32, smem, st>>>(g);

@@ -494,6 +494,18 @@ def orc_mod():
     return oracle
 
 
+@pytest.mark.parametrize("alg1", [False, True])
+@pytest.mark.parametrize("par", [dict(w=14, a0=0, a=2**14 - 1, b0=0, b=2**14 - 1),
+                                 dict(w=17, a0=3, a=2**17 - 2, b0=0, b=2**9 - 1)])
+def test_mrg32k3a_batch_band_test(orc, par, alg1):
+    """Per-batch band test (SPECB: fewer than 1 in 4096 x1 out of band): 1/8192 .. 1/26000 of the
+    x1 fall outside, so ~2-6% of the warp batches take the ring compaction and refill."""
+    p = dict(par, seed=17, n_streams=400, n_per_stream=2050, alg1=alg1, mrg=True,
+             flags=P.PRNGD_FLAG_MRG32K3A | (P.PRNGD_FLAG_ALG1 if alg1 else 0))
+    _, out = gen(p)
+    assert_same(out, orc.generate(p)["out"])
+
+
 def test_mrg32k3a_alg1_bitwise(orc):
     """Alg. 1 consumption on MRG32k3a: a narrow band (most x1 redrawn) and a wide one."""
     for par in (dict(w=16, a0=3000, a=3400, b0=0, b=2**16 - 1),
