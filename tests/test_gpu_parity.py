@@ -529,6 +529,17 @@ def test_mrg32k3a_generate_consume(kind):
     assert g.last_launches == 4
 
 
+def test_mrg32k3a_consume_open_interval_top_bin():
+    """R18 on the memory histogram: Eq.(5) with 1 - z' reaches 1.0, which lands in bin 65535."""
+    p = dict(w=8, a0=0, a=255, b0=0, b=255, seed=31, n_streams=4096, n_per_stream=258, mrg=True,
+             map=5, open=True,
+             flags=P.PRNGD_FLAG_MRG32K3A | P.MAP_FLAGS[5] | P.PRNGD_FLAG_OPEN)
+    g = P.Generator(**p)
+    out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+    _mrg_stats_match(g, p, out)
+    assert bool((out == 1.0).any())
+
+
 def test_mrg32k3a_consume_only_chunks():
     """Consume-only (no output buffer): staged 1 GiB chunks (10944 streams of 96 KiB here),
     the statistics accumulate over the chunks."""
