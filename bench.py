@@ -505,8 +505,9 @@ def main():
                          "achieved": ins * nout / (kern_ms * 1e-3) / 1e9,
                          "peak": 4 * 32.0 * sms * clk_ghz, "unit": "Ginstr/s",
                          "frac": ins * nout / (kern_ms * 1e-3) / 1e9 / (4 * 32.0 * sms * clk_ghz),
-                         "note": "issue/latency-bound with 16 warps per SM: 35.6 issued per "
-                                 "output at 64% issue (profiles/r01g_summary.txt)"}
+                         "note": "issue/latency-bound: 35.6-35.8 issued per output at 64% "
+                                 "issue with 16 warps per SM (profiles/r01h_summary.txt); "
+                                 "12 warps (current) run ~2.5% faster"}
     if consume and args.no_write:
         # Nothing is written: one shared-memory histogram add per output.  Peak = the measured
         # rate of the same packed adds (no return value) at the kernel's 24 warps per SM

@@ -67,11 +67,13 @@ constexpr size_t gen_smem() {
 constexpr int kConsWarpsTiles = 12;         // warps per CTA, consume kernel staging tiles in smem
 constexpr int kConsWarpsRegs = 24;          // warps per CTA, consume kernel without tiles (<= 85 regs)
 
-// consume + ROW store: 16 warps x 4 KiB tiles (128-byte row bursts) + the 128 KiB histogram.
-// A/B on cfg5 (write + histogram + moments): 6 x 16 KiB -> 415, 8 x 8 KiB -> 526,
-// 12 x 8 KiB -> 544, 16 x 4 KiB -> 561-566, 20 x 4 KiB -> 538, 24 x 4 KiB -> 525 Gd/s.
+// consume + ROW store: 12 warps x 4 KiB tiles (128-byte row bursts) + the 128 KiB histogram.
+// A/B on cfg5 (write + histogram + moments), first kernel: 6 x 16 KiB -> 415, 8 x 8 KiB -> 526,
+// 12 x 8 KiB -> 544, 16 x 4 KiB -> 561-566, 20 x 4 KiB -> 538, 24 x 4 KiB -> 525 Gd/s; current
+// kernel (4 KiB tiles): 8 -> 578, 10 -> 533-542, 12 -> 598-600, 14 -> 543-548, 16 -> 582-586,
+// 18 -> 527; 10-11 warps x 8 KiB -> 529-562 (cfg4 + histogram: 12 -> 574-577, 16 -> 572).
 #ifndef PRNGD_CONS_ROW_WARPS
-#define PRNGD_CONS_ROW_WARPS 16
+#define PRNGD_CONS_ROW_WARPS 12
 #define PRNGD_CONS_ROW_COLS 16
 #endif
 constexpr int kConsWarpsRow = PRNGD_CONS_ROW_WARPS;
