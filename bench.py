@@ -505,9 +505,8 @@ def main():
                          "achieved": ins * nout / (kern_ms * 1e-3) / 1e9,
                          "peak": 4 * 32.0 * sms * clk_ghz, "unit": "Ginstr/s",
                          "frac": ins * nout / (kern_ms * 1e-3) / 1e9 / (4 * 32.0 * sms * clk_ghz),
-                         "note": "issue/latency-bound: 35.6-35.8 issued per output at 64% "
-                                 "issue with 16 warps per SM (profiles/r01h_summary.txt); "
-                                 "12 warps (current) run ~2.5% faster"}
+                         "note": "issue/latency-bound: 35.3 issued per output at 64% issue, "
+                                 "ALU pipe 55%, 12 warps per SM (profiles/r01l_summary.txt)"}
     if consume and args.no_write:
         # Nothing is written: one shared-memory histogram add per output.  Peak = the measured
         # rate of the same packed adds (no return value) at the kernel's 24 warps per SM
