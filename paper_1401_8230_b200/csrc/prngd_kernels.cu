@@ -65,7 +65,10 @@ constexpr size_t gen_smem() {
                         : 1024 + (size_t)kGenWarps * (ST == Store::TMA ? 2 : 1) * kTileBytes;
 }
 constexpr int kConsWarpsTiles = 12;         // warps per CTA, consume kernel staging tiles in smem
-constexpr int kConsWarpsRegs = 24;          // warps per CTA, consume kernel without tiles (<= 85 regs)
+#ifndef PRNGD_CONS_REG_WARPS
+#define PRNGD_CONS_REG_WARPS 16  // cfg5 --no-write A/B: 12 -> 754, 16 -> 796, 20 -> 789, 24 -> 761, 28 -> 758, 32 -> 748
+#endif
+constexpr int kConsWarpsRegs = PRNGD_CONS_REG_WARPS;  // warps per CTA, consume kernel without tiles
 
 // consume + ROW store: 12 warps x 4 KiB tiles (128-byte row bursts) + the 128 KiB histogram.
 // A/B on cfg5 (write + histogram + moments), first kernel: 6 x 16 KiB -> 415, 8 x 8 KiB -> 526,
