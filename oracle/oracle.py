@@ -15,7 +15,8 @@ _CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-
 __all__ = [
     "build", "lib", "mix64", "splitmix64_output", "xs128_sequence", "stream_state", "constants",
     "map_pairs", "map_pairs_noclamp", "accept", "generate", "raw", "enumerate_pairs",
-    "map_eq5", "map_eq6", "map_kind", "mrg_sequence", "mrg_stream_state", "GAMMA",
+    "map_eq5", "map_eq6", "map_kind", "mrg_sequence", "mrg_stream_state", "mrg_reduced",
+    "GAMMA",
 ]
 
 GAMMA = 0x9E3779B97F4A7C15
@@ -72,6 +73,8 @@ def lib():
         L.oracle_mrg_next.argtypes = [vp]
         L.oracle_mrg_stream_state.restype = None
         L.oracle_mrg_stream_state.argtypes = [u64, u64, vp]
+        L.oracle_mrg_reduced.restype = u32
+        L.oracle_mrg_reduced.argtypes = [vp, i32, vp]
         L.oracle_map_kind.restype = dbl
         L.oracle_map_kind.argtypes = [i32, i32, u32, u64, u64, u64, u64, u32, u32]
         L.oracle_raw.restype = None
@@ -196,6 +199,14 @@ def mrg_stream_state(seed: int, s: int) -> tuple:
     st = np.zeros(6, dtype=np.int64)
     lib().oracle_mrg_stream_state(seed, s, st.ctypes.data)
     return tuple(int(v) for v in st)
+
+
+def mrg_reduced(state6, width: int, n: int) -> tuple[list[int], int]:
+    """n reduced (R23) values from MRG32k3a state `state6` and the draws they consumed."""
+    st = np.array(state6, dtype=np.int64)
+    d = C.c_uint64(0)
+    vals = [lib().oracle_mrg_reduced(st.ctypes.data, width, C.byref(d)) for _ in range(n)]
+    return vals, int(d.value)
 
 
 def map_kind(p: dict, kind: int, x1, x2, open_interval: bool = False) -> np.ndarray:

@@ -482,6 +482,51 @@ def test_mrg_alg1_consumption(orc):
     assert np.array_equal(np.asarray(z).view(np.int64), r["out"].ravel().view(np.int64))
 
 
+def test_mrg_stream_state_golden_vectors(orc):
+    """R22 pinned by literal vectors: SplitMix64(seed 1) outputs #3s..#3s+2 split (lo, hi) into
+    six words, the first three mod m1, the last three mod m2 (derivation in the golden's cite).
+    A swapped word order, an off-by-one output index or a missing reduction fails here."""
+    g = _gold("paper_examples.json")["mrg32k3a_stream_state_R22"]
+    for s, st in g["streams"].items():
+        assert orc.mrg_stream_state(g["seed"], int(s)) == tuple(st), f"stream {s}"
+    # the words of streams 0/1 are SURVEY Appendix A's independently computed xorshift states
+    a = _gold("survey_appendix_a.json")
+    w = [int(h, 16) for h in a["stream0_state"]] + [int(h, 16) for h in a["stream1_state"]]
+    assert list(g["streams"]["0"]) == w[:6]
+    assert list(g["streams"]["1"])[:2] == w[6:8]
+
+
+def test_mrg_reduce_to_width_literal_threshold(orc):
+    """SPEC S:228-236's literal T = 63 * 2^26 = 4227858432 for w = 26 (R23).  States are hand-cut
+    so the first draw is u = p1 exactly: with x-state (0, s1, *) and y-state (0, *, 0) the first
+    step gives p1 = 1403580 * s1 mod m1 and p2 = 0, so u = p1.  u - 1 = T must be discarded and
+    u - 1 = T - 1 kept as (T - 1) mod 2^26 = 2^26 - 1."""
+    T = _gold("paper_examples.json")["mrg32k3a_reduce_to_width_T"]["T"]
+    assert T == 4227858432
+    inv = pow(1403580, -1, M1)
+
+    def state_for_first_u(u):
+        return [0, (u * inv) % M1, 5, 0, 7, 0]
+
+    st = state_for_first_u(T + 1)                   # u - 1 = T: discarded
+    assert orc.mrg_sequence(list(st), 1) == [T + 1]
+    vals, draws = orc.mrg_reduced(st, 26, 1)
+    assert draws >= 2                                # the first draw was skipped
+    st = state_for_first_u(T)                        # u - 1 = T - 1: the largest kept value
+    vals, draws = orc.mrg_reduced(st, 26, 1)
+    assert (vals, draws) == ([2**26 - 1], 1)
+    st = state_for_first_u(M1)                       # u = m1 (x = y), u - 1 = m1 - 1 > T
+    vals, draws = orc.mrg_reduced(st, 26, 1)
+    assert draws >= 2
+    # and on a real stream: the discards of a long hand-cut sequence match the literal T
+    s0 = list(orc.mrg_stream_state(1, 0))
+    raw = orc.mrg_sequence(list(s0), 5000)
+    kept = [(u - 1) & (2**26 - 1) for u in raw if u - 1 < T]
+    vals, draws = orc.mrg_reduced(s0, 26, len(kept))
+    assert draws == 5000 and vals == kept
+    assert 5000 - len(kept) > 40                     # ~1/64 of the draws were discarded
+
+
 def test_mrg_stream_states_in_range(orc):
     for s in range(300):
         st = orc.mrg_stream_state(1, s)
