@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--workload", default="cfg3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--sustained-s", type=float, default=1.5,
+                    help="length of the sustained-throughput window (0: skip)")
     ap.add_argument("--consume", action="store_true",
                     help="add the fused consumer (S7) to a write workload (cfg5 always has it)")
     ap.add_argument("--no-write", action="store_true",
@@ -305,7 +307,8 @@ def main():
     # Test hooks for exercising the N > 1 code path on a one-GPU box (timings meaningless):
     # PRNGD_BENCH_SAME_GPU=1 puts every rank on cuda:0, PRNGD_BENCH_BACKEND=gloo avoids NCCL's
     # one-rank-per-GPU rule.  The driver's multi-GPU runs use neither.
-    if os.environ.get("PRNGD_BENCH_SAME_GPU") == "1":
+    same_gpu = os.environ.get("PRNGD_BENCH_SAME_GPU") == "1"
+    if same_gpu:
         local = 0
     torch.cuda.set_device(local)
     if world > 1:
@@ -368,9 +371,9 @@ def main():
 
     def step(st=stream):
         if consume and peer is not None:
-            # accumulates over steps into rank 0's peer-mapped buffer (no per-step collective)
-            P.prngd_generate_consume(g.handle, None if args.no_write else out, peer.hist,
-                                     peer.pow, peer.count, st)
+            # accumulates over steps into rank 0's peer-mapped buffer (no per-step collective);
+            # each call also bumps the accumulator's arrival counter (completion protocol)
+            peer.consume(g.handle, None if args.no_write else out, st)
         elif consume:
             hist.zero_(), pw.zero_(), cnt.zero_()
             P.prngd_generate_consume(g.handle, None if args.no_write else out, hist, pw, cnt, st)
@@ -469,6 +472,40 @@ def main():
         total_out = int(tt.item())
     value = total_out / (ms * 1e-3) / 1e9
 
+    # -------------------------------------------------- sustained window (power-capped regime)
+    # The driver's short run (e.g. 20 steps = 26 ms of cfg3) sees burst clocks; the same step
+    # repeated back to back for >= --sustained-s seconds shows the steady state under the
+    # board's power cap, with its own clock / power sample.
+    sustained = None
+    if args.sustained_s > 0 and not l2_flush:
+        n_sus = max(args.steps, int(args.sustained_s * 1e3 / max(ms, 1e-3)) + 1)
+        if world > 1:
+            tn = torch.tensor([n_sus], dtype=torch.int64, device="cuda")
+            dist.all_reduce(tn, op=dist.ReduceOp.MAX)
+            n_sus = int(tn.item())
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(torch.cuda.current_device()) as clk_s:
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for _ in range(n_sus):
+                if graph is not None:
+                    graph.replay()
+                else:
+                    step()
+            s1.record(stream)
+            torch.cuda.synchronize()
+        ts = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        ms_s = ts.item() / n_sus
+        sustained = {"value": total_out / (ms_s * 1e-3) / 1e9, "unit": "Gdoubles/s",
+                     "steps": n_sus, "seconds": ts.item() / 1e3, "ms_per_step": ms_s,
+                     "clocks": clk_s.summary(),
+                     "note": "same step back to back for >= --sustained-s s (device events, max "
+                             "over ranks); the headline value is the driver's short run"}
+
     # -------------------------------------------------- roofline of the dominant kernel
     # For write workloads the step is exactly one generate launch; its average duration is
     # the mean of the per-step event pairs on the launching stream.
@@ -543,6 +580,11 @@ def main():
                 "fp64_ops_per_output": 24.3, "kernel_ms": kern_ms,
                 "hbm_write_gbs": achieved}
 
+    if sustained is not None and roof["bound"] == "hbm":
+        sustained["achieved_gbs"] = bytes_launch * world / (sustained["ms_per_step"] * 1e-3) / 1e9 / world
+        sustained["roofline_frac"] = sustained["achieved_gbs"] / peak
+        sustained["frac_of_8TBs_nominal"] = sustained["achieved_gbs"] / 8000.0
+
     # -------------------------------------------------- pure-store ceiling on the same buffer
     # (B13, tools/write_ceiling.cu: incompressible values, 16/32-byte coalesced stores)
     if not consume:
@@ -584,30 +626,54 @@ def main():
         hh = torch.empty(65536, dtype=torch.int64, pin_memory=True)
         hp = torch.empty(4, dtype=torch.float64, pin_memory=True)
         hc = torch.empty(1, dtype=torch.int64, pin_memory=True)
-        step()
-        torch.cuda.synchronize()
+        if peer is not None:
+            # per-step results from the shared accumulator: start from zero, then every step
+            # rank 0 waits (device-side acquire on the arrival counter) for all ranks' calls,
+            # reads, and zeroes the statistics before the barrier releases the next step
+            torch.cuda.synchronize()
+            dist.barrier()
+            peer.zero(stream)
+            torch.cuda.synchronize()
+            dist.barrier()
+        else:
+            step()
+            torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        e2e_counts = []
         te = time.perf_counter()
-        for _ in range(args.e2e_steps):
+        for k in range(args.e2e_steps):
             step()
             if peer is not None:
+                if same_gpu:  # ranks share one GPU (test hook): host-side completion instead
+                    torch.cuda.synchronize()
+                    dist.barrier()
                 if rank == 0:
+                    if not same_gpu:
+                        peer.wait(peer.expected(k + 1), stream)
                     P.prngd_copy(hh, peer.hist, 65536 * 8, stream)
                     P.prngd_copy(hp, peer.pow, 32, stream)
                     P.prngd_copy(hc, peer.count, 8, stream)
+                    peer.zero(stream, counter=False)
+                torch.cuda.synchronize()
+                dist.barrier()
             else:
                 hh.copy_(hist, non_blocking=True)
                 hp.copy_(pw, non_blocking=True)
                 hc.copy_(cnt, non_blocking=True)
-            torch.cuda.synchronize()
+                torch.cuda.synchronize()
+            e2e_counts.append(int(hc[0]))
         de = torch.tensor([time.perf_counter() - te], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(de, op=dist.ReduceOp.MAX)
         e2e = {"value": world * nout * args.e2e_steps / de.item() / 1e9, "unit": "Gdoubles/s",
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 65536 * 8 + 32 + 8,
+               "counts_per_step_ok": all(c == world * nout for c in e2e_counts) if rank == 0
+                                     else None,
                "note": "prngd_generate_consume per step + D2H of the statistics (histogram, power "
-                       "sums, count) into pinned host memory, synchronised every step"}
+                       "sums, count) into pinned host memory, synchronised every step"
+                       + ("; N > 1: rank 0 waits on the accumulator's arrival counter, reads and "
+                          "zeroes it, then a barrier" if peer is not None else "")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -642,6 +708,7 @@ def main():
             "device": device_facts(torch),
             "gpu_launches": launches_per_step * args.steps,
             "per_step": step_stats,
+            "sustained": sustained,
             "pct_hbm_write_roofline": 100.0 * achieved / peak if roof["bound"] == "hbm" else None,
         }
         print(json.dumps(line), flush=True)

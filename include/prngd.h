@@ -58,8 +58,13 @@ typedef enum {
 /* flags */
 #define PRNGD_FLAG_IEEE_DIV   0x1u  /* use the IEEE division instruction sequence instead of the
                                        reciprocal + 2 FMA correction (R10); same bits, slower */
-/* Store-path selection, bits 3..5 (an A/B switch; every path writes the same bits):
- *   AUTO   (default, 0) SEG where it applies, else ROW; the fused consumer uses DIRECT
+/* Store-path selection, bits 3..5 (every path writes the same bits).  The product library
+ * implements AUTO, ROW and SEG; TMA, TILE, DIRECT, ROW1K and SEGC were measured slower
+ * and exist only in the A/B variant build (-DPRNGD_AB_STORES=1,
+ * tools/ab_variants.sh): the product library returns PRNGD_EUNSUPPORTED for them.
+ *   AUTO   (default, 0) ROW for bulk shapes; for few streams (n_streams < 16384, n_per_stream
+ *          >= 512) SEG when rejection is rare, else the NEXT-3 jump kernel; the fused consumer
+ *          always stages ROW tiles beside its histogram
  *   SEG    row segments: n_per_stream / 128 lanes share a row, lane j starts at pair 128 j of
  *          its stream by GF(2) jump-ahead and owns that 1 KiB segment; each flush writes 512-byte
  *          chunks of every segment.  Needs rare rejection (prngd_info.speculative), pair-drop
@@ -127,7 +132,8 @@ typedef enum {
 typedef struct {
     uint32_t w;             /* k = 2^-w, 1 <= w <= 32                                        */
     uint32_t flags;         /* PRNGD_FLAG_*; 0 = canonical (pair-drop, Eq.(4), clamp)         */
-    uint64_t a0, a;         /* x1 range [a0; a]: a < 2^32, a - a0 >= 2                        */
+    uint64_t a0, a;         /* x1 range [a0; a]: a < 2^32, a - a0 >= 2, and the accept band   */
+                            /* a0 < x1 < a holds >= 2^-16 of the 2^bitlen(a) draw values     */
     uint64_t b0, b;         /* x2 range [b0; b]: b0 == 0, b + 1 a power of two, b < 2^w (R5) */
     uint64_t seed;          /* SplitMix64 seed (R6)                                           */
     uint64_t stream_begin;  /* first GLOBAL stream id of this call (multi-GPU shard)          */
@@ -184,6 +190,23 @@ PRNGD_API prngd_status prngd_generate(const prngd_handle *h, double *d_out, void
 PRNGD_API prngd_status prngd_generate_consume(const prngd_handle *h, double *d_out, int64_t *d_hist,
                                     double *d_pow, int64_t *d_count, void *cuda_stream);
 
+/* As prngd_generate_consume, plus a completion signal for accumulators shared across GPUs:
+ * d_arrive (device, local or peer-mapped, 8-byte aligned; NULL = no signal) is incremented by
+ * one, with a system-scope release, after every statistic of this call has been added.  A
+ * reader that observes *d_arrive >= n (acquire; e.g. prngd_wait_arrivals) sees the complete
+ * statistics of those n calls.  The increment happens inside the call's last (finalize) kernel. */
+PRNGD_API prngd_status prngd_generate_consume_ex(const prngd_handle *h, double *d_out,
+                                                 int64_t *d_hist, double *d_pow, int64_t *d_count,
+                                                 uint64_t *d_arrive, void *cuda_stream);
+
+/* Enqueue on cuda_stream a one-thread kernel that waits (system-scope acquire loads) until
+ * *d_arrive >= target; later work on the stream then sees every add those arrivals covered.
+ * For ranks on DIFFERENT GPUs (a rank waiting on kernels of another process on the same GPU
+ * can starve them).  timeout_ns (0 = 60 s) bounds the wait: on expiry the kernel traps, which
+ * the caller sees as a launch failure at its next synchronisation. */
+PRNGD_API prngd_status prngd_wait_arrivals(const uint64_t *d_arrive, uint64_t target,
+                                           uint64_t timeout_ns, void *cuda_stream);
+
 /* End-to-end form for host memory: h_out (host, >= n_outputs doubles) receives the same
  * values as prngd_generate would write.  Generates in chunks of streams into device scratch
  * owned by the handle and overlaps the device->host copies with generation.  Synchronous:
@@ -204,8 +227,8 @@ PRNGD_API prngd_status prngd_debug_raw(const prngd_handle *h, uint32_t *d_raw, u
                              void *cuda_stream);
 
 /* d_pair_index[i * n_per_stream + j] = 0-based index of the pair that produced output j of
- * stream i (pair p = draws 2p, 2p+1); d_pairs_consumed[i] = pairs consumed by stream i.
- * Either pointer may be NULL. */
+ * stream i (pair p = draws 2p, 2p+1), modulo 2^32; d_pairs_consumed[i] = pairs consumed by
+ * stream i (64-bit).  Either pointer may be NULL. */
 PRNGD_API prngd_status prngd_debug_pairs(const prngd_handle *h, uint32_t *d_pair_index,
                                uint64_t *d_pairs_consumed, void *cuda_stream);
 

@@ -32,6 +32,10 @@ struct prngd_handle {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_gen[2] = {nullptr, nullptr};
     cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+    // recorded after the last reader of stage[0] enqueued by the MRG32k3a consume-only path;
+    // every later user of the staging buffers waits on it (the calls may use other streams)
+    cudaEvent_t ev_stage_free = nullptr;
+    bool stage_pending = false;
 };
 
 static thread_local char g_err[512] = "";
@@ -132,6 +136,22 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
     if (((p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT) > 7)
         return fail(PRNGD_EUNSUPPORTED, "unknown store path %u",
                     (p->flags & PRNGD_STORE_MASK) >> PRNGD_STORE_SHIFT);
+#if !PRNGD_AB_STORES
+    {
+        const uint32_t sp = p->flags & PRNGD_STORE_MASK;
+        if (sp != PRNGD_FLAG_STORE_AUTO && sp != PRNGD_FLAG_STORE_ROW && sp != PRNGD_FLAG_STORE_SEG)
+            return fail(PRNGD_EUNSUPPORTED,
+                        "store path %u is an A/B path of the variant build (-DPRNGD_AB_STORES=1); "
+                        "the product library has AUTO, ROW and SEG", sp >> PRNGD_STORE_SHIFT);
+    }
+#endif
+    // Accept band bound: one output costs 2^bitlen(a) / (a - a0 - 1) pairs on average; bands
+    // accepting fewer than 2^-16 of the x1 draws are refused (a near-empty band would stall a
+    // stream for ~2^31 pairs and wrap the 32-bit pair indices of prngd_debug_pairs).
+    if ((p->a - p->a0 - 1) << 16 < (1ull << bit_length(p->a)))
+        return fail(PRNGD_EINVAL,
+                    "accept band a0 < x1 < a holds %llu of 2^%d draw values: below the 2^-16 "
+                    "acceptance floor", (unsigned long long)(p->a - p->a0 - 1), bit_length(p->a));
 
     prngd_handle *h = new (std::nothrow) prngd_handle();
     if (!h) return fail(PRNGD_ENOMEM, "host allocation of the handle failed");
@@ -269,6 +289,7 @@ prngd_status prngd_destroy(prngd_handle *h) {
             if (h->ev_gen[i]) cudaEventDestroy(h->ev_gen[i]);
             if (h->ev_copy[i]) cudaEventDestroy(h->ev_copy[i]);
         }
+        if (h->ev_stage_free) cudaEventDestroy(h->ev_stage_free);
         if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
         if (cur >= 0) cudaSetDevice(cur);
     }
@@ -294,8 +315,8 @@ uint32_t prngd_last_launches(const prngd_handle *h) { return h ? h->last_launche
 // the next one that is legal (same bits whichever path writes them).
 static Plan plan_for(const prngd_handle *h, const void *out, bool consume) {
     Plan pl = h->plan;
-    // Fused consumer + outputs: 12 warps with 8 KiB row tiles (256-byte row bursts) next to the
-    // 128 KiB histogram (cfg5: 539 Gd/s vs 473 for the register DIRECT store).
+    // Fused consumer + outputs: the ROW tiles of consume_kernel next to its 128 KiB histogram
+    // (S7).
     if (consume && (pl.store == Store::SEG || pl.store == Store::SEGC || pl.store_auto))
         pl.store = Store::ROW;
     const uintptr_t a = (uintptr_t)out;
@@ -330,23 +351,24 @@ static Plan plan_for(const prngd_handle *h, const void *out, bool consume) {
         pl.jump = false;
         pl.store = Store::SEG;
     }
+    if ((pl.store == Store::ROW || pl.store == Store::ROW1K) && !a16) pl.store = Store::STG8;
+#if PRNGD_AB_STORES
     const bool tma_ok = a16 && h->p.n_streams < (1ull << 31) && nps < (1ull << 31);
     if (pl.store == Store::DIRECT && !a32) pl.store = a16 ? Store::STG16 : Store::STG8;
-    if ((pl.store == Store::ROW || pl.store == Store::ROW1K) && !a16) pl.store = Store::STG8;
     if (pl.store == Store::TMA && !tma_ok) pl.store = a16 ? Store::STG16 : Store::STG8;
     if (pl.store == Store::STG16 && !a16) pl.store = Store::STG8;
+#else
+    (void)a32;
+#endif
     return pl;
 }
 
-// Row-parallel generate kernels (one lane per stream, or per 1 KiB stream segment for SEG).
+// xorshift128 generate kernels: NEXT-3 jump (a warp per stream), SEG (a lane per row segment),
+// or one lane per stream (ROW / STG8).
 static cudaError_t launch_rows(const GenArgs &g, const Plan &pl, cudaStream_t st, int sms) {
+    if (pl.jump) return prngd::launch_generate_jump(g, pl, st);
     if (pl.store == Store::SEGC) return prngd::launch_generate_segc(g, pl, st);
-    if (pl.store == Store::SEG) {
-        const void *tables = nullptr;
-        cudaError_t e = prngd::jump_tables(prngd::kSegDraws, &tables);
-        if (e != cudaSuccess) return e;
-        return prngd::launch_generate_seg(g, pl, tables, st);
-    }
+    if (pl.store == Store::SEG) return prngd::launch_generate_seg(g, pl, st);
     return prngd::launch_generate(g, pl, st, sms);
 }
 
@@ -364,11 +386,6 @@ prngd_status prngd_generate(const prngd_handle *h, double *d_out, void *cuda_str
         if (pl.store != Store::ROW && pl.store != Store::ROW1K)
             return fail(PRNGD_EUNSUPPORTED, "MRG32k3a needs a 16-byte aligned output and even n_per_stream");
         e = prngd::launch_generate_mrg(g, pl.alg1, (cudaStream_t)cuda_stream);
-    } else if (pl.jump) {
-        const void *tables = nullptr;
-        if ((e = prngd::jump_tables(prngd::kJumpDraws, &tables)) != cudaSuccess)
-            return cuda_fail(e, "jump tables");
-        e = prngd::launch_generate_jump(g, h->plan, tables, (cudaStream_t)cuda_stream);
     } else {
         e = launch_rows(g, pl, (cudaStream_t)cuda_stream, sms);
     }
@@ -394,7 +411,8 @@ static prngd_status ensure_stage(prngd_handle *h, uint64_t target, int nbuf, uin
     const uint64_t row_bytes = h->p.n_per_stream * 8u;
     uint64_t rows = target / row_bytes;
     if (rows < 1) rows = 1;
-    rows = (rows + 31) / 32 * 32;          // whole warp tasks
+    if (rows >= 32) rows = rows / 32 * 32;  // whole warp tasks when the target holds them
+    // (the kernels handle a partial last warp, so long rows just take fewer, not 32, per chunk)
     if (rows > h->p.n_streams) rows = h->p.n_streams;
     for (int i = 0; i < nbuf; ++i) {
         if (h->stage_rows[i] >= rows) continue;
@@ -413,12 +431,28 @@ static prngd_status ensure_stage(prngd_handle *h, uint64_t target, int nbuf, uin
     return PRNGD_OK;
 }
 
+// The staging buffers may still be read by an earlier MRG32k3a consume-only call on another
+// stream: order this stream after it.
+static prngd_status wait_stage_free(prngd_handle *h, cudaStream_t st) {
+    if (!h->stage_pending) return PRNGD_OK;
+    cudaError_t e = cudaStreamWaitEvent(st, h->ev_stage_free, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent (staging buffer)");
+    return PRNGD_OK;
+}
+
 prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64_t *d_hist,
                                     double *d_pow, int64_t *d_count, void *cuda_stream) {
+    return prngd_generate_consume_ex(hc, d_out, d_hist, d_pow, d_count, nullptr, cuda_stream);
+}
+
+prngd_status prngd_generate_consume_ex(const prngd_handle *hc, double *d_out, int64_t *d_hist,
+                                       double *d_pow, int64_t *d_count, uint64_t *d_arrive,
+                                       void *cuda_stream) {
     if (!hc || !d_hist || !d_pow || !d_count)
         return fail(PRNGD_EINVAL, "null handle or accumulator pointer");
-    if (((uintptr_t)d_hist | (uintptr_t)d_pow | (uintptr_t)d_count) & 7u)
+    if (((uintptr_t)d_hist | (uintptr_t)d_pow | (uintptr_t)d_count | (uintptr_t)d_arrive) & 7u)
         return fail(PRNGD_EINVAL, "accumulators must be 8-byte aligned");
+    unsigned long long *arrive = reinterpret_cast<unsigned long long *>(d_arrive);
     if (d_out && ((uintptr_t)d_out & 7u)) return fail(PRNGD_EINVAL, "d_out must be 8-byte aligned");
     int sms = 0;
     prngd_status s = device_ready(&sms);
@@ -447,7 +481,10 @@ prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64
         cudaStream_t st = (cudaStream_t)cuda_stream;
         const uint64_t nps = h->p.n_per_stream;
         uint64_t rows = h->p.n_streams;
-        if (!d_out && (s = ensure_stage(h, 1ull << 30, 1, &rows)) != PRNGD_OK) return s;
+        if (!d_out) {
+            if ((s = ensure_stage(h, 1ull << 30, 1, &rows)) != PRNGD_OK) return s;
+            if ((s = wait_stage_free(h, st)) != PRNGD_OK) return s;
+        }
         for (uint64_t r0 = 0; r0 < h->p.n_streams; r0 += rows) {
             const uint64_t nr = (h->p.n_streams - r0) < rows ? (h->p.n_streams - r0) : rows;
             GenArgs g = h->args;
@@ -461,16 +498,27 @@ prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64
             cudaError_t e = prngd::launch_generate_mrg(g, pl.alg1, st);
             if (e != cudaSuccess) return cuda_fail(e, "generate kernel launch");
             int l = 0;
+            const bool last = r0 + nr >= h->p.n_streams;  // only the last chunk signals arrival
             e = prngd::launch_consume_memory(h->args, g.out, nr * nps, d_hist, d_pow, d_count,
-                                             h->cons_scratch, h->cons_bytes, st, sms, &l);
+                                             last ? arrive : nullptr, h->cons_scratch,
+                                             h->cons_bytes, st, sms, &l);
             if (e != cudaSuccess) return cuda_fail(e, "consume launch");
             launches += 1 + l;
+        }
+        if (!d_out) {
+            if (!h->ev_stage_free) {
+                cudaError_t e = cudaEventCreateWithFlags(&h->ev_stage_free, cudaEventDisableTiming);
+                if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+            }
+            cudaError_t e = cudaEventRecord(h->ev_stage_free, st);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+            h->stage_pending = true;
         }
         h->last_launches.store((uint32_t)launches);
         return PRNGD_OK;
     }
     cudaError_t e = prngd::launch_generate_consume(h->args, plan_for(h, d_out, true), d_out, d_hist,
-                                                   d_pow, d_count, h->cons_scratch,
+                                                   d_pow, d_count, arrive, h->cons_scratch,
                                                    h->cons_bytes, (cudaStream_t)cuda_stream, sms,
                                                    &launches);
     if (e != cudaSuccess) return cuda_fail(e, "generate_consume launch");
@@ -500,6 +548,7 @@ prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stre
         }
     }
     cudaStream_t gs = (cudaStream_t)cuda_stream;
+    if ((s = wait_stage_free(h, gs)) != PRNGD_OK) return s;
     uint32_t launches = 0;
     bool used[2] = {false, false};
     for (uint64_t r0 = 0, c = 0; r0 < h->p.n_streams; r0 += rows, ++c) {
@@ -515,6 +564,7 @@ prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stre
         if (pl.mrg && pl.store != Store::ROW && pl.store != Store::ROW1K)
             return fail(PRNGD_EUNSUPPORTED, "MRG32k3a needs an even n_per_stream");
         e = pl.mrg ? prngd::launch_generate_mrg(g, pl.alg1, gs) : launch_rows(g, pl, gs, sms);
+        // (launch_rows honours pl.jump, so prngd_get_info's kernel is the one that runs)
         if (e != cudaSuccess) return cuda_fail(e, "generate kernel launch");
         ++launches;
         if ((e = cudaEventRecord(h->ev_gen[b], gs)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
@@ -592,6 +642,15 @@ prngd_status prngd_debug_div_check(const prngd_handle *h, uint64_t n, uint64_t s
     if (e != cudaSuccess) return cuda_fail(e, "debug_div_check launch");
     h->last_launches.store(n ? 1 : 0);
     return PRNGD_OK;
+}
+
+prngd_status prngd_wait_arrivals(const uint64_t *d_arrive, uint64_t target, uint64_t timeout_ns,
+                                 void *cuda_stream) {
+    if (!d_arrive || ((uintptr_t)d_arrive & 7u)) return fail(PRNGD_EINVAL, "null or misaligned counter");
+    cudaError_t e = prngd::launch_wait_arrivals(
+        reinterpret_cast<const unsigned long long *>(d_arrive), target,
+        timeout_ns ? timeout_ns : 60ull * 1000000000ull, (cudaStream_t)cuda_stream);
+    return e == cudaSuccess ? PRNGD_OK : cuda_fail(e, "wait_arrivals launch");
 }
 
 prngd_status prngd_peer_alloc(uint64_t bytes, void **d_ptr) {

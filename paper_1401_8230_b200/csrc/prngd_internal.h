@@ -51,6 +51,13 @@ enum class Store : int {
     TMA = 0, STG16 = 1, STG8 = 2, DIRECT = 3, ROW = 4, ROW1K = 5, SEG = 6, SEGC = 7
 };
 
+// Store paths measured slower than ROW / SEG (TMA, TILE = STG16, DIRECT, ROW1K, SEGC; DESIGN.md
+// section 5) are instantiated only in the A/B variant build (tools/ab_variants.sh passes
+// -DPRNGD_AB_STORES=1); the product library rejects their flags with PRNGD_EUNSUPPORTED.
+#ifndef PRNGD_AB_STORES
+#define PRNGD_AB_STORES 0
+#endif
+
 // Launch descriptors chosen by the host.
 struct Plan {
     bool spec;      // speculative batch acceptance (rare rejection)
@@ -86,21 +93,24 @@ void jump_host(uint64_t n_draws, const uint32_t in[4], uint32_t out[4], int lane
 
 // Launchers (prngd_kernels.cu).  They return cudaGetLastError() of the launch.
 cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, int num_sms);
+// d_arrive (nullable): +1 with a system-scope release once every statistic of the call is added
 cudaError_t launch_generate_consume(const GenArgs &g, const Plan &pl, double *d_out,
                                     int64_t *d_hist, double *d_pow, int64_t *d_count,
-                                    void *scratch, size_t scratch_bytes, cudaStream_t st,
-                                    int num_sms, int *launches);
+                                    unsigned long long *d_arrive, void *scratch,
+                                    size_t scratch_bytes, cudaStream_t st, int num_sms,
+                                    int *launches);
 size_t consume_scratch_bytes(int num_sms);
 // S7 over n values already in device memory (src): histogram kernel, exact pass, finalize
 cudaError_t launch_consume_memory(const GenArgs &g, const double *src, uint64_t n, int64_t *d_hist,
-                                  double *d_pow, int64_t *d_count, void *scratch,
-                                  size_t scratch_bytes, cudaStream_t st, int num_sms,
-                                  int *launches);
+                                  double *d_pow, int64_t *d_count, unsigned long long *d_arrive,
+                                  void *scratch, size_t scratch_bytes, cudaStream_t st,
+                                  int num_sms, int *launches);
+cudaError_t launch_wait_arrivals(const unsigned long long *arrive, unsigned long long target,
+                                 unsigned long long timeout_ns, cudaStream_t st);
 cudaError_t launch_generate_mrg(const GenArgs &g, bool alg1, cudaStream_t st);
-cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *tables,
-                                 cudaStream_t st);
-cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *tables,
-                                cudaStream_t st);
+// the jump / SEG launchers fetch (build once per device) the jump tables they read
+cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, cudaStream_t st);
+cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, cudaStream_t st);
 cudaError_t launch_generate_segc(const GenArgs &g, const Plan &pl, cudaStream_t st);
 cudaError_t launch_debug_raw(const GenArgs &g, uint32_t *d_raw, uint64_t draws, cudaStream_t st);
 cudaError_t launch_debug_pairs(const GenArgs &g, const Plan &pl, uint32_t *d_pidx,

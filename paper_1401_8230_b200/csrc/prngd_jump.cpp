@@ -2,9 +2,10 @@
 //
 // xorshift128 (Marsaglia 2003) is linear over GF(2): one draw maps the 128-bit state
 // s = (x, y, z, w) to T*s.  Advancing a stream by n draws is the matrix power T^n, so the 32
-// lanes of a warp can start at draws 0, 64, 128, ... of the same stream.  The device applies
-// J_l = T^(64 l) with byte tables: tab[l][b][v] = J_l * (v << 8b), so J_l * s is the XOR of 16
-// table entries (16 x 16-byte loads).  Product code; independent of oracle/.
+// lanes of a warp can start at draws 0, d, 2d, ... of the same stream (d = kJumpDraws = 34 for
+// the NEXT-3 jump kernel, 2 * segment length for SEG).  The device applies J_l = T^(d l) with
+// byte tables: tab[l][b][v] = J_l * (v << 8b), so J_l * s is the XOR of 16 table entries
+// (16 x 16-byte loads).  Product code; independent of oracle/.
 #include <cuda_runtime.h>
 
 #include <cstdint>

@@ -86,10 +86,7 @@ constexpr int cons_warps() {
     return (WRITE && ST == Store::ROW) ? kConsWarpsRow
                                        : (ring<ST, WRITE>() > 0 ? kConsWarpsTiles : kConsWarpsRegs);
 }
-#ifndef PRNGD_HIST8_SIM
-#define PRNGD_HIST8_SIM 0  // A/B timing only (wrong histograms): a 64 KiB 8-bit-field histogram
-#endif
-constexpr int kHistWords = PRNGD_HIST8_SIM ? 16384 : 32768;  // 65536 u16 counters in pairs (128 KiB)
+constexpr int kHistWords = 32768;  // 65536 u16 counters in pairs (128 KiB)
 
 // ------------------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -168,15 +165,9 @@ struct ConsumerT {
         // no shifts (bins b and b + 32768 share word b)
         const uint32_t t0 = (uint32_t)__double2uint_rz(__dmul_rn(q, 262144.0));
         const uint32_t t = BELOW1 ? t0 : min(t0, 262143u);  // R18: q = 1 -> top bin
-#if PRNGD_HIST8_SIM
-        const uint32_t off = t & 0xFFFCu;
-        const bool high = false;
-        const uint32_t inc = 1u << ((t >> 13) & 24u);
-#else
         const uint32_t off = t & 0x1FFFCu;
         const bool high = t >= 0x20000u;
         const uint32_t inc = high ? 0x10000u : 1u;
-#endif
         if (RED) {
             // optimistic: no return value, no carry check; a wrapped field is detected after
             // the kernel (field sum != outputs counted) and the exact pass redoes the histogram
@@ -815,7 +806,7 @@ __device__ __forceinline__ void consume_epilogue(const Cons &cons, const uint32_
                 a += part[0][wi];
                 b += part[1][wi];
             }
-            if (a != b && !PRNGD_HIST8_SIM) atomicOr(g.overflow, 1u);
+            if (a != b) atomicOr(g.overflow, 1u);
         }
     }
 }
@@ -910,10 +901,19 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
 }
 
 // Reduce the per-CTA slabs into the caller's accumulators; resets the spill array to zero.
+// The accumulators may live on another GPU (peer memory, prngd_ipc_open), so every add is a
+// system-scope atomic.  With `arrive` != null the call then signals completion: each thread
+// fences its adds at system scope, the last block to finish (counter `done`, in the scratch,
+// reset by that block) bumps *arrive with a system-scope release -- so a reader that acquires
+// *arrive >= target (prngd_wait_arrivals) sees every add of those calls.
+__device__ __forceinline__ void red_release_sys_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int n_slabs,
                                                        int64_t *spill, const double *pow_slab,
                                                        int64_t *d_hist, double *d_pow,
-                                                       int64_t *d_count, uint32_t *overflow) {
+                                                       int64_t *d_count, uint32_t *overflow,
+                                                       uint32_t *done, unsigned long long *arrive) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *overflow = 0u;  // read by the exact pass before
     __shared__ long long part[8];
     long long local = 0;
@@ -932,8 +932,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
         // device atomics: the accumulators may be shared by several shards, also by processes
         // on other GPUs through peer memory (prngd_ipc_open) -- the statistics reduction
         unsigned long long *h = reinterpret_cast<unsigned long long *>(d_hist);
-        if (lo) atomicAdd(&h[wi], (unsigned long long)lo);
-        if (hi) atomicAdd(&h[wi + 32768u], (unsigned long long)hi);
+        if (lo) atomicAdd_system(&h[wi], (unsigned long long)lo);
+        if (hi) atomicAdd_system(&h[wi + 32768u], (unsigned long long)hi);
         local += lo + hi;
     }
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(~0u, local, o);
@@ -942,13 +942,43 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
     if (threadIdx.x == 0) {
         long long t = 0;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
-        atomicAdd(reinterpret_cast<unsigned long long *>(d_count), (unsigned long long)t);
+        atomicAdd_system(reinterpret_cast<unsigned long long *>(d_count), (unsigned long long)t);
     }
     if (blockIdx.x == 0 && threadIdx.x < 4) {
         double acc = 0.0;
         for (int s = 0; s < n_slabs; ++s) acc = __dadd_rn(acc, pow_slab[s * 4 + threadIdx.x]);
-        atomicAdd(&d_pow[threadIdx.x], acc);
+        atomicAdd_system(&d_pow[threadIdx.x], acc);
     }
+    if (arrive) {
+        __threadfence_system();  // this thread's adds are performed before the block arrives
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(done, 1u) == gridDim.x - 1) {
+            __threadfence_system();
+            *done = 0u;  // stream-ordered: the next call's blocks start after this kernel
+            red_release_sys_u64(arrive, 1ull);
+        }
+    }
+}
+
+// Device-side wait for the completion counter of prngd_generate_consume_ex (acquire, system
+// scope).  Traps (a sticky launch error at the caller's next synchronisation) after timeout_ns.
+__global__ void wait_arrivals_kernel(const unsigned long long *arrive, unsigned long long target,
+                                     unsigned long long timeout_ns) {
+    unsigned long long t0, t, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(arrive) : "memory");
+        if (v >= target) return;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > timeout_ns) __trap();
+        __nanosleep(2000);
+    }
+}
+
+cudaError_t launch_wait_arrivals(const unsigned long long *arrive, unsigned long long target,
+                                 unsigned long long timeout_ns, cudaStream_t st) {
+    wait_arrivals_kernel<<<1, 1, 0, st>>>(arrive, target, timeout_ns);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------ NEXT-2 MRG32k3a
@@ -1111,7 +1141,6 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
     uint64_t base = 0;
 #pragma unroll 1
     while (base < g.nps) {
-#ifndef PRNGD_JUMP_NOJUMP_EXPERIMENT
         // every lane jumps the same round-start state: with the lane index innermost in the
         // byte tables ([b][v][lane]) each of the 16 loads reads one contiguous 512-byte run
         Xs128 st = S;
@@ -1129,10 +1158,6 @@ __global__ void __launch_bounds__(kJumpWarps * 32)
             }
             st = Xs128{r0, r1, r2, r3};
         }
-#else
-        Xs128 st = S;
-        st.x ^= lane;  // A/B timing experiment only: wrong bits
-#endif
         double q[kJumpPairs];
         uint32_t mask = 0;
 #pragma unroll
@@ -1270,11 +1295,7 @@ __device__ __forceinline__ void seg_exact(const GenArgs &g, Xs128 st, uint32_t j
 __device__ __forceinline__ Xs128 seg_jump(const uint4 *__restrict__ tabs,
                                           const uint4 *__restrict__ my_tab, uint32_t j,
                                           uint32_t log2S, Xs128 s) {
-#if defined(PRNGD_SEG_NOJUMP_EXPERIMENT)
-    (void)tabs, (void)my_tab, (void)log2S;
-    s.x ^= j;  // A/B timing experiment only: wrong bits
-    return s;
-#elif PRNGD_SEG_JUMP == 0 || PRNGD_SEG_JUMP == 3
+#if PRNGD_SEG_JUMP == 0 || PRNGD_SEG_JUMP == 3
     (void)tabs, (void)log2S;
     return j ? jump_state(my_tab, s) : s;
 #elif PRNGD_SEG_JUMP == 4
@@ -1375,7 +1396,7 @@ __global__ void __launch_bounds__(32, 12)
         Xs128 nxt = stream_start(g.seed, g.stream_begin + tn * rows_per_warp + rloc);
         const bool jump_next = j != 0 && tn < t_end;
         uint4 pf[16];
-#if !defined(PRNGD_SEG_NOJUMP_EXPERIMENT) && (PRNGD_SEG_JUMP == 0 || PRNGD_SEG_JUMP == 4)
+#if PRNGD_SEG_JUMP == 0 || PRNGD_SEG_JUMP == 4
         if (jump_next) {
             const uint32_t words[4] = {nxt.x, nxt.y, nxt.z, nxt.w};
 #pragma unroll
@@ -1388,7 +1409,7 @@ __global__ void __launch_bounds__(32, 12)
 #endif
         bool rej = false;
         seg_batch<MODE, IEEE>(st, rej, my, 0, lane, g);
-#if !defined(PRNGD_SEG_NOJUMP_EXPERIMENT) && (PRNGD_SEG_JUMP == 0 || PRNGD_SEG_JUMP == 4)
+#if PRNGD_SEG_JUMP == 0 || PRNGD_SEG_JUMP == 4
         if (jump_next) {
             uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
 #pragma unroll
@@ -1545,11 +1566,7 @@ __global__ void __launch_bounds__(kSegcWarps * 32, 1)
         const uint64_t rows_left = g.n_streams - row0;
         const uint32_t nrows = rows_left < 32u ? (uint32_t)rows_left : 32u;
         Xs128 st = stream_start(g.seed, g.stream_begin + row);
-#ifndef PRNGD_SEG_NOJUMP_EXPERIMENT
         if (j) st = jump_state_nib_smem(my_tab, st);
-#else
-        st.x ^= j;  // A/B timing experiment only: wrong bits
-#endif
         const Xs128 seg0 = st;
         bool rej = false;
         double *blk = g.out + row0 * g.nps + (uint64_t)j * L + 2 * lane;
@@ -1767,19 +1784,25 @@ cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, i
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
     Store s = pl.store;
+    const int f32 = kernel_mode(g);
+#if PRNGD_AB_STORES
     if (s == Store::TMA && make_tmap(&m, g.out, g.n_streams, g.nps, 32u * kGenWarps) != cudaSuccess)
         s = Store::STG16;  // descriptor refused: fall back to coalesced st.global (same bits)
-    const int f32 = kernel_mode(g);
     switch (s) {
-        case Store::ROW: return gen_dispatch_store<Store::ROW>(m, g, pl, f32, st);
         case Store::ROW1K: return gen_dispatch_store<Store::ROW1K>(m, g, pl, f32, st);
         case Store::DIRECT: return gen_dispatch_store<Store::DIRECT>(m, g, pl, f32, st);
         case Store::TMA: return gen_dispatch_store<Store::TMA>(m, g, pl, f32, st);
         case Store::STG16: return gen_dispatch_store<Store::STG16>(m, g, pl, f32, st);
-        default: return gen_dispatch_store<Store::STG8>(m, g, pl, f32, st);
+        default: break;
     }
+#endif
+    // product paths: 512-byte row bursts, or 8-byte stores for an unaligned output / odd nps
+    return s == Store::ROW ? gen_dispatch_store<Store::ROW>(m, g, pl, f32, st)
+                           : gen_dispatch_store<Store::STG8>(m, g, pl, f32, st);
 }
 
+// slabs, carry array, per-CTA power sums, then 16 bytes: the overflow flag and the finalize
+// kernel's block-arrival counter (both zero between calls)
 size_t consume_scratch_bytes(int num_sms) {
     return (size_t)num_sms * kHistWords * 4u + 65536u * 8u + (size_t)num_sms * 4u * 8u + 16u;
 }
@@ -1819,8 +1842,9 @@ static cudaError_t cons_dispatch(const CUtensorMap &m, const GenArgs &g, const P
 
 cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d_out,
                                     int64_t *d_hist, double *d_pow, int64_t *d_count,
-                                    void *scratch, size_t scratch_bytes, cudaStream_t st,
-                                    int num_sms, int *launches) {
+                                    unsigned long long *d_arrive, void *scratch,
+                                    size_t scratch_bytes, cudaStream_t st, int num_sms,
+                                    int *launches) {
     *launches = 0;
     if (scratch_bytes < consume_scratch_bytes(num_sms)) return cudaErrorInvalidValue;
     GenArgs g = g0;
@@ -1848,19 +1872,23 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
                 : cons_dispatch<Store::STG8, false>(m, g, pl, f32, grid, st);
     } else {
         Store s = pl.store;
-        if (s == Store::TMA && make_tmap(&m, d_out, g.n_streams, g.nps, 32u) != cudaSuccess)
-            s = Store::STG16;
 #define PRNGD_CONS_W(S)                                                                         \
     (red ? cons_dispatch<S, true, true>(m, g, pl, f32, grid, st)                                 \
          : cons_dispatch<S, true>(m, g, pl, f32, grid, st))
+#if PRNGD_AB_STORES
+        if (s == Store::TMA && make_tmap(&m, d_out, g.n_streams, g.nps, 32u) != cudaSuccess)
+            s = Store::STG16;
         switch (s) {
-            case Store::ROW:
-            case Store::ROW1K: e = PRNGD_CONS_W(Store::ROW); break;
             case Store::DIRECT: e = PRNGD_CONS_W(Store::DIRECT); break;
             case Store::TMA: e = PRNGD_CONS_W(Store::TMA); break;
             case Store::STG16: e = PRNGD_CONS_W(Store::STG16); break;
-            default: e = PRNGD_CONS_W(Store::STG8); break;
+            default: e = (s == Store::ROW || s == Store::ROW1K) ? PRNGD_CONS_W(Store::ROW)
+                                                                : PRNGD_CONS_W(Store::STG8);
         }
+#else
+        e = (s == Store::ROW || s == Store::ROW1K) ? PRNGD_CONS_W(Store::ROW)
+                                                   : PRNGD_CONS_W(Store::STG8);
+#endif
 #undef PRNGD_CONS_W
     }
     if (e != cudaSuccess) return e;
@@ -1871,14 +1899,15 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
         *launches = 2;
     }
     finalize_kernel<<<32, 256, 0, st>>>(g.hist_slab, grid, g.hist_spill, g.pow_slab, d_hist,
-                                         d_pow, d_count, g.overflow);
+                                         d_pow, d_count, g.overflow, g.overflow + 1, d_arrive);
     e = cudaGetLastError();
     if (e == cudaSuccess) *launches += 1;
     return e;
 }
 
 cudaError_t launch_consume_memory(const GenArgs &g0, const double *src, uint64_t n,
-                                  int64_t *d_hist, double *d_pow, int64_t *d_count, void *scratch,
+                                  int64_t *d_hist, double *d_pow, int64_t *d_count,
+                                  unsigned long long *d_arrive, void *scratch,
                                   size_t scratch_bytes, cudaStream_t st, int num_sms,
                                   int *launches) {
     *launches = 0;
@@ -1900,7 +1929,7 @@ cudaError_t launch_consume_memory(const GenArgs &g0, const double *src, uint64_t
     hist_mem_kernel<false, true><<<grid, kHistMemWarps * 32, smem, st>>>(src, n, g);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     finalize_kernel<<<32, 256, 0, st>>>(g.hist_slab, grid, g.hist_spill, g.pow_slab, d_hist,
-                                         d_pow, d_count, g.overflow);
+                                         d_pow, d_count, g.overflow, g.overflow + 1, d_arrive);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches = 3;
     return cudaSuccess;
@@ -1933,10 +1962,9 @@ cudaError_t launch_generate_mrg(const GenArgs &g, bool alg1, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *tables,
-                                 cudaStream_t st) {
+cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, cudaStream_t st) {
     (void)pl;
-    (void)tables;  // the kernel reads the lane-interleaved layout of the same matrices
+    const void *tables = nullptr;  // the byte tables with the lane index innermost
     cudaError_t e0 = jump_tables_interleaved(kJumpDraws, &tables);
     if (e0 != cudaSuccess) return e0;
     const size_t smem = 1024 + (size_t)kJumpWarps * kJumpCompBytes;
@@ -1960,8 +1988,8 @@ cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, const void *t
     return cudaGetLastError();
 }
 
-cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *tables,
-                                cudaStream_t st) {
+cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, cudaStream_t st) {
+    const void *tables = nullptr;
     const uint32_t SO = pl.seg_out ? pl.seg_out : (uint32_t)kSegOut;
     const uint64_t S = g.nps / SO;  // host checked: nps = SO * S, S a power of two <= 32
     uint32_t log2S = 0;
@@ -1971,7 +1999,6 @@ cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *ta
     const uint32_t F = SO < (uint32_t)kSegHalf ? SO : (uint32_t)kSegHalf;
     const size_t smem = 1024 + (size_t)32 * (F * 8 + 16);
     cudaError_t e;
-    (void)tables;
 #if PRNGD_SEG_JUMP == 1 || PRNGD_SEG_JUMP == 2
     if ((e = jump_tables_nibble(2 * SO, &tables)) != cudaSuccess) return e;
 #elif PRNGD_SEG_JUMP == 4
@@ -2019,6 +2046,10 @@ cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, const void *ta
 }
 
 cudaError_t launch_generate_segc(const GenArgs &g, const Plan &pl, cudaStream_t st) {
+#if !PRNGD_AB_STORES
+    (void)g, (void)pl, (void)st;
+    return cudaErrorNotSupported;  // A/B variant build only
+#else
     // host checked: nps % (8 * 64) == 0, 16-byte aligned output, speculative, pair-drop
     const uint64_t L = g.nps / kSegcWarps;
     const void *tables = nullptr;
@@ -2053,6 +2084,7 @@ cudaError_t launch_generate_segc(const GenArgs &g, const Plan &pl, cudaStream_t 
     }
 #undef PRNGD_SEGC_LAUNCH
     return cudaGetLastError();
+#endif
 }
 
 cudaError_t launch_debug_raw(const GenArgs &g, uint32_t *d_raw, uint64_t draws, cudaStream_t st) {

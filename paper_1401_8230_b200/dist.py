@@ -72,16 +72,22 @@ def allreduce_stats(hist, pw, count, group=None, deterministic: bool = False):
 
 class PeerStats:
     """Rank `owner`'s statistics accumulator (65536 int64 bins, 1 int64 count, 4 FP64 power
-    sums) mapped into every rank of `group` through CUDA IPC, so prngd_generate_consume on any
-    rank adds into it directly (device atomics in the library's finalize kernel).
+    sums, 1 uint64 arrival counter) mapped into every rank of `group` through CUDA IPC, so
+    prngd_generate_consume_ex on any rank adds into it directly (system-scope atomics in the
+    library's finalize kernel) and then bumps the arrival counter with a system-scope release.
 
-    Usage: ps = PeerStats(group); ps.zero(); barrier; every rank:
-    P.prngd_generate_consume(h, out, ps.hist, ps.pow, ps.count, stream); cuda sync; barrier;
-    on the owner ps.read().  Needs peer access between the ranks' GPUs (NVLink / NVSwitch) or
-    ranks on one GPU; raises otherwise (callers fall back to allreduce_stats)."""
+    Completion protocol: after n calls in total (all ranks), the counter reads n.  The owner
+    enqueues ps.wait(n) (a device-side acquire wait, for ranks on DIFFERENT GPUs) before reading
+    on the same stream, and sees every add of those n calls.  Ranks sharing one GPU (the one-GPU
+    tests) synchronise on the host instead (cuda sync + barrier), which needs no device wait.
+
+    Usage: ps = PeerStats(group); ps.zero(); barrier; every rank: ps.consume(h, out, stream);
+    owner: ps.wait(ps.expected(calls_per_rank)); ps.read().  Needs peer access between the
+    ranks' GPUs (NVLink / NVSwitch) or ranks on one GPU; raises otherwise (callers fall back to
+    allreduce_stats)."""
 
     NBINS = 65536
-    NBYTES = (65536 + 1 + 4) * 8
+    NBYTES = (65536 + 1 + 4 + 1) * 8
 
     def __init__(self, group=None, owner: int = 0):
         import torch.distributed as dist
@@ -107,14 +113,40 @@ class PeerStats:
             raise RuntimeError(f"peer accumulator unavailable: {err}")
         if self.rank != owner:
             self.base = P.prngd_ipc_open(handle)
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.hist = self.base
         self.count = self.base + self.NBINS * 8
         self.pow = self.base + (self.NBINS + 1) * 8
+        self.arrive = self.base + (self.NBINS + 5) * 8
 
-    def zero(self, stream=None):
-        """Owner only: zero the accumulator (stream-ordered)."""
+    def zero(self, stream=None, counter: bool = True):
+        """Owner only: zero the statistics (and the arrival counter unless counter=False),
+        stream-ordered."""
         if self.rank == self.owner:
-            self.P.prngd_zero(self.base, self.NBYTES, stream)
+            n = self.NBYTES if counter else self.NBYTES - 8
+            self.P.prngd_zero(self.base, n, stream)
+
+    def consume(self, handle: int, out, stream=None):
+        """This rank's prngd_generate_consume_ex into the shared accumulator (+1 arrival)."""
+        self.P.prngd_generate_consume_ex(handle, out, self.hist, self.pow, self.count,
+                                         self.arrive, stream)
+
+    def expected(self, calls_per_rank: int) -> int:
+        """Arrival count once every rank has made `calls_per_rank` calls."""
+        return self.world * calls_per_rank
+
+    def wait(self, target: int, stream=None, timeout_ns: int = 0):
+        """Owner: enqueue a device-side wait until the arrival counter reaches `target`
+        (system-scope acquire); work enqueued after it on `stream` sees those calls' adds."""
+        self.P.prngd_wait_arrivals(self.arrive, target, timeout_ns, stream)
+
+    def arrivals(self) -> int:
+        """Current value of the arrival counter (synchronous read)."""
+        import torch
+        buf = torch.empty(1, dtype=torch.int64, device="cuda")
+        self.P.prngd_copy(buf, self.arrive, 8, None)
+        torch.cuda.current_stream().synchronize()
+        return int(buf.item())
 
     def read(self):
         """Owner only: (hist int64[65536], pow float64[4], count int64[1]) torch copies."""
@@ -122,7 +154,8 @@ class PeerStats:
         buf = torch.empty(self.NBYTES // 8, dtype=torch.int64, device="cuda")
         self.P.prngd_copy(buf, self.base, self.NBYTES, None)
         torch.cuda.current_stream().synchronize()
-        return buf[:self.NBINS], buf[self.NBINS + 1:].view(torch.float64), buf[self.NBINS:self.NBINS + 1]
+        return (buf[:self.NBINS], buf[self.NBINS + 1:self.NBINS + 5].view(torch.float64),
+                buf[self.NBINS:self.NBINS + 1])
 
     def close(self):
         if self.base is None:

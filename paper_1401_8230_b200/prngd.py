@@ -39,13 +39,41 @@ STORE_FLAGS = {"auto": PRNGD_FLAG_STORE_AUTO, "seg": PRNGD_FLAG_STORE_SEG,
                "tile": PRNGD_FLAG_STORE_TILE, "direct": PRNGD_FLAG_STORE_DIRECT,
                "row1k": PRNGD_FLAG_STORE_ROW1K}
 
+# A/B store paths present only in the variant build (-DPRNGD_AB_STORES=1, include/prngd.h)
+AB_STORES = ("tma", "tile", "direct", "row1k", "segc")
+_store_ok: dict[str, bool] = {}
+
+
+def store_supported(name: str) -> bool:
+    """Whether the loaded library implements store path `name` (host-only probe)."""
+    if name not in _store_ok:
+        p = prngd_params(w=32, flags=STORE_FLAGS[name], a0=0, a=2**32 - 1, b0=0, b=2**32 - 1,
+                         seed=1, stream_begin=0, n_streams=1, n_per_stream=1)
+        h = C.c_void_p()
+        st = lib().prngd_create(C.byref(p), C.byref(h))
+        if st == PRNGD_OK:
+            lib().prngd_destroy(h)
+        _store_ok[name] = st == PRNGD_OK
+    return _store_ok[name]
+
+
+def stores_available(names) -> list:
+    """The subset of store-path names the loaded library implements (test parametrisation;
+    the product set if the library cannot be loaded here)."""
+    try:
+        return [n for n in names if store_supported(n)]
+    except Exception:
+        return [n for n in names if n not in AB_STORES]
+
+
 EXPORTS = (
     "prngd_create", "prngd_destroy", "prngd_get_info", "prngd_generate", "prngd_generate_consume",
     "prngd_generate_host", "prngd_last_launches", "prngd_status_string", "prngd_last_error",
     "prngd_abi_version", "prngd_debug_raw", "prngd_debug_pairs", "prngd_debug_map",
     "prngd_debug_div_check", "prngd_debug_jump",
     "prngd_peer_alloc", "prngd_peer_free", "prngd_ipc_export", "prngd_ipc_open",
-    "prngd_ipc_close", "prngd_copy", "prngd_zero",
+    "prngd_ipc_close", "prngd_copy", "prngd_zero", "prngd_generate_consume_ex",
+    "prngd_wait_arrivals",
 )
 
 
@@ -87,6 +115,8 @@ def lib():
             "prngd_get_info": (st, [vp, C.POINTER(prngd_info)]),
             "prngd_generate": (st, [vp, vp, vp]),
             "prngd_generate_consume": (st, [vp, vp, vp, vp, vp, vp]),
+            "prngd_generate_consume_ex": (st, [vp, vp, vp, vp, vp, vp, vp]),
+            "prngd_wait_arrivals": (st, [vp, u64, u64, vp]),
             "prngd_generate_host": (st, [vp, vp, vp]),
             "prngd_last_launches": (u32, [vp]),
             "prngd_status_string": (C.c_char_p, [st]),
@@ -130,6 +160,54 @@ def _ptr(t):
     return t.ctypes.data
 
 
+def _check_buf(t, name: str, dtype: str, numel: int, device: str):
+    """Guard the raw pointer handed to the library: a torch tensor / numpy array must have the
+    dtype the C ABI expects, be contiguous, live on the right device and hold >= numel elements
+    (the kernels write that many).  Raw integer pointers (peer-mapped buffers) pass unchecked."""
+    if t is None or isinstance(t, int):
+        return
+    if hasattr(t, "data_ptr"):  # torch
+        import torch
+        want = {"f64": torch.float64, "i64": torch.int64, "i32": (torch.int32,),
+                "u32": (torch.int32,)}[dtype]
+        ok_dtype = t.dtype in want if isinstance(want, tuple) else t.dtype == want
+        if not ok_dtype:
+            raise ValueError(f"{name}: dtype {t.dtype}, the C ABI expects {dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name}: must be contiguous")
+        if device == "cuda":
+            if not t.is_cuda:
+                raise ValueError(f"{name}: must be CUDA device memory, got {t.device}")
+            if t.device.index != torch.cuda.current_device():
+                raise ValueError(f"{name}: on {t.device}, not the current device "
+                                 f"cuda:{torch.cuda.current_device()}")
+        elif t.is_cuda:
+            raise ValueError(f"{name}: must be host memory, got {t.device}")
+        n = t.numel()
+    else:  # numpy (host only)
+        if device == "cuda":
+            raise ValueError(f"{name}: a numpy array is host memory; the call needs device memory")
+        want = {"f64": "float64", "i64": "int64", "i32": "int32", "u32": "uint32"}[dtype]
+        if t.dtype.name not in (want, "int32" if dtype == "u32" else want):
+            raise ValueError(f"{name}: dtype {t.dtype}, the C ABI expects {dtype}")
+        if not t.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name}: must be C-contiguous")
+        n = t.size
+    if n < numel:
+        raise ValueError(f"{name}: {n} elements, the call writes {numel}")
+
+
+_n_outputs: dict[int, int] = {}
+
+
+def _params_of(h: int) -> tuple[int, int]:
+    """(n_outputs, 0) of a handle, cached (the handle is immutable)."""
+    n = _n_outputs.get(h)
+    if n is None:
+        n = _n_outputs[h] = prngd_get_info(h)["n_outputs"]
+    return n, 0
+
+
 def _stream_ptr(stream):
     if stream is None:
         import torch
@@ -149,6 +227,7 @@ def prngd_create(**kw) -> int:
 
 
 def prngd_destroy(h: int):
+    _n_outputs.pop(h, None)
     _check(lib().prngd_destroy(h), "prngd_destroy")
 
 
@@ -158,16 +237,41 @@ def prngd_get_info(h: int) -> dict:
     return {k: getattr(i, k) for k, _ in prngd_info._fields_}
 
 
+def _check_stats(hist, pw, count, arrive=None):
+    _check_buf(hist, "hist", "i64", 65536, "cuda")
+    _check_buf(pw, "pw", "f64", 4, "cuda")
+    _check_buf(count, "count", "i64", 1, "cuda")
+    _check_buf(arrive, "arrive", "i64", 1, "cuda")
+
+
 def prngd_generate(h: int, out, stream=None):
+    _check_buf(out, "out", "f64", _params_of(h)[0], "cuda")
     _check(lib().prngd_generate(h, _ptr(out), _stream_ptr(stream)), "prngd_generate")
 
 
 def prngd_generate_consume(h: int, out, hist, pw, count, stream=None):
+    _check_buf(out, "out", "f64", _params_of(h)[0], "cuda")
+    _check_stats(hist, pw, count)
     _check(lib().prngd_generate_consume(h, _ptr(out), _ptr(hist), _ptr(pw), _ptr(count),
                                         _stream_ptr(stream)), "prngd_generate_consume")
 
 
+def prngd_generate_consume_ex(h: int, out, hist, pw, count, arrive, stream=None):
+    _check_buf(out, "out", "f64", _params_of(h)[0], "cuda")
+    _check_stats(hist, pw, count, arrive)
+    _check(lib().prngd_generate_consume_ex(h, _ptr(out), _ptr(hist), _ptr(pw), _ptr(count),
+                                           _ptr(arrive), _stream_ptr(stream)),
+           "prngd_generate_consume_ex")
+
+
+def prngd_wait_arrivals(arrive, target: int, timeout_ns: int = 0, stream=None):
+    _check_buf(arrive, "arrive", "i64", 1, "cuda")
+    _check(lib().prngd_wait_arrivals(_ptr(arrive), target, timeout_ns, _stream_ptr(stream)),
+           "prngd_wait_arrivals")
+
+
 def prngd_generate_host(h: int, host_out, stream=None):
+    _check_buf(host_out, "host_out", "f64", _params_of(h)[0], "cpu")
     _check(lib().prngd_generate_host(h, _ptr(host_out), _stream_ptr(stream)),
            "prngd_generate_host")
 

@@ -212,3 +212,45 @@ def test_kernel_selection(lib, name, flags, kernel, store):
         assert (info["kernel"], info["store"]) == (kernel, store)
     finally:
         P.prngd_destroy(h)
+
+
+@pytest.mark.parametrize("store", ["tma", "tile", "direct", "row1k", "segc"])
+def test_ab_store_paths_only_in_variant_build(lib, store):
+    """The losing A/B store paths are not in the product library."""
+    if P.store_supported(store):
+        pytest.skip("variant build (-DPRNGD_AB_STORES=1) loaded")
+    with pytest.raises(P.PrngdError) as e:
+        P.prngd_create(**W.FULL32, seed=1, n_streams=1, n_per_stream=2, flags=P.STORE_FLAGS[store])
+    assert e.value.status == P.PRNGD_EUNSUPPORTED and "variant build" in str(e.value)
+
+
+def test_accept_band_floor(lib):
+    """Bands accepting fewer than 2^-16 of the x1 draw values are refused (include/prngd.h)."""
+    top = 2**32 - 1
+    ok = P.prngd_create(w=32, a0=top - 2**16 - 1, a=top, b0=0, b=top, seed=1, n_streams=1,
+                        n_per_stream=2)            # exactly 2^16 of 2^32 values accepted
+    P.prngd_destroy(ok)
+    with pytest.raises(P.PrngdError) as e:
+        P.prngd_create(w=32, a0=top - 2**16, a=top, b0=0, b=top, seed=1, n_streams=1,
+                       n_per_stream=2)
+    assert e.value.status == P.PRNGD_EINVAL and "acceptance floor" in str(e.value)
+    h = P.prngd_create(w=8, a0=0, a=2, b0=0, b=255, seed=1, n_streams=1, n_per_stream=2)
+    P.prngd_destroy(h)                             # tiny ranges: 1 of 4 values, fine
+
+
+def test_binding_checks_buffers_before_the_call(lib):
+    """The binding refuses buffers the kernels would overrun (dtype, size, device, layout)."""
+    import numpy as np
+    torch = pytest.importorskip("torch")
+    h = P.prngd_create(**W.FULL32, seed=1, n_streams=4, n_per_stream=8)
+    try:
+        with pytest.raises(ValueError, match="CUDA device memory"):
+            P.prngd_generate(h, torch.empty(32, dtype=torch.float64))
+        with pytest.raises(ValueError, match="dtype"):
+            P.prngd_generate_host(h, np.empty(32, dtype=np.float32))
+        with pytest.raises(ValueError, match="elements"):
+            P.prngd_generate_host(h, np.empty(31, dtype=np.float64))
+        with pytest.raises(ValueError, match="contiguous"):
+            P.prngd_generate_host(h, torch.empty(64, dtype=torch.float64)[::2])
+    finally:
+        P.prngd_destroy(h)

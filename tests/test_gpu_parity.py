@@ -599,8 +599,8 @@ def test_guard_bands_generate(orc, flags, ns, nps):
     assert_same(out, orc.generate(p, kind=kind, open_interval=bool(flags & P.PRNGD_FLAG_OPEN))["out"])
 
 
-@pytest.mark.parametrize("flags", [P.PRNGD_FLAG_STORE_ROW, P.PRNGD_FLAG_STORE_TMA,
-                                   P.PRNGD_FLAG_STORE_TILE, P.PRNGD_FLAG_STORE_DIRECT])
+@pytest.mark.parametrize("flags", [P.STORE_FLAGS[n] for n in P.stores_available(
+    ["row", "tma", "tile", "direct"])])
 def test_guard_bands_consume(orc, flags):
     p = W.config("cfg2", n_streams=77, n_per_stream=130, flags=flags)
     g = P.Generator(**p)

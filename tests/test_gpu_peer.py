@@ -40,14 +40,15 @@ def _worker(rank, world, port, p, calls, queue):
         dist.barrier()
         out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
         for _ in range(calls):  # the accumulator sums over calls as well as ranks
-            P.prngd_generate_consume(g.handle, out, ps.hist, ps.pow, ps.count,
-                                     torch.cuda.current_stream())
+            ps.consume(g.handle, out, torch.cuda.current_stream())
         torch.cuda.synchronize()
         dist.barrier()
         if rank == 0:
+            # ranks share the GPU: host synchronisation, no device wait (which could starve the
+            # other processes' kernels); the arrival counter must read world x calls
             hist, pw, cnt = ps.read()
             queue.put((hist.cpu().numpy(), pw.cpu().numpy(), int(cnt.item()),
-                       out[:2].cpu().numpy()))
+                       out[:2].cpu().numpy(), ps.arrivals(), ps.expected(calls)))
         dist.barrier()
         if rank != 0:
             ps.close()
@@ -74,7 +75,8 @@ def test_peer_memory_statistics_reduction(orc, world, calls, name):
     for pr in procs:
         pr.join(timeout=300)
         assert pr.exitcode == 0
-    hist, pw, cnt, head = res
+    hist, pw, cnt, head, arrived, expected = res
+    assert arrived == expected == world * calls       # one release per call of every rank
     ref = orc.generate(p, want_stats=True)
     assert cnt == calls * ref["count"]
     assert np.array_equal(hist, calls * ref["hist"])

@@ -37,6 +37,10 @@ def bits(a):
     return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
 
 
+# SEGC is an A/B path of the variant build (-DPRNGD_AB_STORES=1); the product library has SEG
+PATHS = P.stores_available(["seg", "segc"])
+
+
 def assert_same(gpu_out, ref):
     gb, rb = bits(gpu_out).ravel(), bits(ref).ravel()
     bad = np.nonzero(gb != rb)[0]
@@ -62,7 +66,7 @@ def eligible(path, nps):
         else nps % 512 == 0
 
 
-@pytest.mark.parametrize("path", ["seg", "segc"])
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("nps", [128, 256, 512, 1024, 1536, 2048, 4096, 8192])
 @pytest.mark.parametrize("ns", [1, 37, 1000])
 def test_seg_full32_shapes(orc, nps, ns, path):
@@ -73,7 +77,7 @@ def test_seg_full32_shapes(orc, nps, ns, path):
     assert_same(out, orc.generate(p)["out"])
 
 
-@pytest.mark.parametrize("path", ["seg", "segc"])
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("w", [17, 20])
 @pytest.mark.parametrize("nps", [128, 1024, 4096])
 def test_seg_rejections_exact_rewrite(orc, w, nps, path):
@@ -89,7 +93,7 @@ def test_seg_rejections_exact_rewrite(orc, w, nps, path):
     assert_same(out, ref["out"])
 
 
-@pytest.mark.parametrize("path", ["seg", "segc"])
+@pytest.mark.parametrize("path", PATHS)
 def test_seg_rejection_in_last_segment(orc, path):
     """Find rows (w = 17, nps = 512) whose rejections fall in the last segment / block (the
     tail draws past pair n_per_stream come from the row's last lane) and check them bitwise."""
@@ -106,7 +110,7 @@ def test_seg_rejection_in_last_segment(orc, path):
 
 @pytest.mark.parametrize("par", [W.ASYM, dict(w=32, a0=2**12, a=2**32 - 1, b0=0, b=2**32 - 1),
                                  dict(w=24, a0=0, a=2**24 - 1, b0=0, b=2**16 - 1)])
-@pytest.mark.parametrize("path", ["seg", "segc"])
+@pytest.mark.parametrize("path", PATHS)
 def test_seg_general_ranges(orc, par, path):
     p = dict(par, seed=3, stream_begin=1 << 33, n_streams=3000, n_per_stream=2048)
     _, out = run(p, path)
@@ -114,7 +118,7 @@ def test_seg_general_ranges(orc, par, path):
 
 
 @pytest.mark.parametrize("kind,open_", [(5, False), (6, False), (4, True), (6, True)])
-@pytest.mark.parametrize("path", ["seg", "segc"])
+@pytest.mark.parametrize("path", PATHS)
 def test_seg_mappings(orc, kind, open_, path):
     flags = P.MAP_FLAGS[kind] | (P.PRNGD_FLAG_OPEN if open_ else 0)
     p = dict(full(20), seed=11, stream_begin=0, n_streams=2000, n_per_stream=1024, flags=flags)
@@ -122,7 +126,7 @@ def test_seg_mappings(orc, kind, open_, path):
     assert_same(out, orc.generate(p, kind=kind, open_interval=open_)["out"])
 
 
-@pytest.mark.parametrize("path", ["seg", "segc"])
+@pytest.mark.parametrize("path", PATHS)
 def test_seg_ieee_division(orc, path):
     p = dict(full(20), seed=12, stream_begin=0, n_streams=2000, n_per_stream=1024,
              flags=P.PRNGD_FLAG_IEEE_DIV)
@@ -130,7 +134,7 @@ def test_seg_ieee_division(orc, path):
     assert_same(out, orc.generate(p)["out"])
 
 
-@pytest.mark.parametrize("path", ["seg", "segc"])
+@pytest.mark.parametrize("path", PATHS)
 def test_seg_clamp_row_w27(orc, path):
     """w = 27: x1 = a - 1 (the only row the R11 clamp can reach, routed to the exact rewrite)
     appears with probability 2^-27 per pair, rejection 2^-26.  Over these 2^28 pairs seed 2 has
@@ -145,7 +149,8 @@ def test_seg_clamp_row_w27(orc, path):
     assert_same(out, ref)
 
 
-@pytest.mark.parametrize("path,nps", [("seg", 256), ("segc", 512)])
+@pytest.mark.parametrize("path,nps", [(q, n) for q, n in (("seg", 256), ("segc", 512))
+                                      if q in PATHS])
 def test_seg_guard_bands(orc, path, nps):
     GUARD = 4096
     flag = P.PRNGD_FLAG_STORE_SEG if path == "seg" else P.PRNGD_FLAG_STORE_SEGC
@@ -172,7 +177,7 @@ def test_seg_ineligible_shapes_fall_back(orc, nps, kernel):
     assert_same(out[rows], ref)
 
 
-@pytest.mark.parametrize("path", ["seg", "segc"])
+@pytest.mark.parametrize("path", PATHS)
 def test_seg_generate_host_matches_device(orc, path):
     p = dict(full(17), seed=4, stream_begin=0, n_streams=70000, n_per_stream=1024)
     g, out = run(p, path)
