@@ -163,11 +163,14 @@ struct ConsumerT {
         // t = floor(q * 2^18) = 4 bin + 2 fraction bits (the scaling is exact, so t >> 2 is R16's
         // floor(q * 2^16)): the word's byte offset is t & 0x1FFFC and the half is bit 17, with
         // no shifts (bins b and b + 32768 share word b)
-        const uint32_t t0 = (uint32_t)__double2uint_rz(__dmul_rn(q, 262144.0));
+        // One DADD instead of DMUL + F2I: r = q + 2^34 rounded toward zero has ulp 2^-18 on
+        // [2^34, 2^35), so for 0 <= q <= 1 its mantissa is exactly floor(q * 2^18) (<= 2^18)
+        // and that is the low word of r's bit pattern -- the same t as trunc(q * 2^18).
+        const uint32_t t0 = (uint32_t)__double2loint(__dadd_rz(q, 17179869184.0));
         const uint32_t t = BELOW1 ? t0 : min(t0, 262143u);  // R18: q = 1 -> top bin
         const uint32_t off = t & 0x1FFFCu;
         const bool high = t >= 0x20000u;
-        const uint32_t inc = high ? 0x10000u : 1u;
+        const uint32_t inc = (t >> 17) * 0xFFFFu + 1u;  // 1 (low field) or 0x10000 (high)
         if (RED) {
             // optimistic: no return value, no carry check; a wrapped field is detected after
             // the kernel (field sum != outputs counted) and the exact pass redoes the histogram
@@ -1123,8 +1126,13 @@ __device__ __forceinline__ Xs128 jump_state_nib(const uint4 *__restrict__ tab, c
     return Xs128{r0, r1, r2, r3};
 }
 
+// Resident CTAs per SM the register budget must allow: 7 x 4 warps x 148 SMs = 4144 >= cfg2's
+// 4096 streams, so cfg2 runs as ONE wave (74 registers gave 6 CTAs: 1.15 waves).
+#ifndef PRNGD_JUMP_MINB
+#define PRNGD_JUMP_MINB 1  // A/B cfg2: 7 (one wave, 72 regs + spills) 253 vs 1 (74 regs) 252 Gd/s
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(kJumpWarps * 32)
+__global__ void __launch_bounds__(kJumpWarps * 32, PRNGD_JUMP_MINB)
     gen_jump_kernel(const GenArgs g, const uint4 *__restrict__ tabs) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;

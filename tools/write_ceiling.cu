@@ -340,3 +340,39 @@ extern "C" __attribute__((visibility("default"))) int wc_dsmem_hist(uint32_t ite
     cudaLaunchKernelEx(&cfg, dsmem_hist_rate, iters, (unsigned long long *)sink);
     return (int)cudaGetLastError();
 }
+
+// Per-lane rows: a one-warp CTA owns 32 rows, lane r writes ITS OWN row r, `burst` bytes at a
+// time with 32-byte st.global.v4 (burst / 32 consecutive stores), then moves to the next burst
+// of the row.  burst = 128 is the DIRECT store path's pattern (one 16-output batch from
+// registers); burst = 512 / 1024 is what a lane could write after staging 64 / 128 outputs of
+// its row off-register (e.g. in tensor memory).  Occupancy is set by the dynamic smem pad.
+__global__ void __launch_bounds__(32) lane_rows(double *p, uint64_t rows, uint64_t cols,
+                                                uint32_t burst_doubles, uint64_t salt) {
+    extern __shared__ uint8_t pad[];
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t row = (uint64_t)blockIdx.x * 32u + lane;
+    if (row >= rows) return;
+    if (salt == ~0ull) pad[threadIdx.x] = 0;
+    double *q = p + row * cols;
+    for (uint64_t c0 = 0; c0 < cols; c0 += burst_doubles) {
+#pragma unroll 4
+        for (uint32_t k = 0; k < burst_doubles; k += 4) {
+            const uint64_t e = row * cols + c0 + k;
+            asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(q + c0 + k),
+                         "d"(hval(e, salt)), "d"(hval(e + 1, salt)), "d"(hval(e + 2, salt)),
+                         "d"(hval(e + 3, salt))
+                         : "memory");
+        }
+    }
+}
+
+extern "C" __attribute__((visibility("default"))) int wc_lane_rows(double *p, uint64_t n,
+                                                                   uint32_t burst_bytes,
+                                                                   uint32_t smem_pad, uint64_t salt,
+                                                                   void *stream, uint64_t cols) {
+    const uint64_t rows = n / cols;
+    cudaFuncSetAttribute(lane_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    lane_rows<<<(unsigned)((rows + 31) / 32), 32, smem_pad, (cudaStream_t)stream>>>(
+        p, rows, cols, burst_bytes / 8, salt);
+    return (int)cudaGetLastError();
+}
