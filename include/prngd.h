@@ -111,11 +111,9 @@ typedef enum {
  * reduce-to-width rejection (both widths <= 31); each stream's state comes from SplitMix64
  * outputs #3s..#3s+2.  Pair-drop, or Alg. 1 with PRNGD_FLAG_ALG1 (an out-of-band x1 is
  * redrawn alone); needs a 16-byte aligned output and even n_per_stream.
- * prngd_generate, prngd_generate_host, and prngd_generate_consume, which on this generator is
- * not fused: the generator kernel writes the values (to d_out, or to the handle's 256 MiB
- * staging chunks of about 1 GiB when d_out is NULL) and a histogram kernel reads them back (4 launches per
- * chunk: generate, histogram, exact pass, slab reduction).  EUNSUPPORTED for the debug hooks
- * and with PRNGD_FLAG_JUMP. */
+ * prngd_generate, prngd_generate_host, and prngd_generate_consume, whose statistics are fused
+ * into the generator kernel as on xorshift128 (3 launches: generate + bin, exact pass, slab
+ * reduction; outputs optional).  EUNSUPPORTED for the debug hooks and with PRNGD_FLAG_JUMP. */
 #define PRNGD_FLAG_MRG32K3A      0x800u
 /* prngd_generate_consume counts into per-SM 16-bit packed shared-memory counters.  By default the
  * adds are optimistic (no return value, no carry tracking): each CTA checks afterwards that its

@@ -475,6 +475,18 @@ prngd_status prngd_generate_consume_ex(const prngd_handle *hc, double *d_out, in
         h->cons_bytes = need;
     }
     int launches = 0;
+#ifndef PRNGD_MRG_FUSED
+#define PRNGD_MRG_FUSED 1  // 0: generate, then read the values back (round-1 path, A/B only)
+#endif
+    if (h->plan.mrg && PRNGD_MRG_FUSED) {
+        // S7 fused into the MRG32k3a generator (consume_mrg_kernel): no read-back, no staging
+        cudaError_t e = prngd::launch_generate_consume_mrg(
+            h->args, h->plan.alg1, d_out, d_hist, d_pow, d_count, arrive, h->cons_scratch,
+            h->cons_bytes, (cudaStream_t)cuda_stream, sms, &launches);
+        if (e != cudaSuccess) return cuda_fail(e, "generate_consume (MRG32k3a) launch");
+        h->last_launches.store((uint32_t)launches);
+        return PRNGD_OK;
+    }
     if (h->plan.mrg) {
         // MRG32k3a: the generator kernel writes the values (d_out, or staged chunks when d_out
         // is null), then S7 runs over them in memory (launch_consume_memory)

@@ -108,6 +108,12 @@ cudaError_t launch_consume_memory(const GenArgs &g, const double *src, uint64_t 
 cudaError_t launch_wait_arrivals(const unsigned long long *arrive, unsigned long long target,
                                  unsigned long long timeout_ns, cudaStream_t st);
 cudaError_t launch_generate_mrg(const GenArgs &g, bool alg1, cudaStream_t st);
+// S1-S7 on MRG32k3a fused into the generator (d_out null: statistics only); 3 launches
+cudaError_t launch_generate_consume_mrg(const GenArgs &g, bool alg1, double *d_out,
+                                        int64_t *d_hist, double *d_pow, int64_t *d_count,
+                                        unsigned long long *d_arrive, void *scratch,
+                                        size_t scratch_bytes, cudaStream_t st, int num_sms,
+                                        int *launches);
 // the jump / SEG launchers fetch (build once per device) the jump tables they read
 cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, cudaStream_t st);
 cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, cudaStream_t st);

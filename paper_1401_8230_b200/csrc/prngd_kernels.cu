@@ -138,35 +138,58 @@ __device__ __forceinline__ uint32_t tile_off(uint32_t row, uint32_t chunk) {
 // ------------------------------------------------------------------------------ consumer (S7)
 // RED: optimistic no-return adds (see consume_kernel); BELOW1: the mapping never returns 1.0
 // (Eq.(4) closed with the R11 clamp), so the R18 top-bin guard is not needed.
+// Power sums kept in kPowSplit independent partial accumulators (output i of a batch adds into
+// set i % kPowSplit), so the four FP64 add chains of a batch are kPowSplit times shorter; the
+// partials are added in a fixed order at the end (R16 compares sums at relative 1e-12).
+#ifndef PRNGD_POW_SPLIT
+#define PRNGD_POW_SPLIT 2  // cfg5 A/B (same box): 1 -> 579.5-579.6, 2 -> 584.9-586.1 Gd/s
+#endif
+// bin index of S7 by one round-toward-zero DADD (1) or by DMUL + F2I (0)
+#ifndef PRNGD_BIN_RZ
+#define PRNGD_BIN_RZ 1
+#endif
+constexpr int kPowSplit = PRNGD_POW_SPLIT;
 template <bool RED, bool BELOW1 = false>
 struct ConsumerT {
-    double s1, s2, s3, s4;
+    double s1[kPowSplit], s2[kPowSplit], s3[kPowSplit], s4[kPowSplit];
     uint32_t *hist;   // shared: 32768 words; word j holds bin j (low half), bin j + 32768 (high)
     int64_t *spill;   // global: carries of the packed counters, [65536]
     __device__ __forceinline__ void init(uint32_t *h, int64_t *sp) {
-        s1 = s2 = s3 = s4 = 0.0;
+#pragma unroll
+        for (int k = 0; k < kPowSplit; ++k) s1[k] = s2[k] = s3[k] = s4[k] = 0.0;
         hist = h;
         spill = sp;
+    }
+    __device__ __forceinline__ double sum(const double (&a)[kPowSplit]) const {
+        double r = a[0];
+#pragma unroll
+        for (int k = 1; k < kPowSplit; ++k) r = __dadd_rn(r, a[k]);
+        return r;
     }
     // R16 for one output.  A word holds L + 65536*H (mod 2^32) exactly, as a sum of commutative
     // increments.  The one thread whose atomicAdd wraps the field it increments (that field of
     // the new word is 0) records the carry in `spill`, which the finalize kernel adds back:
     //   low field wrapped:  L gains 65536, the carry went into H (H -1), and if H was 0xFFFF the
     //                       word wrapped too (H +65536);   high field wrapped: H gains 65536.
-    __device__ __forceinline__ void add(double q) {
+    __device__ __forceinline__ void add(double q, int i = 0) {
         // power sums: the FMAs round once per term (compared at relative 1e-12, R16)
+        const int k = i % kPowSplit;
         const double z2 = __dmul_rn(q, q);
-        s1 = __dadd_rn(s1, q);
-        s2 = __dadd_rn(s2, z2);
-        s3 = __fma_rn(z2, q, s3);
-        s4 = __fma_rn(z2, z2, s4);
+        s1[k] = __dadd_rn(s1[k], q);
+        s2[k] = __dadd_rn(s2[k], z2);
+        s3[k] = __fma_rn(z2, q, s3[k]);
+        s4[k] = __fma_rn(z2, z2, s4[k]);
         // t = floor(q * 2^18) = 4 bin + 2 fraction bits (the scaling is exact, so t >> 2 is R16's
         // floor(q * 2^16)): the word's byte offset is t & 0x1FFFC and the half is bit 17, with
         // no shifts (bins b and b + 32768 share word b)
         // One DADD instead of DMUL + F2I: r = q + 2^34 rounded toward zero has ulp 2^-18 on
         // [2^34, 2^35), so for 0 <= q <= 1 its mantissa is exactly floor(q * 2^18) (<= 2^18)
         // and that is the low word of r's bit pattern -- the same t as trunc(q * 2^18).
+#if PRNGD_BIN_RZ
         const uint32_t t0 = (uint32_t)__double2loint(__dadd_rz(q, 17179869184.0));
+#else
+        const uint32_t t0 = (uint32_t)__double2uint_rz(__dmul_rn(q, 262144.0));
+#endif
         const uint32_t t = BELOW1 ? t0 : min(t0, 262143u);  // R18: q = 1 -> top bin
         const uint32_t off = t & 0x1FFFCu;
         const bool high = t >= 0x20000u;
@@ -196,7 +219,7 @@ using Consumer = ConsumerT<false, false>;
 
 struct NoConsumer {
     __device__ __forceinline__ void init(uint32_t *, int64_t *) {}
-    __device__ __forceinline__ void add(double) {}
+    __device__ __forceinline__ void add(double, int = 0) {}
 };
 
 // Eq.(4) of one pair on the specialised paths: MODE 2/3 compose v = x1:x2 as a register pair
@@ -349,11 +372,11 @@ __device__ __forceinline__ void run_rows(const CUtensorMap *tmap, const GenArgs 
         if (CONSUME && live) {
             if (full) {
 #pragma unroll
-                for (int i = 0; i < kCols; ++i) cons.add(q[i]);
+                for (int i = 0; i < kCols; ++i) cons.add(q[i], i);
             } else {
 #pragma unroll
                 for (int i = 0; i < kCols; ++i)
-                    if ((uint32_t)i < valid) cons.add(q[i]);
+                    if ((uint32_t)i < valid) cons.add(q[i], i);
             }
         }
         if constexpr (!WRITE) continue;
@@ -495,12 +518,15 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
     uint32_t wr, rd;
     uint32_t bad1;              // 4: the pending x1 lies outside the band, else 0
     uint32_t ring;              // this lane's ring (shared address), kMrgRingBytes aligned
+    // stride: the counters of lane l start at stride * l (8: bank spread; 16: the in-ring output
+    // staging of PRNGD_MRG_STAGE = 2 and of the fused consumer)
     __device__ __forceinline__ MrgProducer2(const GenArgs &g, uint64_t s, uint32_t ring_base,
-                                            uint32_t lane)
+                                            uint32_t lane,
+                                            uint32_t stride = PRNGD_MRG_STAGE == 2 ? 16u : 8u)
         : k(g) {
         const Mrg32k3a m = mrg_stream_start(g.seed, s);
         A = (T1)m.s0, B = (T1)m.s1, C = (T1)m.s2, D = (T2)m.t0, E = (T2)m.t1, F = (T2)m.t2;
-        rd = wr = (PRNGD_MRG_STAGE == 2 ? 16u : 8u) * lane;
+        rd = wr = stride * lane;
         bad1 = 0u;
         ring = ring_base;
     }
@@ -627,11 +653,11 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
                 const uint64_t base = col0 + b * kCols;
                 if (base + kCols <= g.nps) {
 #pragma unroll
-                    for (int i = 0; i < kCols; ++i) cons.add(q[i]);
+                    for (int i = 0; i < kCols; ++i) cons.add(q[i], i);
                 } else {
 #pragma unroll
                     for (int i = 0; i < kCols; ++i)
-                        if (base + i < g.nps) cons.add(q[i]);
+                        if (base + i < g.nps) cons.add(q[i], i);
                 }
             }
 #pragma unroll
@@ -770,7 +796,7 @@ __device__ __forceinline__ void consume_epilogue(const Cons &cons, const uint32_
                                                  const GenArgs &g, unsigned long long expect) {
     __shared__ double red[kWarps][4];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    double s[4] = {cons.s1, cons.s2, cons.s3, cons.s4};
+    double s[4] = {cons.sum(cons.s1), cons.sum(cons.s2), cons.sum(cons.s3), cons.sum(cons.s4)};
 #pragma unroll
     for (int k = 0; k < 4; ++k)
         for (int o = 16; o > 0; o >>= 1) s[k] = __dadd_rn(s[k], __shfl_xor_sync(~0u, s[k], o));
@@ -838,7 +864,7 @@ __global__ void __launch_bounds__(kHistMemWarps * 32, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) q[k] = __ldcs(src + i + k * stride);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) cons.add(q[k]);
+        for (int k = 0; k < 4; ++k) cons.add(q[k], k);
         counted += 4;
     }
 #pragma unroll 1
@@ -1065,6 +1091,97 @@ __global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ Gen
     } else {
         run_rows_burst<false, kMrgCols>(g, base, lane, row0, prod, nc);
     }
+}
+
+// ------------------------------------------------------------------------------ NEXT-2 + S7 fused
+// The fused consumer on the MRG32k3a base generator: persistent, one CTA per SM holding the
+// 128 KiB packed histogram (the same optimistic adds, overflow check, exact pass and slabs as
+// consume_kernel) and kMrgConsWarps warps, each with its lanes' 256-byte rings of valid draws.
+// With outputs, a batch's 16 values are staged in the ring bytes the batch has just consumed
+// (lane l consumed (16 l + 128 b) mod 256 of its ring, free until the next fill) and the warp
+// writes the 32 x 128-byte tile row by row, so no separate tile is needed beside the histogram.
+// Replaces "generate, then read the outputs back" (8 more bytes of HBM traffic per output and
+// a second kernel) by ~11 instructions per output in the generator's epilogue.
+#ifndef PRNGD_MRG_CONS_WARPS
+#define PRNGD_MRG_CONS_WARPS 12
+#endif
+constexpr int kMrgConsWarps = PRNGD_MRG_CONS_WARPS;
+constexpr size_t kMrgConsSmem = 1024 + (size_t)kHistWords * 4u + (size_t)kMrgConsWarps * 32u * kMrgRingBytes;
+static_assert(kMrgRingBytes == 256u, "the in-ring staging assumes 256-byte rings");
+
+template <bool EQ4, bool SAMEW, bool ALG1, bool SPECB, bool WRITE, bool RED, bool EXACT_GUARD>
+__global__ void __launch_bounds__(kMrgConsWarps * 32, 1)
+    consume_mrg_kernel(const __grid_constant__ GenArgs g) {
+    if (EXACT_GUARD && *(volatile const uint32_t *)g.overflow == 0u) return;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base = aligned_smem_base(smem_raw);
+    uint32_t *hist = reinterpret_cast<uint32_t *>(smem_raw + (base - smem_u32(smem_raw)));
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t rings = base + kHistWords * 4u + warp * (32u * kMrgRingBytes);
+    for (uint32_t i = threadIdx.x; i < kHistWords; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    ConsumerT<RED, false> cons;
+    cons.init(hist, g.hist_spill);
+    const uint64_t n_tasks = (g.n_streams + 31u) / 32u;
+    const bool vec = (g.nps % 2u) == 0u && (reinterpret_cast<uintptr_t>(g.out) & 15u) == 0u;
+    const uint32_t c = lane & 7u, rsub = lane >> 3;
+#pragma unroll 1
+    for (uint64_t t = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * warp; t < n_tasks;
+         t += (uint64_t)gridDim.x * kMrgConsWarps) {
+        const uint64_t row0 = t * 32u;
+        MrgProducer2<EQ4, SAMEW, ALG1, SPECB> prod(g, g.stream_begin + row0 + lane,
+                                                  rings + lane * kMrgRingBytes, lane, 16u);
+        const bool live = row0 + lane < g.n_streams;
+        const bool full_rows = row0 + 32u <= g.n_streams;
+        double *dst = WRITE ? g.out + (row0 + lane) * g.nps : nullptr;
+        uint32_t boff = 0u;
+#pragma unroll 1
+        for (uint64_t col0 = 0; col0 < g.nps; col0 += kCols, boff ^= 128u) {
+            double q[kCols];
+            prod(q, g);
+            const bool full = col0 + kCols <= g.nps;
+            if (live) {
+                if (full) {
+#pragma unroll
+                    for (int i = 0; i < kCols; ++i) cons.add(q[i], i);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kCols; ++i)
+                        if (col0 + i < g.nps) cons.add(q[i], i);
+                }
+            }
+            if constexpr (WRITE) {
+                if (vec && full_rows && full) {
+                    const uint32_t my = rings + lane * kMrgRingBytes, o0 = 16u * lane + boff;
+#pragma unroll
+                    for (int k = 0; k < kCols / 2; ++k)
+                        sts_v2(my | ((o0 + 16u * k) & 0xF0u), q[2 * k], q[2 * k + 1]);
+                    __syncwarp();
+                    double *d = g.out + (row0 + rsub) * g.nps + col0 + 2 * c;
+#pragma unroll
+                    for (uint32_t r = rsub; r < 32u; r += 4u) {
+                        double a, b;
+                        lds_v2(rings + r * kMrgRingBytes + ((16u * r + boff + 16u * c) & 0xF0u), a, b);
+                        stg_v2_cs(d, a, b);
+                        d += 4u * g.nps;
+                    }
+                    __syncwarp();  // the staged bytes are read before the next fill reuses them
+                } else if (live) {
+#pragma unroll
+                    for (int i = 0; i < kCols; ++i)
+                        if (col0 + i < g.nps) dst[col0 + i] = q[i];
+                }
+            }
+        }
+    }
+    unsigned long long expect = 0;
+    if (RED && lane == 0)
+        for (uint64_t t = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * warp; t < n_tasks;
+             t += (uint64_t)gridDim.x * kMrgConsWarps) {
+            const uint64_t left = g.n_streams - t * 32u;
+            expect += (left < 32u ? left : 32u) * g.nps;
+        }
+    consume_epilogue<RED, kMrgConsWarps>(cons, hist, g, expect);
 }
 
 // ------------------------------------------------------------------------------ NEXT-3 jump kernel
@@ -1943,17 +2060,95 @@ cudaError_t launch_consume_memory(const GenArgs &g0, const double *src, uint64_t
     return cudaSuccess;
 }
 
-cudaError_t launch_generate_mrg(const GenArgs &g, bool alg1, cudaStream_t st) {
-    const size_t smem = kMrgRingBytes + kMrgStageBytes + (size_t)32 * kMrgRingBytes;
-    const uint64_t grid = (g.n_streams + 31) / 32;
-    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    const bool eq4 = g.map.kind == 4 && g.map.open == 0 && g.w <= 31;
-    const bool samew = g.mrg_t1 == g.mrg_t2 && g.mrg_mask1 == g.mrg_mask2;
+// The MRG32k3a kernel family of a parameter set (shared by the generator and the fused consumer)
+struct MrgKind {
+    bool eq4, samew, specb;
+};
+static MrgKind mrg_kind(const GenArgs &g, bool alg1) {
+    MrgKind k;
+    k.eq4 = g.map.kind == 4 && g.map.open == 0 && g.w <= 31;
+    k.samew = g.mrg_t1 == g.mrg_t2 && g.mrg_mask1 == g.mrg_mask2;
     // band test per batch instead of per draw when fewer than 1 in 4096 x1 are out of band.
     // Alg. 1 drops a single draw, which shifts the x1/x2 roles of the later ones: only when
     // both have the same width (threshold and mask) is that harmless.
     const uint64_t range1 = (uint64_t)g.mrg_mask1 + 1u;
-    const bool specb = (range1 - g.span) * 4096u < range1 && (!alg1 || samew);
+    k.specb = (range1 - g.span) * 4096u < range1 && (!alg1 || k.samew);
+    return k;
+}
+
+// S1-S7 on MRG32k3a: fused pass (optimistic adds) + exact pass + finalize, as
+// launch_generate_consume.
+template <bool EQ4, bool SAMEW, bool ALG1, bool SPECB>
+static cudaError_t cons_mrg_launch(const GenArgs &g, bool write, int grid, cudaStream_t st) {
+    cudaError_t e;
+#define PRNGD_CM(W, R, X)                                                                       \
+    do {                                                                                        \
+        auto k = consume_mrg_kernel<EQ4, SAMEW, ALG1, SPECB, W, R, X>;                          \
+        if ((e = set_smem(k, kMrgConsSmem)) != cudaSuccess) return e;                          \
+        k<<<grid, kMrgConsWarps * 32, kMrgConsSmem, st>>>(g);                                  \
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;                                  \
+    } while (0)
+    if (write)
+        PRNGD_CM(true, true, false);
+    else
+        PRNGD_CM(false, true, false);
+    PRNGD_CM(false, false, true);  // exact pass: returns at once unless a 16-bit field wrapped
+#undef PRNGD_CM
+    return cudaSuccess;
+}
+
+cudaError_t launch_generate_consume_mrg(const GenArgs &g0, bool alg1, double *d_out,
+                                        int64_t *d_hist, double *d_pow, int64_t *d_count,
+                                        unsigned long long *d_arrive, void *scratch,
+                                        size_t scratch_bytes, cudaStream_t st, int num_sms,
+                                        int *launches) {
+    *launches = 0;
+    if (scratch_bytes < consume_scratch_bytes(num_sms)) return cudaErrorInvalidValue;
+    GenArgs g = g0;
+    g.out = d_out;
+    uint8_t *sp = static_cast<uint8_t *>(scratch);
+    g.hist_slab = reinterpret_cast<uint32_t *>(sp);
+    g.hist_spill = reinterpret_cast<int64_t *>(sp + (size_t)num_sms * kHistWords * 4u);
+    g.pow_slab = reinterpret_cast<double *>(sp + (size_t)num_sms * kHistWords * 4u + 65536u * 8u);
+    g.overflow = reinterpret_cast<uint32_t *>(sp + (size_t)num_sms * kHistWords * 4u +
+                                              65536u * 8u + (size_t)num_sms * 4u * 8u);
+    const uint64_t tasks = (g.n_streams + 31u) / 32u;
+    int grid = num_sms;
+    if ((uint64_t)grid > tasks) grid = (int)tasks;
+    if (grid < 1) grid = 1;
+    const MrgKind k = mrg_kind(g, alg1);
+    const bool w = d_out != nullptr;
+    cudaError_t e;
+    if (alg1)
+        e = k.specb ? (k.eq4 ? cons_mrg_launch<true, true, true, true>(g, w, grid, st)
+                             : cons_mrg_launch<false, true, true, true>(g, w, grid, st))
+                    : (k.eq4 ? cons_mrg_launch<true, false, true, false>(g, w, grid, st)
+                             : cons_mrg_launch<false, false, true, false>(g, w, grid, st));
+    else if (k.specb)
+        e = k.eq4 ? (k.samew ? cons_mrg_launch<true, true, false, true>(g, w, grid, st)
+                             : cons_mrg_launch<true, false, false, true>(g, w, grid, st))
+                  : (k.samew ? cons_mrg_launch<false, true, false, true>(g, w, grid, st)
+                             : cons_mrg_launch<false, false, false, true>(g, w, grid, st));
+    else
+        e = k.eq4 ? (k.samew ? cons_mrg_launch<true, true, false, false>(g, w, grid, st)
+                             : cons_mrg_launch<true, false, false, false>(g, w, grid, st))
+                  : (k.samew ? cons_mrg_launch<false, true, false, false>(g, w, grid, st)
+                             : cons_mrg_launch<false, false, false, false>(g, w, grid, st));
+    if (e != cudaSuccess) return e;
+    *launches = 2;
+    finalize_kernel<<<32, 256, 0, st>>>(g.hist_slab, grid, g.hist_spill, g.pow_slab, d_hist,
+                                         d_pow, d_count, g.overflow, g.overflow + 1, d_arrive);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    *launches = 3;
+    return cudaSuccess;
+}
+
+cudaError_t launch_generate_mrg(const GenArgs &g, bool alg1, cudaStream_t st) {
+    const size_t smem = kMrgRingBytes + kMrgStageBytes + (size_t)32 * kMrgRingBytes;
+    const uint64_t grid = (g.n_streams + 31) / 32;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    const MrgKind mk = mrg_kind(g, alg1);
+    const bool eq4 = mk.eq4, samew = mk.samew, specb = mk.specb;
     auto k = alg1 ? (specb ? (eq4 ? gen_mrg_kernel<true, true, true, true>
                                   : gen_mrg_kernel<false, true, true, true>)
                            : (eq4 ? gen_mrg_kernel<true, false, true> : gen_mrg_kernel<false, false, true>))

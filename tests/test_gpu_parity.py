@@ -523,13 +523,29 @@ def test_mrg32k3a_alg1_bitwise(orc):
 
 @pytest.mark.parametrize("kind", [4, 5])
 def test_mrg32k3a_generate_consume(kind):
-    """S7 on the MRG32k3a path (generate, then the histogram kernel over the written values)."""
+    """S7 fused into the MRG32k3a generator (consume_mrg_kernel): outputs written through the
+    in-ring staging, histogram / moments / count; ragged rows and a ragged last batch."""
     p = dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1, seed=9, n_streams=700, n_per_stream=1030,
              flags=P.PRNGD_FLAG_MRG32K3A | P.MAP_FLAGS[kind], mrg=True, map=kind)
     g = P.Generator(**p)
     out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
     _mrg_stats_match(g, p, out)
-    assert g.last_launches == 4
+    assert g.last_launches == 3  # fused pass, exact pass (returns at once), finalize
+
+
+@pytest.mark.parametrize("shape,offset", [((45, 77), 1), ((3, 64), 0), ((5000, 18), 0),
+                                          ((33, 1), 0)])
+def test_mrg32k3a_fused_consume_shapes(orc, shape, offset):
+    """The fused MRG32k3a consumer on odd row lengths, an 8-byte-offset output (scalar stores
+    instead of the staged tile), fewer tasks than SMs, one-output rows, with a stream offset."""
+    ns, nps = shape
+    p = dict(w=26, a0=7, a=2**26 - 9, b0=0, b=2**20 - 1, seed=23, stream_begin=123457,
+             n_streams=ns, n_per_stream=nps, flags=P.PRNGD_FLAG_MRG32K3A, mrg=True)
+    g = P.Generator(**p)
+    buf = torch.full((ns * nps + 8,), -3.0, dtype=torch.float64, device="cuda")
+    out = buf[offset:offset + ns * nps].view(ns, nps)
+    _mrg_stats_match(g, p, out)
+    assert bool((buf[:offset] == -3.0).all()) and bool((buf[offset + ns * nps:] == -3.0).all())
 
 
 def test_mrg32k3a_consume_open_interval_top_bin():
@@ -543,19 +559,19 @@ def test_mrg32k3a_consume_open_interval_top_bin():
     assert bool((out == 1.0).any())
 
 
-def test_mrg32k3a_consume_only_chunks():
-    """Consume-only (no output buffer): staged 1 GiB chunks (10944 streams of 96 KiB here),
-    the statistics accumulate over the chunks."""
+def test_mrg32k3a_consume_only_long_rows():
+    """Consume-only (no output buffer) on long rows: the fused kernel keeps nothing but the
+    statistics, whatever the size (no staging chunks)."""
     p = dict(w=26, a0=5, a=2**26 - 3, b0=0, b=2**20 - 1, seed=3, n_streams=11500,
              n_per_stream=12288, flags=P.PRNGD_FLAG_MRG32K3A, mrg=True)
     g = P.Generator(**p)
     _mrg_stats_match(g, p)
-    assert g.last_launches == 8  # two chunks x (generate, histogram, exact pass, finalize)
+    assert g.last_launches == 3
 
 
 def test_mrg32k3a_consume_counter_wrap():
     """8 distinct values over 2^26.3 outputs: every CTA's 16-bit fields wrap, the exact pass
-    must take over (memory histogram kernel)."""
+    (the fused kernel again, with carry-tracking adds) must take over."""
     p = dict(w=2, a0=0, a=3, b0=0, b=3, seed=4, n_streams=8192, n_per_stream=10240,
              flags=P.PRNGD_FLAG_MRG32K3A, mrg=True)
     g = P.Generator(**p)
