@@ -55,8 +55,10 @@ def parse():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank its own per-GPU shard (default); strong: one global "
                          "stream space split over the ranks")
-    ap.add_argument("--reduce", default="p2p", choices=["p2p", "nccl"],
-                    help="N > 1 statistics exchange: peer-memory atomics in the kernel, or NCCL")
+    ap.add_argument("--reduce", default="auto", choices=["auto", "nvls", "p2p", "nccl"],
+                    help="N > 1 statistics exchange: NVLS multicast reductions in the finalize "
+                         "kernel (NEXT-4), peer-memory atomics in the kernel, or NCCL; auto = "
+                         "the first of nvls, p2p, nccl that works on every rank")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay each step from a CUDA graph (auto: steps under 0.2 ms, N=1)")
     ap.add_argument("--streams", type=int, default=0,
@@ -338,9 +340,22 @@ def main():
     # (CUDA IPC, peer memory over NVLink) and each rank's finalize kernel adds into it with device
     # atomics -- fused into the library's own launches; NCCL all-reduce is the fallback.
     peer, reduce_mode = None, None
-    if consume and world > 1:
-        reduce_mode = "nccl"
-        if args.reduce == "p2p":
+    mc_err = None
+    if consume and world > 1 and args.reduce in ("auto", "nvls"):
+        # NEXT-4: in-switch reduction through an NVLS multicast object (every rank's copy gets
+        # the all-reduced statistics inside the finalize kernels); raises consistently on every
+        # rank when the fabric cannot provide it
+        try:
+            peer = D.McStats()
+            peer.zero(stream)
+            torch.cuda.synchronize()
+            dist.barrier()
+            reduce_mode = "nvls"
+        except Exception as e:
+            peer, mc_err = None, str(e)
+    if consume and world > 1 and peer is None:
+        reduce_mode = "nccl" + (f" (multicast unavailable: {mc_err})" if mc_err else "")
+        if args.reduce in ("auto", "p2p"):
             err = None
             try:
                 peer = D.PeerStats()
@@ -368,6 +383,8 @@ def main():
                     dist.barrier()
                 reduce_mode = "nccl (peer memory unavailable" + (f": {err})" if err else " on a rank)")
             dist.barrier()
+            if reduce_mode == "p2p" and mc_err:
+                reduce_mode = f"p2p (multicast unavailable: {mc_err})"
 
     def step(st=stream):
         if consume and peer is not None:
@@ -712,7 +729,10 @@ def main():
             "pct_hbm_write_roofline": 100.0 * achieved / peak if roof["bound"] == "hbm" else None,
         }
         print(json.dumps(line), flush=True)
-    if peer is not None:  # the owner frees only after every other rank unmapped
+    if isinstance(peer, D.McStats):
+        torch.cuda.synchronize()
+        peer.close()  # barrier, then every rank releases its mappings
+    elif peer is not None:  # the owner frees only after every other rank unmapped
         torch.cuda.synchronize()
         dist.barrier()
         if rank != 0:

@@ -265,6 +265,43 @@ PRNGD_API prngd_status prngd_ipc_close(void *d_ptr);
 PRNGD_API prngd_status prngd_copy(void *dst, const void *src, uint64_t bytes, void *cuda_stream);
 PRNGD_API prngd_status prngd_zero(void *d_ptr, uint64_t bytes, void *cuda_stream);
 
+/* ---- NEXT-4: NVLS multicast statistics (in-switch all-reduce inside the finalize kernel).
+ * Layout of a shared statistics buffer (PeerStats and multicast alike), 8-byte words:
+ *   [0, 65536) int64 histogram | count int64 | 4 x double power sums | uint64 arrival counter */
+#define PRNGD_STATS_COUNT_OFFSET  (65536u * 8u)
+#define PRNGD_STATS_POW_OFFSET    (65537u * 8u)
+#define PRNGD_STATS_ARRIVE_OFFSET (65541u * 8u)
+#define PRNGD_STATS_BYTES         (65542u * 8u)
+
+/* As prngd_generate_consume_ex with the statistics buffer (layout above) given by its NVLS
+ * MULTICAST address (prngd_mc_bind_map's *mc_ptr): the finalize kernel adds the histogram, count
+ * and power sums with multimem.red (the NVSwitch performs each add on every member GPU's copy)
+ * and then increments the arrival counter with a multimem.red.release -- so after R ranks' calls
+ * every rank's LOCAL copy holds the all-reduced statistics and an arrival count of R, with no
+ * collective call.  Requires a multicast object bound on every rank (below). */
+PRNGD_API prngd_status prngd_generate_consume_mc(const prngd_handle *h, double *d_out,
+                                                 void *mc_stats, void *cuda_stream);
+
+/* Multicast accumulator setup, one process per GPU, driven by the caller's process group:
+ *   1. owner: prngd_mc_create(bytes, R, &m, &fd); broadcast (getpid(), fd)
+ *   2. others: prngd_mc_import(owner_pid, fd, prngd_mc_bytes, &m)  (pidfd_getfd)
+ *   3. every rank: prngd_mc_add_device(m); barrier
+ *   4. every rank: prngd_mc_bind_map(m, &mc_ptr, &local_ptr) (zeroed local copy); barrier
+ *   5. prngd_mc_destroy(m) on every rank (after a barrier) when done.
+ * prngd_mc_supported reports CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED for the current device.
+ * Any step returns PRNGD_ECUDA / PRNGD_EUNSUPPORTED with the driver's reason when the fabric or
+ * the driver cannot provide the object (e.g. one-GPU leases: cuMulticastCreate refuses); callers
+ * then fall back to peer memory or NCCL (paper_1401_8230_b200.dist). */
+typedef struct prngd_mc prngd_mc;
+PRNGD_API prngd_status prngd_mc_supported(int *supported);
+PRNGD_API prngd_status prngd_mc_create(uint64_t bytes, uint32_t n_devices, prngd_mc **out,
+                                       int *export_fd);
+PRNGD_API prngd_status prngd_mc_import(int owner_pid, int owner_fd, uint64_t bytes, prngd_mc **out);
+PRNGD_API uint64_t prngd_mc_bytes(const prngd_mc *m);
+PRNGD_API prngd_status prngd_mc_add_device(prngd_mc *m);
+PRNGD_API prngd_status prngd_mc_bind_map(prngd_mc *m, void **mc_ptr, void **local_ptr);
+PRNGD_API prngd_status prngd_mc_destroy(prngd_mc *m);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,7 +15,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libprngd_b200.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("prngd_kernels.cu", "prngd_host.cpp", "prngd_jump.cpp")]
+SOURCES = [os.path.join(CSRC, f) for f in ("prngd_kernels.cu", "prngd_host.cpp", "prngd_jump.cpp",
+                                           "prngd_mc.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("prngd_device.cuh", "prngd_internal.h")] + [
     os.path.join(ROOT, "include", "prngd.h"), os.path.abspath(__file__)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

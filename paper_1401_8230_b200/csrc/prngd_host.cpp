@@ -48,6 +48,10 @@ static prngd_status fail(prngd_status s, const char *fmt, ...) {
     return s;
 }
 
+void prngd::set_last_error(const char *msg) {
+    std::snprintf(g_err, sizeof(g_err), "%s", msg);
+}
+
 static prngd_status cuda_fail(cudaError_t e, const char *what) {
     return fail(PRNGD_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
 }
@@ -440,14 +444,36 @@ static prngd_status wait_stage_free(prngd_handle *h, cudaStream_t st) {
     return PRNGD_OK;
 }
 
+static prngd_status generate_consume_impl(const prngd_handle *hc, double *d_out, int64_t *d_hist,
+                                          double *d_pow, int64_t *d_count, uint64_t *d_arrive,
+                                          bool mc, void *cuda_stream);
+
 prngd_status prngd_generate_consume(const prngd_handle *hc, double *d_out, int64_t *d_hist,
                                     double *d_pow, int64_t *d_count, void *cuda_stream) {
-    return prngd_generate_consume_ex(hc, d_out, d_hist, d_pow, d_count, nullptr, cuda_stream);
+    return generate_consume_impl(hc, d_out, d_hist, d_pow, d_count, nullptr, false, cuda_stream);
 }
 
 prngd_status prngd_generate_consume_ex(const prngd_handle *hc, double *d_out, int64_t *d_hist,
                                        double *d_pow, int64_t *d_count, uint64_t *d_arrive,
                                        void *cuda_stream) {
+    return generate_consume_impl(hc, d_out, d_hist, d_pow, d_count, d_arrive, false, cuda_stream);
+}
+
+prngd_status prngd_generate_consume_mc(const prngd_handle *hc, double *d_out, void *mc_stats,
+                                       void *cuda_stream) {
+    if (!mc_stats || ((uintptr_t)mc_stats & 7u))
+        return fail(PRNGD_EINVAL, "null or misaligned multicast statistics address");
+    uint8_t *b = static_cast<uint8_t *>(mc_stats);
+    return generate_consume_impl(hc, d_out, reinterpret_cast<int64_t *>(b),
+                                 reinterpret_cast<double *>(b + PRNGD_STATS_POW_OFFSET),
+                                 reinterpret_cast<int64_t *>(b + PRNGD_STATS_COUNT_OFFSET),
+                                 reinterpret_cast<uint64_t *>(b + PRNGD_STATS_ARRIVE_OFFSET), true,
+                                 cuda_stream);
+}
+
+static prngd_status generate_consume_impl(const prngd_handle *hc, double *d_out, int64_t *d_hist,
+                                          double *d_pow, int64_t *d_count, uint64_t *d_arrive,
+                                          bool mc, void *cuda_stream) {
     if (!hc || !d_hist || !d_pow || !d_count)
         return fail(PRNGD_EINVAL, "null handle or accumulator pointer");
     if (((uintptr_t)d_hist | (uintptr_t)d_pow | (uintptr_t)d_count | (uintptr_t)d_arrive) & 7u)
@@ -478,10 +504,12 @@ prngd_status prngd_generate_consume_ex(const prngd_handle *hc, double *d_out, in
 #ifndef PRNGD_MRG_FUSED
 #define PRNGD_MRG_FUSED 1  // 0: generate, then read the values back (round-1 path, A/B only)
 #endif
+    if (mc && h->plan.mrg && !PRNGD_MRG_FUSED)
+        return fail(PRNGD_EUNSUPPORTED, "multicast statistics need the fused MRG32k3a consumer");
     if (h->plan.mrg && PRNGD_MRG_FUSED) {
         // S7 fused into the MRG32k3a generator (consume_mrg_kernel): no read-back, no staging
         cudaError_t e = prngd::launch_generate_consume_mrg(
-            h->args, h->plan.alg1, d_out, d_hist, d_pow, d_count, arrive, h->cons_scratch,
+            h->args, h->plan.alg1, d_out, d_hist, d_pow, d_count, arrive, mc, h->cons_scratch,
             h->cons_bytes, (cudaStream_t)cuda_stream, sms, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "generate_consume (MRG32k3a) launch");
         h->last_launches.store((uint32_t)launches);
@@ -530,7 +558,7 @@ prngd_status prngd_generate_consume_ex(const prngd_handle *hc, double *d_out, in
         return PRNGD_OK;
     }
     cudaError_t e = prngd::launch_generate_consume(h->args, plan_for(h, d_out, true), d_out, d_hist,
-                                                   d_pow, d_count, arrive, h->cons_scratch,
+                                                   d_pow, d_count, arrive, mc, h->cons_scratch,
                                                    h->cons_bytes, (cudaStream_t)cuda_stream, sms,
                                                    &launches);
     if (e != cudaSuccess) return cuda_fail(e, "generate_consume launch");

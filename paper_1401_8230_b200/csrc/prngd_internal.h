@@ -91,12 +91,16 @@ cudaError_t jump_tables_nibble(uint64_t lane_draws, const void **out);
 cudaError_t jump_tables_interleaved(uint64_t lane_draws, const void **out);
 void jump_host(uint64_t n_draws, const uint32_t in[4], uint32_t out[4], int lane_table);
 
+// detail string of prngd_last_error() (thread-local), for the other translation units
+void set_last_error(const char *msg);
+
 // Launchers (prngd_kernels.cu).  They return cudaGetLastError() of the launch.
 cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, int num_sms);
 // d_arrive (nullable): +1 with a system-scope release once every statistic of the call is added
+// mc: the accumulators are an NVLS multicast address (multimem.red in the finalize kernel)
 cudaError_t launch_generate_consume(const GenArgs &g, const Plan &pl, double *d_out,
                                     int64_t *d_hist, double *d_pow, int64_t *d_count,
-                                    unsigned long long *d_arrive, void *scratch,
+                                    unsigned long long *d_arrive, bool mc, void *scratch,
                                     size_t scratch_bytes, cudaStream_t st, int num_sms,
                                     int *launches);
 size_t consume_scratch_bytes(int num_sms);
@@ -111,7 +115,7 @@ cudaError_t launch_generate_mrg(const GenArgs &g, bool alg1, cudaStream_t st);
 // S1-S7 on MRG32k3a fused into the generator (d_out null: statistics only); 3 launches
 cudaError_t launch_generate_consume_mrg(const GenArgs &g, bool alg1, double *d_out,
                                         int64_t *d_hist, double *d_pow, int64_t *d_count,
-                                        unsigned long long *d_arrive, void *scratch,
+                                        unsigned long long *d_arrive, bool mc, void *scratch,
                                         size_t scratch_bytes, cudaStream_t st, int num_sms,
                                         int *launches);
 // the jump / SEG launchers fetch (build once per device) the jump tables they read

@@ -935,9 +935,31 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
 // fences its adds at system scope, the last block to finish (counter `done`, in the scratch,
 // reset by that block) bumps *arrive with a system-scope release -- so a reader that acquires
 // *arrive >= target (prngd_wait_arrivals) sees every add of those calls.
-__device__ __forceinline__ void red_release_sys_u64(unsigned long long *p, unsigned long long v) {
-    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// MC (NEXT-4): the accumulators are an NVLS multicast address (prngd_mc_bind_map): every add is
+// a multimem.red, which the NVSwitch performs on every member GPU's copy (an all-reduce inside
+// this kernel), and the arrival increment a multimem.red with release semantics.
+template <bool MC>
+__device__ __forceinline__ void stat_add_u64(unsigned long long *p, unsigned long long v) {
+    if (MC)
+        asm volatile("multimem.red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else
+        atomicAdd_system(p, v);
 }
+template <bool MC>
+__device__ __forceinline__ void stat_add_f64(double *p, double v) {
+    if (MC)
+        asm volatile("multimem.red.relaxed.sys.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+    else
+        atomicAdd_system(p, v);
+}
+template <bool MC>
+__device__ __forceinline__ void red_release_sys_u64(unsigned long long *p, unsigned long long v) {
+    if (MC)
+        asm volatile("multimem.red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else
+        asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+template <bool MC>
 __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int n_slabs,
                                                        int64_t *spill, const double *pow_slab,
                                                        int64_t *d_hist, double *d_pow,
@@ -961,8 +983,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
         // device atomics: the accumulators may be shared by several shards, also by processes
         // on other GPUs through peer memory (prngd_ipc_open) -- the statistics reduction
         unsigned long long *h = reinterpret_cast<unsigned long long *>(d_hist);
-        if (lo) atomicAdd_system(&h[wi], (unsigned long long)lo);
-        if (hi) atomicAdd_system(&h[wi + 32768u], (unsigned long long)hi);
+        if (lo) stat_add_u64<MC>(&h[wi], (unsigned long long)lo);
+        if (hi) stat_add_u64<MC>(&h[wi + 32768u], (unsigned long long)hi);
         local += lo + hi;
     }
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(~0u, local, o);
@@ -971,12 +993,12 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
     if (threadIdx.x == 0) {
         long long t = 0;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
-        atomicAdd_system(reinterpret_cast<unsigned long long *>(d_count), (unsigned long long)t);
+        stat_add_u64<MC>(reinterpret_cast<unsigned long long *>(d_count), (unsigned long long)t);
     }
     if (blockIdx.x == 0 && threadIdx.x < 4) {
         double acc = 0.0;
         for (int s = 0; s < n_slabs; ++s) acc = __dadd_rn(acc, pow_slab[s * 4 + threadIdx.x]);
-        atomicAdd_system(&d_pow[threadIdx.x], acc);
+        stat_add_f64<MC>(&d_pow[threadIdx.x], acc);
     }
     if (arrive) {
         __threadfence_system();  // this thread's adds are performed before the block arrives
@@ -984,9 +1006,21 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
         if (threadIdx.x == 0 && atomicAdd(done, 1u) == gridDim.x - 1) {
             __threadfence_system();
             *done = 0u;  // stream-ordered: the next call's blocks start after this kernel
-            red_release_sys_u64(arrive, 1ull);
+            red_release_sys_u64<MC>(arrive, 1ull);
         }
     }
+}
+
+static void finalize_launch(bool mc, cudaStream_t st, const uint32_t *slab, int n_slabs,
+                            int64_t *spill, const double *pow_slab, int64_t *d_hist,
+                            double *d_pow, int64_t *d_count, uint32_t *overflow, uint32_t *done,
+                            unsigned long long *arrive) {
+    if (mc)
+        finalize_kernel<true><<<32, 256, 0, st>>>(slab, n_slabs, spill, pow_slab, d_hist, d_pow,
+                                                   d_count, overflow, done, arrive);
+    else
+        finalize_kernel<false><<<32, 256, 0, st>>>(slab, n_slabs, spill, pow_slab, d_hist, d_pow,
+                                                    d_count, overflow, done, arrive);
 }
 
 // Device-side wait for the completion counter of prngd_generate_consume_ex (acquire, system
@@ -1967,7 +2001,7 @@ static cudaError_t cons_dispatch(const CUtensorMap &m, const GenArgs &g, const P
 
 cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d_out,
                                     int64_t *d_hist, double *d_pow, int64_t *d_count,
-                                    unsigned long long *d_arrive, void *scratch,
+                                    unsigned long long *d_arrive, bool mc, void *scratch,
                                     size_t scratch_bytes, cudaStream_t st, int num_sms,
                                     int *launches) {
     *launches = 0;
@@ -2023,7 +2057,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
         if (e != cudaSuccess) return e;
         *launches = 2;
     }
-    finalize_kernel<<<32, 256, 0, st>>>(g.hist_slab, grid, g.hist_spill, g.pow_slab, d_hist,
+    finalize_launch(mc, st, g.hist_slab, grid, g.hist_spill, g.pow_slab, d_hist,
                                          d_pow, d_count, g.overflow, g.overflow + 1, d_arrive);
     e = cudaGetLastError();
     if (e == cudaSuccess) *launches += 1;
@@ -2035,6 +2069,7 @@ cudaError_t launch_consume_memory(const GenArgs &g0, const double *src, uint64_t
                                   unsigned long long *d_arrive, void *scratch,
                                   size_t scratch_bytes, cudaStream_t st, int num_sms,
                                   int *launches) {
+    const bool mc = false;
     *launches = 0;
     if (scratch_bytes < consume_scratch_bytes(num_sms)) return cudaErrorInvalidValue;
     GenArgs g = g0;
@@ -2053,7 +2088,7 @@ cudaError_t launch_consume_memory(const GenArgs &g0, const double *src, uint64_t
     if ((e = set_smem(hist_mem_kernel<false, true>, smem)) != cudaSuccess) return e;
     hist_mem_kernel<false, true><<<grid, kHistMemWarps * 32, smem, st>>>(src, n, g);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    finalize_kernel<<<32, 256, 0, st>>>(g.hist_slab, grid, g.hist_spill, g.pow_slab, d_hist,
+    finalize_launch(mc, st, g.hist_slab, grid, g.hist_spill, g.pow_slab, d_hist,
                                          d_pow, d_count, g.overflow, g.overflow + 1, d_arrive);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches = 3;
@@ -2099,7 +2134,7 @@ static cudaError_t cons_mrg_launch(const GenArgs &g, bool write, int grid, cudaS
 
 cudaError_t launch_generate_consume_mrg(const GenArgs &g0, bool alg1, double *d_out,
                                         int64_t *d_hist, double *d_pow, int64_t *d_count,
-                                        unsigned long long *d_arrive, void *scratch,
+                                        unsigned long long *d_arrive, bool mc, void *scratch,
                                         size_t scratch_bytes, cudaStream_t st, int num_sms,
                                         int *launches) {
     *launches = 0;
@@ -2136,7 +2171,7 @@ cudaError_t launch_generate_consume_mrg(const GenArgs &g0, bool alg1, double *d_
                              : cons_mrg_launch<false, false, false, false>(g, w, grid, st));
     if (e != cudaSuccess) return e;
     *launches = 2;
-    finalize_kernel<<<32, 256, 0, st>>>(g.hist_slab, grid, g.hist_spill, g.pow_slab, d_hist,
+    finalize_launch(mc, st, g.hist_slab, grid, g.hist_spill, g.pow_slab, d_hist,
                                          d_pow, d_count, g.overflow, g.overflow + 1, d_arrive);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     *launches = 3;

@@ -167,6 +167,112 @@ class PeerStats:
         self.base = None
 
 
+def _agree(ok: bool, group=None) -> bool:
+    """True iff `ok` on every rank of `group` (all-reduce MIN of a flag)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        return ok
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return bool(t.item())
+
+
+class McStats:
+    """NEXT-4: the statistics buffer as an NVLS multicast object spanning the ranks' GPUs (one
+    process per GPU).  prngd_generate_consume_mc on any rank adds its statistics with
+    multimem.red through the multicast address, so the NVSwitch reduces them into EVERY rank's
+    local copy (an all-reduce inside the finalize kernel) and bumps every copy's arrival counter
+    with a release.  After R ranks x n calls each rank's wait(R*n) + read() returns the global
+    statistics.  Raises RuntimeError on every rank (consistently) when the driver / fabric cannot
+    create the object (one-GPU leases, no NVSwitch); callers fall back to PeerStats / NCCL."""
+
+    def __init__(self, group=None, owner: int = 0):
+        import os
+
+        import torch.distributed as dist
+        from . import prngd as P
+        self.P, self.group, self.owner = P, group, owner
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.m = None
+        err = None
+        try:
+            if not P.prngd_mc_supported():
+                raise RuntimeError("CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED = 0")
+        except Exception as e:
+            err = str(e)
+        if not _agree(err is None, group):
+            raise RuntimeError(f"multicast unavailable: {err or 'on another rank'}")
+        info = [None]
+        if self.rank == owner:
+            try:
+                self.m, fd = P.prngd_mc_create(P.STATS_BYTES, self.world)
+                info = [(os.getpid(), fd, P.prngd_mc_bytes(self.m), None)]
+            except Exception as e:
+                info = [(None, None, None, str(e))]
+        if dist.is_initialized():
+            dist.broadcast_object_list(info, src=owner, group=group)
+        pid, fd, nbytes, err = info[0]
+        if err is not None:
+            raise RuntimeError(f"multicast object unavailable: {err}")
+        err = None
+        try:
+            if self.rank != owner:
+                self.m = P.prngd_mc_import(pid, fd, nbytes)
+            P.prngd_mc_add_device(self.m)
+        except Exception as e:
+            err = str(e)
+        if not _agree(err is None, group):
+            self.close(barrier=False)
+            raise RuntimeError(f"multicast setup failed: {err or 'on another rank'}")
+        try:  # every device is in the team before any rank binds memory
+            self.mc, self.local = P.prngd_mc_bind_map(self.m)
+        except Exception as e:
+            err = str(e)
+        if not _agree(err is None, group):
+            self.close(barrier=False)
+            raise RuntimeError(f"multicast bind failed: {err or 'on another rank'}")
+        self.hist = self.local
+        self.count = self.local + P.STATS_COUNT_OFFSET
+        self.pow = self.local + P.STATS_POW_OFFSET
+        self.arrive = self.local + P.STATS_ARRIVE_OFFSET
+
+    def consume(self, handle: int, out, stream=None):
+        """This rank's prngd_generate_consume_mc (in-switch reduction into every copy)."""
+        self.P.prngd_generate_consume_mc(handle, out, self.mc, stream)
+
+    def expected(self, calls_per_rank: int) -> int:
+        return self.world * calls_per_rank
+
+    def wait(self, target: int, stream=None, timeout_ns: int = 0):
+        """Device-side acquire wait on this rank's local arrival counter."""
+        self.P.prngd_wait_arrivals(self.arrive, target, timeout_ns, stream)
+
+    def zero(self, stream=None, counter: bool = True):
+        """Zero THIS rank's local copy (every rank zeroes its own, then a barrier)."""
+        n = self.P.STATS_BYTES if counter else self.P.STATS_ARRIVE_OFFSET
+        self.P.prngd_zero(self.local, n, stream)
+
+    def read(self):
+        import torch
+        buf = torch.empty(self.P.STATS_BYTES // 8, dtype=torch.int64, device="cuda")
+        self.P.prngd_copy(buf, self.local, self.P.STATS_BYTES, None)
+        torch.cuda.current_stream().synchronize()
+        n = 65536
+        return buf[:n], buf[n + 1:n + 5].view(torch.float64), buf[n:n + 1]
+
+    def close(self, barrier: bool = True):
+        import torch.distributed as dist
+        if self.m is None:
+            return
+        if barrier and dist.is_initialized():
+            dist.barrier(group=self.group)
+        self.P.prngd_mc_destroy(self.m)
+        self.m = None
+
+
 def generate_sharded(p: dict, mode: str = STRONG, consume: bool = False, write: bool = True,
                      group=None, deterministic: bool = False,
                      local: Callable | None = None):

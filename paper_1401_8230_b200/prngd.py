@@ -73,7 +73,9 @@ EXPORTS = (
     "prngd_debug_div_check", "prngd_debug_jump",
     "prngd_peer_alloc", "prngd_peer_free", "prngd_ipc_export", "prngd_ipc_open",
     "prngd_ipc_close", "prngd_copy", "prngd_zero", "prngd_generate_consume_ex",
-    "prngd_wait_arrivals",
+    "prngd_wait_arrivals", "prngd_generate_consume_mc", "prngd_mc_supported", "prngd_mc_create",
+    "prngd_mc_import", "prngd_mc_bytes", "prngd_mc_add_device", "prngd_mc_bind_map",
+    "prngd_mc_destroy",
 )
 
 
@@ -117,6 +119,14 @@ def lib():
             "prngd_generate_consume": (st, [vp, vp, vp, vp, vp, vp]),
             "prngd_generate_consume_ex": (st, [vp, vp, vp, vp, vp, vp, vp]),
             "prngd_wait_arrivals": (st, [vp, u64, u64, vp]),
+            "prngd_generate_consume_mc": (st, [vp, vp, vp, vp]),
+            "prngd_mc_supported": (st, [C.POINTER(C.c_int)]),
+            "prngd_mc_create": (st, [u64, u32, C.POINTER(vp), C.POINTER(C.c_int)]),
+            "prngd_mc_import": (st, [C.c_int, C.c_int, u64, C.POINTER(vp)]),
+            "prngd_mc_bytes": (u64, [vp]),
+            "prngd_mc_add_device": (st, [vp]),
+            "prngd_mc_bind_map": (st, [vp, C.POINTER(vp), C.POINTER(vp)]),
+            "prngd_mc_destroy": (st, [vp]),
             "prngd_generate_host": (st, [vp, vp, vp]),
             "prngd_last_launches": (u32, [vp]),
             "prngd_status_string": (C.c_char_p, [st]),
@@ -299,6 +309,55 @@ def prngd_debug_map(h: int, x1, x2, z, stream=None):
 def prngd_debug_div_check(h: int, n: int, seed: int, mismatch, stream=None):
     _check(lib().prngd_debug_div_check(h, n, seed, _ptr(mismatch), _stream_ptr(stream)),
            "prngd_debug_div_check")
+
+
+def prngd_generate_consume_mc(h: int, out, mc_stats: int, stream=None):
+    _check_buf(out, "out", "f64", _params_of(h)[0], "cuda")
+    _check(lib().prngd_generate_consume_mc(h, _ptr(out), mc_stats, _stream_ptr(stream)),
+           "prngd_generate_consume_mc")
+
+
+# statistics buffer layout (include/prngd.h PRNGD_STATS_*)
+STATS_COUNT_OFFSET, STATS_POW_OFFSET, STATS_ARRIVE_OFFSET = 65536 * 8, 65537 * 8, 65541 * 8
+STATS_BYTES = 65542 * 8
+
+
+def prngd_mc_supported() -> bool:
+    v = C.c_int(0)
+    _check(lib().prngd_mc_supported(C.byref(v)), "prngd_mc_supported")
+    return bool(v.value)
+
+
+def prngd_mc_create(nbytes: int, n_devices: int) -> tuple[int, int]:
+    """Owner: (handle, exported POSIX fd) of a new multicast object."""
+    m, fd = C.c_void_p(), C.c_int(-1)
+    _check(lib().prngd_mc_create(nbytes, n_devices, C.byref(m), C.byref(fd)), "prngd_mc_create")
+    return m.value, fd.value
+
+
+def prngd_mc_import(owner_pid: int, owner_fd: int, nbytes: int) -> int:
+    m = C.c_void_p()
+    _check(lib().prngd_mc_import(owner_pid, owner_fd, nbytes, C.byref(m)), "prngd_mc_import")
+    return m.value
+
+
+def prngd_mc_bytes(m: int) -> int:
+    return int(lib().prngd_mc_bytes(m))
+
+
+def prngd_mc_add_device(m: int):
+    _check(lib().prngd_mc_add_device(m), "prngd_mc_add_device")
+
+
+def prngd_mc_bind_map(m: int) -> tuple[int, int]:
+    """(multicast address, local copy address) of this rank's bound buffer (zeroed)."""
+    mc, local = C.c_void_p(), C.c_void_p()
+    _check(lib().prngd_mc_bind_map(m, C.byref(mc), C.byref(local)), "prngd_mc_bind_map")
+    return mc.value, local.value
+
+
+def prngd_mc_destroy(m: int):
+    _check(lib().prngd_mc_destroy(m), "prngd_mc_destroy")
 
 
 IPC_HANDLE_BYTES = 64

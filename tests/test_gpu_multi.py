@@ -8,6 +8,8 @@ One process per device, NCCL process group with `device_id` (as bench.py under t
   accumulator, system-scope atomics in every rank's finalize kernel, completion counter with a
   device-side acquire wait on rank 0) and through NCCL (dist.allreduce_stats) both equal the
   oracle's histogram / count (bit-exact) and power sums (relative 1e-12, R16);
+* NEXT-4: the NVLS multicast reduction (dist.McStats, multimem.red in the finalize kernel) when
+  the fabric provides the object: every rank's local copy holds the all-reduce;
 * the per-step protocol of bench.py's N > 1 e2e (wait, read, zero, barrier) returns each step's
   own statistics.
 
@@ -82,8 +84,30 @@ def _worker(rank, world, port, p, mode, queue):
                 ps.zero(st, counter=False)
             torch.cuda.synchronize()
             dist.barrier()
+        # 5. NEXT-4: NVLS multicast reduction (every rank's local copy gets the all-reduce), when
+        #    the fabric provides the object; recorded as unavailable otherwise
+        mc = None
+        try:
+            mc = D.McStats()
+        except RuntimeError as e:
+            mc_res = ("unavailable", str(e))
+        if mc is not None:
+            mc.zero(st)
+            torch.cuda.synchronize()
+            dist.barrier()
+            for _ in range(2):
+                mc.consume(g.handle, None, st)
+            mc.wait(mc.expected(2), st)           # each rank waits on its OWN copy
+            mh, mp, mcnt = mc.read()
+            hs = torch.tensor([int(mh.sum().item()), int(mcnt.item())], device="cuda")
+            both = [torch.empty_like(hs) for _ in range(world)]
+            dist.all_gather(both, hs)              # every rank holds the same all-reduce
+            mc_res = ("ok", mh.cpu().numpy(), mp.cpu().numpy(), int(mcnt.item()),
+                      [tuple(int(v) for v in b.cpu()) for b in both])
+            mc.close()
         if rank == 0:
             res["steps"] = steps
+            res["mc"] = mc_res
             queue.put(res)
         torch.cuda.synchronize()
         dist.barrier()
@@ -140,6 +164,11 @@ def test_shards_and_reductions_across_devices(orc, world, mode):
     assert np.array_equal(res["peer_hist"], 2 * ref["hist"])
     assert np.allclose(res["peer_pow"], 2 * ref["pow"], rtol=1e-12, atol=0)
     assert res["steps"] == [(ref["count"], ref["count"])] * 3
+    if res["mc"][0] == "ok":
+        _, mh, mp, mcnt, per_rank = res["mc"]
+        assert mcnt == 2 * ref["count"] and np.array_equal(mh, 2 * ref["hist"])
+        assert np.allclose(mp, 2 * ref["pow"], rtol=1e-12, atol=0)
+        assert per_rank == [(2 * ref["count"], 2 * ref["count"])] * world
     assert D.shard_range(n_global, world - 1, world)[1] == n_global
 
 

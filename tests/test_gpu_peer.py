@@ -82,3 +82,37 @@ def test_peer_memory_statistics_reduction(orc, world, calls, name):
     assert np.array_equal(hist, calls * ref["hist"])
     assert np.allclose(pw, calls * ref["pow"], rtol=1e-12, atol=0)
     assert np.array_equal(head.view(np.int64), ref["out"][:2].view(np.int64))  # rank 0's rows
+
+
+def test_multicast_statistics_single_process_or_clean_refusal(orc):
+    """NEXT-4 on whatever this box offers: with the NVLS multicast object available even for one
+    device, prngd_generate_consume_mc's in-switch reduction (multimem.red in the finalize
+    kernel) must equal the oracle's statistics and bump the arrival counter; where the driver
+    refuses the object (one-GPU leases), McStats raises RuntimeError naming the driver's reason
+    and nothing is left allocated, so dist / bench fall back to peer memory."""
+    from paper_1401_8230_b200 import dist as D
+    from paper_1401_8230_b200 import prngd as P
+    from paper_1401_8230_b200 import workloads as W
+    torch.cuda.set_device(0)
+    supported = P.prngd_mc_supported()
+    try:
+        ms = D.McStats()
+    except RuntimeError as e:
+        msg = str(e)
+        assert "multicast" in msg and ("Multicast" in msg or "MULTICAST" in msg or "CUresult" in msg
+                                       or "cuMulticast" in msg), msg
+        return
+    assert supported
+    try:
+        p = W.config("cfg1", n_streams=640, n_per_stream=520)
+        g = P.Generator(**p)
+        for _ in range(2):
+            ms.consume(g.handle, None)
+        ms.wait(2)
+        hist, pw, cnt = ms.read()
+        ref = orc.generate(p, want_stats=True)
+        assert int(cnt.item()) == 2 * ref["count"]
+        assert np.array_equal(hist.cpu().numpy(), 2 * ref["hist"])
+        assert np.allclose(pw.cpu().numpy(), 2 * ref["pow"], rtol=1e-12, atol=0)
+    finally:
+        ms.close()
