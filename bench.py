@@ -612,10 +612,18 @@ def main():
     # -------------------------------------------------- end to end through the C ABI, host buffer
     e2e = None
     if args.e2e_steps > 0 and not consume:
-        # prngd_generate_host into pinned host memory.  The sample is bounded at 2^17 streams
-        # (1 GiB at cfg3's row length) per rank so N ranks do not pin N x 8 GiB of host memory;
-        # the call is PCIe-bound, so the rate does not depend on the sample size.
-        ns_e = min(p["n_streams"], 1 << 17)
+        # prngd_generate_host into pinned host memory: the whole per-rank workload when the host
+        # has the memory to pin it for every local rank (3x headroom), else a 2^17-stream
+        # sample (the call is PCIe-bound, so the rate does not depend on the sample size)
+        ns_e = p["n_streams"]
+        try:
+            with open("/proc/meminfo") as f:
+                avail = int(next(l for l in f if l.startswith("MemAvailable")).split()[1]) * 1024
+        except Exception:
+            avail = 0
+        local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        if 3 * local_ranks * 8 * nout > avail:
+            ns_e = min(p["n_streams"], 1 << 17)
         ge = P.Generator(**dict(p, n_streams=ns_e))
         ne = ns_e * p["n_per_stream"]
         host = torch.empty((ns_e, p["n_per_stream"]), dtype=torch.float64, pin_memory=True)
@@ -631,6 +639,7 @@ def main():
             dist.all_reduce(de, op=dist.ReduceOp.MAX)
         e2e = {"value": world * ne * args.e2e_steps / de.item() / 1e9, "unit": "Gdoubles/s",
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * ne,
+               "full_workload": ns_e == p["n_streams"],
                "note": f"prngd_generate_host: chunked generate + pinned D2H, overlapped; inputs "
                        f"are the parameter struct only; {ns_e} streams x {p['n_per_stream']} "
                        f"per rank per step"}
