@@ -551,17 +551,17 @@ def main():
     if consume and not args.no_write and not p.get("mrg"):
         # The fused write + statistics kernel is not HBM-bound (S7): its
         # instruction-issue share, from the algorithmic count per output -- generator 18
-        # (2 xorshift128 draws x 6, band test 1, Eq.(4) 5), statistics 11 (power sums 5; bin and
-        # packed add 6), store 1.5 (STS, LDS, STG per 2 outputs): 30.5 -- against 4 schedulers x
-        # 32 lanes x SMs x max SM clock.
-        ins = 30.5
+        # (2 xorshift128 draws x 6, band test 1, Eq.(4) 5), statistics 10 (power sums 5; bin by
+        # one round-toward-zero DADD, word mask, field increment 2, packed add), store 1.5 (STS,
+        # LDS, STG per 2 outputs): 29.5 -- against 4 schedulers x 32 lanes x SMs x max SM clock.
+        ins = 29.5
         roof["issue"] = {"algorithmic_instructions_per_output": ins,
                          "achieved": ins * nout / (kern_ms * 1e-3) / 1e9,
                          "peak": 4 * 32.0 * sms * clk_ghz, "unit": "Ginstr/s",
                          "frac": ins * nout / (kern_ms * 1e-3) / 1e9 / (4 * 32.0 * sms * clk_ghz),
-                         "note": "issue/latency-bound: 35.3 issued per output at 64% issue, "
-                                 "ALU pipe 55%, 12 warps per SM (profiles/r01l_summary.txt)"}
-    if consume and args.no_write:
+                         "note": "issue/latency-bound: 34.6 issued per output at 62% issue, "
+                                 "ALU pipe 51%, 12 warps per SM (profiles/r02c_summary.txt)"}
+    if consume and args.no_write and not p.get("mrg"):
         # Nothing is written: one shared-memory histogram add per output.  Peak = the measured
         # rate of the same packed adds (no return value) at the kernel's 16 warps per SM
         # (tools/smem_hist_rate.py, profiles/r01b_smem_hist_rate.json); DESIGN.md section 8.
@@ -584,13 +584,16 @@ def main():
         # remainder; combination 9: two exact conversions, two canonical-representative fixes
         # of 2, subtract-and-wrap 3; R23 test + mask 2; ring append 3: address, predicated store,
         # counter), 2.03 draws per output (26-bit reduce-to-width rejects 1/64), plus 11 per
-        # output (Eq.(4) 6, ring read 2, band test 2, store 1): 24 x 2.03 + 11 = 60.
+        # output (Eq.(4) 6, ring read 2, band test 2, store 1): 24 x 2.03 + 11 = 60.  The fused
+        # consumer (consume_mrg_kernel) adds the statistics' 10 (power sums 5, bin 5) and drops
+        # the store (1) when nothing is written.
         # Peak: 4 schedulers x 32 lanes per clock per SM x SMs x max SM clock.
-        ops = 60.0
+        ops = 60.0 + (10.0 if consume else 0.0) - (1.0 if consume and args.no_write else 0.0)
         ach = ops * nout / (kern_ms * 1e-3) / 1e9
         pk = 4 * 32.0 * sms * clk_ghz
         roof = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "Ginstr/s", "frac": ach / pk,
-                "traffic": None, "kernel": "gen_mrg_kernel",
+                "traffic": None,
+                "kernel": "consume_mrg_kernel+finalize" if consume else "gen_mrg_kernel",
                 "peak_source": "derived: 4 warp-instructions/clk/SM (one per scheduler) x 32 "
                                "lanes x SMs x max SM clock",
                 "algorithmic_instructions_per_output": ops,
