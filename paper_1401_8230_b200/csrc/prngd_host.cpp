@@ -321,12 +321,32 @@ static Plan plan_for(const prngd_handle *h, const void *out, bool consume) {
     Plan pl = h->plan;
     // Fused consumer + outputs: the ROW tiles of consume_kernel next to its 128 KiB histogram
     // (S7).
-    if (consume && (pl.store == Store::SEG || pl.store == Store::SEGC || pl.store_auto))
-        pl.store = Store::ROW;
     const uintptr_t a = (uintptr_t)out;
     const uint64_t nps = h->p.n_per_stream;
     const bool a32 = (a & 31u) == 0 && (nps & 3u) == 0;
     const bool a16 = (a & 15u) == 0 && (nps & 1u) == 0;
+#ifndef PRNGD_CONS_SEG
+#define PRNGD_CONS_SEG 1  // fused consumer with 1 KiB row segments where they apply
+#endif
+    if (consume && (pl.store == Store::SEG || pl.store == Store::SEGC || pl.store_auto)) {
+        // the row-segment consumer needs rare rejection, pair-drop, 16-byte stores and
+        // nps = 128 * 2^m <= 4096 (the kernel also checks the mapping); else ROW tiles
+        const uint64_t S = nps / 128u;
+        const bool seg = PRNGD_CONS_SEG && !pl.mrg && pl.spec && !pl.alg1 && !pl.ieee_div && a16 &&
+                         nps % 128u == 0 && S >= 1 && S <= 32 && (S & (S - 1)) == 0;
+        pl.store = seg ? Store::SEG : Store::ROW;
+        pl.jump = false;
+    }
+    if (consume) {  // an explicit store path for the consumer, with the same alignment fallbacks
+        if (pl.store == Store::SEG) return pl;  // checked above
+        if ((pl.store == Store::ROW || pl.store == Store::ROW1K) && !a16) pl.store = Store::STG8;
+#if PRNGD_AB_STORES
+        if (pl.store == Store::DIRECT && !a32) pl.store = a16 ? Store::STG16 : Store::STG8;
+        if (pl.store == Store::STG16 && !a16) pl.store = Store::STG8;
+        if (pl.store == Store::TMA && !a16) pl.store = Store::STG8;
+#endif
+        return pl;
+    }
     // SEG: rare rejection (speculative), pair-drop, nps = 128 * S with S a power of two <= 32,
     // and 16-byte stores; otherwise the ROW path.  AUTO takes SEG instead of the NEXT-3 jump
     // kernel for few-stream generate calls (cfg1: 76 vs 64 Gd/s); for bulk shapes ROW stays

@@ -37,6 +37,10 @@ struct GenArgs {
     int64_t *hist_spill;    // [65536] int64 carries of the packed counters
     double *pow_slab;       // [gridDim.x][4]
     uint32_t *overflow;     // set by an optimistic (RED) consume kernel whose 16-bit fields wrapped
+    // fused consumer with row segments (Store::SEG): log2 of the lanes per row and the
+    // lane-interleaved jump tables of distance kSegDraws
+    uint32_t seg_log2;
+    const uint4 *jump_tab;
 };
 
 // How a warp's outputs reach HBM (include/prngd.h PRNGD_FLAG_STORE_*):

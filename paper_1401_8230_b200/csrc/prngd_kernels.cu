@@ -83,7 +83,7 @@ constexpr int kConsWarpsRow = PRNGD_CONS_ROW_WARPS;
 constexpr int kConsRowCols = PRNGD_CONS_ROW_COLS;
 template <Store ST, bool WRITE>
 constexpr int cons_warps() {
-    return (WRITE && ST == Store::ROW) ? kConsWarpsRow
+    return (WRITE && (ST == Store::ROW || ST == Store::SEG)) ? kConsWarpsRow
                                        : (ring<ST, WRITE>() > 0 ? kConsWarpsTiles : kConsWarpsRegs);
 }
 constexpr int kHistWords = 32768;  // 65536 u16 counters in pairs (128 KiB)
@@ -881,6 +881,11 @@ __global__ void __launch_bounds__(kHistMemWarps * 32, 1)
 // to the number of outputs it counted (any wrapped field makes the sum short) and raises
 // g.overflow.  EXACT_GUARD: the exact (carry-tracking) kernel of the fallback pass, which
 // returns at once unless that flag is set and then rewrites every slab.
+// one warp-task of the row-segment consumer (defined with the SEG kernel below)
+template <int MODE, class Cons>
+__device__ __forceinline__ void run_task_seg_consume(const GenArgs &g, uint32_t tile,
+                                                     uint32_t lane, uint64_t t, Cons &cons);
+
 template <int MODE, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE, bool RED = false,
           bool EXACT_GUARD = false>
 __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
@@ -898,7 +903,10 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     ConsumerT<RED, (MODE >= 1 && MODE <= 3)> cons;
     cons.init(hist, g.hist_spill);
     uint32_t it = 0;
-    const uint64_t n_tasks = (g.n_streams + 31u) / 32u;
+    // rows per warp-task: 32, or 32 / S with S lanes per row (SEG)
+    constexpr bool kSeg = WRITE && ST == Store::SEG;
+    const uint32_t rpw = kSeg ? (32u >> g.seg_log2) : 32u;
+    const uint64_t n_tasks = (g.n_streams + rpw - 1u) / rpw;
 #pragma unroll 1
     // task t = blockIdx.x + gridDim.x * (warp + kWarps * k): the tasks in flight at any time
     // are one contiguous block (as with CTA-major order), and a small config's few tasks land
@@ -910,8 +918,10 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
             run_rows_burst<true, kConsRowCols>(
                 g, base + kHistWords * 4u + warp * (32u * (kConsRowCols * 8u + 16u)), lane, t * 32u, prod,
                 cons);
-        }
-        else
+        } else if constexpr (kSeg) {
+            run_task_seg_consume<MODE>(
+                g, base + kHistWords * 4u + warp * (32u * (kConsRowCols * 8u + 16u)), lane, t, cons);
+        } else
             run_rows<MODE, SPEC, IEEE, ALG1, ST, WRITE, true, NB>(&tmap, g, tiles, lane, t * 32u,
                                                                      cons, it);
     }
@@ -923,8 +933,8 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     if (RED && lane == 0)
         for (uint64_t t = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * warp; t < n_tasks;
              t += (uint64_t)gridDim.x * kWarps) {
-            const uint64_t left = g.n_streams - t * 32u;
-            expect += (left < 32u ? left : 32u) * g.nps;
+            const uint64_t left = g.n_streams - t * rpw;
+            expect += (left < rpw ? left : rpw) * g.nps;
         }
     consume_epilogue<RED, kWarps>(cons, hist, g, expect);
 }
@@ -1506,6 +1516,123 @@ __device__ __forceinline__ void seg_batch(Xs128 &st, bool &rej, uint32_t my, uin
         sts_v2(my + ((b * (kCols / 2) + c) << 4), q[2 * c], q[2 * c + 1]);
 }
 
+// Row-segment layout of the fused consumer (Store::SEG with S7): a warp-task is 32 / S rows of
+// nps = 128 S outputs, lane j of a row owns its pairs [128 j, 128 j + 128) and starts there by
+// jump-ahead, so each 16-output batch flush writes 32 chunks of 128 bytes 1 KiB apart inside one
+// contiguous 32 KiB block (pure-store ceiling 6.12 vs 5.31 TB/s for one lane per row,
+// profiles/r02f_consumer_store_patterns.json), from the same 4.6 KiB tile as the ROW layout.
+// Speculation as in SEG: a batch is computed assuming every x1 is accepted and below a - 1; the
+// warp vote comes BEFORE the batch is counted, so the statistics only ever see values of
+// accepted pairs.  On an anomaly the warp finishes the task exactly: each lane counts its
+// remaining pairs (statistics of the accepted ones, R11 clamp included), the row's last lane
+// continues past pair nps for the outputs the rejections cost, and seg_exact rewrites the rows'
+// outputs at their shifted positions.  The statistics are position-free, so nothing counted
+// before the anomaly needs retracting.
+template <int MODE, class Cons>
+__device__ __forceinline__ void run_task_seg_consume(const GenArgs &g, uint32_t tile,
+                                                     uint32_t lane, uint64_t t, Cons &cons) {
+    constexpr bool FULL32 = MODE == 2;
+    const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
+    const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
+    const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
+    const uint32_t span_fast = FULL32 ? 0xFFFFFFFDu : g.span_fast;
+    const uint32_t log2S = g.seg_log2, S = 1u << log2S, j = lane & (S - 1u);
+    const uint32_t rpw = 32u >> log2S;
+    const uint64_t row0 = t * rpw, row = row0 + (lane >> log2S);
+    const bool live = row < g.n_streams;
+    const uint64_t rows_left = g.n_streams - row0;
+    const uint32_t nchunks = rows_left >= rpw ? 32u : (uint32_t)rows_left << log2S;
+    Xs128 st = stream_start(g.seed, g.stream_begin + row);
+    if (j) {  // T^(256 j) s: byte tables with the lane index innermost (one run per row)
+        const uint32_t words[4] = {st.x, st.y, st.z, st.w};
+        uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t v = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+            const uint4 tv = __ldg(&g.jump_tab[((uint32_t)k * 256u + v) * 32u + j]);
+            r0 ^= tv.x;
+            r1 ^= tv.y;
+            r2 ^= tv.z;
+            r3 ^= tv.w;
+        }
+        st = Xs128{r0, r1, r2, r3};
+    }
+    const Xs128 seg0 = st;
+    constexpr uint32_t RS = kCols * 8u + 16u;  // padded tile row (one batch per lane)
+    const uint32_t my = tile + lane * RS;
+    double *blk = g.out + row0 * g.nps;      // tile row r -> blk + 128 r + 16 b (nps = 128 S)
+    constexpr uint32_t kB = (uint32_t)kSegOut / kCols;
+    uint32_t b = 0;
+#pragma unroll 1
+    for (; b < kB; ++b) {
+        const Xs128 save = st;
+        double q[kCols];
+        bool rej = false;
+#pragma unroll
+        for (int i = 0; i < kCols; ++i) {
+            const uint32_t x1 = draw(st) >> sh1;
+            const uint32_t x2 = draw(st) >> sh2;
+            rej |= !accepted(x1, lo, span_fast);
+            q[i] = eq4_mode<MODE, false>(x1, x2, g);
+        }
+        if (__builtin_expect(__any_sync(0xFFFFFFFFu, rej), 0)) {
+            st = save;
+            break;
+        }
+        if (live) {
+#pragma unroll
+            for (int i = 0; i < kCols; ++i) cons.add(q[i], i);
+        }
+#pragma unroll
+        for (int c = 0; c < kCols / 2; ++c) sts_v2(my + (c << 4), q[2 * c], q[2 * c + 1]);
+        __syncwarp();
+        const uint32_t c = lane & 7u, rsub = lane >> 3;
+        double *dst = blk + (uint64_t)rsub * kSegOut + b * kCols + 2 * c;
+        if (nchunks == 32u) {
+#pragma unroll
+            for (uint32_t r = rsub; r < 32u; r += 4u) {
+                double a0, a1;
+                lds_v2(tile + r * RS + (c << 4), a0, a1);
+                stg_v2_cs(dst, a0, a1);
+                dst += 4u * kSegOut;
+            }
+        } else {
+#pragma unroll 1
+            for (uint32_t r = rsub; r < nchunks; r += 4u) {
+                double a0, a1;
+                lds_v2(tile + r * RS + (c << 4), a0, a1);
+                stg_v2_cs(dst, a0, a1);
+                dst += 4u * kSegOut;
+            }
+        }
+        __syncwarp();
+    }
+    if (__builtin_expect(b < kB, 0)) {  // warp-uniform: the vote above
+        // statistics of this lane's remaining pairs, exactly (R11 clamp included)
+        uint32_t cnt = b * (uint32_t)kCols;  // every earlier pair was accepted
+#pragma unroll 1
+        for (uint32_t i = b * (uint32_t)kCols; i < (uint32_t)kSegOut; ++i) {
+            const uint32_t x1 = draw(st) >> sh1;
+            const uint32_t x2 = draw(st) >> sh2;
+            if (accepted(x1, lo, span)) {
+                if (live) cons.add(eq4_pair<false, true>(x1, x2, w, g.Cs, g.Ds, g.y));
+                ++cnt;
+            }
+        }
+        uint32_t tot = cnt;  // the row's accepted pairs among its nps pairs
+        for (uint32_t o = 1; o < S; o <<= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
+        if (j == S - 1u) {   // the outputs the rejections cost, past pair nps
+#pragma unroll 1
+            for (uint64_t p = tot; p < g.nps; ++p) {
+                const double q = exact_output<true, false, false>(st, sh1, sh2, w, lo, span, g);
+                if (live) cons.add(q);
+            }
+        }
+        __syncwarp();  // the speculative stores above come before the exact rewrite
+        seg_exact<MODE, false, (int)kSegOut>(g, seg0, j, S, row, live);
+    }
+}
+
 // One-warp CTAs (12 per SM, smem-bound), each running `tpc` consecutive warp tasks of 32
 // lane segments (a task = 32 / S rows = one contiguous 32 KiB block of the output), so the
 // hardware's in-order CTA dispatch keeps the blocks being written in one moving window (a
@@ -1973,8 +2100,9 @@ static cudaError_t cons_launch(const CUtensorMap &m, const GenArgs &g, int grid,
     constexpr int kWarps = cons_warps<ST, WRITE>();
     auto k = consume_kernel<MODE, SPEC, IEEE, ALG1, ST, WRITE, RED, EXACT_GUARD>;
     const size_t smem = 1024 + (size_t)kHistWords * 4u +
-                        (WRITE && ST == Store::ROW ? (size_t)kWarps * 32 * (kConsRowCols * 8 + 16)
-                                                   : (size_t)kWarps * ring<ST, WRITE>() * kTileBytes);
+                        (WRITE && (ST == Store::ROW || ST == Store::SEG)
+                             ? (size_t)kWarps * 32 * (kConsRowCols * 8 + 16)
+                             : (size_t)kWarps * ring<ST, WRITE>() * kTileBytes);
     cudaError_t e = set_smem(k, smem);
     if (e != cudaSuccess) return e;
     k<<<grid, kWarps * 32, smem, st>>>(m, g);
@@ -2031,6 +2159,25 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
                 : cons_dispatch<Store::STG8, false>(m, g, pl, f32, grid, st);
     } else {
         Store s = pl.store;
+        // row segments (SEG): the closed Eq.(4) kernels with speculation (rare rejection) only
+        if (s == Store::SEG && !(pl.spec && !pl.ieee_div && !pl.alg1 && f32 >= 1 && f32 <= 3 &&
+                                 g.nps % kSegOut == 0 && g.nps / kSegOut <= 32 &&
+                                 ((g.nps / kSegOut) & (g.nps / kSegOut - 1)) == 0))
+            s = Store::ROW;
+        if (s == Store::SEG) {
+            const void *tab = nullptr;
+            if ((e = jump_tables_interleaved(kSegDraws, &tab)) != cudaSuccess) return e;
+            g.jump_tab = static_cast<const uint4 *>(tab);
+            g.seg_log2 = 0;
+            while ((kSegOut << g.seg_log2) < g.nps) ++g.seg_log2;
+            const uint64_t seg_tasks = (g.n_streams + (32u >> g.seg_log2) - 1) / (32u >> g.seg_log2);
+            if ((uint64_t)grid > seg_tasks) grid = (int)seg_tasks;  // (>= the 32-row task count)
+#define PRNGD_CONS_SEG(M)                                                                       \
+    (red ? cons_launch<M, true, false, false, Store::SEG, true, true>(m, g, grid, st)            \
+         : cons_launch<M, true, false, false, Store::SEG, true>(m, g, grid, st))
+            e = f32 == 2 ? PRNGD_CONS_SEG(2) : f32 == 3 ? PRNGD_CONS_SEG(3) : PRNGD_CONS_SEG(1);
+#undef PRNGD_CONS_SEG
+        } else {
 #define PRNGD_CONS_W(S)                                                                         \
     (red ? cons_dispatch<S, true, true>(m, g, pl, f32, grid, st)                                 \
          : cons_dispatch<S, true>(m, g, pl, f32, grid, st))
@@ -2049,6 +2196,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
                                                    : PRNGD_CONS_W(Store::STG8);
 #endif
 #undef PRNGD_CONS_W
+        }
     }
     if (e != cudaSuccess) return e;
     *launches = 1;

@@ -196,3 +196,48 @@ def test_seg_multi_task_ctas_with_prefetched_jumps(orc):
     ref = orc.generate(p, want_consumed=True)
     assert (ref["consumed"] > 256).sum() > 50
     assert_same(out, ref["out"])
+
+
+# ------------------------------------------------------------------ fused consumer, row segments
+
+def _consume(p, flags):
+    g = P.Generator(**dict(p, flags=flags))
+    out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+    _, hist, pw, cnt = g.generate_consume(out)
+    torch.cuda.synchronize()
+    return out, hist.cpu().numpy(), pw.cpu().numpy(), int(cnt.item())
+
+
+@pytest.mark.parametrize("par", [W.FULL32,
+                                 dict(w=17, a0=0, a=2**17 - 1, b0=0, b=2**17 - 1),
+                                 dict(w=32, a0=2**16, a=2**32 - 1, b0=0, b=2**31 - 1),
+                                 dict(w=27, a0=0, a=2**27 - 1, b0=0, b=2**27 - 1)])
+@pytest.mark.parametrize("nps,ns", [(128, 70), (1024, 1000), (2048, 517), (4096, 97)])
+def test_consume_row_segments(orc, par, nps, ns):
+    """The fused consumer with 1 KiB row segments (run_task_seg_consume; AUTO and explicit SEG)
+    and with ROW tiles: outputs, histogram, count bitwise and power sums (relative 1e-12) equal
+    the oracle's.  w = 17 and the 2^-16 band on 32-bit draws reject often enough that many warps
+    take the exact finish (remaining pairs counted exactly, the row's tail past pair nps, the
+    outputs rewritten at their shifted positions); w = 27 has the R11 clamp row."""
+    p = dict(par, seed=77, stream_begin=31337, n_streams=ns, n_per_stream=nps)
+    ref = orc.generate(p, want_stats=True)
+    for flags in (P.PRNGD_FLAG_STORE_AUTO, P.PRNGD_FLAG_STORE_SEG, P.PRNGD_FLAG_STORE_ROW):
+        out, hist, pw, cnt = _consume(p, flags)
+        assert_same(out, ref["out"])
+        assert cnt == ref["count"] and np.array_equal(hist, ref["hist"]), flags
+        assert np.allclose(pw, ref["pow"], rtol=1e-12, atol=0), flags
+
+
+def test_consume_row_segments_misaligned_falls_back(orc):
+    """An 8-byte-offset output cannot take the 16-byte row-segment flush: the consumer falls back
+    to 8-byte stores with the same bits and statistics."""
+    p = dict(W.FULL32, seed=5, stream_begin=0, n_streams=300, n_per_stream=1024)
+    ref = orc.generate(p, want_stats=True)
+    g = P.Generator(**p)
+    buf = torch.full((300 * 1024 + 2,), -1.0, dtype=torch.float64, device="cuda")
+    out = buf[1:1 + 300 * 1024].view(300, 1024)
+    _, hist, pw, cnt = g.generate_consume(out)
+    torch.cuda.synchronize()
+    assert_same(out, ref["out"])
+    assert np.array_equal(hist.cpu().numpy(), ref["hist"]) and int(cnt.item()) == ref["count"]
+    assert float(buf[0]) == -1.0 and float(buf[-1]) == -1.0
