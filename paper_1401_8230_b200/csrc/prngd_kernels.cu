@@ -81,9 +81,17 @@ constexpr int kConsWarpsRegs = PRNGD_CONS_REG_WARPS;  // warps per CTA, consume 
 #endif
 constexpr int kConsWarpsRow = PRNGD_CONS_ROW_WARPS;
 constexpr int kConsRowCols = PRNGD_CONS_ROW_COLS;
+// The row-segment consumer keeps only 2-4 rows per warp in flight, so it takes 16 warps
+// (A/B, same box, cfg5 / cfg3 + statistics: 12 -> 597-606 / 608-617, 14 -> 571-574 / 581-589,
+// 16 -> 611-616 / 618-649 Gd/s; the ROW-tile consumer loses with 16: 559 vs 580)
+#ifndef PRNGD_CONS_SEG_WARPS
+#define PRNGD_CONS_SEG_WARPS 16
+#endif
+constexpr int kConsWarpsSeg = PRNGD_CONS_SEG_WARPS;
 template <Store ST, bool WRITE>
 constexpr int cons_warps() {
-    return (WRITE && (ST == Store::ROW || ST == Store::SEG)) ? kConsWarpsRow
+    return (WRITE && ST == Store::SEG) ? kConsWarpsSeg
+           : (WRITE && ST == Store::ROW) ? kConsWarpsRow
                                        : (ring<ST, WRITE>() > 0 ? kConsWarpsTiles : kConsWarpsRegs);
 }
 constexpr int kHistWords = 32768;  // 65536 u16 counters in pairs (128 KiB)
