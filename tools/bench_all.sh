@@ -1,18 +1,21 @@
 #!/bin/bash
-# Run bench.py over every BASELINE config on one B200 (under gpurun); JSON lines -> gpurun_out/
+# Run bench.py over every BASELINE config and the NEXT workloads on one B200 (under gpurun);
+# JSON lines -> gpurun_out/bench_all.jsonl.  Write workloads carry the >= 1.5 s sustained record.
 out=gpurun_out/bench_all.jsonl; : > $out
 run() { timeout 900 python bench.py --e2e-steps 0 --no-cpu-baseline "$@" 2>/dev/null | tail -1 >> $out; }
 run --workload cfg1 --steps 200
 run --workload cfg2 --steps 200
 run --workload cfg3 --steps 200
-run --workload cfg3 --steps 1000            # sustained (power-capped) steady state
 run --workload cfg3 --steps 200 --store seg
+run --workload cfg3 --steps 50 --consume
 run --workload cfg4 --steps 50
 run --workload cfg4 --steps 50 --consume
 run --workload cfg5 --steps 50
+run --workload cfg5 --steps 50 --store row
 run --workload cfg5 --steps 50 --no-write
 run --workload mrg26 --steps 50
 run --workload mrg26 --steps 20 --consume
+run --workload mrg26 --steps 20 --consume --no-write
 run --workload eq5 --steps 100
 run --workload eq6 --steps 100
 run --workload open4 --steps 100
