@@ -532,8 +532,10 @@ def main():
     tr = traffic_per_launch()
     traffic, traffic_src = None, None
     path_name = STORES.get(g.info["store"])
+    kind = "consume" if consume else "generate"
     for ent in (tr or {}).get("entries", []):
-        if ent.get("workload") == args.workload and ent.get("store") == path_name:
+        if (ent.get("workload") == args.workload and ent.get("kind", "generate") == kind and
+                args.store == "auto" and not args.no_write):
             traffic, traffic_src = ent.get("dram_bytes_per_launch"), ent.get("source")
     if consume:
         # dominant kernel = fused generate+consume; its own duration needs the launch list.

@@ -30,7 +30,7 @@ KEYS = [
 STALLS = "smsp__pcsamp_warps_issue_stalled_"
 # workload -> (bench store label, algorithmic bytes per launch)
 WORK = {"cfg3": ("ROW", 8 << 30), "cfg4": ("ROW", 32 << 30), "cfg5": ("ROW", 16 << 30),
-        "mrg26": ("ROW", 8 << 30), "cfg1": ("SEG", 8 << 20)}
+        "mrg26": ("ROW", 8 << 30), "cfg1": ("SEG", 8 << 20), "cfg2": ("JUMP", 32 << 20)}
 
 
 def load(path):
@@ -59,7 +59,9 @@ def main():
             return float(v) * scale.get(u, 1)
         wr, rd = val("dram__bytes_write.sum"), val("dram__bytes_read.sum")
         if wl in WORK:
-            traffic.append({"workload": wl, "store": WORK[wl][0],
+            kind = "consume" if "consume" in name else "generate"
+            traffic.append({"workload": wl, "kind": kind,
+                            "store": "SEG" if (kind == "consume" and wl == "cfg5") else WORK[wl][0],
                             "kernel": d.get("Kernel Name", ("", "?"))[1],
                             "dram_bytes_per_launch": int(wr + rd), "dram_bytes_write": int(wr),
                             "dram_bytes_read": int(rd),
@@ -73,8 +75,9 @@ def main():
             prev = json.load(f).get("entries", [])
     except (OSError, ValueError):
         prev = []
-    fresh = {e["workload"]: e for e in traffic}
-    traffic = [fresh.pop(e["workload"], e) for e in prev] + list(fresh.values())
+    key = lambda e: (e["workload"], e.get("kind", "generate"))  # noqa: E731
+    fresh = {key(e): e for e in traffic}
+    traffic = [fresh.pop(key(e), e) for e in prev] + list(fresh.values())
     with open("profiles/traffic.json", "w") as f:
         json.dump({"entries": traffic,
                    "note": "write bytes sit slightly below the algorithmic bytes: dirty lines "
