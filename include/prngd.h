@@ -101,9 +101,10 @@ typedef enum {
 #define PRNGD_FLAG_MAP_EQ6       (2u << PRNGD_MAP_SHIFT)
 #define PRNGD_FLAG_OPEN          0x100u  /* return 1 - z': never 0; the histogram puts
                                             1.0 in bin 65535 (R18) */
-/* NEXT-3 intra-stream parallelism: one warp per stream, lanes start at draws 0, 32, 64, ... of
- * the stream via GF(2) jump-ahead of xorshift128 and a warp scan of accepted counts places every
- * output exactly where the sequential order puts it.  Chosen automatically by prngd_generate
+/* NEXT-3 intra-stream parallelism: one warp per stream, lanes start at draws 0, 2P, 4P, ... of
+ * the stream via GF(2) jump-ahead of xorshift128 (P = 33 pairs per lane for rows of >= 1000
+ * outputs, else 17) and a warp scan of accepted counts places every output exactly where the
+ * sequential order puts it.  Chosen automatically by prngd_generate
  * when there are too few streams to fill the GPU (AUTO store path, n_streams < 16384 and n_per_stream >= 512,
  * pair-drop consumption); these flags force it on or off. */
 /* NEXT-2: MRG32k3a base generator (L'Ecuyer 1999; P:165 names it) instead of xorshift128.

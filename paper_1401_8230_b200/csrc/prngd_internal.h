@@ -78,7 +78,8 @@ struct Plan {
 
 // NEXT-3 jump-ahead (prngd_jump.cpp): lane l of a warp starts a round at draw l*kJumpDraws of
 // its stream (kJumpDraws / 2 = 17 pairs per lane per round, 32 lanes per stream: two rounds
-// cover a 1024-output row with up to 5.9% rejection, so no sequential tail is needed).
+// cover a 1024-output row with up to 5.9% rejection, so no sequential tail is needed); rows of
+// >= 1000 outputs use 33-pair rounds instead (prngd_kernels.cu kJumpPairsLong, distance 66).
 #ifndef PRNGD_JUMP_PAIRS
 #define PRNGD_JUMP_PAIRS 17  // cfg2 A/B: 16 -> 224, 17 -> 249-251, 18 -> 232, 24 -> 224 Gd/s
 #endif

@@ -22,6 +22,7 @@
 #include <cstring>
 #include <mutex>
 #include <set>
+#include <type_traits>
 #include <utility>
 
 #include "prngd_device.cuh"
@@ -1237,14 +1238,19 @@ __global__ void __launch_bounds__(kMrgConsWarps * 32, 1)
 }
 
 // ------------------------------------------------------------------------------ NEXT-3 jump kernel
-// One warp per stream, kJumpWarps streams per CTA (a 4096-stream config is a single wave).  Each round, lane
-// l jumps the round-start state by l * kJumpDraws draws (J_l = T^(34 l), byte tables) and draws
-// kJumpPairs = 16 consecutive pairs, keeping the outputs in registers; a warp scan of the
-// per-lane accepted counts gives every accepted output its sequential position (pair-drop, R2),
-// the lanes scatter them into a compact shared-memory run, and the warp writes the run with
-// coalesced stores.  Lane 31's final state starts the next round; a short remainder is finished
-// by one lane sequentially.
+// One warp per stream, kJumpWarps streams per CTA.  Each round, lane l jumps the round-start
+// state by l * 2P draws (J_l = T^(2P l), byte tables) and draws P consecutive pairs, keeping the
+// outputs in registers; a warp scan of the per-lane accepted counts gives every accepted output
+// its sequential position (pair-drop, R2), the lanes scatter them into a compact shared-memory
+// run, and the warp writes the run with coalesced stores.  Lane 31's final state starts the next
+// round; a short remainder is finished by one lane sequentially.  P = 17 (two rounds per
+// 1024-output row, the short-row kernel) or P = kJumpPairsLong = 33 for rows of >= 1000 outputs:
+// 1056 pairs cover a 1024-output row in ONE round unless more than 32 pairs are rejected (at
+// w = 8, 8.3 expected), halving the jumps and scans per output; 128 registers, 4 CTAs per SM
+// (cfg2, same box: 250.6 -> 273.4-273.6 Gd/s; 33 pairs unconstrained, 142 registers: 259;
+// capped at 96 registers with spills: 251; 25 pairs: 223, `profiles/r02m_jump_pairs_ab.txt`).
 constexpr int kJumpPairs = (int)(kJumpDraws / 2);
+constexpr int kJumpPairsLong = 33;
 #ifndef PRNGD_JUMP_TAIL
 #define PRNGD_JUMP_TAIL 24
 #endif
@@ -1257,11 +1263,14 @@ constexpr int kJumpWarps = PRNGD_JUMP_WARPS;  // warps (streams) per CTA
 // accepted output near p = 16 l + i, so without the pad every lane of a store hits the same
 // bank (a 128-byte stride); with it they spread over the banks.  Reads of consecutive p stay
 // contiguous within each run of 16.
-// (An odd kJumpPairs spreads the lanes by itself: no pad.)
-constexpr uint32_t kJumpPad = (kJumpPairs % 2 == 0) ? 1u : 0u;
-constexpr uint32_t kJumpCompBytes = 32u * kJumpPairs * 8u + (32u * kJumpPairs / 16u + 2u) * 8u;
+// (An odd pair count spreads the lanes by itself: no pad.)
+template <int P>
+constexpr uint32_t jump_pad() { return (P % 2 == 0) ? 1u : 0u; }
+template <int P>
+constexpr uint32_t jump_comp_bytes() { return 32u * P * 8u + (32u * P / 16u + 2u) * 8u; }
+template <int P>
 __device__ __forceinline__ uint32_t jump_comp_off(uint32_t p) {
-    return (p + kJumpPad * (p >> 4)) << 3;
+    return (p + jump_pad<P>() * (p >> 4)) << 3;
 }
 
 __device__ __forceinline__ Xs128 jump_state(const uint4 *__restrict__ tab, const Xs128 &s) {
@@ -1300,8 +1309,8 @@ __device__ __forceinline__ Xs128 jump_state_nib(const uint4 *__restrict__ tab, c
 #ifndef PRNGD_JUMP_MINB
 #define PRNGD_JUMP_MINB 1  // A/B cfg2: 7 (one wave, 72 regs + spills) 253 vs 1 (74 regs) 252 Gd/s
 #endif
-template <int MODE>
-__global__ void __launch_bounds__(kJumpWarps * 32, PRNGD_JUMP_MINB)
+template <int MODE, int P>
+__global__ void __launch_bounds__(kJumpWarps * 32, P > 32 ? 4 : PRNGD_JUMP_MINB)
     gen_jump_kernel(const GenArgs g, const uint4 *__restrict__ tabs) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -1312,7 +1321,8 @@ __global__ void __launch_bounds__(kJumpWarps * 32, PRNGD_JUMP_MINB)
     const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
     const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
-    const uint32_t comp = aligned_smem_base(smem_raw) + warp * kJumpCompBytes;
+    const uint32_t comp = aligned_smem_base(smem_raw) + warp * jump_comp_bytes<P>();
+
     double *row_out = g.out + row * g.nps;
     Xs128 S = stream_start(g.seed, g.stream_begin + row);
     uint64_t base = 0;
@@ -1335,20 +1345,21 @@ __global__ void __launch_bounds__(kJumpWarps * 32, PRNGD_JUMP_MINB)
             }
             st = Xs128{r0, r1, r2, r3};
         }
-        double q[kJumpPairs];
-        uint32_t mask = 0;
+        double q[P];
+        using MaskT = typename std::conditional<(P > 32), uint64_t, uint32_t>::type;
+        MaskT mask = 0;
 #pragma unroll
-        for (int i = 0; i < kJumpPairs; ++i) {
+        for (int i = 0; i < P; ++i) {
             const uint32_t x1 = draw(st) >> sh1;
             const uint32_t x2 = draw(st) >> sh2;
-            mask |= (accepted(x1, lo, span) ? 1u : 0u) << i;
+            mask |= (MaskT)(accepted(x1, lo, span) ? 1u : 0u) << i;
             q[i] = EQ4 ? eq4_mode<MODE, false>(x1, x2, g) : map_pair<false, true>(x1, x2, g.map);
         }
         if (EQ4 && g.span != g.span_fast) {  // R11 clamp only where the host found it needed
 #pragma unroll
-            for (int i = 0; i < kJumpPairs; ++i) q[i] = fmin(q[i], kBelowOne);
+            for (int i = 0; i < P; ++i) q[i] = fmin(q[i], kBelowOne);
         }
-        const uint32_t cnt = __popc(mask);
+        const uint32_t cnt = P > 32 ? (uint32_t)__popcll(mask) : (uint32_t)__popc((uint32_t)mask);
         uint32_t incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1359,17 +1370,19 @@ __global__ void __launch_bounds__(kJumpWarps * 32, PRNGD_JUMP_MINB)
         // compact: accepted output k of this lane at position incl - cnt + k of the round
         uint32_t pos = incl - cnt;
 #pragma unroll
-        for (int i = 0; i < kJumpPairs; ++i) {
-            if ((mask >> i) & 1u) {
-                sts_f64(comp + jump_comp_off(pos), q[i]);
+        for (int i = 0; i < P; ++i) {
+            if ((mask >> i) & (MaskT)1) {
+                sts_f64(comp + jump_comp_off<P>(pos), q[i]);
                 ++pos;
             }
         }
         __syncwarp();
+        // (16-byte copies of slot pairs, with the run shifted to the output's parity: more
+        // registers, spills at P = 33, cfg2 255 vs 272 Gd/s -- not kept)
         const uint64_t n = (g.nps - base) < (uint64_t)total ? (g.nps - base) : (uint64_t)total;
         for (uint32_t j = lane; j < (uint32_t)n; j += 32u) {
             double v;
-            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(comp + jump_comp_off(j)));
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(comp + jump_comp_off<P>(j)));
             row_out[base + j] = v;
         }
         __syncwarp();
@@ -2356,21 +2369,20 @@ cudaError_t launch_generate_mrg(const GenArgs &g, bool alg1, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, cudaStream_t st) {
-    (void)pl;
+template <int P>
+static cudaError_t jump_launch(const GenArgs &g, cudaStream_t st) {
     const void *tables = nullptr;  // the byte tables with the lane index innermost
-    cudaError_t e0 = jump_tables_interleaved(kJumpDraws, &tables);
-    if (e0 != cudaSuccess) return e0;
-    const size_t smem = 1024 + (size_t)kJumpWarps * kJumpCompBytes;
+    cudaError_t e = jump_tables_interleaved(2u * P, &tables);
+    if (e != cudaSuccess) return e;
+    const size_t smem = 1024 + (size_t)kJumpWarps * jump_comp_bytes<P>();
     const uint64_t grid = (g.n_streams + kJumpWarps - 1) / kJumpWarps;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     const uint4 *t = static_cast<const uint4 *>(tables);
     const int mode = kernel_mode(g);
-    cudaError_t e;
 #define PRNGD_JUMP_LAUNCH(M)                                                                    \
     do {                                                                                        \
-        if ((e = set_smem(gen_jump_kernel<M>, smem)) != cudaSuccess) return e;                  \
-        gen_jump_kernel<M><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);               \
+        if ((e = set_smem(gen_jump_kernel<M, P>, smem)) != cudaSuccess) return e;               \
+        gen_jump_kernel<M, P><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);            \
     } while (0)
     switch (mode) {
         case 3: PRNGD_JUMP_LAUNCH(3); break;
@@ -2380,6 +2392,12 @@ cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, cudaStream_t 
     }
 #undef PRNGD_JUMP_LAUNCH
     return cudaGetLastError();
+}
+
+cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, cudaStream_t st) {
+    (void)pl;
+    // long rows: one 33-pair round per 1024 outputs; short rows: 17-pair rounds
+    return g.nps >= 1000 ? jump_launch<kJumpPairsLong>(g, st) : jump_launch<kJumpPairs>(g, st);
 }
 
 cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, cudaStream_t st) {
