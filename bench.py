@@ -347,10 +347,11 @@ def main():
         # rank when the fabric cannot provide it
         try:
             peer = D.McStats()
-            peer.zero(stream)
-            torch.cuda.synchronize()
-            dist.barrier()
-            reduce_mode = "nvls"
+            ok, why = D.verify_reduction(peer, device_wait=not same_gpu)
+            if not ok:
+                peer.close()
+                raise RuntimeError(f"self-check against NCCL failed: {why}")
+            reduce_mode = "nvls (verified against NCCL on a small workload)"
         except Exception as e:
             peer, mc_err = None, str(e)
     if consume and world > 1 and peer is None:
@@ -369,8 +370,12 @@ def main():
             ok = torch.tensor([0 if err else 1], dtype=torch.int32, device="cuda")
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             if ok.item() == 1:
-                reduce_mode = "p2p"
-            else:
+                vok, why = D.verify_reduction(peer, device_wait=not same_gpu)
+                if vok:
+                    reduce_mode = "p2p (verified against NCCL on a small workload)"
+                else:
+                    err = f"self-check against NCCL failed: {why}"
+            if ok.item() != 1 or err:
                 if peer is not None:
                     torch.cuda.synchronize()
                     if rank != 0:
@@ -383,8 +388,8 @@ def main():
                     dist.barrier()
                 reduce_mode = "nccl (peer memory unavailable" + (f": {err})" if err else " on a rank)")
             dist.barrier()
-            if reduce_mode == "p2p" and mc_err:
-                reduce_mode = f"p2p (multicast unavailable: {mc_err})"
+            if reduce_mode.startswith("p2p") and mc_err:
+                reduce_mode += f"; multicast unavailable: {mc_err}"
 
     def step(st=stream):
         if consume and peer is not None:

@@ -273,6 +273,54 @@ class McStats:
         self.m = None
 
 
+def verify_reduction(ps, group=None, device_wait: bool = True) -> tuple[bool, str]:
+    """Self-check of a shared statistics buffer (PeerStats or McStats) before it is trusted: every
+    rank reduces a small known workload through it and the result is compared, bin for bin, with
+    the NCCL all-reduce of the same workload's local statistics.  Returns (ok on every rank,
+    detail); leaves the buffer zeroed.  device_wait=False synchronises on the host instead of the
+    device-side acquire wait (ranks sharing one GPU)."""
+    import torch
+    import torch.distributed as dist
+    from . import prngd as P
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    st = torch.cuda.current_stream()
+    p = dict(w=32, a0=0, a=2**32 - 1, b0=0, b=2**32 - 1, seed=0x5EED, stream_begin=64 * rank,
+             n_streams=64, n_per_stream=256)
+    g = P.Generator(**p)
+    try:
+        _, h, pw, c = g.generate_consume(None)
+        allreduce_stats(h, pw, c, group=group)
+        ps.zero(st)
+        torch.cuda.synchronize()
+        if dist.is_initialized():
+            dist.barrier(group=group)
+        ps.consume(g.handle, None, st)
+        reader = isinstance(ps, McStats) or rank == getattr(ps, "owner", 0)
+        if not device_wait:
+            torch.cuda.synchronize()
+            if dist.is_initialized():
+                dist.barrier(group=group)
+        ok, detail = True, "ok"
+        if reader:
+            if device_wait:
+                ps.wait(ps.expected(1), st)
+            gh, gp, gc = ps.read()
+            if int(gc.item()) != int(c.item()) or not torch.equal(gh, h):
+                ok, detail = False, f"count {int(gc.item())} vs {int(c.item())} or histogram differs"
+            elif not torch.allclose(gp, pw, rtol=1e-12, atol=0):
+                ok, detail = False, "power sums differ"
+        torch.cuda.synchronize()
+        ok = _agree(ok, group)
+        ps.zero(st)
+        torch.cuda.synchronize()
+        if dist.is_initialized():
+            dist.barrier(group=group)
+        return ok, detail if ok else (detail if detail != "ok" else "failed on another rank")
+    finally:
+        g.close()
+
+
 def generate_sharded(p: dict, mode: str = STRONG, consume: bool = False, write: bool = True,
                      group=None, deterministic: bool = False,
                      local: Callable | None = None):

@@ -60,6 +60,8 @@ def _worker(rank, world, port, p, mode, queue):
         D.allreduce_stats(hist, pw, cnt)
         # 3. peer-memory reduction, two calls per rank, completion by the arrival counter
         ps = D.PeerStats()
+        vok, why = D.verify_reduction(ps)          # device-side wait across GPUs
+        assert vok, why
         ps.zero(st)
         torch.cuda.synchronize()
         dist.barrier()

@@ -35,6 +35,10 @@ def _worker(rank, world, port, p, calls, queue):
         q = D.shard_params(p, rank, world, D.STRONG)
         g = P.Generator(**q)
         ps = D.PeerStats()
+        # the bench's self-check of a shared buffer against the all-reduce (host-side
+        # completion: the ranks share one GPU)
+        vok, why = D.verify_reduction(ps, device_wait=False)
+        assert vok, why
         ps.zero()
         torch.cuda.synchronize()
         dist.barrier()
