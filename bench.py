@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--workload", default="cfg3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--warm-l2", action="store_true",
+                    help="experiments only: no L2 flush between the steps of small workloads "
+                         "(the line says so in config.l2); never a bench value")
     ap.add_argument("--sustained-s", type=float, default=1.5,
                     help="length of the sustained-throughput window (0: skip)")
     ap.add_argument("--consume", action="store_true",
@@ -420,7 +423,7 @@ def main():
     # Outputs smaller than twice the 126 MB L2 would stay cache-resident between steps: those
     # workloads write a 256 MiB scratch buffer between timed steps (an L2 flush) and are timed
     # by per-step events around the step alone.
-    l2_flush = 8 * nout < (256 << 20)
+    l2_flush = 8 * nout < (256 << 20) and not args.warm_l2
     # (written, then a second buffer read, so the flush's own dirty lines are written back
     # before the timed step rather than during it)
     scratch = torch.empty(32 << 20, dtype=torch.float64, device="cuda") if l2_flush else None
@@ -727,7 +730,9 @@ def main():
             "config": {"workload": f"{args.workload}: {desc}",
                        "streams_per_gpu": p["n_streams"], "n_per_stream": p["n_per_stream"],
                        "seed": p["seed"], "bytes_written_per_step_per_gpu": 8 * nout,
-                       "l2": ("outputs fit in the 126 MB L2: a 256 MiB buffer is written and "
+                       "l2": ("EXPERIMENT: warm L2, no flush between steps (--warm-l2)"
+                              if args.warm_l2 and 8 * nout < (256 << 20) else
+                              "outputs fit in the 126 MB L2: a 256 MiB buffer is written and "
                               "another read between timed steps (L2 flush, write-back drained); "
                               "per-step events time the step"
                               if l2_flush else
