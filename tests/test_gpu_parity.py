@@ -182,6 +182,21 @@ def test_generate_host_matches_device(orc):
     assert_same(host, dev.cpu().numpy())
 
 
+def test_generate_host_jump_kernel_chunks(orc):
+    """prngd_generate_host takes the kernel prngd_get_info reports (here the NEXT-3 jump kernel,
+    33-pair rounds) for each staging chunk (2720 rows of 96 KiB per 256 MiB chunk: 2 chunks)."""
+    p = W.config("cfg2", n_streams=4000, n_per_stream=12288)
+    g = P.Generator(**p)
+    assert g.info["kernel"] == 2
+    host = g.generate_host().numpy()
+    dev = g.generate()
+    torch.cuda.synchronize()
+    assert np.array_equal(host.view(np.int64), dev.cpu().numpy().view(np.int64))
+    for r in (0, 1, 2719, 2720, 3999):
+        ref = orc.generate(p, stream_begin=r, n_streams=1)["out"]
+        assert np.array_equal(host[r].view(np.int64), ref.ravel().view(np.int64))
+
+
 # ------------------------------------------------------------------ the mapping alone
 
 def test_map_exhaustive_w8(orc):
@@ -460,7 +475,7 @@ def test_mrg32k3a_generate_host(orc):
     dev = g.generate()
     torch.cuda.synchronize()
     assert np.array_equal(host.view(np.int64), dev.cpu().numpy().view(np.int64))
-    rows = [0, 1, 2751, 2752, 4999]  # 256 MiB chunks: 2752 rows (whole warp tasks)
+    rows = [0, 1, 2719, 2720, 4999]  # 256 MiB chunks: 2720 rows (whole warp tasks)
     for r in rows:
         ref = orc.generate(p, stream_begin=r, n_streams=1)["out"]
         assert np.array_equal(host[r].view(np.int64), ref.ravel().view(np.int64))
