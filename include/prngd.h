@@ -289,6 +289,9 @@ PRNGD_API prngd_status prngd_generate_consume_mc(const prngd_handle *h, double *
  *   3. every rank: prngd_mc_add_device(m); barrier
  *   4. every rank: prngd_mc_bind_map(m, &mc_ptr, &local_ptr) (zeroed local copy); barrier
  *   5. prngd_mc_destroy(m) on every rank (after a barrier) when done.
+ * To let the other ranks fetch the descriptor with pidfd_getfd, prngd_mc_create allows ptrace
+ * attachment to the owner process (PR_SET_PTRACER_ANY, Yama) until the owner's
+ * prngd_mc_bind_map, which withdraws it and closes the exported descriptor.
  * prngd_mc_supported reports CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED for the current device.
  * Any step returns PRNGD_ECUDA / PRNGD_EUNSUPPORTED with the driver's reason when the fabric or
  * the driver cannot provide the object (e.g. one-GPU leases: cuMulticastCreate refuses); callers

@@ -233,6 +233,13 @@ PRNGD_API prngd_status prngd_mc_add_device(prngd_mc *m) {
 PRNGD_API prngd_status prngd_mc_bind_map(prngd_mc *m, void **mc_ptr, void **local_ptr) {
     if (!m || !mc_ptr || !local_ptr) return mc_fail(PRNGD_EINVAL, "null argument");
     const Drv &d = drv();
+    if (m->export_fd >= 0) {
+        // every rank has imported the descriptor by now (the caller's barrier after step 2):
+        // withdraw the ptrace permission prngd_mc_create granted and close the export
+        prctl(PR_SET_PTRACER, 0, 0, 0, 0);
+        close(m->export_fd);
+        m->export_fd = -1;
+    }
     CUmemAllocationProp ap;
     std::memset(&ap, 0, sizeof(ap));
     ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
