@@ -33,7 +33,7 @@ struct GenArgs {
     uint32_t mrg_mask1, mrg_mask2;  //         and the width masks
     double mrg_m1, mrg_inv1, mrg_m2, mrg_inv2;  // MRG32k3a moduli and RN(1/m) (binary64 form)
     // consumer (S7)
-    uint32_t *hist_slab;    // [gridDim.x][32768] packed u16 pairs (consume kernels only)
+    uint32_t *hist_slab;    // [gridDim.x][65536] one u32 per bin (consume kernels only)
     int64_t *hist_spill;    // [65536] int64 carries of the packed counters
     double *pow_slab;       // [gridDim.x][4]
     uint32_t *overflow;     // set by an optimistic (RED) consume kernel whose 16-bit fields wrapped

@@ -96,6 +96,9 @@ constexpr int cons_warps() {
                                        : (ring<ST, WRITE>() > 0 ? kConsWarpsTiles : kConsWarpsRegs);
 }
 constexpr int kHistWords = 32768;  // 65536 u16 counters in pairs (128 KiB)
+constexpr int kBins = 65536;
+// Per-CTA slabs in global memory hold one u32 per bin (256 KiB): the epilogues unpack their
+// shared-memory fields into it, and the 8-bit-field consumer (H8) adds its periodic flushes.
 
 // ------------------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -817,15 +820,18 @@ __device__ __forceinline__ void consume_epilogue(const Cons &cons, const uint32_
         for (int wi = 0; wi < kWarps; ++wi) acc = __dadd_rn(acc, red[wi][threadIdx.x]);
         g.pow_slab[blockIdx.x * 4 + threadIdx.x] = acc;
     }
-    uint4 *dst = reinterpret_cast<uint4 *>(g.hist_slab + (size_t)blockIdx.x * kHistWords);
+    // unpack word j (bins j, j + 32768) into the u32-per-bin slab
+    uint4 *lo_dst = reinterpret_cast<uint4 *>(g.hist_slab + (size_t)blockIdx.x * kBins);
+    uint4 *hi_dst = lo_dst + kHistWords / 4;
     const uint4 *src = reinterpret_cast<const uint4 *>(hist);
     unsigned long long fsum = 0;  // sum of this thread's 16-bit fields (RED check)
     for (uint32_t i = threadIdx.x; i < kHistWords / 4; i += blockDim.x) {
         const uint4 v = src[i];
-        dst[i] = v;
-        if (RED)
-            fsum += (v.x & 0xFFFFu) + (v.x >> 16) + (v.y & 0xFFFFu) + (v.y >> 16) +
-                    (v.z & 0xFFFFu) + (v.z >> 16) + (v.w & 0xFFFFu) + (v.w >> 16);
+        const uint4 lo = make_uint4(v.x & 0xFFFFu, v.y & 0xFFFFu, v.z & 0xFFFFu, v.w & 0xFFFFu);
+        const uint4 hi = make_uint4(v.x >> 16, v.y >> 16, v.z >> 16, v.w >> 16);
+        lo_dst[i] = lo;
+        hi_dst[i] = hi;
+        if (RED) fsum += lo.x + lo.y + lo.z + lo.w + hi.x + hi.y + hi.z + hi.w;
     }
     if (RED) {
         for (int o = 16; o > 0; o >>= 1) {
@@ -987,24 +993,16 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
     if (blockIdx.x == 0 && threadIdx.x == 0) *overflow = 0u;  // read by the exact pass before
     __shared__ long long part[8];
     long long local = 0;
-    for (uint32_t wi = blockIdx.x * blockDim.x + threadIdx.x; wi < kHistWords;
-         wi += gridDim.x * blockDim.x) {
-        long long lo = 0, hi = 0;
-        for (int s = 0; s < n_slabs; ++s) {
-            const uint32_t v = slab[(size_t)s * kHistWords + wi];
-            lo += v & 0xFFFFu;
-            hi += v >> 16;
-        }
-        lo += spill[wi];  // word wi: bin wi (low half) and bin wi + 32768 (high half)
-        hi += spill[wi + 32768u];
-        spill[wi] = 0;
-        spill[wi + 32768u] = 0;
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < (uint32_t)kBins;
+         b += gridDim.x * blockDim.x) {
+        long long c = spill[b];  // carries of the packed counters (exact pass)
+        for (int s = 0; s < n_slabs; ++s) c += slab[(size_t)s * kBins + b];
+        spill[b] = 0;
         // device atomics: the accumulators may be shared by several shards, also by processes
         // on other GPUs through peer memory (prngd_ipc_open) -- the statistics reduction
         unsigned long long *h = reinterpret_cast<unsigned long long *>(d_hist);
-        if (lo) stat_add_u64<MC>(&h[wi], (unsigned long long)lo);
-        if (hi) stat_add_u64<MC>(&h[wi + 32768u], (unsigned long long)hi);
-        local += lo + hi;
+        if (c) stat_add_u64<MC>(&h[b], (unsigned long long)c);
+        local += c;
     }
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(~0u, local, o);
     if ((threadIdx.x & 31u) == 0) part[threadIdx.x >> 5] = local;
@@ -2108,10 +2106,18 @@ cudaError_t launch_generate(const GenArgs &g, const Plan &pl, cudaStream_t st, i
                            : gen_dispatch_store<Store::STG8>(m, g, pl, f32, st);
 }
 
-// slabs, carry array, per-CTA power sums, then 16 bytes: the overflow flag and the finalize
-// kernel's block-arrival counter (both zero between calls)
+// slabs (one u32 per bin per CTA), carry array, per-CTA power sums, then 16 bytes: the overflow
+// flag and the finalize kernel's block-arrival counter (both zero between calls)
 size_t consume_scratch_bytes(int num_sms) {
-    return (size_t)num_sms * kHistWords * 4u + 65536u * 8u + (size_t)num_sms * 4u * 8u + 16u;
+    return (size_t)num_sms * kBins * 4u + 65536u * 8u + (size_t)num_sms * 4u * 8u + 16u;
+}
+static void scratch_layout(GenArgs &g, void *scratch, int num_sms) {
+    uint8_t *sp = static_cast<uint8_t *>(scratch);
+    const size_t slabs = (size_t)num_sms * kBins * 4u;
+    g.hist_slab = reinterpret_cast<uint32_t *>(sp);
+    g.hist_spill = reinterpret_cast<int64_t *>(sp + slabs);
+    g.pow_slab = reinterpret_cast<double *>(sp + slabs + 65536u * 8u);
+    g.overflow = reinterpret_cast<uint32_t *>(sp + slabs + 65536u * 8u + (size_t)num_sms * 4u * 8u);
 }
 
 template <int MODE, bool SPEC, bool IEEE, bool ALG1, Store ST, bool WRITE, bool RED = false,
@@ -2157,12 +2163,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
     if (scratch_bytes < consume_scratch_bytes(num_sms)) return cudaErrorInvalidValue;
     GenArgs g = g0;
     g.out = d_out;
-    uint8_t *sp = static_cast<uint8_t *>(scratch);
-    g.hist_slab = reinterpret_cast<uint32_t *>(sp);
-    g.hist_spill = reinterpret_cast<int64_t *>(sp + (size_t)num_sms * kHistWords * 4u);
-    g.pow_slab = reinterpret_cast<double *>(sp + (size_t)num_sms * kHistWords * 4u + 65536u * 8u);
-    g.overflow = reinterpret_cast<uint32_t *>(sp + (size_t)num_sms * kHistWords * 4u +
-                                              65536u * 8u + (size_t)num_sms * 4u * 8u);
+    scratch_layout(g, scratch, num_sms);
     const uint64_t tasks = (g.n_streams + 31u) / 32u;
     int grid = num_sms;  // persistent, one CTA per SM; every CTA gets a task when tasks >= grid
     if ((uint64_t)grid > tasks) grid = (int)tasks;
@@ -2242,12 +2243,7 @@ cudaError_t launch_consume_memory(const GenArgs &g0, const double *src, uint64_t
     *launches = 0;
     if (scratch_bytes < consume_scratch_bytes(num_sms)) return cudaErrorInvalidValue;
     GenArgs g = g0;
-    uint8_t *sp = static_cast<uint8_t *>(scratch);
-    g.hist_slab = reinterpret_cast<uint32_t *>(sp);
-    g.hist_spill = reinterpret_cast<int64_t *>(sp + (size_t)num_sms * kHistWords * 4u);
-    g.pow_slab = reinterpret_cast<double *>(sp + (size_t)num_sms * kHistWords * 4u + 65536u * 8u);
-    g.overflow = reinterpret_cast<uint32_t *>(sp + (size_t)num_sms * kHistWords * 4u +
-                                              65536u * 8u + (size_t)num_sms * 4u * 8u);
+    scratch_layout(g, scratch, num_sms);
     const int grid = num_sms;  // every CTA writes its slab (empty ones too): finalize reads all
     const size_t smem = 1024 + (size_t)kHistWords * 4u;
     cudaError_t e;
@@ -2310,12 +2306,7 @@ cudaError_t launch_generate_consume_mrg(const GenArgs &g0, bool alg1, double *d_
     if (scratch_bytes < consume_scratch_bytes(num_sms)) return cudaErrorInvalidValue;
     GenArgs g = g0;
     g.out = d_out;
-    uint8_t *sp = static_cast<uint8_t *>(scratch);
-    g.hist_slab = reinterpret_cast<uint32_t *>(sp);
-    g.hist_spill = reinterpret_cast<int64_t *>(sp + (size_t)num_sms * kHistWords * 4u);
-    g.pow_slab = reinterpret_cast<double *>(sp + (size_t)num_sms * kHistWords * 4u + 65536u * 8u);
-    g.overflow = reinterpret_cast<uint32_t *>(sp + (size_t)num_sms * kHistWords * 4u +
-                                              65536u * 8u + (size_t)num_sms * 4u * 8u);
+    scratch_layout(g, scratch, num_sms);
     const uint64_t tasks = (g.n_streams + 31u) / 32u;
     int grid = num_sms;
     if ((uint64_t)grid > tasks) grid = (int)tasks;
