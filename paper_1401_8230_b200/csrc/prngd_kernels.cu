@@ -89,10 +89,7 @@ constexpr int kConsRowCols = PRNGD_CONS_ROW_COLS;
 #define PRNGD_CONS_SEG_WARPS 16
 #endif
 constexpr int kConsWarpsSeg = PRNGD_CONS_SEG_WARPS;
-// the row-segment consumer with 8-bit fields and 256-byte chunks (consume_seg8_kernel)
-#ifndef PRNGD_CONS_H8
-#define PRNGD_CONS_H8 0  // A/B: cfg5 594-595 (H8) vs 606-610 Gd/s, isolated 3.186 ms -- not kept
-#endif
+
 template <Store ST, bool WRITE>
 constexpr int cons_warps() {
     return (WRITE && ST == Store::SEG) ? kConsWarpsSeg
@@ -102,7 +99,7 @@ constexpr int cons_warps() {
 constexpr int kHistWords = 32768;  // 65536 u16 counters in pairs (128 KiB)
 constexpr int kBins = 65536;
 // Per-CTA slabs in global memory hold one u32 per bin (256 KiB): the epilogues unpack their
-// shared-memory fields into it, and the 8-bit-field consumer (H8) adds its periodic flushes.
+// shared-memory fields into it.
 
 // ------------------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -165,9 +162,7 @@ __device__ __forceinline__ uint32_t tile_off(uint32_t row, uint32_t chunk) {
 #define PRNGD_BIN_RZ 1
 #endif
 constexpr int kPowSplit = PRNGD_POW_SPLIT;
-// H8: 8-bit fields (the row-segment consumer's 64 KiB histogram, flushed periodically into the
-// per-CTA u32 slab; consume_seg8_kernel): word j holds bins j, j + 16384, j + 32768, j + 49152.
-template <bool RED, bool BELOW1 = false, bool H8 = false>
+template <bool RED, bool BELOW1 = false>
 struct ConsumerT {
     double s1[kPowSplit], s2[kPowSplit], s3[kPowSplit], s4[kPowSplit];
     uint32_t *hist;   // shared: 32768 words; word j holds bin j (low half), bin j + 32768 (high)
@@ -209,14 +204,6 @@ struct ConsumerT {
         const uint32_t t0 = (uint32_t)__double2uint_rz(__dmul_rn(q, 262144.0));
 #endif
         const uint32_t t = BELOW1 ? t0 : min(t0, 262143u);  // R18: q = 1 -> top bin
-        if (H8) {
-            // bin = t >> 2: word (bin mod 16384) at byte offset t & 0xFFFC, byte bin >> 14 =
-            // t >> 16, i.e. the increment 1 << 8 (bin >> 14) = 1 << ((t >> 13) & 24)
-            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(hist) + (t & 0xFFFCu)),
-                         "r"(1u << ((t >> 13) & 24u))
-                         : "memory");
-            return;
-        }
         const uint32_t off = t & 0x1FFFCu;
         const bool high = t >= 0x20000u;
         const uint32_t inc = (t >> 17) * 0xFFFFu + 1u;  // 1 (low field) or 0x10000 (high)
@@ -1666,225 +1653,6 @@ __device__ __forceinline__ void run_task_seg_consume(const GenArgs &g, uint32_t 
     }
 }
 
-// ------------------------------------------------------------------------------ S7, H8 layout
-// The row-segment consumer with a 64 KiB histogram of 8-bit fields (consume_seg8_kernel): the
-// freed shared memory holds two batches per lane, so every flush writes 256-byte chunks (the
-// pure-store ceiling of the layout: 6.8 vs 5.8 TB/s with 128-byte chunks at 16 warps,
-// profiles/r02f_consumer_store_patterns.json).  A byte field would wrap after 256 adds, so all
-// warps stop every kH8FlushIters task iterations, the CTA adds its fields into its u32-per-bin
-// slab in global memory and clears them; at <= 64 adds per bin per interval on the (near
-// uniform) speculative workloads this kernel serves, a wrap is practically impossible, and
-// any wrap is still caught exactly: the field sums over all flushes must equal the outputs
-// counted, else the overflow flag sends the call to the exact (16-bit, carry-tracking) pass.
-#ifndef PRNGD_CONS_H8_WARPS
-#define PRNGD_CONS_H8_WARPS 16
-#endif
-constexpr int kH8Warps = PRNGD_CONS_H8_WARPS;
-constexpr int kH8Words = 16384;                    // 64 KiB of 8-bit fields
-constexpr uint32_t kH8Cols = 2 * kCols;            // outputs per lane per flush (256 bytes)
-constexpr uint32_t kH8RS = kH8Cols * 8u + 16u;     // padded tile row
-#ifndef PRNGD_H8_FLUSH_ITERS
-#define PRNGD_H8_FLUSH_ITERS 64  // task iterations between histogram flushes (~64 adds per bin)
-#endif
-constexpr uint32_t kH8FlushIters = PRNGD_H8_FLUSH_ITERS;
-constexpr size_t kH8Smem = 1024 + (size_t)kH8Words * 4u + (size_t)kH8Warps * 32u * kH8RS;
-
-template <int MODE, class Cons>
-__device__ __forceinline__ void run_task_seg_consume8(const GenArgs &g, uint32_t tile,
-                                                      uint32_t lane, uint64_t t, Cons &cons) {
-    constexpr bool FULL32 = MODE == 2;
-    const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
-    const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
-    const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
-    const uint32_t span_fast = FULL32 ? 0xFFFFFFFDu : g.span_fast;
-    const uint32_t log2S = g.seg_log2, S = 1u << log2S, j = lane & (S - 1u);
-    const uint32_t rpw = 32u >> log2S;
-    const uint64_t row0 = t * rpw, row = row0 + (lane >> log2S);
-    const bool live = row < g.n_streams;
-    const uint64_t rows_left = g.n_streams - row0;
-    const uint32_t nchunks = rows_left >= rpw ? 32u : (uint32_t)rows_left << log2S;
-    Xs128 st = stream_start(g.seed, g.stream_begin + row);
-    if (j) {  // T^(256 j) s (lane-interleaved byte tables)
-        const uint32_t words[4] = {st.x, st.y, st.z, st.w};
-        uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const uint32_t v = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-            const uint4 tv = __ldg(&g.jump_tab[((uint32_t)k * 256u + v) * 32u + j]);
-            r0 ^= tv.x;
-            r1 ^= tv.y;
-            r2 ^= tv.z;
-            r3 ^= tv.w;
-        }
-        st = Xs128{r0, r1, r2, r3};
-    }
-    const Xs128 seg0 = st;
-    const uint32_t my = tile + lane * kH8RS;
-    double *blk = g.out + row0 * g.nps;      // tile row r -> blk + 128 r + 32 h (nps = 128 S)
-    constexpr uint32_t kB = (uint32_t)kSegOut / kCols;
-    uint32_t b = 0;
-#pragma unroll 1
-    for (; b < kB; ++b) {
-        const Xs128 save = st;
-        double q[kCols];
-        bool rej = false;
-#pragma unroll
-        for (int i = 0; i < kCols; ++i) {
-            const uint32_t x1 = draw(st) >> sh1;
-            const uint32_t x2 = draw(st) >> sh2;
-            rej |= !accepted(x1, lo, span_fast);
-            q[i] = eq4_mode<MODE, false>(x1, x2, g);
-        }
-        if (__builtin_expect(__any_sync(0xFFFFFFFFu, rej), 0)) {
-            st = save;
-            break;
-        }
-        if (live) {
-#pragma unroll
-            for (int i = 0; i < kCols; ++i) cons.add(q[i], i);
-        }
-        const uint32_t half = b & 1u;
-#pragma unroll
-        for (int c = 0; c < kCols / 2; ++c)
-            sts_v2(my + ((half * (kCols / 2) + c) << 4), q[2 * c], q[2 * c + 1]);
-        if (!half) continue;
-        __syncwarp();
-        // 32 chunks of 256 bytes: one instruction writes two of them (16 lanes each)
-        const uint32_t c = lane & 15u, rsub = lane >> 4;
-        double *dst = blk + (uint64_t)rsub * kSegOut + (b >> 1) * kH8Cols + 2 * c;
-        if (nchunks == 32u) {
-#pragma unroll
-            for (uint32_t r = rsub; r < 32u; r += 2u) {
-                double a0, a1;
-                lds_v2(tile + r * kH8RS + (c << 4), a0, a1);
-                stg_v2_cs(dst, a0, a1);
-                dst += 2u * kSegOut;
-            }
-        } else {
-#pragma unroll 1
-            for (uint32_t r = rsub; r < nchunks; r += 2u) {
-                double a0, a1;
-                lds_v2(tile + r * kH8RS + (c << 4), a0, a1);
-                stg_v2_cs(dst, a0, a1);
-                dst += 2u * kSegOut;
-            }
-        }
-        __syncwarp();
-    }
-    if (__builtin_expect(b < kB, 0)) {  // warp-uniform: as run_task_seg_consume
-        uint32_t cnt = b * (uint32_t)kCols;
-#pragma unroll 1
-        for (uint32_t i = b * (uint32_t)kCols; i < (uint32_t)kSegOut; ++i) {
-            const uint32_t x1 = draw(st) >> sh1;
-            const uint32_t x2 = draw(st) >> sh2;
-            if (accepted(x1, lo, span)) {
-                if (live) cons.add(eq4_pair<false, true>(x1, x2, w, g.Cs, g.Ds, g.y));
-                ++cnt;
-            }
-        }
-        uint32_t tot = cnt;
-        for (uint32_t o = 1; o < S; o <<= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
-        if (j == S - 1u) {
-#pragma unroll 1
-            for (uint64_t p = tot; p < g.nps; ++p) {
-                const double q = exact_output<true, false, false>(st, sh1, sh2, w, lo, span, g);
-                if (live) cons.add(q);
-            }
-        }
-        __syncwarp();
-        seg_exact<MODE, false, (int)kSegOut>(g, seg0, j, S, row, live);
-    }
-}
-
-// Add this CTA's 8-bit fields into its u32 slab and clear them (between two CTA barriers);
-// returns the sum of the fields this thread flushed (the wrap check).
-__device__ __forceinline__ unsigned long long h8_flush(uint32_t *hist, uint32_t *slab) {
-    unsigned long long fsum = 0;
-    for (uint32_t wi = threadIdx.x; wi < (uint32_t)kH8Words; wi += blockDim.x) {
-        const uint32_t v = hist[wi];
-        if (v) {
-            hist[wi] = 0u;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t f = (v >> (8 * k)) & 0xFFu;
-                slab[wi + kH8Words * k] += f;
-                fsum += f;
-            }
-        }
-    }
-    return fsum;
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(kH8Warps * 32, 1)
-    consume_seg8_kernel(const __grid_constant__ GenArgs g) {
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t base = aligned_smem_base(smem_raw);
-    uint32_t *hist = reinterpret_cast<uint32_t *>(smem_raw + (base - smem_u32(smem_raw)));
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    uint32_t *slab = g.hist_slab + (size_t)blockIdx.x * kBins;
-    for (uint32_t i = threadIdx.x; i < (uint32_t)kH8Words; i += blockDim.x) {
-        hist[i] = 0u;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) slab[i + kH8Words * k] = 0u;  // the same thread flushes it
-    }
-    __syncthreads();
-    ConsumerT<true, true, true> cons;
-    cons.init(hist, g.hist_spill);
-    const uint32_t rpw = 32u >> g.seg_log2;
-    const uint64_t n_tasks = (g.n_streams + rpw - 1u) / rpw;
-    const uint64_t per_iter = (uint64_t)gridDim.x * kH8Warps;
-    const uint64_t iters = (n_tasks + per_iter - 1) / per_iter;  // the same for every warp
-    const uint32_t tile = base + kH8Words * 4u + warp * (32u * kH8RS);
-    unsigned long long fsum = 0, expect = 0;
-#pragma unroll 1
-    for (uint64_t k = 0; k < iters; ++k) {
-        const uint64_t t = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * (warp + kH8Warps * k);
-        if (t < n_tasks) {
-            run_task_seg_consume8<MODE>(g, tile, lane, t, cons);
-            if (lane == 0) {
-                const uint64_t left = g.n_streams - t * rpw;
-                expect += (left < rpw ? left : rpw) * g.nps;
-            }
-        }
-        if ((k + 1) % kH8FlushIters == 0 || k + 1 == iters) {
-            __syncthreads();
-            fsum += h8_flush(hist, slab);
-            __syncthreads();
-        }
-    }
-    // power sums and the wrap check (field sums of every flush vs the outputs counted)
-    __shared__ double red[kH8Warps][4];
-    double sp[4] = {cons.sum(cons.s1), cons.sum(cons.s2), cons.sum(cons.s3), cons.sum(cons.s4)};
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-        for (int o = 16; o > 0; o >>= 1) sp[q] = __dadd_rn(sp[q], __shfl_xor_sync(~0u, sp[q], o));
-    for (int o = 16; o > 0; o >>= 1) {
-        fsum += __shfl_xor_sync(~0u, fsum, o);
-        expect += __shfl_xor_sync(~0u, expect, o);
-    }
-    __shared__ unsigned long long part[2][kH8Warps];
-    if (lane == 0) {
-        for (int q = 0; q < 4; ++q) red[warp][q] = sp[q];
-        part[0][warp] = fsum;
-        part[1][warp] = expect;
-    }
-    __syncthreads();
-    if (threadIdx.x < 4) {
-        double acc = 0.0;
-        for (int wi = 0; wi < kH8Warps; ++wi) acc = __dadd_rn(acc, red[wi][threadIdx.x]);
-        g.pow_slab[blockIdx.x * 4 + threadIdx.x] = acc;
-    }
-    if (threadIdx.x == 0) {
-        unsigned long long a = 0, bsum = 0;
-        for (int wi = 0; wi < kH8Warps; ++wi) {
-            a += part[0][wi];
-            bsum += part[1][wi];
-        }
-        if (a != bsum) atomicOr(g.overflow, 1u);
-    }
-}
-
 // One-warp CTAs (12 per SM, smem-bound), each running `tpc` consecutive warp tasks of 32
 // lane segments (a task = 32 / S rows = one contiguous 32 KiB block of the output), so the
 // hardware's in-order CTA dispatch keeps the blocks being written in one moving window (a
@@ -2427,27 +2195,11 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
             while ((kSegOut << g.seg_log2) < g.nps) ++g.seg_log2;
             const uint64_t seg_tasks = (g.n_streams + (32u >> g.seg_log2) - 1) / (32u >> g.seg_log2);
             if ((uint64_t)grid > seg_tasks) grid = (int)seg_tasks;  // (>= the 32-row task count)
-#if PRNGD_CONS_H8
-            if (red) {  // the 8-bit-field histogram with 256-byte chunks
-#define PRNGD_CONS_SEG8(M)                                                                      \
-    do {                                                                                        \
-        if ((e = set_smem(consume_seg8_kernel<M>, kH8Smem)) != cudaSuccess) return e;           \
-        consume_seg8_kernel<M><<<grid, kH8Warps * 32, kH8Smem, st>>>(g);                       \
-        e = cudaGetLastError();                                                                 \
-    } while (0)
-                if (f32 == 2) PRNGD_CONS_SEG8(2);
-                else if (f32 == 3) PRNGD_CONS_SEG8(3);
-                else PRNGD_CONS_SEG8(1);
-#undef PRNGD_CONS_SEG8
-            } else
-#endif
-            {
 #define PRNGD_CONS_SEG(M)                                                                       \
     (red ? cons_launch<M, true, false, false, Store::SEG, true, true>(m, g, grid, st)            \
          : cons_launch<M, true, false, false, Store::SEG, true>(m, g, grid, st))
             e = f32 == 2 ? PRNGD_CONS_SEG(2) : f32 == 3 ? PRNGD_CONS_SEG(3) : PRNGD_CONS_SEG(1);
 #undef PRNGD_CONS_SEG
-            }
         } else {
 #define PRNGD_CONS_W(S)                                                                         \
     (red ? cons_dispatch<S, true, true>(m, g, pl, f32, grid, st)                                 \
