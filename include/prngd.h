@@ -135,7 +135,8 @@ typedef struct {
                             /* a0 < x1 < a holds >= 2^-16 of the 2^bitlen(a) draw values     */
     uint64_t b0, b;         /* x2 range [b0; b]: b0 == 0, b + 1 a power of two, b < 2^w (R5) */
     uint64_t seed;          /* SplitMix64 seed (R6)                                           */
-    uint64_t stream_begin;  /* first GLOBAL stream id of this call (multi-GPU shard)          */
+    uint64_t stream_begin;  /* first GLOBAL stream id of this call (multi-GPU shard);         */
+                            /* stream_begin + n_streams - 1 <= 2^64 - 1                      */
     uint64_t n_streams;     /* >= 1                                                           */
     uint64_t n_per_stream;  /* >= 1; n_streams * n_per_stream < 2^62; n_per_stream < 2^32     */
 } prngd_params;

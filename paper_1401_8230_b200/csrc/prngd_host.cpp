@@ -120,8 +120,8 @@ prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
         return fail(PRNGD_EINVAL, "n_per_stream must be < 2^32");
     if (p->n_streams > (1ull << 62) / p->n_per_stream)
         return fail(PRNGD_EINVAL, "n_streams * n_per_stream overflows (limit 2^62)");
-    if (p->stream_begin > ~0ull - p->n_streams)
-        return fail(PRNGD_EINVAL, "stream_begin + n_streams overflows 64 bits");
+    if (p->n_streams - 1 > ~0ull - p->stream_begin)  // the last stream id must fit 64 bits
+        return fail(PRNGD_EINVAL, "stream_begin + n_streams - 1 overflows 64 bits");
     const uint32_t known = PRNGD_FLAG_IEEE_DIV | PRNGD_FLAG_ALG1 | PRNGD_STORE_MASK |
                            PRNGD_MAP_MASK | PRNGD_FLAG_OPEN | PRNGD_FLAG_JUMP | PRNGD_FLAG_NO_JUMP |
                            PRNGD_FLAG_MRG32K3A | PRNGD_FLAG_EXACT_HIST;

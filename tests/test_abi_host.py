@@ -254,3 +254,14 @@ def test_binding_checks_buffers_before_the_call(lib):
             P.prngd_generate_host(h, torch.empty(64, dtype=torch.float64)[::2])
     finally:
         P.prngd_destroy(h)
+
+
+def test_stream_id_range_reaches_the_top(lib):
+    """Streams [stream_begin, stream_begin + n) may end at id 2^64 - 1, not beyond."""
+    h = P.prngd_create(**W.FULL32, seed=1, stream_begin=2**64 - 1000, n_streams=1000,
+                       n_per_stream=2)
+    P.prngd_destroy(h)
+    with pytest.raises(P.PrngdError) as e:
+        P.prngd_create(**W.FULL32, seed=1, stream_begin=2**64 - 999, n_streams=1000,
+                       n_per_stream=2)
+    assert e.value.status == P.PRNGD_EINVAL and "overflows" in str(e.value)

@@ -241,3 +241,15 @@ def test_consume_row_segments_misaligned_falls_back(orc):
     assert_same(out, ref["out"])
     assert np.array_equal(hist.cpu().numpy(), ref["hist"]) and int(cnt.item()) == ref["count"]
     assert float(buf[0]) == -1.0 and float(buf[-1]) == -1.0
+
+
+@pytest.mark.parametrize("nps", [256, 512])
+def test_consume_row_segments_high_stream_ids(orc, nps):
+    """Row-segment consumer near the top of the 64-bit stream-id space (counter addressing)."""
+    p = dict(W.FULL32, seed=0x0123456789ABCDEF, stream_begin=2**64 - 1000, n_streams=1000,
+             n_per_stream=nps)
+    ref = orc.generate(p, want_stats=True)
+    out, hist, pw, cnt = _consume(p, P.PRNGD_FLAG_STORE_AUTO)
+    assert_same(out, ref["out"])
+    assert cnt == ref["count"] and np.array_equal(hist, ref["hist"])
+    assert np.allclose(pw, ref["pow"], rtol=1e-12, atol=0)
