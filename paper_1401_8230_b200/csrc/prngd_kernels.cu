@@ -60,9 +60,12 @@ template <Store ST>
 constexpr int row_cols() { return ST == Store::ROW1K ? 2 * kRowCols : kRowCols; }
 template <Store ST>
 constexpr int gen_warps() { return is_row<ST>() ? 1 : kGenWarps; }
+#ifndef PRNGD_ROW_PAD
+#define PRNGD_ROW_PAD 1024  // ROW tile alignment (its 16-B vector stores need 16)
+#endif
 template <Store ST>
 constexpr size_t gen_smem() {
-    return is_row<ST>() ? 1024 + (size_t)32 * (row_cols<ST>() * 8 + 16)
+    return is_row<ST>() ? PRNGD_ROW_PAD + (size_t)32 * (row_cols<ST>() * 8 + 16)
                         : 1024 + (size_t)kGenWarps * (ST == Store::TMA ? 2 : 1) * kTileBytes;
 }
 constexpr int kConsWarpsTiles = 12;         // warps per CTA, consume kernel staging tiles in smem
@@ -758,7 +761,7 @@ __global__ void __launch_bounds__(gen_warps<ST>() * 32)
         NoConsumer nc;
         XsProducer<MODE, SPEC, IEEE, ALG1> prod(g, g.stream_begin + row0 + lane);
         run_rows_burst<false, row_cols<ST>(), decltype(prod), NoConsumer,
-                       (PRNGD_ROW_BULK != 0 && ST == Store::ROW)>(g, aligned_smem_base(smem_raw),
+                       (PRNGD_ROW_BULK != 0 && ST == Store::ROW)>(g, (smem_u32(smem_raw) + (PRNGD_ROW_PAD - 1u)) & ~(PRNGD_ROW_PAD - 1u),
                                                                   lane, row0, prod, nc);
     } else if constexpr (ST == Store::TMA) {
         // CTA-level staging: the 4 warps fill one 128-row x 16-column slab (16 KiB, two slots)
