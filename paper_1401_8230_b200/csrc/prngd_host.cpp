@@ -1,6 +1,7 @@
 // prngd_host.cpp -- C ABI (include/prngd.h): validation, Eq.(3)/(4) constants, dispatch,
 // host-buffer pipeline.  Product code; written independently of oracle/.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cmath>
@@ -79,6 +80,17 @@ static prngd_status device_ready(int *num_sms) {
     return PRNGD_OK;
 }
 
+// NVTX ranges around the public calls (SURVEY section 5 "tracing"): free unless a profiler such as
+// nsys injects its tool library.
+namespace {
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+}  // namespace
+
 extern "C" {
 
 const char *prngd_status_string(prngd_status s) {
@@ -97,6 +109,7 @@ const char *prngd_last_error(void) { return g_err; }
 int prngd_abi_version(void) { return PRNGD_ABI_VERSION; }
 
 prngd_status prngd_create(const prngd_params *p, prngd_handle **out) {
+    NvtxRange nvtx_range("prngd_create");
     g_err[0] = 0;
     if (!p || !out) return fail(PRNGD_EINVAL, "null argument");
     *out = nullptr;
@@ -397,6 +410,7 @@ static cudaError_t launch_rows(const GenArgs &g, const Plan &pl, cudaStream_t st
 }
 
 prngd_status prngd_generate(const prngd_handle *h, double *d_out, void *cuda_stream) {
+    NvtxRange nvtx_range("prngd_generate");
     if (!h || !d_out) return fail(PRNGD_EINVAL, "null handle or output pointer");
     if ((uintptr_t)d_out & 7u) return fail(PRNGD_EINVAL, "d_out must be 8-byte aligned");
     int sms = 0;
@@ -494,6 +508,7 @@ prngd_status prngd_generate_consume_mc(const prngd_handle *hc, double *d_out, vo
 static prngd_status generate_consume_impl(const prngd_handle *hc, double *d_out, int64_t *d_hist,
                                           double *d_pow, int64_t *d_count, uint64_t *d_arrive,
                                           bool mc, void *cuda_stream) {
+    NvtxRange nvtx_range("prngd_generate_consume");
     if (!hc || !d_hist || !d_pow || !d_count)
         return fail(PRNGD_EINVAL, "null handle or accumulator pointer");
     if (((uintptr_t)d_hist | (uintptr_t)d_pow | (uintptr_t)d_count | (uintptr_t)d_arrive) & 7u)
@@ -587,6 +602,7 @@ static prngd_status generate_consume_impl(const prngd_handle *hc, double *d_out,
 }
 
 prngd_status prngd_generate_host(prngd_handle *h, double *h_out, void *cuda_stream) {
+    NvtxRange nvtx_range("prngd_generate_host");
     if (!h || !h_out) return fail(PRNGD_EINVAL, "null handle or host pointer");
     int sms = 0;
     prngd_status s = device_ready(&sms);
@@ -706,6 +722,7 @@ prngd_status prngd_debug_div_check(const prngd_handle *h, uint64_t n, uint64_t s
 
 prngd_status prngd_wait_arrivals(const uint64_t *d_arrive, uint64_t target, uint64_t timeout_ns,
                                  void *cuda_stream) {
+    NvtxRange nvtx_range("prngd_wait_arrivals");
     if (!d_arrive || ((uintptr_t)d_arrive & 7u)) return fail(PRNGD_EINVAL, "null or misaligned counter");
     cudaError_t e = prngd::launch_wait_arrivals(
         reinterpret_cast<const unsigned long long *>(d_arrive), target,

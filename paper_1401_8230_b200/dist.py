@@ -56,18 +56,29 @@ def allreduce_stats(hist, pw, count, group=None, deterministic: bool = False):
 
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return hist, pw, count
-    dist.all_reduce(hist, group=group)
-    dist.all_reduce(count, group=group)
-    if deterministic:
-        parts = [torch.empty_like(pw) for _ in range(dist.get_world_size(group))]
-        dist.all_gather(parts, pw, group=group)
-        acc = torch.zeros_like(pw)
-        for t in parts:
-            acc += t
-        pw.copy_(acc)
-    else:
-        dist.all_reduce(pw, group=group)
+    with _nvtx("prngd_allreduce_stats"):
+        dist.all_reduce(hist, group=group)
+        dist.all_reduce(count, group=group)
+        if deterministic:
+            parts = [torch.empty_like(pw) for _ in range(dist.get_world_size(group))]
+            dist.all_gather(parts, pw, group=group)
+            acc = torch.zeros_like(pw)
+            for t in parts:
+                acc += t
+            pw.copy_(acc)
+        else:
+            dist.all_reduce(pw, group=group)
     return hist, pw, count
+
+
+def _nvtx(name: str):
+    """An NVTX range on CUDA builds (for nsys), else nothing."""
+    import contextlib
+
+    import torch
+    if torch.cuda.is_available():
+        return torch.cuda.nvtx.range(name)
+    return contextlib.nullcontext()
 
 
 class PeerStats:
