@@ -569,8 +569,9 @@ def main():
                          "achieved": ins * nout / (kern_ms * 1e-3) / 1e9,
                          "peak": 4 * 32.0 * sms * clk_ghz, "unit": "Ginstr/s",
                          "frac": ins * nout / (kern_ms * 1e-3) / 1e9 / (4 * 32.0 * sms * clk_ghz),
-                         "note": "issue/latency-bound: 34.6 issued per output at 62% issue, "
-                                 "ALU pipe 51%, 12 warps per SM (profiles/r02c_summary.txt)"}
+                         "note": "issue/latency-bound: 34.0 issued per output at 67% issue, "
+                                 "ALU pipe 57%, 16 warps per SM (row-segment consumer, "
+                                 "profiles/r02s_summary.txt)"}
     if consume and args.no_write and not p.get("mrg"):
         # Nothing is written: one shared-memory histogram add per output.  Peak = the measured
         # rate of the same packed adds (no return value) at the kernel's 16 warps per SM
