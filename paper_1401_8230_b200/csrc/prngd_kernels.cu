@@ -1275,6 +1275,31 @@ __device__ __forceinline__ uint32_t jump_comp_off(uint32_t p) {
     return (p + jump_pad<P>() * (p >> 4)) << 3;
 }
 
+// Jump-kernel modes for Eq.(4) with w = 8 or 16 and both draws at full width (sh1 = sh2 =
+// 32 - w, e.g. cfg2's top bytes): v = x1 2^w + x2 is the top w bits of d1 followed by the top w
+// bits of d2, ONE byte permute (instead of two shifts, a wide multiply-add and a move), and
+// converts exactly from 16 / 32 bits -- the same v, the same Eq.(4) operations, the same bits.
+#ifndef PRNGD_JUMP_NARROW
+#define PRNGD_JUMP_NARROW 1
+#endif
+constexpr int kJumpMode8 = 8, kJumpMode16 = 9;
+template <bool W8>
+__device__ __forceinline__ double eq4_narrow(uint32_t d1, uint32_t d2, const GenArgs &g) {
+    double z;
+    if (W8) {
+        // bytes (d2.b3, d1.b3, d2.b0, d2.b0): the low 16 bits are v; convert them alone
+        const uint32_t v = __byte_perm(d2, d1, 0x0073);
+        asm("{\n\t.reg .u16 h;\n\tcvt.u16.u32 h, %1;\n\tcvt.rn.f64.u16 %0, h;\n\t}"
+            : "=d"(z) : "r"(v));
+    } else {
+        z = __uint2double_rn(__byte_perm(d2, d1, 0x7632));  // (d1 >> 16) << 16 | d2 >> 16
+    }
+    const double n = __dsub_rn(z, g.Cs);
+    const double q0 = __dmul_rn(n, g.y);  // Markstein, as eq4_scaled
+    const double r = __fma_rn(-q0, g.Ds, n);
+    return __fma_rn(r, g.y, q0);
+}
+
 __device__ __forceinline__ Xs128 jump_state(const uint4 *__restrict__ tab, const Xs128 &s) {
     const uint32_t words[4] = {s.x, s.y, s.z, s.w};
     uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
@@ -1320,9 +1345,13 @@ __global__ void __launch_bounds__(kJumpWarps * 32, P > 32 ? 4 : PRNGD_JUMP_MINB)
     if (row >= g.n_streams) return;
     constexpr bool FULL32 = MODE == 2;
     constexpr bool EQ4 = MODE >= 1;
+    constexpr bool NARROW = MODE == kJumpMode8 || MODE == kJumpMode16;
     const uint32_t sh1 = (MODE == 2 || MODE == 3) ? 0u : g.sh1, sh2 = FULL32 ? 0u : g.sh2;
     const uint32_t w = (MODE == 2 || MODE == 3) ? 32u : g.w;
     const uint32_t lo = FULL32 ? 1u : g.lo, span = FULL32 ? 0xFFFFFFFEu : g.span;
+    // NARROW: the band test on the raw draw, x1 = d >> sh1 in [lo, lo + span) <=> d in
+    // [lo 2^sh1, (lo + span) 2^sh1) (lo + span = a < 2^w, so no overflow)
+    const uint32_t lo_s = NARROW ? lo << sh1 : 0u, span_s = NARROW ? span << sh1 : 0u;
     const uint32_t comp = aligned_smem_base(smem_raw) + warp * jump_comp_bytes<P>();
 
     double *row_out = g.out + row * g.nps;
@@ -1352,10 +1381,18 @@ __global__ void __launch_bounds__(kJumpWarps * 32, P > 32 ? 4 : PRNGD_JUMP_MINB)
         MaskT mask = 0;
 #pragma unroll
         for (int i = 0; i < P; ++i) {
-            const uint32_t x1 = draw(st) >> sh1;
-            const uint32_t x2 = draw(st) >> sh2;
-            mask |= (MaskT)(accepted(x1, lo, span) ? 1u : 0u) << i;
-            q[i] = EQ4 ? eq4_mode<MODE, false>(x1, x2, g) : map_pair<false, true>(x1, x2, g.map);
+            if constexpr (NARROW) {
+                const uint32_t d1 = draw(st);
+                const uint32_t d2 = draw(st);
+                mask |= (MaskT)(d1 - lo_s < span_s ? 1u : 0u) << i;
+                q[i] = eq4_narrow<MODE == kJumpMode8>(d1, d2, g);
+            } else {
+                const uint32_t x1 = draw(st) >> sh1;
+                const uint32_t x2 = draw(st) >> sh2;
+                mask |= (MaskT)(accepted(x1, lo, span) ? 1u : 0u) << i;
+                q[i] = EQ4 ? eq4_mode<MODE, false>(x1, x2, g)
+                           : map_pair<false, true>(x1, x2, g.map);
+            }
         }
         if (EQ4 && g.span != g.span_fast) {  // R11 clamp only where the host found it needed
 #pragma unroll
@@ -2379,10 +2416,16 @@ static cudaError_t jump_launch(const GenArgs &g, cudaStream_t st) {
         if ((e = set_smem(gen_jump_kernel<M, P>, smem)) != cudaSuccess) return e;               \
         gen_jump_kernel<M, P><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);            \
     } while (0)
+    const bool narrow = PRNGD_JUMP_NARROW && mode == 1 && g.sh1 == 32u - g.w &&
+                        g.sh2 == 32u - g.w;
     switch (mode) {
         case 3: PRNGD_JUMP_LAUNCH(3); break;
         case 2: PRNGD_JUMP_LAUNCH(2); break;
-        case 1: PRNGD_JUMP_LAUNCH(1); break;
+        case 1:
+            if (narrow && g.w == 8) PRNGD_JUMP_LAUNCH(kJumpMode8);
+            else if (narrow && g.w == 16) PRNGD_JUMP_LAUNCH(kJumpMode16);
+            else PRNGD_JUMP_LAUNCH(1);
+            break;
         default: PRNGD_JUMP_LAUNCH(0); break;
     }
 #undef PRNGD_JUMP_LAUNCH

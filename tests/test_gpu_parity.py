@@ -452,6 +452,21 @@ def test_jump_general_ranges(orc):
         assert_same(out, orc.generate(p)["out"])
 
 
+@pytest.mark.parametrize("par", [dict(w=8, a0=0, a=255, b0=0, b=255),
+                                 dict(w=8, a0=17, a=200, b0=0, b=255),
+                                 dict(w=8, a0=0, a=128, b0=0, b=255),
+                                 dict(w=16, a0=0, a=65535, b0=0, b=65535),
+                                 dict(w=16, a0=999, a=40000, b0=0, b=65535)])
+@pytest.mark.parametrize("nps", [700, 1500])
+def test_jump_narrow_modes(orc, par, nps):
+    """w = 8 / 16 with both draws at full width (sh1 = sh2 = 32 - w) take the jump kernel's
+    byte-permute composition and raw-draw band test (kJumpMode8 / kJumpMode16), 17- and
+    33-pair rounds; narrow bands make rejection frequent."""
+    p = dict(par, seed=5, n_streams=45, n_per_stream=nps, stream_begin=3, flags=P.PRNGD_FLAG_JUMP)
+    _, out = gen(p)
+    assert_same(out, orc.generate(p)["out"])
+
+
 # ------------------------------------------------------------------ NEXT-2 MRG32k3a base generator
 
 @pytest.mark.parametrize("par", [dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1),
