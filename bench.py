@@ -552,8 +552,9 @@ def main():
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
             "peak_source": peak_src,
-            "kernel": KERNELS[g.info["kernel"]] + f" (store path {STORES[g.info['store']]})"
-                      if not consume else "consume_kernel+finalize",
+            "kernel": ("consume_kernel+finalize" if consume else
+                       KERNELS[g.info["kernel"]] if g.info["kernel"] == 2 else  # no store path
+                       KERNELS[g.info["kernel"]] + f" (store path {STORES[g.info['store']]})"),
             "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kern_ms,
             "frac_of_8TBs_nominal": achieved / 8000.0}
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count

@@ -16,7 +16,7 @@ __all__ = [
     "build", "lib", "mix64", "splitmix64_output", "xs128_sequence", "stream_state", "constants",
     "map_pairs", "map_pairs_noclamp", "accept", "generate", "raw", "enumerate_pairs",
     "map_eq5", "map_eq6", "map_kind", "mrg_sequence", "mrg_stream_state", "mrg_reduced",
-    "GAMMA",
+    "generate_chunk", "GAMMA",
 ]
 
 GAMMA = 0x9E3779B97F4A7C15
@@ -223,3 +223,13 @@ def map_eq5(p: dict, x1: int, x2: int) -> float:
 
 def map_eq6(w: int, x1: int, x2: int) -> float:
     return lib().oracle_map_eq6(w, x1, x2)
+
+
+def generate_chunk(args):
+    """generate() over one stream chunk, for a multiprocessing pool (picklable by reference):
+    args = (p, stream_begin, n_streams, stats) -> (stream_begin, out or None, hist, pow, count)."""
+    p, s0, ns, stats = args
+    r = generate(p, stream_begin=s0, n_streams=ns, want_out=not stats, want_stats=stats)
+    if stats:
+        return s0, None, r["hist"], r["pow"], r["count"]
+    return s0, r["out"], None, None, None

@@ -14,24 +14,18 @@ torch = pytest.importorskip("torch")
 
 from paper_1401_8230_b200 import prngd as P  # noqa: E402
 from paper_1401_8230_b200 import workloads as W  # noqa: E402
+import oracle  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
 CHUNK = 8192  # streams per oracle task
 
 
-def _oracle_chunk(args):
-    import oracle
-    p, s0, ns, stats = args
-    r = oracle.generate(p, stream_begin=s0, n_streams=ns, want_out=not stats, want_stats=stats)
-    if stats:
-        return s0, None, r["hist"], r["pow"], r["count"]
-    return s0, r["out"], None, None, None
-
-
 def _pool():
+    # forkserver: the workers fork from a clean server process (no CUDA context, no threads)
+    # and import only the oracle (oracle.generate_chunk is picklable by reference)
     n = max(1, min(32, len(os.sched_getaffinity(0))))
-    return mp.get_context("fork").Pool(n)
+    return mp.get_context("forkserver").Pool(n)
 
 
 def _chunks(p, stats):
@@ -48,7 +42,7 @@ def test_every_output_bitwise(orc, name):
     assert g.last_launches == 1
     bad = 0
     with _pool() as pool:
-        for s0, ref, *_ in pool.imap_unordered(_oracle_chunk, _chunks(p, False)):
+        for s0, ref, *_ in pool.imap_unordered(oracle.generate_chunk, _chunks(p, False)):
             r0 = s0 - p["stream_begin"]
             gpu = out[r0:r0 + ref.shape[0]].cpu().numpy()
             bad += int(np.count_nonzero(gpu.view(np.int64) != ref.view(np.int64)))
@@ -68,7 +62,7 @@ def test_cfg5_shard_statistics(orc):
     s = np.zeros(4)
     c = 0
     with _pool() as pool:
-        for _, _, hh, pp, cc in pool.imap_unordered(_oracle_chunk, _chunks(p, True)):
+        for _, _, hh, pp, cc in pool.imap_unordered(oracle.generate_chunk, _chunks(p, True)):
             h += hh
             s += pp
             c += cc
