@@ -240,10 +240,21 @@ struct NoConsumer {
 
 // Eq.(4) of one pair on the specialised paths: MODE 2/3 compose v = x1:x2 as a register pair
 // (w = 32), MODE 1 as one wide multiply-add x1 * 2^w + x2 (w <= 31).
+#ifndef PRNGD_COMPOSE_HILO
+#define PRNGD_COMPOSE_HILO 1
+#endif
 template <int MODE, bool IEEE>
 __device__ __forceinline__ double eq4_mode(uint32_t x1, uint32_t x2, const GenArgs &g) {
+#if PRNGD_COMPOSE_HILO
+    // MODE 1: the two words of x1 2^w + x2 directly (x2 < 2^w, so the low word cannot carry):
+    // a 32-bit multiply-add and a high multiply, no 64-bit addend to assemble
+    const uint64_t v = (MODE == 2 || MODE == 3)
+                           ? (((uint64_t)x1 << 32) | (uint64_t)x2)
+                           : (((uint64_t)__umulhi(x1, g.pow2w) << 32) | (uint64_t)(x1 * g.pow2w + x2));
+#else
     const uint64_t v = (MODE == 2 || MODE == 3) ? (((uint64_t)x1 << 32) | (uint64_t)x2)
                                                 : (uint64_t)x1 * g.pow2w + (uint64_t)x2;
+#endif
     return eq4_scaled<IEEE, false>(v, g.Cs, g.Ds, g.y);
 }
 
@@ -486,8 +497,8 @@ static_assert(kMrgRingBytes >= 8u * kCols + 4u * kMrgStep, "MRG ring smaller tha
 #endif
 template <int FP> struct MrgWord { using T = uint32_t; };
 template <> struct MrgWord<1> { using T = double; };
-// SPECB slow path: rewrite a lane's buffered draws [rd, wr) of its ring (kMrgRingBytes at
-// `ring`) without the out-of-band x1 (and, pair-drop, its x2), in order; a trailing pending x1
+// SPECB slow path: rewrite a lane's buffered draws [rd, wr) of its ring (counter c at shared
+// address (c & (kMrgRingBytes - 4)) ^ ring, `ring` = MrgProducer2::cx) without the out-of-band x1 (and, pair-drop, its x2), in order; a trailing pending x1
 // stays pending (pair-drop drops its pair once the x2 is drawn).  Returns the new write counter.
 template <bool ALG1>
 __device__ __noinline__ uint32_t mrg_drop_out_of_band(uint32_t ring, uint32_t rd, uint32_t wr,
@@ -496,7 +507,7 @@ __device__ __noinline__ uint32_t mrg_drop_out_of_band(uint32_t ring, uint32_t rd
     bool expect_x1 = true;
     while (src != wr) {
         uint32_t x;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(ring | (src & (kMrgRingBytes - 4u))));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"((src & (kMrgRingBytes - 4u)) ^ ring));
         bool keep = true;
         if (expect_x1 && !accepted(x, lo, span)) {
             if (ALG1) {
@@ -507,7 +518,7 @@ __device__ __noinline__ uint32_t mrg_drop_out_of_band(uint32_t ring, uint32_t rd
             }                             // else pending: kept, dropped once its pair completes
         }
         if (keep) {
-            asm volatile("st.shared.u32 [%0], %1;" ::"r"(ring | (dst & (kMrgRingBytes - 4u))), "r"(x)
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"((dst & (kMrgRingBytes - 4u)) ^ ring), "r"(x)
                          : "memory");
             dst += 4u;
             expect_x1 = !expect_x1;
@@ -521,19 +532,30 @@ __device__ __noinline__ uint32_t mrg_drop_out_of_band(uint32_t ring, uint32_t rd
 // 1 in 4096 x1 fall outside the band): every valid draw is appended, a batch checks its 16 x1
 // when it is read, and a warp with an out-of-band x1 compacts those lanes' rings (dropping the
 // pair, or the x1 alone for Alg. 1), refills and reads again.
-template <bool EQ4, bool SAMEW, bool ALG1 = false, bool SPECB = false>
+// SWZ: the ring entries are XOR-swizzled by 16 (lane mod 16) bytes instead of the counters being
+// staggered, so every batch is one ring half (counter 0 or 128 mod 256) and reads its 16 pairs
+// with eight 16-byte loads at base ^ 16 c (conflict-free: lane l's chunk c sits in bank group
+// c ^ (l mod 8)) instead of sixteen 8-byte loads with a wrapped address each; appends at equal
+// counters meet at most two lanes per bank, as the stagger did.  A/B on mrg26: 71.4 instead of
+// ~73.4 instructions per output, but 368.4 against 374.5 Gd/s (more fixed-latency "wait" stalls,
+// issue 75% -> 72%; profiles/r02z_mrg_swz_ab.txt), so it stays a build knob.
+#ifndef PRNGD_MRG_SWZ
+#define PRNGD_MRG_SWZ 0
+#endif
+template <bool EQ4, bool SAMEW, bool ALG1 = false, bool SPECB = false, bool SWZ = false>
 struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold and mask)
     using T1 = typename MrgWord<PRNGD_MRG_FP64 >= 1 ? 1 : 0>::T;  // component 1 word
     using T2 = typename MrgWord<PRNGD_MRG_FP64 >= 2 ? 1 : 0>::T;  // component 2 word
     const GenArgs &k;  // moduli and reciprocals (constant bank)
     T1 A, B, C;                 // component 1, oldest..newest (rotating roles)
     T2 D, E, F;                 // component 2
-    // ring byte counters (free-running, 4 per draw).  Both start at 8 * lane: lane l's entries
-    // are rotated by 2 l so lanes at equal counts use different banks (the ring is 256-byte
-    // aligned, so an entry's address is ring | (counter & (kMrgRingBytes - 4)))
+    // ring byte counters (free-running, 4 per draw).  Without SWZ both start at stride * lane:
+    // lane l's entries are rotated so lanes at equal counts use different banks; with SWZ both
+    // start at 0 and the addresses carry the bank spread.  The ring is kMrgRingBytes aligned, so
+    // an entry's address is (counter & (kMrgRingBytes - 4)) ^ cx
     uint32_t wr, rd;
     uint32_t bad1;              // 4: the pending x1 lies outside the band, else 0
-    uint32_t ring;              // this lane's ring (shared address), kMrgRingBytes aligned
+    uint32_t cx;                // this lane's ring (shared address) | its SWZ swizzle
     // stride: the counters of lane l start at stride * l (8: bank spread; 16: the in-ring output
     // staging of PRNGD_MRG_STAGE = 2 and of the fused consumer)
     __device__ __forceinline__ MrgProducer2(const GenArgs &g, uint64_t s, uint32_t ring_base,
@@ -542,9 +564,9 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
         : k(g) {
         const Mrg32k3a m = mrg_stream_start(g.seed, s);
         A = (T1)m.s0, B = (T1)m.s1, C = (T1)m.s2, D = (T2)m.t0, E = (T2)m.t1, F = (T2)m.t2;
-        rd = wr = stride * lane;
+        rd = wr = SWZ ? 0u : stride * lane;
         bad1 = 0u;
-        ring = ring_base;
+        cx = SWZ ? (ring_base | (16u * (lane & 15u))) : ring_base;
     }
     static __device__ __forceinline__ uint32_t c1(uint32_t a, uint32_t b) { return mrg_c1(a, b); }
     __device__ __forceinline__ double c1(double a, double b) const {
@@ -569,8 +591,12 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
         const uint32_t odd = wr & 4u;  // 4: this draw would be an x2
         const bool v = x < (SAMEW ? g.mrg_t1 : (odd ? g.mrg_t2 : g.mrg_t1));  // R23
         const uint32_t xm = x & (SAMEW ? g.mrg_mask1 : (odd ? g.mrg_mask2 : g.mrg_mask1));
+        // entry address (wr & (kMrgRingBytes - 4)) ^ cx as ONE three-input LOP3 (ptxas splits
+        // the C expression into an AND and an XOR)
+        uint32_t ea;
+        asm("lop3.b32 %0, %1, %2, %3, 0x6a;" : "=r"(ea) : "r"(wr), "r"(kMrgRingBytes - 4u), "r"(cx));
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
-                     "@p st.shared.u32 [%0], %1;\n\t}" ::"r"(ring | (wr & (kMrgRingBytes - 4u))),
+                     "@p st.shared.u32 [%0], %1;\n\t}" ::"r"(ea),
                      "r"(xm), "r"((uint32_t)v)
                      : "memory");
         // a valid x2 completes the pair: kept (+4) or dropped with its x1 (-4).  bad1
@@ -613,17 +639,28 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
 #pragma unroll 1
         while (true) {
             fill(g);
+            if constexpr (SWZ) {
+                static_assert(8u * kCols == kMrgRingBytes / 2, "SWZ: a batch is half a ring");
+                const uint32_t bh = cx ^ (rd & (kMrgRingBytes / 2));  // this batch's half
 #pragma unroll
-            for (int i = 0; i < kCols; ++i)
-                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
-                             : "=r"(a1[i]), "=r"(a2[i])
-                             : "r"(ring | ((rd + 8u * i) & (kMrgRingBytes - 8u))));
+                for (int c = 0; c < kCols / 2; ++c)
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(a1[2 * c]), "=r"(a2[2 * c]), "=r"(a1[2 * c + 1]),
+                                   "=r"(a2[2 * c + 1])
+                                 : "r"(bh ^ (16u * c)));
+            } else {
+#pragma unroll
+                for (int i = 0; i < kCols; ++i)
+                    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                                 : "=r"(a1[i]), "=r"(a2[i])
+                                 : "r"(((rd + 8u * i) & (kMrgRingBytes - 8u)) ^ cx));
+            }
             if (!SPECB) break;
             bool bad = false;
 #pragma unroll
             for (int i = 0; i < kCols; ++i) bad |= !accepted(a1[i], g.lo, g.span);
             if (__builtin_expect(!__any_sync(0xFFFFFFFFu, bad), 1)) break;
-            if (bad) wr = mrg_drop_out_of_band<ALG1>(ring, rd, wr, g.lo, g.span);
+            if (bad) wr = mrg_drop_out_of_band<ALG1>(cx, rd, wr, g.lo, g.span);
         }
 #pragma unroll
         for (int i = 0; i < kCols; ++i)
@@ -1083,8 +1120,9 @@ __global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ Gen
     // 256-byte alignment is all the rings need (no TMA here): a smaller footprint, more warps
     const uint32_t base = (smem_u32(smem_raw) + (kMrgRingBytes - 1)) & ~(kMrgRingBytes - 1);
     static_assert(kMrgTileBytes % kMrgRingBytes == 0, "rings must stay kMrgRingBytes aligned");
-    MrgProducer2<EQ4, SAMEW, ALG1, SPECB> prod(g, g.stream_begin + row0 + lane,
-                                  base + (uint32_t)kMrgStageBytes + lane * kMrgRingBytes, lane);
+    MrgProducer2<EQ4, SAMEW, ALG1, SPECB, PRNGD_MRG_SWZ && PRNGD_MRG_STAGE != 2> prod(
+        g, g.stream_begin + row0 + lane, base + (uint32_t)kMrgStageBytes + lane * kMrgRingBytes,
+        lane);
     if constexpr (PRNGD_MRG_STAGE == 2) {
         // Every lane consumes exactly 128 bytes of its ring per batch, and its read counter
         // started at 16 * lane, so the bytes batch b consumed sit at (16 l + 128 b) mod 256 of
