@@ -261,6 +261,14 @@ class McStats:
         """Device-side acquire wait on this rank's local arrival counter."""
         self.P.prngd_wait_arrivals(self.arrive, target, timeout_ns, stream)
 
+    def arrivals(self) -> int:
+        """Current value of this rank's local arrival counter (synchronous read)."""
+        import torch
+        buf = torch.empty(1, dtype=torch.int64, device="cuda")
+        self.P.prngd_copy(buf, self.arrive, 8, None)
+        torch.cuda.current_stream().synchronize()
+        return int(buf.item())
+
     def zero(self, stream=None, counter: bool = True):
         """Zero THIS rank's local copy (every rank zeroes its own, then a barrier)."""
         n = self.P.STATS_BYTES if counter else self.P.STATS_ARRIVE_OFFSET
@@ -284,12 +292,16 @@ class McStats:
         self.m = None
 
 
-def verify_reduction(ps, group=None, device_wait: bool = True) -> tuple[bool, str]:
+def verify_reduction(ps, group=None, device_wait: bool = True,
+                     timeout_s: float = 20.0) -> tuple[bool, str]:
     """Self-check of a shared statistics buffer (PeerStats or McStats) before it is trusted: every
     rank reduces a small known workload through it and the result is compared, bin for bin, with
     the NCCL all-reduce of the same workload's local statistics.  Returns (ok on every rank,
-    detail); leaves the buffer zeroed.  device_wait=False synchronises on the host instead of the
-    device-side acquire wait (ranks sharing one GPU)."""
+    detail); leaves the buffer zeroed.  device_wait=False synchronises every rank on the host
+    (ranks sharing one GPU); otherwise the reader polls the arrival counter until it reaches the
+    ranks' count, for at most timeout_s (a buffer whose arrivals never land fails the check)."""
+    import time
+
     import torch
     import torch.distributed as dist
     from . import prngd as P
@@ -315,12 +327,22 @@ def verify_reduction(ps, group=None, device_wait: bool = True) -> tuple[bool, st
         ok, detail = True, "ok"
         if reader:
             if device_wait:
-                ps.wait(ps.expected(1), st)
-            gh, gp, gc = ps.read()
-            if int(gc.item()) != int(c.item()) or not torch.equal(gh, h):
-                ok, detail = False, f"count {int(gc.item())} vs {int(c.item())} or histogram differs"
-            elif not torch.allclose(gp, pw, rtol=1e-12, atol=0):
-                ok, detail = False, "power sums differ"
+                # poll the arrival counter from the host with a deadline instead of the device
+                # wait (whose timeout traps and would leave this process unable to fall back)
+                deadline = time.monotonic() + timeout_s
+                while ps.arrivals() < ps.expected(1):
+                    if time.monotonic() > deadline:
+                        ok, detail = False, (f"arrival counter below {ps.expected(1)} after "
+                                             f"{timeout_s:g} s")
+                        break
+                    time.sleep(0.001)
+            if ok:
+                gh, gp, gc = ps.read()
+                if int(gc.item()) != int(c.item()) or not torch.equal(gh, h):
+                    ok, detail = False, (f"count {int(gc.item())} vs {int(c.item())} or "
+                                         "histogram differs")
+                elif not torch.allclose(gp, pw, rtol=1e-12, atol=0):
+                    ok, detail = False, "power sums differ"
         torch.cuda.synchronize()
         ok = _agree(ok, group)
         ps.zero(st)

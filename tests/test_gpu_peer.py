@@ -23,7 +23,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, p, calls, queue):
+def _worker(rank, world, port, p, calls, queue, poll=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -35,9 +35,10 @@ def _worker(rank, world, port, p, calls, queue):
         q = D.shard_params(p, rank, world, D.STRONG)
         g = P.Generator(**q)
         ps = D.PeerStats()
-        # the bench's self-check of a shared buffer against the all-reduce (host-side
-        # completion: the ranks share one GPU)
-        vok, why = D.verify_reduction(ps, device_wait=False)
+        # the bench's self-check of a shared buffer against the all-reduce: host-side completion
+        # (the ranks share one GPU), or the reader polling the arrival counter (poll=True, the
+        # separate-GPU path; host polling never blocks the other ranks' kernels)
+        vok, why = D.verify_reduction(ps, device_wait=poll)
         assert vok, why
         ps.zero()
         torch.cuda.synchronize()
@@ -63,15 +64,16 @@ def _worker(rank, world, port, p, calls, queue):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,calls,name", [(2, 1, "cfg1"), (3, 2, "cfg2")])
-def test_peer_memory_statistics_reduction(orc, world, calls, name):
+@pytest.mark.parametrize("world,calls,name,poll", [(2, 1, "cfg1", False), (3, 2, "cfg2", False),
+                                                   (2, 1, "cfg1", True)])
+def test_peer_memory_statistics_reduction(orc, world, calls, name, poll):
     import torch.multiprocessing as mp
     from paper_1401_8230_b200 import workloads as W
     p = W.config(name, n_streams=3000, n_per_stream=520)
     ctx = mp.get_context("spawn")
     queue = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, p, calls, queue))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, p, calls, queue, poll))
              for r in range(world)]
     for pr in procs:
         pr.start()
@@ -120,3 +122,36 @@ def test_multicast_statistics_single_process_or_clean_refusal(orc):
         assert np.allclose(pw.cpu().numpy(), 2 * ref["pow"], rtol=1e-12, atol=0)
     finally:
         ms.close()
+
+
+def test_verify_reduction_fails_cleanly_when_arrivals_never_land():
+    """A shared buffer whose arrivals never reach the reader must fail the self-check after the
+    deadline -- no device-side wait, no trap -- so the caller can still fall back to NCCL."""
+    import time
+    from paper_1401_8230_b200 import dist as D
+    torch.cuda.set_device(0)
+
+    class Lost:  # adds go nowhere; the counter stays 0
+        owner = 0
+
+        def zero(self, stream=None, counter=True):
+            pass
+
+        def consume(self, handle, out, stream=None):
+            pass
+
+        def expected(self, calls):
+            return calls
+
+        def arrivals(self):
+            return 0
+
+        def read(self):
+            raise AssertionError("read before the arrivals landed")
+
+    t0 = time.monotonic()
+    ok, why = D.verify_reduction(Lost(), device_wait=True, timeout_s=0.3)
+    assert not ok and "arrival counter" in why
+    assert time.monotonic() - t0 < 30
+    torch.cuda.synchronize()  # the context is still usable
+
