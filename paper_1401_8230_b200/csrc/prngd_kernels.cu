@@ -1482,6 +1482,159 @@ __global__ void __launch_bounds__(kJumpWarps * 32, P > 32 ? 4 : PRNGD_JUMP_MINB)
     }
 }
 
+// NEXT-3 for the narrow modes (w = 8 / 16, both draws at full width: cfg2): the same rounds as
+// gen_jump_kernel, but a lane keeps the 16 / 32-bit pair value v = x1 2^w + x2 of each draw
+// pair instead of its double (P registers instead of 2P), the compaction run holds these u32
+// values (4 B per output instead of 8), and Eq.(4) is evaluated in the copy-out, two outputs
+// per lane and store.  That halves the registers and the shared memory per warp, so cfg2's 4096
+// streams run as ONE wave (32 warps per SM) instead of 1.7 waves at 16 warps per SM.  Same
+// pairs, same v, same operations: the same bits as gen_jump_kernel.
+template <int P>
+constexpr uint32_t jumpn_comp_bytes() { return (32u * P + 2u) * 4u; }
+#ifndef PRNGD_JUMPN_MINB
+#define PRNGD_JUMPN_MINB 8
+#endif
+template <bool W8>
+__device__ __forceinline__ uint32_t narrow_v(uint32_t d1, uint32_t d2) {
+    // W8: bytes (d2.b3, d1.b3) = v in the low 16 bits (the high half is not used); W16:
+    // (d1 >> 16) << 16 | d2 >> 16
+    return W8 ? __byte_perm(d2, d1, 0x0073) : __byte_perm(d2, d1, 0x7632);
+}
+template <bool W8, bool CLAMP>
+__device__ __forceinline__ double eq4_narrow_v(uint32_t v, const GenArgs &g) {
+    // exact conversion of v (W8: the low 16 bits of the word; its high half is not v), then
+    // Eq.(4) as eq4_narrow
+    double z;
+    if (W8)
+        asm("{\n\t.reg .u16 h;\n\tcvt.u16.u32 h, %1;\n\tcvt.rn.f64.u16 %0, h;\n\t}"
+            : "=d"(z) : "r"(v));
+    else
+        z = __uint2double_rn(v);
+    const double n = __dsub_rn(z, g.Cs);
+    const double q0 = __dmul_rn(n, g.y);
+    const double r = __fma_rn(-q0, g.Ds, n);
+    const double q = __fma_rn(r, g.y, q0);
+    return CLAMP ? fmin(q, kBelowOne) : q;  // R11 where the host found it needed
+}
+__device__ __forceinline__ void stg_v2(double *p, double a, double b) {
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+#ifndef PRNGD_JUMP_NARROW_V
+#define PRNGD_JUMP_NARROW_V 1  // 0: the narrow modes run gen_jump_kernel<kJumpMode8/16> (A/B)
+#endif
+template <bool W8, bool CLAMP, int P>
+__global__ void __launch_bounds__(kJumpWarps * 32, PRNGD_JUMPN_MINB)
+    gen_jump_narrow_kernel(const GenArgs g, const uint4 *__restrict__ tabs) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t row = (uint64_t)blockIdx.x * kJumpWarps + warp;
+    if (row >= g.n_streams) return;
+    // band test on the raw draw: x1 = d >> sh1 in [lo, lo + span) <=> d in [lo 2^sh1,
+    // (lo + span) 2^sh1)
+    const uint32_t lo_s = g.lo << g.sh1, span_s = g.span << g.sh1;
+    const uint32_t comp = ((smem_u32(smem_raw) + 15u) & ~15u) + warp * jumpn_comp_bytes<P>();
+
+    double *row_out = g.out + row * g.nps;
+    Xs128 S = stream_start(g.seed, g.stream_begin + row);
+    uint64_t base = 0;
+#pragma unroll 1
+    while (base < g.nps) {
+        Xs128 st = S;
+        if (lane) {  // lane l starts at draw 2 P l of the round (lane-interleaved byte tables)
+            const uint32_t words[4] = {S.x, S.y, S.z, S.w};
+            uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const uint32_t v = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+                const uint4 t = __ldg(&tabs[((uint32_t)k * 256u + v) * 32u + lane]);
+                r0 ^= t.x;
+                r1 ^= t.y;
+                r2 ^= t.z;
+                r3 ^= t.w;
+            }
+            st = Xs128{r0, r1, r2, r3};
+        }
+        uint32_t v[P];
+        using MaskT = typename std::conditional<(P > 32), uint64_t, uint32_t>::type;
+        MaskT mask = 0;
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const uint32_t d1 = draw(st);
+            const uint32_t d2 = draw(st);
+            mask |= (MaskT)(d1 - lo_s < span_s ? 1u : 0u) << i;
+            v[i] = narrow_v<W8>(d1, d2);
+        }
+        const uint32_t cnt = P > 32 ? (uint32_t)__popcll(mask) : (uint32_t)__popc((uint32_t)mask);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += t;
+        }
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        // output p of the round goes to global element row_out[base + p] and to slot p + j0 of
+        // the run, j0 = 1 when that element is odd: output pairs (p, p + 1) with p = j0 (mod 2)
+        // are then 8-byte aligned in the run and 16-byte aligned in the output
+        const uint32_t j0 = (uint32_t)(((uintptr_t)(row_out + base) >> 3) & 1u);
+        uint32_t slot = incl - cnt + j0;
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const uint32_t bit = (uint32_t)(mask >> i) & 1u;
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+                         "@p st.shared.u32 [%0], %1;\n\t}" ::"r"(comp + 4u * slot), "r"(v[i]), "r"(bit)
+                         : "memory");
+            slot += bit;
+        }
+        __syncwarp();
+        const uint32_t n = (g.nps - base) < (uint64_t)total ? (uint32_t)(g.nps - base) : total;
+        double *out = row_out + base;
+        if (n > 0) {
+            const uint32_t npair = (n - j0) >> 1;  // full 16-byte pairs after the odd head
+            double *dst = out + j0 + 2u * lane;
+            uint32_t sa = comp + 8u * (lane + j0);
+#pragma unroll 4
+            for (uint32_t k = lane; k < npair; k += 32u, dst += 64, sa += 256u) {
+                uint32_t a, b;
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(sa) : "memory");
+                stg_v2(dst, eq4_narrow_v<W8, CLAMP>(a, g), eq4_narrow_v<W8, CLAMP>(b, g));
+            }
+            if (lane == 0 && j0) {  // odd head (slot 1)
+                uint32_t a;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a) : "r"(comp + 4u) : "memory");
+                out[0] = eq4_narrow_v<W8, CLAMP>(a, g);
+            }
+            if (lane == 31 && ((n - j0) & 1u)) {  // odd tail: output n - 1, slot n - 1 + j0
+                uint32_t a;
+                asm volatile("ld.shared.u32 %0, [%1];"
+                             : "=r"(a) : "r"(comp + 4u * (n - 1u + j0)) : "memory");
+                out[n - 1u] = eq4_narrow_v<W8, CLAMP>(a, g);
+            }
+        }
+        __syncwarp();
+        S.x = __shfl_sync(0xFFFFFFFFu, st.x, 31);
+        S.y = __shfl_sync(0xFFFFFFFFu, st.y, 31);
+        S.z = __shfl_sync(0xFFFFFFFFu, st.z, 31);
+        S.w = __shfl_sync(0xFFFFFFFFu, st.w, 31);
+        base += total;
+        const uint64_t rem = g.nps > base ? g.nps - base : 0;
+        if (rem > 0 && rem <= kJumpTail) {  // short remainder: one lane, sequentially
+            if (lane == 0) {
+                Xs128 t = S;
+                for (uint64_t i = 0; i < rem; ++i) {
+                    uint32_t d1, d2;
+                    do {
+                        d1 = draw(t);
+                        d2 = draw(t);
+                    } while (!(d1 - lo_s < span_s));
+                    row_out[base + i] = eq4_narrow_v<W8, CLAMP>(narrow_v<W8>(d1, d2), g);
+                }
+            }
+            break;
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------ SEG store path
 // Row segments: a lane owns one 1 KiB segment (kSegOut = 128 outputs) of a row, so the S =
 // nps / 128 lanes of a row write it side by side and each flush puts S 512-byte chunks, 1 KiB
@@ -2460,6 +2613,19 @@ static cudaError_t jump_launch(const GenArgs &g, cudaStream_t st) {
         case 3: PRNGD_JUMP_LAUNCH(3); break;
         case 2: PRNGD_JUMP_LAUNCH(2); break;
         case 1:
+#if PRNGD_JUMP_NARROW_V
+            if (narrow && (g.w == 8 || g.w == 16)) {
+                const size_t sn = 16 + (size_t)kJumpWarps * jumpn_comp_bytes<P>();
+                const bool clamp = g.span != g.span_fast;  // R11 (never at w <= 26)
+                auto kn = g.w == 8 ? (clamp ? gen_jump_narrow_kernel<true, true, P>
+                                            : gen_jump_narrow_kernel<true, false, P>)
+                                   : (clamp ? gen_jump_narrow_kernel<false, true, P>
+                                            : gen_jump_narrow_kernel<false, false, P>);
+                if ((e = set_smem(kn, sn)) != cudaSuccess) return e;
+                kn<<<(unsigned)grid, kJumpWarps * 32, sn, st>>>(g, t);
+                break;
+            }
+#endif
             if (narrow && g.w == 8) PRNGD_JUMP_LAUNCH(kJumpMode8);
             else if (narrow && g.w == 16) PRNGD_JUMP_LAUNCH(kJumpMode16);
             else PRNGD_JUMP_LAUNCH(1);

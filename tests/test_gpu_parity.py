@@ -457,11 +457,12 @@ def test_jump_general_ranges(orc):
                                  dict(w=8, a0=0, a=128, b0=0, b=255),
                                  dict(w=16, a0=0, a=65535, b0=0, b=65535),
                                  dict(w=16, a0=999, a=40000, b0=0, b=65535)])
-@pytest.mark.parametrize("nps", [700, 1500])
+@pytest.mark.parametrize("nps", [700, 1500, 701, 1025])
 def test_jump_narrow_modes(orc, par, nps):
-    """w = 8 / 16 with both draws at full width (sh1 = sh2 = 32 - w) take the jump kernel's
-    byte-permute composition and raw-draw band test (kJumpMode8 / kJumpMode16), 17- and
-    33-pair rounds; narrow bands make rejection frequent."""
+    """w = 8 / 16 with both draws at full width (sh1 = sh2 = 32 - w) take the narrow jump
+    kernel (pair values compacted, Eq.(4) in the copy-out), 17- and 33-pair rounds; narrow
+    bands make rejection frequent; odd rows start rounds at odd elements (the one-output head
+    and tail of the paired copy-out)."""
     p = dict(par, seed=5, n_streams=45, n_per_stream=nps, stream_begin=3, flags=P.PRNGD_FLAG_JUMP)
     _, out = gen(p)
     assert_same(out, orc.generate(p)["out"])
