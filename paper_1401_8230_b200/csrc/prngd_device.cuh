@@ -98,8 +98,23 @@ __device__ __forceinline__ uint32_t mrg_next(Mrg32k3a &m) {
 // draw is combined (mrg_combined_b, integer).  m and 1/m come from the kernel parameters, so
 // the FMAs read them from the constant bank.
 constexpr double kRoundShift = 6755399441055744.0;  // 2^52 + 2^51
+// PRNGD_MRG_FLOOR (default): k = floor(p * (1/m)) instead of the nearest integer, by the same
+// shift added in round-down mode.  Then r = p - k m lies in [0, m]: with |p| <= 1403580 m1 <
+// 6.1e15 the product p * RN(1/m) differs from p / m by less than 1.6e-10 < 1/m, so the floor is
+// floor(p / m) except when m divides p exactly, where it may come out one lower and give r = m
+// (= 0 mod m).  Values in [0, m] keep every product below 2^53 (the two terms of a recurrence
+// have opposite signs: |p| <= max(a, a') m < 6.1e15), so no correction is ever needed between
+// draws, and the combination takes r itself as the canonical value (component 2 maps m2 to 0
+// with one min; component 1's m1 is handled by mrg_combine_m1 as 0).
+#ifndef PRNGD_MRG_FLOOR
+#define PRNGD_MRG_FLOOR 1
+#endif
 __device__ __forceinline__ double mrg_modb(double p, double m, double inv_m) {
+#if PRNGD_MRG_FLOOR
+    const double k = __dsub_rn(__fma_rd(p, inv_m, kRoundShift), kRoundShift);
+#else
     const double k = __dsub_rn(__fma_rn(p, inv_m, kRoundShift), kRoundShift);
+#endif
     return __fma_rn(-k, m, p);
 }
 __device__ __forceinline__ double mrg_c1d(double xm2, double xm3, double m1, double inv_m1) {
@@ -113,12 +128,27 @@ __device__ __forceinline__ uint32_t mrg_combine_m1(uint32_t p1, uint32_t p2) {
     const uint32_t z = p1 - p2 - 1u;
     return p1 > p2 ? z : z - 209u;
 }
-// u - 1 from balanced p1 = x_n (mod m1), p2 = y_n (mod m2)
+// u - 1 from p1 = x_n (mod m1), p2 = y_n (mod m2): balanced representatives, or with
+// PRNGD_MRG_FLOOR values in [0, m] (see mrg_modb)
+__device__ __forceinline__ uint32_t mrg_canon1(double p1) {
+#if PRNGD_MRG_FLOOR
+    return __double2uint_rz(p1);  // exact; m1 (= 0 mod m1) is handled by mrg_combine_m1
+#else
+    const int32_t i1 = __double2int_rz(p1);
+    return i1 < 0 ? (uint32_t)i1 + kM1 : (uint32_t)i1;
+#endif
+}
+__device__ __forceinline__ uint32_t mrg_canon2(double p2) {
+#if PRNGD_MRG_FLOOR
+    const uint32_t c2 = __double2uint_rz(p2);
+    return min(c2, c2 - kM2);  // m2 -> 0; below m2, c2 - m2 wraps above c2
+#else
+    const int32_t i2 = __double2int_rz(p2);
+    return i2 < 0 ? (uint32_t)i2 + kM2 : (uint32_t)i2;
+#endif
+}
 __device__ __forceinline__ uint32_t mrg_combined_b_m1(double p1, double p2) {
-    const int32_t i1 = __double2int_rz(p1), i2 = __double2int_rz(p2);  // exact: integers
-    const uint32_t c1 = i1 < 0 ? (uint32_t)i1 + kM1 : (uint32_t)i1;
-    const uint32_t c2 = i2 < 0 ? (uint32_t)i2 + kM2 : (uint32_t)i2;
-    return mrg_combine_m1(c1, c2);
+    return mrg_combine_m1(mrg_canon1(p1), mrg_canon2(p2));
 }
 
 // R23: uniform width-bit value: discard u with u - 1 >= T = floor(m1 / 2^width) * 2^width.

@@ -584,8 +584,7 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
         return mrg_combined_b_m1(p1, p2);
     }
     static __device__ __forceinline__ uint32_t combine(double p1, uint32_t p2) {
-        const int32_t i1 = __double2int_rz(p1);
-        return mrg_combine_m1(i1 < 0 ? (uint32_t)i1 + kM1 : (uint32_t)i1, p2);
+        return mrg_combine_m1(mrg_canon1(p1), p2);
     }
     __device__ __forceinline__ void take(uint32_t x, const GenArgs &g) {  // x = u - 1
         const uint32_t odd = wr & 4u;  // 4: this draw would be an x2

@@ -1,0 +1,42 @@
+"""CPU check of the argument behind PRNGD_MRG_FLOOR (csrc/prngd_device.cuh, mrg_modb).
+
+The GPU MRG32k3a components reduce p = a x - a' x' (an exact integer in binary64) as
+r = p - k m with k = floor(p * RN(1/m)) (the round-down FMA with the 2^52 + 2^51 shift).  The
+kernels rely on r lying in [0, m], with r = m only when m divides p, for every p a recurrence
+can produce from values in [0, m].  This test evaluates that floor exactly (rational
+arithmetic on the binary64 value of RN(1/m)) at the extremes of the product range, around
+every multiple of m near them, and on random products; the GPU parity tests then check the
+generator's outputs bit for bit against the oracle's integer recurrence.
+"""
+import math
+import random
+from fractions import Fraction
+
+import pytest
+
+M1, M2 = 4294967087, 4294944443
+# (modulus, coefficient of the newer term, coefficient of the subtracted term): L'Ecuyer 1999
+RECS = [(M1, 1403580, 810728), (M2, 527612, 1370589)]
+
+
+@pytest.mark.parametrize("m,a,a2", RECS)
+def test_floor_reduction_stays_in_0_m(m, a, a2):
+    inv = Fraction(1.0 / m)  # the binary64 RN(1/m) the kernel receives
+    lo, hi = -a2 * m, a * m  # p = a x - a2 x' with x, x' in [0, m]
+    assert max(abs(lo), abs(hi)) < 2 ** 53  # every product and difference is exact
+    rng = random.Random(8230)
+    ps = set()
+    for n in list(range(lo // m, lo // m + 40)) + list(range(-40, 40)) + list(range(hi // m - 40, hi // m + 1)):
+        for f in (0, 1, 2, m // 2, m - 2, m - 1):
+            ps.add(n * m + f)
+    ps.update(rng.randint(lo, hi) for _ in range(20000))
+    ps.update(a * rng.randint(0, m) - a2 * rng.randint(0, m) for _ in range(20000))
+    for p in ps:
+        if not lo <= p <= hi:
+            continue
+        k = math.floor(p * inv)
+        r = p - k * m
+        assert 0 <= r <= m, p
+        assert r % m == p % m
+        if r == m:
+            assert p % m == 0
