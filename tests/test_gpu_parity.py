@@ -552,6 +552,25 @@ def test_mrg32k3a_alg1_bitwise(orc):
         _mrg_stats_match(g, p)
 
 
+@pytest.mark.parametrize("alg1", [False, True])
+@pytest.mark.parametrize("seed,stream,draw,comp", [(1, 7790325, 1190, 1), (1, 16147924, 918, 2),
+                                                   (1, 19033657, 1147, 2), (1, 33099832, 1992, 1)])
+def test_mrg32k3a_floor_edge(seed, stream, draw, comp, alg1):
+    """PRNGD_MRG_FLOOR's one edge: a component value that is exactly 0 with the sign of p for
+    which the GPU's floor is one low, so the kernel carries r = m (= 0 mod m) into the next
+    draws and the combination (tests/test_mrg_floor_reduction.py pins that these streams hit
+    it, from the oracle).  Outputs and fused statistics bit for bit against the oracle, with the
+    event inside the rows (draw <= 1992 ~ output 980 of 1100)."""
+    flags = P.PRNGD_FLAG_MRG32K3A | (P.PRNGD_FLAG_ALG1 if alg1 else 0)
+    p = dict(w=26, a0=0, a=2**26 - 1, b0=0, b=2**26 - 1, seed=seed, stream_begin=stream - 3,
+             n_streams=7, n_per_stream=1100, flags=flags, mrg=True, alg1=alg1)
+    _, out = gen(p)
+    ref = orc_mod().generate(p)["out"]
+    assert_same(out, ref)
+    g = P.Generator(**p)
+    _mrg_stats_match(g, p, out=torch.empty_like(out))
+
+
 @pytest.mark.parametrize("kind", [4, 5])
 def test_mrg32k3a_generate_consume(kind):
     """S7 fused into the MRG32k3a generator (consume_mrg_kernel): outputs written through the

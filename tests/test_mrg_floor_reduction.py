@@ -40,3 +40,30 @@ def test_floor_reduction_stays_in_0_m(m, a, a2):
         assert r % m == p % m
         if r == m:
             assert p % m == 0
+
+
+# (seed, stream, draw index, component) where a component's new value is exactly 0 and p has
+# the sign for which the GPU's floor comes out one low (r = m): found by tools/find_mrg_zero.c,
+# an input search; the GPU test test_mrg32k3a_floor_edge runs these streams against the oracle.
+FLOOR_EDGE_EVENTS = [(1, 7790325, 1190, 1), (1, 16147924, 918, 2), (1, 19033657, 1147, 2),
+                     (1, 33099832, 1992, 1)]
+
+
+@pytest.mark.parametrize("seed,stream,draw,comp", FLOOR_EDGE_EVENTS)
+def test_floor_edge_events_exist(seed, stream, draw, comp):
+    """The oracle's own MRG32k3a (R21/R22) confirms each event: the draw's component value is
+    0, from p < 0 (component 1) or p > 0 (component 2)."""
+    import ctypes
+
+    import numpy as np
+
+    from oracle import oracle as orc
+    st = np.array(orc.mrg_stream_state(seed, stream), dtype=np.int64)
+    L = orc.lib()
+    for _ in range(draw):
+        L.oracle_mrg_next(st.ctypes.data_as(ctypes.c_void_p))
+    p = 1403580 * int(st[1]) - 810728 * int(st[0]) if comp == 1 else \
+        527612 * int(st[5]) - 1370589 * int(st[3])
+    L.oracle_mrg_next(st.ctypes.data_as(ctypes.c_void_p))
+    assert (int(st[2]) if comp == 1 else int(st[5])) == 0
+    assert p % (M1 if comp == 1 else M2) == 0 and ((p < 0) if comp == 1 else (p > 0))
