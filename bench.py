@@ -32,7 +32,7 @@ from paper_1401_8230_b200 import workloads as W  # noqa: E402
 METRIC = "Gdoubles/s generated (1/2/4/8 B200) and % of HBM-write roofline"
 FALLBACK_HBM = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
 KERNELS = {0: "gen_kernel", 1: "gen_seg_kernel", 2: "gen_jump_kernel", 3: "gen_mrg_kernel",
-           4: "gen_segc_kernel"}
+           4: "gen_segc_kernel", 5: "gen_jump_narrow_kernel"}
 STORES = {0: "TMA", 1: "TILE", 2: "STG8", 3: "DIRECT", 4: "ROW", 5: "ROW1K", 6: "SEG", 7: "SEGC"}
 
 
@@ -553,7 +553,7 @@ def main():
             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
             "peak_source": peak_src,
             "kernel": ("consume_kernel+finalize" if consume else
-                       KERNELS[g.info["kernel"]] if g.info["kernel"] == 2 else  # no store path
+                       KERNELS[g.info["kernel"]] if g.info["kernel"] in (2, 5) else  # no store path
                        KERNELS[g.info["kernel"]] + f" (store path {STORES[g.info['store']]})"),
             "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kern_ms,
             "frac_of_8TBs_nominal": achieved / 8000.0}

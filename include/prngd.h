@@ -155,7 +155,8 @@ typedef struct {
     uint32_t kernel;        /* kernel prngd_generate launches for a 256-byte aligned output:
                                0 gen_kernel (one lane per stream), 1 gen_seg_kernel (SEG),
                                2 gen_jump_kernel (NEXT-3), 3 gen_mrg_kernel (NEXT-2),
-                               4 gen_segc_kernel (SEGC)                                        */
+                               4 gen_segc_kernel (SEGC), 5 gen_jump_narrow_kernel (NEXT-3,
+                               w = 8 / 16 with both draws at full width)                       */
     uint32_t store;         /* its store path: 0 TMA, 1 TILE, 2 8-byte, 3 DIRECT, 4 ROW,
                                5 ROW1K, 6 SEG, 7 SEGC                                         */
 } prngd_info;

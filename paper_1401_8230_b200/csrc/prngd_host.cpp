@@ -321,8 +321,10 @@ prngd_status prngd_get_info(const prngd_handle *h, prngd_info *info) {
     *info = h->info;
     const Plan pl = plan_for(h, reinterpret_cast<const void *>(uintptr_t{256}));
     info->store = (uint32_t)pl.store;
-    info->kernel = pl.mrg ? 3u : pl.jump ? 2u : pl.store == Store::SEG ? 1u
-                                                : pl.store == Store::SEGC ? 4u : 0u;
+    info->kernel = pl.mrg ? 3u
+                   : pl.jump ? (prngd::jump_uses_narrow_kernel(h->args) ? 5u : 2u)
+                   : pl.store == Store::SEG ? 1u
+                   : pl.store == Store::SEGC ? 4u : 0u;
     return PRNGD_OK;
 }
 

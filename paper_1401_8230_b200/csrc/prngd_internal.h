@@ -125,6 +125,7 @@ cudaError_t launch_generate_consume_mrg(const GenArgs &g, bool alg1, double *d_o
                                         int *launches);
 // the jump / SEG launchers fetch (build once per device) the jump tables they read
 cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, cudaStream_t st);
+bool jump_uses_narrow_kernel(const GenArgs &g);  // the jump plan runs gen_jump_narrow_kernel
 cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, cudaStream_t st);
 cudaError_t launch_generate_segc(const GenArgs &g, const Plan &pl, cudaStream_t st);
 cudaError_t launch_debug_raw(const GenArgs &g, uint32_t *d_raw, uint64_t draws, cudaStream_t st);

@@ -2591,6 +2591,14 @@ cudaError_t launch_generate_mrg(const GenArgs &g, bool alg1, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// Eq.(4) with w = 8 or 16 and both draws at full width: the byte-permute composition of the
+// jump kernel (and, with PRNGD_JUMP_NARROW_V, gen_jump_narrow_kernel)
+bool jump_is_narrow(const GenArgs &g) {
+    return PRNGD_JUMP_NARROW && kernel_mode(g) == 1 && (g.w == 8 || g.w == 16) &&
+           g.sh1 == 32u - g.w && g.sh2 == 32u - g.w;
+}
+bool jump_uses_narrow_kernel(const GenArgs &g) { return PRNGD_JUMP_NARROW_V && jump_is_narrow(g); }
+
 template <int P>
 static cudaError_t jump_launch(const GenArgs &g, cudaStream_t st) {
     const void *tables = nullptr;  // the byte tables with the lane index innermost
@@ -2606,14 +2614,13 @@ static cudaError_t jump_launch(const GenArgs &g, cudaStream_t st) {
         if ((e = set_smem(gen_jump_kernel<M, P>, smem)) != cudaSuccess) return e;               \
         gen_jump_kernel<M, P><<<(unsigned)grid, kJumpWarps * 32, smem, st>>>(g, t);            \
     } while (0)
-    const bool narrow = PRNGD_JUMP_NARROW && mode == 1 && g.sh1 == 32u - g.w &&
-                        g.sh2 == 32u - g.w;
+    const bool narrow = jump_is_narrow(g);
     switch (mode) {
         case 3: PRNGD_JUMP_LAUNCH(3); break;
         case 2: PRNGD_JUMP_LAUNCH(2); break;
         case 1:
 #if PRNGD_JUMP_NARROW_V
-            if (narrow && (g.w == 8 || g.w == 16)) {
+            if (narrow) {
                 const size_t sn = 16 + (size_t)kJumpWarps * jumpn_comp_bytes<P>();
                 const bool clamp = g.span != g.span_fast;  // R11 (never at w <= 26)
                 auto kn = g.w == 8 ? (clamp ? gen_jump_narrow_kernel<true, true, P>

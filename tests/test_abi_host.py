@@ -196,7 +196,7 @@ def test_mrg_flag_rules(lib):
 
 @pytest.mark.parametrize("name,flags,kernel,store", [
     ("cfg1", 0, 1, 6),                          # AUTO, few streams, rare rejection: SEG
-    ("cfg2", 0, 2, 4),                          # AUTO, few streams, w = 8: NEXT-3 jump kernel
+    ("cfg2", 0, 5, 4),                          # AUTO, few streams, w = 8: NEXT-3 narrow jump kernel
     ("cfg3", 0, 0, 4),                          # AUTO, bulk: ROW
     ("cfg4", 0, 0, 4),
     ("cfg3", P.PRNGD_FLAG_STORE_SEG, 1, 6),     # explicit SEG

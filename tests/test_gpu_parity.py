@@ -187,7 +187,7 @@ def test_generate_host_jump_kernel_chunks(orc):
     33-pair rounds) for each staging chunk (2720 rows of 96 KiB per 256 MiB chunk: 2 chunks)."""
     p = W.config("cfg2", n_streams=4000, n_per_stream=12288)
     g = P.Generator(**p)
-    assert g.info["kernel"] == 2
+    assert g.info["kernel"] == 5  # w = 8: the narrow jump kernel
     host = g.generate_host().numpy()
     dev = g.generate()
     torch.cuda.synchronize()
