@@ -2597,7 +2597,9 @@ bool jump_is_narrow(const GenArgs &g) {
     return PRNGD_JUMP_NARROW && kernel_mode(g) == 1 && (g.w == 8 || g.w == 16) &&
            g.sh1 == 32u - g.w && g.sh2 == 32u - g.w;
 }
-bool jump_uses_narrow_kernel(const GenArgs &g) { return PRNGD_JUMP_NARROW_V && jump_is_narrow(g); }
+bool jump_uses_narrow_kernel(const GenArgs &g) {
+    return PRNGD_JUMP_NARROW_V && jump_is_narrow(g) && g.span == g.span_fast;
+}
 
 template <int P>
 static cudaError_t jump_launch(const GenArgs &g, cudaStream_t st) {
@@ -2620,13 +2622,12 @@ static cudaError_t jump_launch(const GenArgs &g, cudaStream_t st) {
         case 2: PRNGD_JUMP_LAUNCH(2); break;
         case 1:
 #if PRNGD_JUMP_NARROW_V
-            if (narrow) {
+            // (Eq.(4) is exact for w <= 26, so the R11 clamp is never needed here: the host's
+            // span_fast == span; the check keeps the kernel honest if that ever changed)
+            if (jump_uses_narrow_kernel(g)) {
                 const size_t sn = 16 + (size_t)kJumpWarps * jumpn_comp_bytes<P>();
-                const bool clamp = g.span != g.span_fast;  // R11 (never at w <= 26)
-                auto kn = g.w == 8 ? (clamp ? gen_jump_narrow_kernel<true, true, P>
-                                            : gen_jump_narrow_kernel<true, false, P>)
-                                   : (clamp ? gen_jump_narrow_kernel<false, true, P>
-                                            : gen_jump_narrow_kernel<false, false, P>);
+                auto kn = g.w == 8 ? gen_jump_narrow_kernel<true, false, P>
+                                   : gen_jump_narrow_kernel<false, false, P>;
                 if ((e = set_smem(kn, sn)) != cudaSuccess) return e;
                 kn<<<(unsigned)grid, kJumpWarps * 32, sn, st>>>(g, t);
                 break;
