@@ -62,6 +62,31 @@ def test_cfg2_bitwise_rejection_path(orc, seed):
     assert_same(out, orc.generate(p)["out"])
 
 
+@pytest.mark.parametrize("name,over", [
+    ("cfg1", {}),                                           # SEG (few streams, rare rejection)
+    ("cfg2", {}),                                           # NEXT-3 narrow jump kernel
+    ("cfg3", dict(n_streams=4096)),                         # ROW, bulk shape (a slice)
+    ("cfg4", dict(n_streams=2048)),                         # ROW, MODE 3 (asymmetric ranges)
+    ("mrg26", dict(n_streams=2048)),                        # NEXT-2 MRG32k3a
+])
+def test_second_seed_repeat_run(orc, name, over):
+    """SURVEY 8(d)'s repeat parity run with the second seed 0x0123456789ABCDEF, on the kernel
+    each BASELINE shape takes by default (AUTO), plus the fused statistics on the same inputs."""
+    p = W.config(name, seed=W.SEED2, **over)
+    if p.get("mrg"):
+        p["flags"] = p.get("flags", 0) | P.PRNGD_FLAG_MRG32K3A
+    _, out = gen(p)
+    ref = orc.generate(p, want_stats=True)
+    assert_same(out, ref["out"])
+    g = P.Generator(**p)
+    buf = torch.empty_like(out)
+    _, hist, pw, cnt = g.generate_consume(buf)
+    torch.cuda.synchronize()
+    assert_same(buf, ref["out"])
+    assert np.array_equal(hist.cpu().numpy(), ref["hist"]) and cnt.item() == ref["count"]
+    assert np.allclose(pw.cpu().numpy(), ref["pow"], rtol=1e-12, atol=0)
+
+
 def test_cfg2_pair_indices_and_consumed(orc):
     p = W.CONFIGS["cfg2"]
     g = P.Generator(**p)
