@@ -591,16 +591,18 @@ def main():
                 "note": "issue-bound below this peak (DESIGN.md section 8)"}
     elif p.get("mrg"):
         # MRG32k3a (NEXT-2): instruction-issue bound.  Algorithmic
-        # instructions per output (mrg26 runs the per-batch band test): per MRG32k3a draw 24
-        # (two binary64 components x 5: product, fused product-difference, rounding-shift pair,
-        # remainder; combination 9: two exact conversions, two canonical-representative fixes
-        # of 2, subtract-and-wrap 3; R23 test + mask 2; ring append 3: address, predicated store,
-        # counter), 2.03 draws per output (26-bit reduce-to-width rejects 1/64), plus 11 per
-        # output (Eq.(4) 6, ring read 2, band test 2, store 1): 24 x 2.03 + 11 = 60.  The fused
-        # consumer (consume_mrg_kernel) adds the statistics' 10 (power sums 5, bin 5) and drops
-        # the store (1) when nothing is written.
+        # instructions per output (mrg26 runs the per-batch band test): per MRG32k3a draw 21
+        # (two binary64 components x 5: product, fused product-difference, round-down shift
+        # pair, remainder; combination 6 with the floor reduction's values in [0, m]: two exact
+        # conversions, component 2's m2 -> 0 min, subtract-and-wrap 3; R23 test + mask 2; ring
+        # append 3: address, predicated store, counter), 2.03 draws per output (26-bit
+        # reduce-to-width rejects 1/64), plus 11 per output (Eq.(4) 6, ring read 2, band test 2,
+        # store 1): 21 x 2.03 + 11 = 54 (60 with round 2's balanced representatives, whose
+        # combination needed two sign fixes of 2 more).  The fused consumer (consume_mrg_kernel)
+        # adds the statistics' 10 (power sums 5, bin 5) and drops the store (1) when nothing is
+        # written.
         # Peak: 4 schedulers x 32 lanes per clock per SM x SMs x max SM clock.
-        ops = 60.0 + (10.0 if consume else 0.0) - (1.0 if consume and args.no_write else 0.0)
+        ops = 54.0 + (10.0 if consume else 0.0) - (1.0 if consume and args.no_write else 0.0)
         ach = ops * nout / (kern_ms * 1e-3) / 1e9
         pk = 4 * 32.0 * sms * clk_ghz
         roof = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "Ginstr/s", "frac": ach / pk,
