@@ -693,6 +693,24 @@ def test_guard_bands_generate(orc, flags, ns, nps):
     assert_same(out, orc.generate(p, kind=kind, open_interval=bool(flags & P.PRNGD_FLAG_OPEN))["out"])
 
 
+@pytest.mark.parametrize("offset", [0, 1])
+@pytest.mark.parametrize("ns,nps", [(45, 70), (31, 1030), (1, 6), (5, 1025)])
+def test_guard_bands_narrow_jump(orc, ns, nps, offset):
+    """gen_jump_narrow_kernel (w = 8): sentinels on both sides, and with offset 1 an output that
+    is 8- but not 16-byte aligned, so rounds start on odd elements (head / tail outputs)."""
+    p = W.config("cfg2", n_streams=ns, n_per_stream=nps, flags=P.PRNGD_FLAG_JUMP)
+    g = P.Generator(**p)
+    assert g.info["kernel"] == 5
+    n = ns * nps
+    buf = torch.full((n + 2 * GUARD + 1,), -3.25, dtype=torch.float64, device="cuda")
+    out = buf[GUARD + offset:GUARD + offset + n].view(ns, nps)
+    g.generate(out)
+    torch.cuda.synchronize()
+    assert bool((buf[:GUARD + offset] == -3.25).all())
+    assert bool((buf[GUARD + offset + n:] == -3.25).all())
+    assert_same(out, orc.generate(p)["out"])
+
+
 @pytest.mark.parametrize("flags", [P.STORE_FLAGS[n] for n in P.stores_available(
     ["row", "tma", "tile", "direct"])])
 def test_guard_bands_consume(orc, flags):
