@@ -495,6 +495,12 @@ static_assert(kMrgRingBytes >= 8u * kCols + 4u * kMrgStep, "MRG ring smaller tha
 #ifndef PRNGD_MRG_FP64
 #define PRNGD_MRG_FP64 2
 #endif
+// REGCONST: the moduli and reciprocals pinned in registers for the generate kernel (A/B on
+// mrg26, same box, two alternating repetitions: write 387.6 -> 394.6 Gd/s; the fused consumer,
+// short of registers, 301.0 -> 299.4, so it keeps the constant-bank operands)
+#ifndef PRNGD_MRG_REGCONST
+#define PRNGD_MRG_REGCONST 1
+#endif
 template <int FP> struct MrgWord { using T = uint32_t; };
 template <> struct MrgWord<1> { using T = double; };
 // SPECB slow path: rewrite a lane's buffered draws [rd, wr) of its ring (counter c at shared
@@ -542,7 +548,8 @@ __device__ __noinline__ uint32_t mrg_drop_out_of_band(uint32_t ring, uint32_t rd
 #ifndef PRNGD_MRG_SWZ
 #define PRNGD_MRG_SWZ 0
 #endif
-template <bool EQ4, bool SAMEW, bool ALG1 = false, bool SPECB = false, bool SWZ = false>
+template <bool EQ4, bool SAMEW, bool ALG1 = false, bool SPECB = false, bool SWZ = false,
+          bool RC = false>
 struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold and mask)
     using T1 = typename MrgWord<PRNGD_MRG_FP64 >= 1 ? 1 : 0>::T;  // component 1 word
     using T2 = typename MrgWord<PRNGD_MRG_FP64 >= 2 ? 1 : 0>::T;  // component 2 word
@@ -556,12 +563,22 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
     uint32_t wr, rd;
     uint32_t bad1;              // 4: the pending x1 lies outside the band, else 0
     uint32_t cx;                // this lane's ring (shared address) | its SWZ swizzle
+    // RC: moduli and reciprocals pinned in registers (passed through a warp shuffle, which ptxas
+    // cannot rematerialise as a constant-bank load inside the fill loop: the round-down FMA's
+    // immediate shift takes its one non-register operand slot)
+    double m1r, i1r, m2r, i2r;
     // stride: the counters of lane l start at stride * l (8: bank spread; 16: the in-ring output
     // staging of PRNGD_MRG_STAGE = 2 and of the fused consumer)
     __device__ __forceinline__ MrgProducer2(const GenArgs &g, uint64_t s, uint32_t ring_base,
                                             uint32_t lane,
                                             uint32_t stride = PRNGD_MRG_STAGE == 2 ? 16u : 8u)
         : k(g) {
+        if constexpr (RC) {
+            m1r = __shfl_sync(0xFFFFFFFFu, g.mrg_m1, 0);
+            i1r = __shfl_sync(0xFFFFFFFFu, g.mrg_inv1, 0);
+            m2r = __shfl_sync(0xFFFFFFFFu, g.mrg_m2, 0);
+            i2r = __shfl_sync(0xFFFFFFFFu, g.mrg_inv2, 0);
+        }
         const Mrg32k3a m = mrg_stream_start(g.seed, s);
         A = (T1)m.s0, B = (T1)m.s1, C = (T1)m.s2, D = (T2)m.t0, E = (T2)m.t1, F = (T2)m.t2;
         rd = wr = SWZ ? 0u : stride * lane;
@@ -570,11 +587,11 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
     }
     static __device__ __forceinline__ uint32_t c1(uint32_t a, uint32_t b) { return mrg_c1(a, b); }
     __device__ __forceinline__ double c1(double a, double b) const {
-        return mrg_c1d(a, b, k.mrg_m1, k.mrg_inv1);
+        return RC ? mrg_c1d(a, b, m1r, i1r) : mrg_c1d(a, b, k.mrg_m1, k.mrg_inv1);
     }
     static __device__ __forceinline__ uint32_t c2(uint32_t a, uint32_t b) { return mrg_c2(a, b); }
     __device__ __forceinline__ double c2(double a, double b) const {
-        return mrg_c2d(a, b, k.mrg_m2, k.mrg_inv2);
+        return RC ? mrg_c2d(a, b, m2r, i2r) : mrg_c2d(a, b, k.mrg_m2, k.mrg_inv2);
     }
     // u - 1 of the combined draw (R21), the value R23 tests
     static __device__ __forceinline__ uint32_t combine(uint32_t p1, uint32_t p2) {
@@ -1119,7 +1136,8 @@ __global__ void __launch_bounds__(32) gen_mrg_kernel(const __grid_constant__ Gen
     // 256-byte alignment is all the rings need (no TMA here): a smaller footprint, more warps
     const uint32_t base = (smem_u32(smem_raw) + (kMrgRingBytes - 1)) & ~(kMrgRingBytes - 1);
     static_assert(kMrgTileBytes % kMrgRingBytes == 0, "rings must stay kMrgRingBytes aligned");
-    MrgProducer2<EQ4, SAMEW, ALG1, SPECB, PRNGD_MRG_SWZ && PRNGD_MRG_STAGE != 2> prod(
+    MrgProducer2<EQ4, SAMEW, ALG1, SPECB, PRNGD_MRG_SWZ && PRNGD_MRG_STAGE != 2,
+                 PRNGD_MRG_REGCONST != 0> prod(
         g, g.stream_begin + row0 + lane, base + (uint32_t)kMrgStageBytes + lane * kMrgRingBytes,
         lane);
     if constexpr (PRNGD_MRG_STAGE == 2) {
