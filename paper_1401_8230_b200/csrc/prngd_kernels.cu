@@ -481,14 +481,26 @@ constexpr uint32_t kMrgRingBytes = kMrgRing * 8u;  // per lane: 2 kMrgRing 4-byt
 #define PRNGD_MRG_STAGE 0
 #endif
 #ifndef PRNGD_MRG_STEP
-#define PRNGD_MRG_STEP 9  // draws per lane per fill-loop step (a multiple of the period 3);
-                          // A/B on mrg26: 3 -> 304, 6 -> 326, 9 -> 330, 12-18 -> 328-331, 24 -> 313
+// draws per lane per fill-loop step of the generate kernel (a multiple of the period 3); round 1
+// A/B on mrg26: 3 -> 304, 6 -> 326, 9 -> 330, 12-18 -> 328-331, 24 -> 313 Gd/s; after the round-2
+// cuts 15 is best (table below)
+#define PRNGD_MRG_STEP 15
 #endif
 constexpr uint32_t kMrgStep = PRNGD_MRG_STEP;
-static_assert(kMrgStep % 3 == 0, "the register rotation has period 3");
+// the fused consumer's fill step (its own optimum: A/B after the round-2 cuts, mrg26, same box,
+// two alternating repetitions, write / write + statistics / statistics only in Gd/s:
+//   step 9: 394.4 / 305.4 / 332.7;  12: 395.7 / 310.6 / -;  15: 400.0 / 316.2 / 344.2;
+//   18: 397.4 / 318.1 / 342.0;  21: 389.5 / 309.6 / 337.7;  24: 379.0 / 304.8 / 328.2;
+//   30: 351.2 / 282.2 / 301.7 -- profiles/s2j_mrg_step_ab.txt)
+#ifndef PRNGD_MRG_STEP_CONS
+#define PRNGD_MRG_STEP_CONS 18
+#endif
+constexpr uint32_t kMrgStepCons = PRNGD_MRG_STEP_CONS;
+static_assert(kMrgStep % 3 == 0 && kMrgStepCons % 3 == 0, "the register rotation has period 3");
 // a lane one draw short of a batch must still have room for a whole step (else the fill loop
 // never ends)
-static_assert(kMrgRingBytes >= 8u * kCols + 4u * kMrgStep, "MRG ring smaller than batch + step");
+static_assert(kMrgRingBytes >= 8u * kCols + 4u * (kMrgStep > kMrgStepCons ? kMrgStep : kMrgStepCons),
+              "MRG ring smaller than batch + step");
 
 // MRG_FP64: 0 = both components in 32-bit integer arithmetic, 1 = component 1 in binary64,
 // 2 = both in binary64 (exact either way; A/B of INT32 vs FP64 pipe load)
@@ -549,7 +561,7 @@ __device__ __noinline__ uint32_t mrg_drop_out_of_band(uint32_t ring, uint32_t rd
 #define PRNGD_MRG_SWZ 0
 #endif
 template <bool EQ4, bool SAMEW, bool ALG1 = false, bool SPECB = false, bool SWZ = false,
-          bool RC = false>
+          bool RC = false, uint32_t STEP = kMrgStep>
 struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold and mask)
     using T1 = typename MrgWord<PRNGD_MRG_FP64 >= 1 ? 1 : 0>::T;  // component 1 word
     using T2 = typename MrgWord<PRNGD_MRG_FP64 >= 2 ? 1 : 0>::T;  // component 2 word
@@ -637,9 +649,9 @@ struct MrgProducer2 {  // SAMEW: x1 and x2 have the same width (one threshold an
     __device__ __forceinline__ void fill(const GenArgs &g) {
 #pragma unroll 1
         while (__any_sync(0xFFFFFFFFu, wr - rd < 8u * (uint32_t)kCols)) {
-            if (wr - rd <= kMrgRingBytes - 4u * kMrgStep) {  // room for kMrgStep more draws
+            if (wr - rd <= kMrgRingBytes - 4u * STEP) {  // room for STEP more draws
 #pragma unroll
-                for (int r = 0; r < kMrgStep / 3; ++r) {
+                for (int r = 0; r < (int)STEP / 3; ++r) {
                     A = c1(B, A), D = c2(F, D);
                     take(combine(A, D), g);
                     B = c1(C, B), E = c2(D, E);
@@ -1272,7 +1284,7 @@ __global__ void __launch_bounds__(kMrgConsWarps * 32, 1)
     for (uint64_t t = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * warp; t < n_tasks;
          t += (uint64_t)gridDim.x * kMrgConsWarps) {
         const uint64_t row0 = t * 32u;
-        MrgProducer2<EQ4, SAMEW, ALG1, SPECB> prod(g, g.stream_begin + row0 + lane,
+        MrgProducer2<EQ4, SAMEW, ALG1, SPECB, false, false, kMrgStepCons> prod(g, g.stream_begin + row0 + lane,
                                                   rings + lane * kMrgRingBytes, lane, 16u);
         const bool live = row0 + lane < g.n_streams;
         const bool full_rows = row0 + 32u <= g.n_streams;
