@@ -513,6 +513,10 @@ static_assert(kMrgRingBytes >= 8u * kCols + 4u * (kMrgStep > kMrgStepCons ? kMrg
 #ifndef PRNGD_MRG_REGCONST
 #define PRNGD_MRG_REGCONST 1
 #endif
+#ifndef PRNGD_MRG_REGCONST_CONS
+#define PRNGD_MRG_REGCONST_CONS 0  // the same for the fused consumer (A/B only: at fill step 18
+                                   // 316.8 vs 318.3 Gd/s write + statistics, 341.4 vs 342.0 stats only)
+#endif
 template <int FP> struct MrgWord { using T = uint32_t; };
 template <> struct MrgWord<1> { using T = double; };
 // SPECB slow path: rewrite a lane's buffered draws [rd, wr) of its ring (counter c at shared
@@ -1284,7 +1288,7 @@ __global__ void __launch_bounds__(kMrgConsWarps * 32, 1)
     for (uint64_t t = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * warp; t < n_tasks;
          t += (uint64_t)gridDim.x * kMrgConsWarps) {
         const uint64_t row0 = t * 32u;
-        MrgProducer2<EQ4, SAMEW, ALG1, SPECB, false, false, kMrgStepCons> prod(g, g.stream_begin + row0 + lane,
+        MrgProducer2<EQ4, SAMEW, ALG1, SPECB, false, PRNGD_MRG_REGCONST_CONS != 0, kMrgStepCons> prod(g, g.stream_begin + row0 + lane,
                                                   rings + lane * kMrgRingBytes, lane, 16u);
         const bool live = row0 + lane < g.n_streams;
         const bool full_rows = row0 + 32u <= g.n_streams;
