@@ -1435,6 +1435,24 @@ __device__ __forceinline__ Xs128 jump_state_nib(const uint4 *__restrict__ tab, c
     return Xs128{r0, r1, r2, r3};
 }
 
+// J_l * s through the lane-interleaved byte tables ([b][v][lane], jump_tables_interleaved): the
+// lanes that jump the same state s read one contiguous run per table row (16 x 16-byte loads).
+__device__ __forceinline__ Xs128 jump_state_lane(const uint4 *__restrict__ tabs, const Xs128 &s,
+                                                 uint32_t lane) {
+    const uint32_t words[4] = {s.x, s.y, s.z, s.w};
+    uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint32_t v = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+        const uint4 t = __ldg(&tabs[((uint32_t)k * 256u + v) * 32u + lane]);
+        r0 ^= t.x;
+        r1 ^= t.y;
+        r2 ^= t.z;
+        r3 ^= t.w;
+    }
+    return Xs128{r0, r1, r2, r3};
+}
+
 // Resident CTAs per SM the register budget must allow: 7 x 4 warps x 148 SMs = 4144 >= cfg2's
 // 4096 streams, so cfg2 runs as ONE wave (74 registers gave 6 CTAs: 1.15 waves).
 #ifndef PRNGD_JUMP_MINB
@@ -1465,21 +1483,7 @@ __global__ void __launch_bounds__(kJumpWarps * 32, P > 32 ? 4 : PRNGD_JUMP_MINB)
     while (base < g.nps) {
         // every lane jumps the same round-start state: with the lane index innermost in the
         // byte tables ([b][v][lane]) each of the 16 loads reads one contiguous 512-byte run
-        Xs128 st = S;
-        if (lane) {
-            const uint32_t words[4] = {S.x, S.y, S.z, S.w};
-            uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const uint32_t v = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-                const uint4 t = __ldg(&tabs[((uint32_t)k * 256u + v) * 32u + lane]);
-                r0 ^= t.x;
-                r1 ^= t.y;
-                r2 ^= t.z;
-                r3 ^= t.w;
-            }
-            st = Xs128{r0, r1, r2, r3};
-        }
+        Xs128 st = lane ? jump_state_lane(tabs, S, lane) : S;
         double q[P];
         using MaskT = typename std::conditional<(P > 32), uint64_t, uint32_t>::type;
         MaskT mask = 0;
@@ -1606,21 +1610,8 @@ __global__ void __launch_bounds__(kJumpWarps * 32, PRNGD_JUMPN_MINB)
     uint64_t base = 0;
 #pragma unroll 1
     while (base < g.nps) {
-        Xs128 st = S;
-        if (lane) {  // lane l starts at draw 2 P l of the round (lane-interleaved byte tables)
-            const uint32_t words[4] = {S.x, S.y, S.z, S.w};
-            uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const uint32_t v = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-                const uint4 t = __ldg(&tabs[((uint32_t)k * 256u + v) * 32u + lane]);
-                r0 ^= t.x;
-                r1 ^= t.y;
-                r2 ^= t.z;
-                r3 ^= t.w;
-            }
-            st = Xs128{r0, r1, r2, r3};
-        }
+        // lane l starts at draw 2 P l of the round (lane-interleaved byte tables)
+        Xs128 st = lane ? jump_state_lane(tabs, S, lane) : S;
         uint32_t v[P];
         using MaskT = typename std::conditional<(P > 32), uint64_t, uint32_t>::type;
         MaskT mask = 0;
@@ -1786,19 +1777,7 @@ __device__ __forceinline__ Xs128 seg_jump(const uint4 *__restrict__ tabs,
     return j ? jump_state(my_tab, s) : s;
 #elif PRNGD_SEG_JUMP == 4
     (void)my_tab, (void)log2S;
-    if (!j) return s;
-    const uint32_t words[4] = {s.x, s.y, s.z, s.w};
-    uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        const uint32_t v = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-        const uint4 t = __ldg(&tabs[((uint32_t)k * 256u + v) * 32u + j]);
-        r0 ^= t.x;
-        r1 ^= t.y;
-        r2 ^= t.z;
-        r3 ^= t.w;
-    }
-    return Xs128{r0, r1, r2, r3};
+    return j ? jump_state_lane(tabs, s, j) : s;
 #elif PRNGD_SEG_JUMP == 1
     (void)tabs, (void)log2S;
     return j ? jump_state_nib(my_tab, s) : s;
@@ -1860,20 +1839,7 @@ __device__ __forceinline__ void run_task_seg_consume(const GenArgs &g, uint32_t 
     const uint64_t rows_left = g.n_streams - row0;
     const uint32_t nchunks = rows_left >= rpw ? 32u : (uint32_t)rows_left << log2S;
     Xs128 st = stream_start(g.seed, g.stream_begin + row);
-    if (j) {  // T^(256 j) s: byte tables with the lane index innermost (one run per row)
-        const uint32_t words[4] = {st.x, st.y, st.z, st.w};
-        uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const uint32_t v = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-            const uint4 tv = __ldg(&g.jump_tab[((uint32_t)k * 256u + v) * 32u + j]);
-            r0 ^= tv.x;
-            r1 ^= tv.y;
-            r2 ^= tv.z;
-            r3 ^= tv.w;
-        }
-        st = Xs128{r0, r1, r2, r3};
-    }
+    if (j) st = jump_state_lane(g.jump_tab, st, j);  // T^(256 j) s (one run per row)
     const Xs128 seg0 = st;
     constexpr uint32_t RS = kCols * 8u + 16u;  // padded tile row (one batch per lane)
     const uint32_t my = tile + lane * RS;
