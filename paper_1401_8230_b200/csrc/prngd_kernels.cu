@@ -87,7 +87,9 @@ constexpr int kConsWarpsRow = PRNGD_CONS_ROW_WARPS;
 constexpr int kConsRowCols = PRNGD_CONS_ROW_COLS;
 // The row-segment consumer keeps only 2-4 rows per warp in flight, so it takes 16 warps
 // (A/B, same box, cfg5 / cfg3 + statistics: 12 -> 597-606 / 608-617, 14 -> 571-574 / 581-589,
-// 16 -> 611-616 / 618-649 Gd/s; the ROW-tile consumer loses with 16: 559 vs 580)
+// 16 -> 611-616 / 618-649 Gd/s; the ROW-tile consumer loses with 16: 559 vs 580).  Session 2,
+// cfg5 best step of 10-step runs: 16 -> 692.5-694.5, 18 (96 registers, spills) -> 636-640,
+// 20 (96 registers) -> 677-678 Gd/s (profiles/s2k_consumer_warps_ab.txt)
 #ifndef PRNGD_CONS_SEG_WARPS
 #define PRNGD_CONS_SEG_WARPS 16
 #endif
