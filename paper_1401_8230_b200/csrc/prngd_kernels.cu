@@ -1359,6 +1359,9 @@ __global__ void __launch_bounds__(kMrgConsWarps * 32, 1)
 // capped at 96 registers with spills: 251; 25 pairs: 223, `profiles/r02m_jump_pairs_ab.txt`).
 constexpr int kJumpPairs = (int)(kJumpDraws / 2);
 constexpr int kJumpPairsLong = 33;
+#ifndef PRNGD_JUMP_LONG_MIN
+#define PRNGD_JUMP_LONG_MIN 1000  // rows of at least this many outputs take the 33-pair rounds
+#endif
 #ifndef PRNGD_JUMP_TAIL
 #define PRNGD_JUMP_TAIL 24
 #endif
@@ -2681,7 +2684,8 @@ static cudaError_t jump_launch(const GenArgs &g, cudaStream_t st) {
 cudaError_t launch_generate_jump(const GenArgs &g, const Plan &pl, cudaStream_t st) {
     (void)pl;
     // long rows: one 33-pair round per 1024 outputs; short rows: 17-pair rounds
-    return g.nps >= 1000 ? jump_launch<kJumpPairsLong>(g, st) : jump_launch<kJumpPairs>(g, st);
+    return g.nps >= PRNGD_JUMP_LONG_MIN ? jump_launch<kJumpPairsLong>(g, st)
+                                        : jump_launch<kJumpPairs>(g, st);
 }
 
 cudaError_t launch_generate_seg(const GenArgs &g, const Plan &pl, cudaStream_t st) {
