@@ -336,9 +336,11 @@ def main():
     out = torch.empty((p["n_streams"], p["n_per_stream"]), dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
     if consume:
-        hist = torch.zeros(65536, dtype=torch.int64, device="cuda")
-        pw = torch.zeros(4, dtype=torch.float64, device="cuda")
-        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        # one buffer for the three accumulators, so a step clears them with one fill
+        acc = torch.zeros(65536 + 4 + 1, dtype=torch.int64, device="cuda")
+        hist = acc[:65536]
+        pw = acc[65536:65540].view(torch.float64)
+        cnt = acc[65540:]
     # The statistics exchange (N > 1): by default rank 0's accumulator is mapped into every rank
     # (CUDA IPC, peer memory over NVLink) and each rank's finalize kernel adds into it with device
     # atomics -- fused into the library's own launches; NCCL all-reduce is the fallback.
@@ -400,7 +402,7 @@ def main():
             # each call also bumps the accumulator's arrival counter (completion protocol)
             peer.consume(g.handle, None if args.no_write else out, st)
         elif consume:
-            hist.zero_(), pw.zero_(), cnt.zero_()
+            acc.zero_()
             P.prngd_generate_consume(g.handle, None if args.no_write else out, hist, pw, cnt, st)
             if world > 1:  # the path's only exchange: NCCL all-reduce of the statistics
                 D.allreduce_stats(hist, pw, cnt)
