@@ -297,14 +297,27 @@ def small_step_floor(out, stream, torch, scratch, scratch_rd, steps: int = 50) -
                     "this step's"}
 
 
+def shared_config(args, p: dict, world: int) -> dict:
+    """The workload keys both arms report (this implementation's line adds its launch details,
+    the reference arm its CPU sample), so the driver's ratio compares like with like."""
+    consume = args.workload == "cfg5" or args.consume
+    return {"workload": f"{args.workload}: {W.DESCRIPTIONS.get(args.workload, args.workload)}",
+            "streams_per_gpu": p["n_streams"], "n_per_stream": p["n_per_stream"],
+            "seed": p["seed"], "bytes_written_per_step_per_gpu": 8 * p["n_streams"] * p["n_per_stream"],
+            "parallelism": f"stream-range shards x{world}",
+            "method_flags": args.flags | p.get("map_flags", 0),
+            "base_generator": "MRG32k3a" if p.get("mrg") else "xorshift128",
+            "write_outputs": not (consume and args.no_write)}
+
+
 def run_reference(args, rank, world):
     """Reference arm = the CPU oracle (this tier has no upstream code)."""
     if rank != 0:
         return 0
     import oracle
     oracle.build()
-    p = workload_params(args.workload, 0, 1)
-    cons = args.workload == "cfg5"
+    p = workload_params(args.workload, 0, 1, args.scaling)
+    cons = args.workload == "cfg5" or args.consume
     ns = 4096  # bounded sample per step: 4096 streams x n_per_stream
     nout = ns * p["n_per_stream"]
     for _ in range(args.warmup):
@@ -319,7 +332,7 @@ def run_reference(args, rank, world):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "sample": sample},
+            "config": dict(shared_config(args, p, world), sample=sample),
             "cpu_baseline": {"value": v, "unit": "Gdoubles/s", "cores": 1, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": v, "unit": "Gdoubles/s", "h2d_bytes_per_step": 0,
@@ -767,15 +780,12 @@ def main():
         cpu = cpu_baseline(q)
 
     if rank == 0:
-        desc = W.DESCRIPTIONS.get(args.workload, args.workload)
         line = {
             "metric": METRIC, "value": value, "unit": "Gdoubles/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"{args.workload}: {desc}",
-                       "streams_per_gpu": p["n_streams"], "n_per_stream": p["n_per_stream"],
-                       "seed": p["seed"], "bytes_written_per_step_per_gpu": 8 * nout,
+            "config": dict(shared_config(args, p, world), **{
                        "l2": ("EXPERIMENT: warm L2, no flush between steps (--warm-l2)"
                               if args.warm_l2 and 8 * nout < (256 << 20) else
                               "outputs fit in the 126 MB L2: a 256 MiB buffer is written and "
@@ -783,11 +793,9 @@ def main():
                               "per-step events time the step"
                               if l2_flush else
                               "inputs none; 8 B/output written, >126 MB L2 per step (no flush)"),
-                       "parallelism": f"stream-range shards x{world}",
                        "flags": p["flags"], "store": args.store,
                        "cuda_graph": graph is not None,
-                       "stats_reduce": reduce_mode,
-                       "write_outputs": not (consume and args.no_write)},
+                       "stats_reduce": reduce_mode}),
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

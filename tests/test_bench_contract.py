@@ -22,13 +22,21 @@ def _run(args, timeout=600):
     return json.loads(lines[0])
 
 
+SHARED_CONFIG_KEYS = {"workload", "streams_per_gpu", "n_per_stream", "seed",
+                      "bytes_written_per_step_per_gpu", "parallelism", "method_flags",
+                      "base_generator", "write_outputs"}
+
+
 def test_reference_arm_line():
     d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0"])
     assert BASE_KEYS <= set(d) and d["impl"] == "reference"
     assert d["value"] > 0 and d["higher_is_better"] is True and d["n_gpus"] == 1
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
-    assert d["config"]["workload"] == "cfg3"
+    # the same workload keys as this implementation's line (bench.shared_config), plus the sample
+    assert d["config"]["workload"].startswith("cfg3: ")
+    assert SHARED_CONFIG_KEYS <= set(d["config"]) and "sample" in d["config"]
+    assert d["config"]["streams_per_gpu"] == 1 << 20 and d["config"]["n_per_stream"] == 1024
 
 
 @pytest.mark.gpu
@@ -45,4 +53,5 @@ def test_implementation_line():
     assert d["e2e"]["d2h_bytes_per_step"] == 8 * 1024 * 1024
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["gpu_launches"] == 3
+    assert SHARED_CONFIG_KEYS <= set(d["config"]) and d["config"]["workload"].startswith("cfg1: ")
     assert "L2 flush" in d["config"]["l2"] or "flush" in d["config"]["l2"]
