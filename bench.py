@@ -49,6 +49,9 @@ def parse():
                          "(the line says so in config.l2); never a bench value")
     ap.add_argument("--sustained-s", type=float, default=1.5,
                     help="length of the sustained-throughput window (0: skip)")
+    ap.add_argument("--hist-only", action="store_true",
+                    help="consume workloads on one GPU: histogram + count only (d_pow = NULL; "
+                         "BASELINE cfg4's 'fused 2^16-bin histogram'), no power sums")
     ap.add_argument("--consume", action="store_true",
                     help="add the fused consumer (S7) to a write workload (cfg5 always has it)")
     ap.add_argument("--no-write", action="store_true",
@@ -307,7 +310,9 @@ def shared_config(args, p: dict, world: int) -> dict:
             "parallelism": f"stream-range shards x{world}",
             "method_flags": args.flags | p.get("map_flags", 0),
             "base_generator": "MRG32k3a" if p.get("mrg") else "xorshift128",
-            "write_outputs": not (consume and args.no_write)}
+            "write_outputs": not (consume and args.no_write),
+            **({"statistics": "histogram + count" if getattr(args, "hist_only", False)
+                else "histogram + count + 4 power sums"} if consume else {})}
 
 
 def run_reference(args, rank, world):
@@ -449,7 +454,8 @@ def main():
             peer.consume(g.handle, None if args.no_write else out, st)
         elif consume:
             acc.zero_()
-            P.prngd_generate_consume(g.handle, None if args.no_write else out, hist, pw, cnt, st)
+            P.prngd_generate_consume(g.handle, None if args.no_write else out, hist,
+                                     None if args.hist_only else pw, cnt, st)
             if world > 1:  # the path's only exchange: NCCL all-reduce of the statistics
                 D.allreduce_stats(hist, pw, cnt)
         else:

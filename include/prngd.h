@@ -185,7 +185,9 @@ PRNGD_API prngd_status prngd_generate(const prngd_handle *h, double *d_out, void
  * All three accumulate with device atomics, so shards -- including other processes on other
  * GPUs that mapped the same buffer with prngd_ipc_open (peer memory over NVLink) -- may add
  * into one buffer concurrently: the statistics reduction then happens inside this call's own
- * kernels.  d_hist, d_pow, d_count: device (local or peer-mapped), 8-byte aligned, required.
+ * kernels.  d_hist, d_count: device (local or peer-mapped), 8-byte aligned, required.  d_pow: the
+ * same, or NULL for a histogram-only call (BASELINE cfg4's "fused 2^16-bin histogram": d_hist and
+ * d_count as above, no power sums; the kernel then skips their five FP64 operations per output).
  * Three kernel launches (generate + bin, the exact pass that returns at once unless a 16-bit
  * counter wrapped, slab reduction); two with PRNGD_FLAG_EXACT_HIST. */
 PRNGD_API prngd_status prngd_generate_consume(const prngd_handle *h, double *d_out, int64_t *d_hist,

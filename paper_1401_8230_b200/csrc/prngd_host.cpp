@@ -511,7 +511,7 @@ static prngd_status generate_consume_impl(const prngd_handle *hc, double *d_out,
                                           double *d_pow, int64_t *d_count, uint64_t *d_arrive,
                                           bool mc, void *cuda_stream) {
     NvtxRange nvtx_range("prngd_generate_consume");
-    if (!hc || !d_hist || !d_pow || !d_count)
+    if (!hc || !d_hist || !d_count)  // d_pow == NULL: histogram-only call
         return fail(PRNGD_EINVAL, "null handle or accumulator pointer");
     if (((uintptr_t)d_hist | (uintptr_t)d_pow | (uintptr_t)d_count | (uintptr_t)d_arrive) & 7u)
         return fail(PRNGD_EINVAL, "accumulators must be 8-byte aligned");

@@ -40,6 +40,9 @@ struct GenArgs {
     // fused consumer with row segments (Store::SEG): log2 of the lanes per row and the
     // lane-interleaved jump tables of distance kSegDraws
     uint32_t seg_log2;
+    // histogram-only consumer (the caller passed no power-sum accumulator: BASELINE cfg4's "fused
+    // 2^16-bin histogram"): the full-batch fast paths skip the five FP64 power-sum operations
+    uint32_t hist_only;
     const uint4 *jump_tab;
 };
 

@@ -172,11 +172,13 @@ struct ConsumerT {
     double s1[kPowSplit], s2[kPowSplit], s3[kPowSplit], s4[kPowSplit];
     uint32_t *hist;   // shared: 32768 words; word j holds bin j (low half), bin j + 32768 (high)
     int64_t *spill;   // global: carries of the packed counters, [65536]
-    __device__ __forceinline__ void init(uint32_t *h, int64_t *sp) {
+    bool hist_only;   // warp-uniform: the full-batch paths call add_hist (no power sums)
+    __device__ __forceinline__ void init(uint32_t *h, int64_t *sp, bool ho = false) {
 #pragma unroll
         for (int k = 0; k < kPowSplit; ++k) s1[k] = s2[k] = s3[k] = s4[k] = 0.0;
         hist = h;
         spill = sp;
+        hist_only = ho;
     }
     __device__ __forceinline__ double sum(const double (&a)[kPowSplit]) const {
         double r = a[0];
@@ -197,6 +199,11 @@ struct ConsumerT {
         s2[k] = __dadd_rn(s2[k], z2);
         s3[k] = __fma_rn(z2, q, s3[k]);
         s4[k] = __fma_rn(z2, z2, s4[k]);
+        add_hist(q);
+    }
+    // The histogram half of R16 alone (histogram-only calls; the power sums such a call still
+    // accumulates on its slow paths are never read).
+    __device__ __forceinline__ void add_hist(double q) {
         // t = floor(q * 2^18) = 4 bin + 2 fraction bits (the scaling is exact, so t >> 2 is R16's
         // floor(q * 2^16)): the word's byte offset is t & 0x1FFFC and the half is bit 17, with
         // no shifts (bins b and b + 32768 share word b)
@@ -236,9 +243,24 @@ struct ConsumerT {
 using Consumer = ConsumerT<false, false>;
 
 struct NoConsumer {
+    static constexpr bool hist_only = false;
     __device__ __forceinline__ void init(uint32_t *, int64_t *) {}
     __device__ __forceinline__ void add(double, int = 0) {}
+    __device__ __forceinline__ void add_hist(double) {}
 };
+
+// S7 for one full batch: histogram + power sums, or (one warp-uniform branch per batch) the
+// histogram alone when the call has no power-sum accumulator.
+template <class Cons, int N>
+__device__ __forceinline__ void consume_batch(Cons &cons, const double (&q)[N]) {
+    if (cons.hist_only) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) cons.add_hist(q[i]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) cons.add(q[i], i);
+    }
+}
 
 // Eq.(4) of one pair on the specialised paths: MODE 2/3 compose v = x1:x2 as a register pair
 // (w = 32), MODE 1 as one wide multiply-add x1 * 2^w + x2 (w <= 31).
@@ -400,8 +422,7 @@ __device__ __forceinline__ void run_rows(const CUtensorMap *tmap, const GenArgs 
         const uint32_t valid = full ? (uint32_t)kCols : (uint32_t)(g.nps - col0);
         if (CONSUME && live) {
             if (full) {
-#pragma unroll
-                for (int i = 0; i < kCols; ++i) cons.add(q[i], i);
+                consume_batch(cons, q);
             } else {
 #pragma unroll
                 for (int i = 0; i < kCols; ++i)
@@ -739,8 +760,7 @@ __device__ __forceinline__ void run_rows_burst(const GenArgs &g, uint32_t tile, 
             if (CONSUME && live) {
                 const uint64_t base = col0 + b * kCols;
                 if (base + kCols <= g.nps) {
-#pragma unroll
-                    for (int i = 0; i < kCols; ++i) cons.add(q[i], i);
+                    consume_batch(cons, q);
                 } else {
 #pragma unroll
                     for (int i = 0; i < kCols; ++i)
@@ -991,7 +1011,7 @@ __global__ void __launch_bounds__(cons_warps<ST, WRITE>() * 32, 1)
     for (uint32_t i = threadIdx.x; i < kHistWords; i += blockDim.x) hist[i] = 0u;
     __syncthreads();
     ConsumerT<RED, (MODE >= 1 && MODE <= 3)> cons;
-    cons.init(hist, g.hist_spill);
+    cons.init(hist, g.hist_spill, g.hist_only != 0u);
     uint32_t it = 0;
     // rows per warp-task: 32, or 32 / S with S lanes per row (SEG)
     constexpr bool kSeg = WRITE && ST == Store::SEG;
@@ -1120,7 +1140,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const uint32_t *slab, int
     if (blockIdx.x == 0 && threadIdx.x < 4) {
         double acc = 0.0;
         for (int s = 0; s < n_slabs; ++s) acc = __dadd_rn(acc, pow_slab[s * 4 + threadIdx.x]);
-        stat_add_f64<MC>(&d_pow[threadIdx.x], acc);
+        if (d_pow) stat_add_f64<MC>(&d_pow[threadIdx.x], acc);  // null: histogram-only call
     }
     if (arrive) {
         __threadfence_system();  // this thread's adds are performed before the block arrives
@@ -1282,7 +1302,7 @@ __global__ void __launch_bounds__(kMrgConsWarps * 32, 1)
     for (uint32_t i = threadIdx.x; i < kHistWords; i += blockDim.x) hist[i] = 0u;
     __syncthreads();
     ConsumerT<RED, false> cons;
-    cons.init(hist, g.hist_spill);
+    cons.init(hist, g.hist_spill, g.hist_only != 0u);
     const uint64_t n_tasks = (g.n_streams + 31u) / 32u;
     const bool vec = (g.nps % 2u) == 0u && (reinterpret_cast<uintptr_t>(g.out) & 15u) == 0u;
     const uint32_t c = lane & 7u, rsub = lane >> 3;
@@ -1303,8 +1323,7 @@ __global__ void __launch_bounds__(kMrgConsWarps * 32, 1)
             const bool full = col0 + kCols <= g.nps;
             if (live) {
                 if (full) {
-#pragma unroll
-                    for (int i = 0; i < kCols; ++i) cons.add(q[i], i);
+                    consume_batch(cons, q);
                 } else {
 #pragma unroll
                     for (int i = 0; i < kCols; ++i)
@@ -1867,10 +1886,7 @@ __device__ __forceinline__ void run_task_seg_consume(const GenArgs &g, uint32_t 
             st = save;
             break;
         }
-        if (live) {
-#pragma unroll
-            for (int i = 0; i < kCols; ++i) cons.add(q[i], i);
-        }
+        if (live) consume_batch(cons, q);
 #pragma unroll
         for (int c = 0; c < kCols / 2; ++c) sts_v2(my + (c << 4), q[2 * c], q[2 * c + 1]);
         __syncwarp();
@@ -2431,6 +2447,7 @@ cudaError_t launch_generate_consume(const GenArgs &g0, const Plan &pl, double *d
     *launches = 0;
     if (scratch_bytes < consume_scratch_bytes(num_sms)) return cudaErrorInvalidValue;
     GenArgs g = g0;
+    g.hist_only = d_pow == nullptr ? 1u : 0u;
     g.out = d_out;
     scratch_layout(g, scratch, num_sms);
     const uint64_t tasks = (g.n_streams + 31u) / 32u;
@@ -2512,6 +2529,7 @@ cudaError_t launch_consume_memory(const GenArgs &g0, const double *src, uint64_t
     *launches = 0;
     if (scratch_bytes < consume_scratch_bytes(num_sms)) return cudaErrorInvalidValue;
     GenArgs g = g0;
+    g.hist_only = d_pow == nullptr ? 1u : 0u;
     scratch_layout(g, scratch, num_sms);
     const int grid = num_sms;  // every CTA writes its slab (empty ones too): finalize reads all
     const size_t smem = 1024 + (size_t)kHistWords * 4u;
@@ -2574,6 +2592,7 @@ cudaError_t launch_generate_consume_mrg(const GenArgs &g0, bool alg1, double *d_
     *launches = 0;
     if (scratch_bytes < consume_scratch_bytes(num_sms)) return cudaErrorInvalidValue;
     GenArgs g = g0;
+    g.hist_only = d_pow == nullptr ? 1u : 0u;
     g.out = d_out;
     scratch_layout(g, scratch, num_sms);
     const uint64_t tasks = (g.n_streams + 31u) / 32u;

@@ -437,11 +437,16 @@ class Generator:
         prngd_generate(self.handle, out, stream)
         return out
 
-    def generate_consume(self, out=None, hist=None, pw=None, count=None, stream=None):
+    def generate_consume(self, out=None, hist=None, pw=None, count=None, stream=None,
+                         moments=True):
+        """moments=False: histogram-only call (d_pow = NULL in the C ABI); pw is returned as None."""
         import torch
         dev = "cuda"
         hist = torch.zeros(65536, dtype=torch.int64, device=dev) if hist is None else hist
-        pw = torch.zeros(4, dtype=torch.float64, device=dev) if pw is None else pw
+        if moments:
+            pw = torch.zeros(4, dtype=torch.float64, device=dev) if pw is None else pw
+        else:
+            pw = None
         count = torch.zeros(1, dtype=torch.int64, device=dev) if count is None else count
         prngd_generate_consume(self.handle, out, hist, pw, count, stream)
         return out, hist, pw, count
